@@ -1,0 +1,172 @@
+/*
+ * ttb.h — C ABI of the B200 (sm_100a) TT-EmbeddingBag hot path.
+ *
+ * One handle per TT table. All array arguments are DEVICE pointers owned by
+ * the caller (PyTorch tensors on the Python side); the library never
+ * allocates device memory — the caller sizes and passes a workspace. Every
+ * call is stream-ordered and asynchronous unless documented as syncing, and
+ * the compute calls (plan / forward / backward / update) are CUDA-graph
+ * capturable: batch-dependent counts (distinct prefixes P, segments S,
+ * distinct rows U) stay on the device and kernels are launched over upper
+ * bounds.
+ *
+ * Each entry point replaces one reference (numpy) operator of Rec-AD's TT
+ * path; citations are file:line in the reference artifact (pkg/src/ttemb):
+ *
+ *   ttb_plan          lookup.py:97-124   prepare_reuse_plan (first-occurrence
+ *                                        prefix slots, hits/misses)
+ *                     lookup.py:254-260, 280-284  bag validation, bag ids,
+ *                                        (bag, slot) segments via np.unique
+ *                     tt_core.py:210-224 linear_index_to_tt_index (digits)
+ *   ttb_forward       lookup.py:127-149  execute_prefix_products (reuse buffer)
+ *                     lookup.py:286-296  forward_batch close + sum pooling
+ *   ttb_backward      backward.py:72-87  unique_aggregate (row-gradient merge)
+ *                     backward.py:101-183 tt_core_grads (core gradients)
+ *   ttb_aggregate     backward.py:72-87  unique_aggregate alone
+ *   ttb_backward_sgd  backward.py:207-227 backward_batch = aggregate + grads +
+ *                                        fused_update, in one device pass
+ *   ttb_sgd_update    backward.py:186-204 fused_update / model.py:353-364
+ *                                        DlrmModel.train_step update loop
+ *   ttb_export_*      read back plan / unique-row outputs for parity checks
+ *                     (ReusePlan.work / slot_of, seg ids, unique_aggregate)
+ *
+ * Status codes: 0 ok, negative on failure (see TTB_E*). Data-dependent
+ * errors (index out of range, empty bag, malformed offsets) are detected on
+ * the device and latched in the workspace; ttb_read_status() returns them.
+ * The Python wrapper maps them to ValueError exactly where the reference
+ * raises ValueError (lookup.py:88-94, 254-255).
+ */
+#ifndef TTB_H
+#define TTB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TTB_ABI_VERSION 1
+
+#define TTB_OK 0
+#define TTB_EINVAL (-1)     /* bad geometry / argument / capacity */
+#define TTB_ERANGE (-2)     /* an index lies outside [0, rows_padded) */
+#define TTB_EEMPTY (-3)     /* empty batch or an empty bag */
+#define TTB_EOFFSETS (-4)   /* offsets not 0 .. T, or decreasing */
+#define TTB_ENONFINITE (-5) /* non-finite gradient */
+#define TTB_ECUDA (-6)      /* CUDA launch / runtime failure */
+#define TTB_ESTATE (-7)     /* call order violated (forward before plan, ...) */
+
+/* device error-word bits (ttb_read_status status[0]) */
+#define TTB_ERRBIT_RANGE 1
+#define TTB_ERRBIT_EMPTY_BAG 2
+#define TTB_ERRBIT_OFFSETS 4
+#define TTB_ERRBIT_NONFINITE 8
+
+/*
+ * Table geometry, reference TtShape (tt_core.py:41-82) with d = 3.
+ * A d = 2 table (m1, m2), (n1, n2), (1, R, 1) is passed as
+ * m = (1, m1, m2), n = (1, n1, n2), r = (1, 1, R, 1) with a 1x1x1 core of
+ * value 1 in front: the arithmetic is identical.
+ * Core k has the reference layout (r[k], m[k] * n[k], r[k+1]), C order.
+ */
+typedef struct ttb_geom {
+  int64_t m[3];
+  int32_t n[3];
+  int32_t r[4];
+} ttb_geom;
+
+typedef struct ttb_handle ttb_handle; /* opaque host-side handle */
+typedef void *ttb_stream;             /* a cudaStream_t */
+
+int ttb_abi_version(void);
+const char *ttb_strerror(int code);
+/* number of kernels this library has launched in the process (a counter) */
+int64_t ttb_launch_count(void);
+
+/* device workspace bytes for tables of geometry g, batches up to max_T
+ * indices in up to max_B bags */
+int ttb_workspace_bytes(const ttb_geom *g, int64_t max_T, int64_t max_B,
+                        size_t *bytes);
+/* bind a caller-owned workspace (>= ttb_workspace_bytes) to a new handle and
+ * initialise it on `stream`. Returns NULL on bad arguments. */
+ttb_handle *ttb_create(const ttb_geom *g, int64_t max_T, int64_t max_B,
+                       void *workspace, size_t bytes, ttb_stream stream);
+void ttb_destroy(ttb_handle *h);
+
+/* K1: plan one batch. indices: T int64 (idx_is_64 = 1) or int32 values;
+ * offsets: B + 1 int64 bag boundaries (offsets[0] = 0, offsets[B] = T). */
+int ttb_plan(ttb_handle *h, const void *indices, int idx_is_64,
+             const int64_t *offsets, int64_t T, int64_t B, ttb_stream stream);
+
+/* K2 + K3: pooled bag embeddings out (B, N) fp32, N = n1 n2 n3. Also fills
+ * the prefix-product (reuse) buffer kept in the workspace for backward. */
+int ttb_forward(ttb_handle *h, const float *core0, const float *core1,
+                const float *core2, float *out, ttb_stream stream);
+
+/* K4: core gradients (fp32, core layout) for upstream grad_out (B, N).
+ * Requires ttb_forward on the same plan with the same cores. */
+int ttb_backward(ttb_handle *h, const float *core0, const float *core1,
+                 const float *core2, const float *grad_out, float *grad0,
+                 float *grad1, float *grad2, ttb_stream stream);
+
+/* K4 first stage alone: order the indices by row and sum each distinct
+ * row's upstream gradients (unique_aggregate, backward.py:72-87); read the
+ * result back with ttb_export_unique. Requires ttb_plan only. */
+int ttb_aggregate(ttb_handle *h, const float *grad_out, ttb_stream stream);
+
+/* K4 + K5: core gradients applied in place as SGD(+momentum):
+ *   v <- momentum * v + g (fp64 velocity); core <- f32(f64(core) - lr * v)
+ * (momentum == 0: velocity pointers may be NULL). update_mask bit k enables
+ * the update of core k (a d = 2 table disables its leading unit core). */
+int ttb_backward_sgd(ttb_handle *h, float *core0, float *core1, float *core2,
+                     const float *grad_out, double *vel0, double *vel1,
+                     double *vel2, double lr, double momentum,
+                     int update_mask, ttb_stream stream);
+
+/* K5 alone on a flat parameter: used after the data-parallel all-reduce
+ * and for dense parameters. velocity may be NULL when momentum == 0. */
+int ttb_sgd_update(float *param, const float *grad, double *velocity,
+                   int64_t n, double lr, double momentum, ttb_stream stream);
+
+/* SYNCS `stream`. status[0] = device error bits (TTB_ERRBIT_*), [1] = T,
+ * [2] = B, [3] = P (distinct prefixes), [4] = S (bag-prefix segments),
+ * [5] = U (distinct rows; valid after backward), [6] = plan generation. */
+int ttb_read_status(ttb_handle *h, int64_t status[8], ttb_stream stream);
+
+/* Plan read-back (after ttb_plan). Any pointer may be NULL. Sizes use the
+ * counts of ttb_read_status.
+ *   work      P x 4 int64: (prefix key, i1, i2, slot), first-occurrence order
+ *   slot_occ  T int64: buffer slot of each index's prefix
+ *   seg_ids   S int64: sorted bag * P + slot
+ *   seg_inv   T int64: segment of each index
+ *   digits    T x 3 int64: (i1, i2, i3) of each index                   */
+int ttb_export_plan(ttb_handle *h, int64_t *work, int64_t *slot_occ,
+                    int64_t *seg_ids, int64_t *seg_inv, int64_t *digits,
+                    ttb_stream stream);
+
+/* unique_aggregate read-back (after ttb_backward / ttb_backward_sgd):
+ * rows U int64 in first-occurrence order, grads U x N fp32 (nullable) —
+ * the per-row summed upstream gradients (backward.py:72-87). */
+int ttb_export_unique(ttb_handle *h, int64_t *rows, float *grads,
+                      ttb_stream stream);
+
+/* prefix-product (reuse) buffer read-back: P x (n1 n2) x r2 fp32, slot
+ * order (ReuseBuffer.slots, lookup.py:79-85). After ttb_forward. */
+int ttb_export_slots(ttb_handle *h, float *slots, ttb_stream stream);
+
+/* ---- measurement hooks (not part of the reference interface) ----------
+ * Per-kernel CUDA-event timing of one handle's launches: enable, run, then
+ * read the accumulated milliseconds and launch counts per kernel name
+ * (names: cap x 32 chars). Reading syncs and resets the accumulators. */
+int ttb_profile_enable(ttb_handle *h, int on);
+int ttb_profile_read(ttb_handle *h, char *names, double *ms, int64_t *calls,
+                     int cap, int *count);
+/* FP32 FMA throughput probe: blocks x 256 threads x iters x 16 flops; the
+ * caller times it with CUDA events to get the measured FP32 peak. */
+int ttb_fma_peak(float *sink, int iters, int blocks, ttb_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TTB_H */

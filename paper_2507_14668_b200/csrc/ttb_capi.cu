@@ -1,0 +1,289 @@
+// extern "C" entry points (include/ttb.h): handle, workspace layout, checks.
+#include <stdlib.h>
+#include <string.h>
+
+#include "ttb_internal.h"
+
+namespace ttb {
+long long g_launches = 0;
+size_t max_smem_needed(const DynDims& d);
+}  // namespace ttb
+
+using namespace ttb;
+
+namespace {
+
+int bits_for(uint64_t maxval) {  // bits to represent values in [0, maxval]
+  int b = 0;
+  while (b < 63 && (maxval >> b) != 0) ++b;
+  return b < 1 ? 1 : b;
+}
+
+bool geom_ok(const ttb_geom* g) {
+  if (!g) return false;
+  for (int k = 0; k < 3; ++k)
+    if (g->m[k] < 1 || g->n[k] < 1) return false;
+  if (g->r[0] != 1 || g->r[3] != 1 || g->r[1] < 1 || g->r[2] < 1) return false;
+  const double rows = (double)g->m[0] * (double)g->m[1] * (double)g->m[2];
+  if (rows >= 2147483647.0) return false;
+  return true;
+}
+
+struct Carver {
+  char* base;
+  size_t off = 0;
+  template <class T>
+  T* take(size_t count) {
+    off = (off + 255) & ~(size_t)255;
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += sizeof(T) * (count ? count : 1);
+    return p;
+  }
+};
+
+// Lays the workspace out (base == nullptr: sizing only). Fills h.
+void layout(ttb_handle& h, char* base) {
+  const ttb_geom& g = h.geom;
+  const int64_t T = h.maxT, B = h.maxB;
+  const int64_t m1m2 = g.m[0] * g.m[1];
+  const DynDims& d = h.dims;
+  const int64_t N = (int64_t)d.n1 * d.n2 * d.n3;
+  const int64_t SL = (int64_t)d.n1 * d.n2 * d.r2, G1S = (int64_t)d.n1 * d.r1, G2S = (int64_t)d.r1 * d.n2 * d.r2,
+                G3S = (int64_t)d.r2 * d.n3;
+  h.Pmax = T < m1m2 ? T : m1m2;
+  h.cmax = (g.m[0] + kPrefixChunk - 1) / kPrefixChunk;
+  h.sort_tiles = (T + kTile - 1) / kTile + 1;
+  int64_t st = (T + kTile - 1) / kTile;
+  const int64_t bt = (B + 31) / 32;
+  h.scan_tiles = (st > bt ? st : bt) + 1;
+  Carver c{base};
+  Workspace& w = h.w;
+  w.err = c.take<int>(16);
+  w.counts = w.err ? w.err + 0 : nullptr;  // counts share the header block; index 1.. used
+  w.pmap = c.take<unsigned>(m1m2);
+  w.pslot = c.take<int>(m1m2);
+  w.work_key = c.take<unsigned>(h.Pmax);
+  w.keys32 = c.take<unsigned>(T);
+  w.bag_of = c.take<int>(T);
+  w.occ_slot = c.take<int>(T);
+  w.seg_inv = c.take<int>(T);
+  w.occ_tmp = c.take<int>(T);
+  w.seg_slot = c.take<int>(T);
+  w.seg_bag = c.take<int>(T);
+  w.bag_seg = c.take<int>(B + 1);
+  w.bag_off = c.take<int>(B + 1);
+  w.slots = c.take<float>((size_t)h.Pmax * SL);
+  w.skA = c.take<unsigned>(T);
+  w.svA = c.take<unsigned>(T);
+  w.skB = c.take<unsigned>(T);
+  w.svB = c.take<unsigned>(T);
+  w.sort_hist = c.take<unsigned>(2 * 4 * 256);
+  w.sort_status = c.take<unsigned>((size_t)2 * 4 * h.sort_tiles * 256);
+  w.sort_ctr = c.take<unsigned>(8);
+  w.urow = c.take<unsigned>(T + 1);
+  w.urow_start = c.take<int>(T + 1);
+  w.urow_i3 = c.take<unsigned>(T);
+  w.prow_begin = c.take<int>(h.Pmax);
+  w.prow_end = c.take<int>(h.Pmax);
+  w.gU = c.take<float>((size_t)T * N);
+  w.dH = c.take<float>((size_t)T * G3S);
+  w.E = c.take<float>((size_t)h.Pmax * G1S);
+  w.dG2part = c.take<float>((size_t)g.m[1] * h.cmax * G2S);
+  w.i3_start = c.take<int>(g.m[2] + 1);
+  w.grp_cnt = c.take<int>(g.m[1]);
+  w.rkA = c.take<unsigned>(T);
+  w.rvA = c.take<unsigned>(T);
+  w.rkB = c.take<unsigned>(T);
+  w.rvB = c.take<unsigned>(T);
+  w.uid_first = c.take<int>(T);
+  w.scan_status = c.take<unsigned long long>((size_t)kNumScans * h.scan_tiles);
+  w.scan_ctr = c.take<unsigned>(16);
+  w.scratch1 = c.take<float>(16);
+  h.bytes = c.off + 256;
+}
+
+bool init_handle(ttb_handle& h, const ttb_geom* g, int64_t max_T, int64_t max_B) {
+  if (!geom_ok(g) || max_T < 1 || max_B < 1 || max_T >= (1ll << 29) || max_B > max_T) return false;
+  memset(&h, 0, sizeof(h));
+  h.geom = *g;
+  h.kg.m1 = (unsigned)g->m[0];
+  h.kg.m2 = (unsigned)g->m[1];
+  h.kg.m3 = (unsigned)g->m[2];
+  h.kg.m1m2 = (unsigned)(g->m[0] * g->m[1]);
+  h.kg.rows = (unsigned)(g->m[0] * g->m[1] * g->m[2]);
+  h.dims = DynDims{g->n[0], g->n[1], g->n[2], g->r[1], g->r[2]};
+  if (max_smem_needed(h.dims) > 227 * 1024) return false;
+  h.maxT = max_T;
+  h.maxB = max_B;
+  h.idx_bits = bits_for((uint64_t)h.kg.rows - 1);
+  h.i3_bits = bits_for((uint64_t)h.kg.m3 - 1);
+  layout(h, nullptr);
+  return true;
+}
+
+int cuda_status(cudaError_t e) { return e == cudaSuccess ? TTB_OK : TTB_ECUDA; }
+
+}  // namespace
+
+extern "C" {
+
+int ttb_abi_version(void) { return TTB_ABI_VERSION; }
+
+const char* ttb_strerror(int code) {
+  switch (code) {
+    case TTB_OK: return "ok";
+    case TTB_EINVAL: return "invalid argument or geometry";
+    case TTB_ERANGE: return "index outside [0, rows)";
+    case TTB_EEMPTY: return "empty batch or empty bag";
+    case TTB_EOFFSETS: return "malformed bag offsets";
+    case TTB_ENONFINITE: return "non-finite gradient";
+    case TTB_ECUDA: return "CUDA error";
+    case TTB_ESTATE: return "call order violated";
+    default: return "unknown error";
+  }
+}
+
+int64_t ttb_launch_count(void) { return (int64_t)__atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
+int ttb_workspace_bytes(const ttb_geom* g, int64_t max_T, int64_t max_B, size_t* bytes) {
+  if (!bytes) return TTB_EINVAL;
+  ttb_handle h;
+  if (!init_handle(h, g, max_T, max_B)) return TTB_EINVAL;
+  *bytes = h.bytes;
+  return TTB_OK;
+}
+
+ttb_handle* ttb_create(const ttb_geom* g, int64_t max_T, int64_t max_B, void* workspace, size_t bytes,
+                       ttb_stream stream) {
+  ttb_handle tmp;
+  if (!init_handle(tmp, g, max_T, max_B) || !workspace || bytes < tmp.bytes) return nullptr;
+  ttb_handle* h = (ttb_handle*)malloc(sizeof(ttb_handle));
+  if (!h) return nullptr;
+  *h = tmp;
+  // align the base to 256 bytes inside the caller's buffer
+  char* base = (char*)(((uintptr_t)workspace + 255) & ~(uintptr_t)255);
+  layout(*h, base);
+  h->base = base;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(h->w.err, 0, sizeof(int) * 16, s) != cudaSuccess ||
+      cudaMemsetAsync(h->w.pmap, 0xFF, sizeof(unsigned) * h->kg.m1m2, s) != cudaSuccess) {
+    free(h);
+    return nullptr;
+  }
+  return h;
+}
+
+void ttb_destroy(ttb_handle* h) { free(h); }
+
+int ttb_plan(ttb_handle* h, const void* indices, int idx_is_64, const int64_t* offsets, int64_t T, int64_t B,
+             ttb_stream stream) {
+  if (!h || !indices || !offsets) return TTB_EINVAL;
+  if (T < 1 || B < 1) return TTB_EEMPTY;
+  if (T > h->maxT || B > h->maxB) return TTB_EINVAL;
+  h->T = T;
+  h->B = B;
+  h->planned = 0;
+  h->forwarded = 0;
+  h->backwarded = 0;
+  cudaError_t e = launch_plan(h, indices, idx_is_64, offsets, (cudaStream_t)stream);
+  if (e != cudaSuccess) return TTB_ECUDA;
+  h->planned = 1;
+  ++h->gen;
+  return TTB_OK;
+}
+
+int ttb_forward(ttb_handle* h, const float* c0, const float* c1, const float* c2, float* out, ttb_stream stream) {
+  if (!h || !c0 || !c1 || !c2 || !out) return TTB_EINVAL;
+  if (!h->planned) return TTB_ESTATE;
+  cudaError_t e = launch_forward(h, c0, c1, c2, out, (cudaStream_t)stream);
+  if (e != cudaSuccess) return TTB_ECUDA;
+  h->forwarded = 1;
+  return TTB_OK;
+}
+
+int ttb_backward(ttb_handle* h, const float* c0, const float* c1, const float* c2, const float* grad_out, float* g0,
+                 float* g1, float* g2, ttb_stream stream) {
+  if (!h || !c0 || !c1 || !c2 || !grad_out || !g0 || !g1 || !g2) return TTB_EINVAL;
+  if (!h->forwarded) return TTB_ESTATE;
+  cudaError_t e = launch_backward(h, c0, c1, c2, grad_out, g0, g1, g2, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                  nullptr, 0.0, 0.0, 0, 0, (cudaStream_t)stream);
+  if (e != cudaSuccess) return TTB_ECUDA;
+  h->backwarded = 1;
+  return TTB_OK;
+}
+
+int ttb_aggregate(ttb_handle* h, const float* grad_out, ttb_stream stream) {
+  if (!h || !grad_out) return TTB_EINVAL;
+  if (!h->planned) return TTB_ESTATE;
+  cudaError_t e = launch_aggregate(h, grad_out, (cudaStream_t)stream);
+  if (e != cudaSuccess) return TTB_ECUDA;
+  h->backwarded = 1;
+  return TTB_OK;
+}
+
+int ttb_backward_sgd(ttb_handle* h, float* c0, float* c1, float* c2, const float* grad_out, double* v0, double* v1,
+                     double* v2, double lr, double momentum, int update_mask, ttb_stream stream) {
+  if (!h || !c0 || !c1 || !c2 || !grad_out) return TTB_EINVAL;
+  if (!(lr >= 0.0) || !(momentum >= 0.0 && momentum < 1.0)) return TTB_EINVAL;
+  if (momentum > 0.0 && (((update_mask & 1) && !v0) || ((update_mask & 2) && !v1) || ((update_mask & 4) && !v2)))
+    return TTB_EINVAL;
+  if (!h->forwarded) return TTB_ESTATE;
+  if (momentum == 0.0) v0 = v1 = v2 = nullptr;
+  cudaError_t e = launch_backward(h, c0, c1, c2, grad_out, nullptr, nullptr, nullptr, c0, c1, c2, v0, v1, v2, lr,
+                                  momentum, update_mask, 1, (cudaStream_t)stream);
+  if (e != cudaSuccess) return TTB_ECUDA;
+  h->backwarded = 1;
+  return TTB_OK;
+}
+
+int ttb_sgd_update(float* param, const float* grad, double* velocity, int64_t n, double lr, double momentum,
+                   ttb_stream stream) {
+  if (!param || !grad || n < 0) return TTB_EINVAL;
+  if (!(lr >= 0.0) || !(momentum >= 0.0 && momentum < 1.0)) return TTB_EINVAL;
+  if (momentum > 0.0 && !velocity) return TTB_EINVAL;
+  if (momentum == 0.0) velocity = nullptr;
+  return cuda_status(launch_sgd(param, grad, velocity, n, lr, momentum, (cudaStream_t)stream));
+}
+
+int ttb_read_status(ttb_handle* h, int64_t status[8], ttb_stream stream) {
+  if (!h || !status) return TTB_EINVAL;
+  int hdr[16];
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemcpyAsync(hdr, h->w.err, sizeof(hdr), cudaMemcpyDeviceToHost, s) != cudaSuccess) return TTB_ECUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return TTB_ECUDA;
+  status[0] = hdr[0];
+  status[1] = h->T;
+  status[2] = h->B;
+  status[3] = hdr[1];
+  status[4] = hdr[2];
+  status[5] = h->backwarded ? hdr[3] : 0;
+  status[6] = h->gen;
+  status[7] = 0;
+  return TTB_OK;
+}
+
+int ttb_export_plan(ttb_handle* h, int64_t* work, int64_t* slot_occ, int64_t* seg_ids, int64_t* seg_inv,
+                    int64_t* digits, ttb_stream stream) {
+  if (!h) return TTB_EINVAL;
+  if (!h->planned) return TTB_ESTATE;
+  return cuda_status(launch_export_plan(h, work, slot_occ, seg_ids, seg_inv, digits, (cudaStream_t)stream));
+}
+
+int ttb_export_unique(ttb_handle* h, int64_t* rows, float* grads, ttb_stream stream) {
+  if (!h) return TTB_EINVAL;
+  if (!h->backwarded) return TTB_ESTATE;
+  return cuda_status(launch_export_unique(h, rows, grads, (cudaStream_t)stream));
+}
+
+int ttb_export_slots(ttb_handle* h, float* slots, ttb_stream stream) {
+  if (!h || !slots) return TTB_EINVAL;
+  if (!h->forwarded) return TTB_ESTATE;
+  int64_t st[8];
+  int rc = ttb_read_status(h, st, stream);
+  if (rc) return rc;
+  const size_t n = (size_t)st[3] * h->dims.n1 * h->dims.n2 * h->dims.r2;
+  return cuda_status(
+      cudaMemcpyAsync(slots, h->w.slots, n * sizeof(float), cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+}
+
+}  // extern "C"

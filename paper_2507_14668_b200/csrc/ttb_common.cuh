@@ -1,0 +1,180 @@
+// Shared device helpers for the TT-EmbeddingBag kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ttb {
+
+constexpr unsigned kEmpty = 0xFFFFFFFFu;
+constexpr int kBlock = 256;  // threads per CTA for the streaming kernels
+constexpr int kItems = 8;    // items per thread for the scan / sort tiles
+constexpr int kTile = kBlock * kItems;
+
+// Geometry as the kernels see it (d = 3; d = 2 tables arrive embedded).
+struct KGeom {
+  unsigned m1, m2, m3;  // row factors
+  unsigned m1m2;        // number of prefix keys
+  unsigned rows;        // padded rows m1 m2 m3 (< 2^31)
+};
+
+// Core dims. DynDims carries them at run time; FixDims bakes them into the
+// instantiation so the contraction loops fully unroll.
+struct DynDims {
+  int n1, n2, n3, r1, r2;
+};
+template <int N1, int N2, int N3, int R1, int R2>
+struct FixDims {
+  static constexpr int n1 = N1, n2 = N2, n3 = N3, r1 = R1, r2 = R2;
+};
+template <class D>
+__host__ __device__ inline D make_dims(const DynDims& d);
+template <>
+__host__ __device__ inline DynDims make_dims<DynDims>(const DynDims& d) {
+  return d;
+}
+template <class D>
+__host__ __device__ inline D make_dims(const DynDims&) {
+  return D{};
+}
+
+// Derived extents (floats).
+template <class D> __host__ __device__ inline int dN(const D& d) { return d.n1 * d.n2 * d.n3; }
+template <class D> __host__ __device__ inline int dX(const D& d) { return d.n1 * d.n2; }          // slot rows
+template <class D> __host__ __device__ inline int dSlot(const D& d) { return d.n1 * d.n2 * d.r2; }  // slot size
+template <class D> __host__ __device__ inline int dC(const D& d) { return d.n2 * d.r2; }          // G2 slice cols
+template <class D> __host__ __device__ inline int dG1s(const D& d) { return d.n1 * d.r1; }
+template <class D> __host__ __device__ inline int dG2s(const D& d) { return d.r1 * d.n2 * d.r2; }
+template <class D> __host__ __device__ inline int dG3s(const D& d) { return d.r2 * d.n3; }
+
+// ---------------------------------------------------------------- lookback
+// Decoupled look-back for single-pass scans. Status word: bits 62-63 flag
+// (1 = tile aggregate, 2 = inclusive prefix), bits 0-61 value.
+constexpr unsigned long long kFlagAgg = 1ull << 62;
+constexpr unsigned long long kFlagInc = 2ull << 62;
+constexpr unsigned long long kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Called by ONE thread of the tile. Returns the exclusive prefix of `agg`
+// over all earlier tiles and publishes this tile's inclusive prefix.
+__device__ inline long long lookback_exclusive(unsigned long long* status, int tile, long long agg) {
+  if (tile == 0) {
+    st_release_u64(&status[0], kFlagInc | (unsigned long long)agg);
+    return 0;
+  }
+  st_release_u64(&status[tile], kFlagAgg | (unsigned long long)agg);
+  long long excl = 0;
+  int j = tile - 1;
+  while (true) {
+    unsigned long long s = ld_acquire_u64(&status[j]);
+    unsigned long long f = s & ~kValMask;
+    if (f == 0) continue;
+    excl += (long long)(s & kValMask);
+    if (f == kFlagInc) break;
+    --j;
+  }
+  st_release_u64(&status[tile], kFlagInc | (unsigned long long)(excl + agg));
+  return excl;
+}
+
+// Dynamic tile id (blocks are numbered in start order, so look-back never
+// waits on a block that has not started).
+__device__ __forceinline__ int claim_tile(unsigned* counter, int* s_tile) {
+  if (threadIdx.x == 0) *s_tile = (int)atomicAdd(counter, 1u);
+  __syncthreads();
+  return *s_tile;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Exclusive scan of 0/1 flags over a striped tile: element (k, tid) sits at
+// position base + k * kBlock + tid. Writes the global exclusive rank of each
+// element and returns the global total up to and including this tile via
+// *incl_out (valid in all threads). s_tmp: kItems * (kBlock / 32) + 2 ints.
+__device__ inline void tile_flag_scan(const bool (&f)[kItems], int (&rank)[kItems],
+                                      unsigned long long* status, int tile, int* s_tmp,
+                                      long long* incl_out) {
+  constexpr int NW = kBlock / 32;
+  constexpr int NV = kItems * NW;  // 64 values, in (k, warp) order
+  static_assert(NV % 32 == 0, "scan layout");
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = lanemask_lt();
+  int within[kItems];
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    unsigned m = __ballot_sync(0xffffffffu, f[k]);
+    within[k] = __popc(m & lt);
+    if (lane == 0) s_tmp[k * NW + w] = __popc(m);
+  }
+  __syncthreads();
+  if (w == 0) {
+    constexpr int PER = NV / 32;
+    int v[PER];
+    int sum = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      v[i] = s_tmp[lane * PER + i];
+      sum += v[i];
+    }
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int run = incl - sum;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      s_tmp[lane * PER + i] = run;
+      run += v[i];
+    }
+    int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (lane == 0) {
+      long long ex = lookback_exclusive(status, tile, total);
+      s_tmp[NV] = (int)ex;
+      s_tmp[NV + 1] = (int)(ex + total);
+    }
+  }
+  __syncthreads();
+  const int g = s_tmp[NV];
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) rank[k] = g + s_tmp[k * NW + w] + within[k];
+  *incl_out = s_tmp[NV + 1];
+}
+
+// fp64 SGD(+momentum) step matching numpy's rounding in the reference:
+//   vel *= mu; vel += g; core = f32(f64(core) - lr * vel)       (backward.py:195-197)
+//   core = f32(f64(core) - lr * g)                              (backward.py:200)
+// __dmul_rn / __dsub_rn keep nvcc from contracting into an FMA.
+__device__ __forceinline__ float sgd_apply(float p, float g, double* vel, double lr, double mu) {
+  double step;
+  if (vel != nullptr) {
+    double v = __dadd_rn(__dmul_rn(*vel, mu), (double)g);
+    *vel = v;
+    step = __dmul_rn(lr, v);
+  } else {
+    step = __dmul_rn(lr, (double)g);
+  }
+  return (float)__dsub_rn((double)p, step);
+}
+
+}  // namespace ttb

@@ -1,0 +1,127 @@
+// Host-side handle and workspace layout shared by the launchers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/ttb.h"
+#include "ttb_common.cuh"
+
+namespace ttb {
+
+// Prefixes handled per CTA in the i2-grouped prefix kernels.
+constexpr int kPrefixChunk = 32;
+
+struct Workspace {
+  // error word + device counters: [0] err bits, [1] P, [2] S, [3] U
+  int* err;
+  int* counts;
+  // prefix table over the m1*m2 prefix keys (first position, then slot)
+  unsigned* pmap;
+  int* pslot;
+  unsigned* work_key;  // P: prefix key of each slot, first-occurrence order
+  // per index (T)
+  unsigned* keys32;    // row index as u32
+  int* bag_of;
+  int* occ_slot;
+  int* seg_inv;
+  int* occ_tmp;
+  // segments
+  int* seg_slot;  // S
+  int* seg_bag;   // S
+  int* bag_seg;   // B + 1
+  int* bag_off;   // B + 1 (copied, clamped offsets)
+  // reuse buffer
+  float* slots;   // Pmax x slot
+  // radix sort (T items)
+  unsigned *skA, *svA, *skB, *svB;
+  unsigned* sort_hist;    // 4 passes x 256
+  unsigned* sort_status;  // 4 passes x tiles x 256
+  unsigned* sort_ctr;     // 8 counters
+  // rows (U <= T), sorted by row index
+  unsigned* urow;
+  int* urow_start;  // U + 1
+  unsigned* urow_i3;
+  int* prow_begin;  // by slot
+  int* prow_end;
+  float* gU;        // U x N aggregated row gradients
+  float* dH;        // U x (r2 n3) per-row G3 gradient blocks
+  float* E;         // Pmax x (n1 r1) per-prefix G1 gradient blocks
+  float* dG2part;   // m2 x cmax x G2 slice
+  int* i3_start;    // m3 + 1
+  int* grp_cnt;     // m2: present prefixes per i2
+  unsigned *rkA, *rvA, *rkB, *rvB;  // rows-by-i3 sort buffers
+  int* uid_first;   // T: first-occurrence rank flags / scratch
+  // look-back scan state, one region per scan kernel
+  unsigned long long* scan_status;  // kNumScans x scan_tiles
+  unsigned* scan_ctr;               // kNumScans counters
+  float* scratch1;                  // 1-float sink for the unit core of d = 2 tables
+};
+
+enum ScanId { kScanSlots = 0, kScanSegs = 1, kScanRuns = 2, kScanFirst = 3, kNumScans = 4 };
+
+}  // namespace ttb
+
+namespace ttb {
+// Optional per-kernel CUDA-event timing (ttb_profile_*): each launch site
+// records an event pair on its stream; ttb_profile_read accumulates them.
+constexpr int kMaxProfEvents = 256;
+constexpr int kMaxProfNames = 48;
+struct Profiler {
+  int on;
+  int n;  // pending event pairs
+  cudaEvent_t ev[kMaxProfEvents][2];
+  const char* pend_name[kMaxProfEvents];
+  const char* names[kMaxProfNames];
+  double ms[kMaxProfNames];
+  long long calls[kMaxProfNames];
+  int nnames;
+};
+}  // namespace ttb
+
+struct ttb_handle {
+  ttb_geom geom;
+  ttb::KGeom kg;
+  ttb::DynDims dims;
+  int64_t maxT, maxB, Pmax, cmax, scan_tiles, sort_tiles;
+  int idx_bits, i3_bits;
+  char* base;
+  size_t bytes;
+  ttb::Workspace w;
+  // host-side state of the current plan
+  int64_t T, B;
+  int planned, forwarded, backwarded;
+  int64_t gen;
+  ttb::Profiler prof;
+};
+
+namespace ttb {
+extern long long g_launches;
+inline void count_launch(int n = 1) { __atomic_add_fetch(&g_launches, n, __ATOMIC_RELAXED); }
+
+// RAII timing scope around one (or a few) launches; free when profiling is off.
+struct ProfScope {
+  Profiler* p;
+  cudaStream_t s;
+  int slot;
+  ProfScope(ttb_handle* h, cudaStream_t st, const char* name);
+  ~ProfScope();
+};
+
+// launchers (return cudaError_t of the last launch)
+cudaError_t launch_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* offsets, cudaStream_t s);
+cudaError_t launch_forward(ttb_handle* h, const float* c0, const float* c1, const float* c2, float* out,
+                           cudaStream_t s);
+cudaError_t launch_aggregate(ttb_handle* h, const float* gout, cudaStream_t s);
+// mode 0: write grads into g0..g2; mode 1: SGD update in place
+cudaError_t launch_backward(ttb_handle* h, const float* c0, const float* c1, const float* c2,
+                            const float* gout, float* g0, float* g1, float* g2, float* p0, float* p1,
+                            float* p2, double* v0, double* v1, double* v2, double lr, double mu,
+                            int update_mask, int mode, cudaStream_t s);
+cudaError_t launch_sort(ttb_handle* h, const unsigned* keys_in, const unsigned* vals_in, unsigned* kA,
+                        unsigned* vA, unsigned* kB, unsigned* vB, const int* d_count, int max_n,
+                        int bits, int region, unsigned** keys_out, unsigned** vals_out, cudaStream_t s);
+cudaError_t launch_sgd(float* p, const float* g, double* v, int64_t n, double lr, double mu, cudaStream_t s);
+cudaError_t launch_export_plan(ttb_handle* h, int64_t* work, int64_t* slot_occ, int64_t* seg_ids,
+                               int64_t* seg_inv, int64_t* digits, cudaStream_t s);
+cudaError_t launch_export_unique(ttb_handle* h, int64_t* rows, float* grads, cudaStream_t s);
+}  // namespace ttb

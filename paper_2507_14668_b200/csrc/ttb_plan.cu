@@ -1,0 +1,304 @@
+// K1: per-batch plan — digits, first-occurrence prefix slots, (bag, slot)
+// segments. Reference: lookup.py:88-124 (prepare_reuse_plan, _check_bag),
+// lookup.py:254-260 and 280-284 (bag ids, np.unique of bag*P + slot).
+//
+// First-occurrence order without a sort: every index does an atomicMin of
+// its position into a dense table over the m1*m2 prefix keys; the index that
+// wins is the first occurrence, and an exclusive scan of the "I won" flags in
+// index order numbers the slots exactly as the reference's sequential
+// dictionary walk does (lookup.py:115-119).
+#include "ttb_internal.h"
+
+namespace ttb {
+
+// ---------------------------------------------------------------- P1: mark
+template <typename IdxT>
+__global__ void __launch_bounds__(kBlock) k_plan_mark(const IdxT* __restrict__ idx,
+                                                      const int64_t* __restrict__ offsets, int T, int B,
+                                                      KGeom g, unsigned* __restrict__ pmap,
+                                                      unsigned* __restrict__ keys32, int* __restrict__ bag_of,
+                                                      int* __restrict__ bag_off, int* __restrict__ err) {
+  const int stride = gridDim.x * blockDim.x;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  int bits = 0;
+  for (int b = tid; b <= B; b += stride) {
+    const int64_t ob = offsets[b];
+    bag_off[b] = (int)(ob < 0 ? 0 : (ob > T ? T : ob));
+    if (b == 0 && ob != 0) bits |= 4;
+    if (b == B && ob != (int64_t)T) bits |= 4;
+    if (b < B) {
+      const int64_t on = offsets[b + 1];
+      if (on == ob) bits |= 2;
+      else if (on < ob) bits |= 4;
+    }
+  }
+  for (int t = tid; t < T; t += stride) {
+    long long v = (long long)idx[t];
+    if (v < 0 || v >= (long long)g.rows) {
+      bits |= 1;
+      v = 0;
+    }
+    const unsigned i = (unsigned)v;
+    keys32[t] = i;
+    atomicMin(&pmap[i / g.m3], (unsigned)t);
+    // bag id: last b with offsets[b] <= t
+    int lo = 0, hi = B - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (offsets[mid] <= (int64_t)t) lo = mid;
+      else hi = mid - 1;
+    }
+    bag_of[t] = lo;
+  }
+  if (bits) atomicOr(err, bits);
+}
+
+// ---------------------------------------------------------------- P2: slots
+__global__ void __launch_bounds__(kBlock) k_plan_slots(const unsigned* __restrict__ keys32, int T, KGeom g,
+                                                       const unsigned* __restrict__ pmap, int* __restrict__ pslot,
+                                                       unsigned* __restrict__ work_key, int* __restrict__ counts,
+                                                       unsigned long long* status, unsigned* ctr) {
+  __shared__ int s_tile;
+  __shared__ int s_tmp[kItems * (kBlock / 32) + 2];
+  const int tile = claim_tile(ctr, &s_tile);
+  const int base = tile * kTile;
+  bool f[kItems];
+  unsigned key[kItems];
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    const int t = base + k * kBlock + threadIdx.x;
+    f[k] = false;
+    key[k] = 0;
+    if (t < T) {
+      key[k] = keys32[t] / g.m3;
+      f[k] = (pmap[key[k]] == (unsigned)t);
+    }
+  }
+  int rank[kItems];
+  long long incl;
+  tile_flag_scan(f, rank, status, tile, s_tmp, &incl);
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    if (f[k]) {
+      work_key[rank[k]] = key[k];
+      pslot[key[k]] = rank[k];
+    }
+  }
+  if (tile == (int)((T + kTile - 1) / kTile) - 1 && threadIdx.x == 0) counts[1] = (int)incl;
+}
+
+// ---------------------------------------------------------------- P3: segments
+// One warp per bag; a tile is 8 warps x kBagsPerWarp bags. The distinct
+// slots of a bag, in ascending order, are its segments (np.unique sorts the
+// keys bag * P + slot). The bag's segment base comes from a look-back scan
+// of the per-bag distinct counts.
+constexpr int kBagsPerWarp = 4;
+constexpr int kBagsPerTile = (kBlock / 32) * kBagsPerWarp;
+
+__global__ void __launch_bounds__(kBlock) k_plan_segs(const unsigned* __restrict__ keys32,
+                                                      const int64_t* __restrict__ offsets, int T, int B, KGeom g,
+                                                      const int* __restrict__ pslot, int* __restrict__ occ_slot,
+                                                      int* __restrict__ occ_tmp, int* __restrict__ seg_inv,
+                                                      int* __restrict__ seg_slot, int* __restrict__ seg_bag,
+                                                      int* __restrict__ bag_seg, int* __restrict__ counts,
+                                                      unsigned long long* status, unsigned* ctr) {
+  __shared__ int s_tile;
+  __shared__ int s_cnt[kBagsPerTile];
+  __shared__ int s_base;
+  const int tile = claim_tile(ctr, &s_tile);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = lanemask_lt();
+
+  int my_slot[kBagsPerWarp], my_rank[kBagsPerWarp], o0s[kBagsPerWarp], lens[kBagsPerWarp];
+  bool my_first[kBagsPerWarp];
+#pragma unroll
+  for (int k = 0; k < kBagsPerWarp; ++k) {
+    const int b = tile * kBagsPerTile + w * kBagsPerWarp + k;
+    int cnt = 0;
+    my_slot[k] = 0x7fffffff;
+    my_rank[k] = 0;
+    my_first[k] = false;
+    o0s[k] = 0;
+    lens[k] = 0;
+    if (b < B) {
+      long long o0 = offsets[b], o1 = offsets[b + 1];
+      o0 = o0 < 0 ? 0 : (o0 > T ? T : o0);
+      o1 = o1 < o0 ? o0 : (o1 > T ? T : o1);
+      const int L = (int)(o1 - o0);
+      o0s[k] = (int)o0;
+      lens[k] = L;
+      if (L <= 32) {
+        const bool act = lane < L;
+        int s = 0x7fffffff;
+        if (act) {
+          s = pslot[keys32[o0 + lane] / g.m3];
+          occ_slot[o0 + lane] = s;
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, s);
+        const bool first = act && ((peers & lt) == 0);
+        int r = 0;
+        for (int i = 0; i < 32; ++i) {
+          const int si = __shfl_sync(0xffffffffu, s, i);
+          const bool fi = __shfl_sync(0xffffffffu, first, i);
+          r += (fi && si < s) ? 1 : 0;
+        }
+        cnt = __popc(__ballot_sync(0xffffffffu, first));
+        my_slot[k] = s;
+        my_rank[k] = r;
+        my_first[k] = first;
+      } else {
+        // long bag: O(L^2 / 32) per warp, through global scratch
+        for (int t = (int)o0 + lane; t < (int)o1; t += 32) occ_slot[t] = pslot[keys32[t] / g.m3];
+        __syncwarp();
+        for (int t = (int)o0 + lane; t < (int)o1; t += 32) {
+          const int s = occ_slot[t];
+          int first = 1;
+          for (int u = (int)o0; u < t; ++u)
+            if (occ_slot[u] == s) {
+              first = 0;
+              break;
+            }
+          occ_tmp[t] = first;
+        }
+        __syncwarp();
+        int c = 0;
+        for (int t = (int)o0 + lane; t < (int)o1; t += 32) {
+          const int s = occ_slot[t];
+          int r = 0;
+          for (int u = (int)o0; u < (int)o1; ++u) r += (occ_tmp[u] && occ_slot[u] < s) ? 1 : 0;
+          seg_inv[t] = r;  // local rank for now
+          c += occ_tmp[t];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        cnt = c;
+      }
+    }
+    if (lane == 0) s_cnt[w * kBagsPerWarp + k] = cnt;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int v = s_cnt[lane];
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    s_cnt[lane] = incl - v;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (lane == 0) s_base = (int)lookback_exclusive(status, tile, total);
+    const int ntiles = (B + kBagsPerTile - 1) / kBagsPerTile;
+    if (lane == 0 && tile == ntiles - 1) {
+      const int S = s_base + total;
+      bag_seg[B] = S;
+      counts[2] = S;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kBagsPerWarp; ++k) {
+    const int b = tile * kBagsPerTile + w * kBagsPerWarp + k;
+    if (b >= B) continue;
+    const int base = s_base + s_cnt[w * kBagsPerWarp + k];
+    if (lane == 0) bag_seg[b] = base;
+    const int o0 = o0s[k], L = lens[k];
+    if (L <= 32) {
+      if (lane < L) {
+        const int sg = base + my_rank[k];
+        seg_inv[o0 + lane] = sg;
+        if (my_first[k]) {
+          seg_slot[sg] = my_slot[k];
+          seg_bag[sg] = b;
+        }
+      }
+    } else {
+      for (int t = o0 + lane; t < o0 + L; t += 32) {
+        const int sg = base + seg_inv[t];
+        seg_inv[t] = sg;
+        if (occ_tmp[t]) {
+          seg_slot[sg] = occ_slot[t];
+          seg_bag[sg] = b;
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- launcher
+cudaError_t launch_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* offsets, cudaStream_t s) {
+  Workspace& w = h->w;
+  const int T = (int)h->T, B = (int)h->B;
+  cudaError_t e;
+  // fresh prefix table, error word/counters and look-back state
+  if ((e = cudaMemsetAsync(w.pmap, 0xFF, sizeof(unsigned) * h->kg.m1m2, s))) return e;
+  if ((e = cudaMemsetAsync(w.err, 0, sizeof(int) * 8, s))) return e;
+  if ((e = cudaMemsetAsync(w.scan_status, 0, sizeof(unsigned long long) * h->scan_tiles * kNumScans, s))) return e;
+  if ((e = cudaMemsetAsync(w.scan_ctr, 0, sizeof(unsigned) * 16, s))) return e;
+
+  const int work = T > B + 1 ? T : B + 1;
+  int grid = (work + kBlock - 1) / kBlock;
+  if (grid > 148 * 16) grid = 148 * 16;
+  {
+  ProfScope _ps(h, s, "plan_mark");
+  if (idx64)
+    k_plan_mark<long long><<<grid, kBlock, 0, s>>>((const long long*)idx, offsets, T, B, h->kg, w.pmap, w.keys32,
+                                                   w.bag_of, w.bag_off, w.err);
+  else
+    k_plan_mark<int><<<grid, kBlock, 0, s>>>((const int*)idx, offsets, T, B, h->kg, w.pmap, w.keys32, w.bag_of,
+                                             w.bag_off, w.err);
+  }
+  count_launch();
+  const int tiles = (T + kTile - 1) / kTile;
+  { ProfScope _ps(h, s, "plan_slots");
+  k_plan_slots<<<tiles, kBlock, 0, s>>>(w.keys32, T, h->kg, w.pmap, w.pslot, w.work_key, w.counts,
+                                        w.scan_status + kScanSlots * h->scan_tiles, w.scan_ctr + kScanSlots);
+  }
+  count_launch();
+  const int btiles = (B + kBagsPerTile - 1) / kBagsPerTile;
+  { ProfScope _ps(h, s, "plan_segs");
+  k_plan_segs<<<btiles, kBlock, 0, s>>>(w.keys32, offsets, T, B, h->kg, w.pslot, w.occ_slot, w.occ_tmp, w.seg_inv,
+                                        w.seg_slot, w.seg_bag, w.bag_seg, w.counts,
+                                        w.scan_status + kScanSegs * h->scan_tiles, w.scan_ctr + kScanSegs);
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- export
+__global__ void k_export_plan(const Workspace w, KGeom g, int T, int64_t* work, int64_t* slot_occ, int64_t* seg_ids,
+                              int64_t* seg_invo, int64_t* digits) {
+  const int P = w.counts[1], S = w.counts[2];
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < T; i += stride) {
+    if (work && i < P) {
+      const unsigned key = w.work_key[i];
+      work[4 * i + 0] = key;
+      work[4 * i + 1] = key / g.m2;
+      work[4 * i + 2] = key % g.m2;
+      work[4 * i + 3] = i;
+    }
+    if (slot_occ) slot_occ[i] = w.occ_slot[i];
+    if (seg_invo) seg_invo[i] = w.seg_inv[i];
+    if (seg_ids && i < S) seg_ids[i] = (int64_t)w.seg_bag[i] * P + w.seg_slot[i];
+    if (digits) {
+      const unsigned r = w.keys32[i];
+      const unsigned key = r / g.m3;
+      digits[3 * i + 0] = key / g.m2;
+      digits[3 * i + 1] = key % g.m2;
+      digits[3 * i + 2] = r % g.m3;
+    }
+  }
+}
+
+cudaError_t launch_export_plan(ttb_handle* h, int64_t* work, int64_t* slot_occ, int64_t* seg_ids, int64_t* seg_inv,
+                               int64_t* digits, cudaStream_t s) {
+  const int T = (int)h->T;
+  int grid = (T + kBlock - 1) / kBlock;
+  if (grid > 148 * 8) grid = 148 * 8;
+  k_export_plan<<<grid, kBlock, 0, s>>>(h->w, h->kg, T, work, slot_occ, seg_ids, seg_inv, digits);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace ttb

@@ -1,0 +1,276 @@
+"""CUDA path vs the oracle and the reference's golden vectors (B200).
+
+Bars (BASELINE.json north_star): plan / digits / segments / unique rows
+bit-exact; forward within 1e-5 scale-relative (the reference's own metric,
+test_lookup.py:176-177); core gradients within 1e-4 scale-relative per core.
+Ground truth: the oracle evaluated in fp64 on the fp32 cores."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import ttb_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+FWD_TOL = 1e-5
+GRAD_TOL = 1e-4
+
+
+def rel_err(got, want, floor=1e-3):
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    return float(np.abs(got - want).max() / max(floor, float(np.abs(want).max())))
+
+
+def golden_geom(s, p):
+    return O.Geometry(tuple(int(v) for v in s[f"{p}.m"]), tuple(int(v) for v in s[f"{p}.n"]),
+                      tuple(int(v) for v in s[f"{p}.r"]))
+
+
+def make_engine(g, T, B):
+    from paper_2507_14668_b200.engine import TtEngine
+    from paper_2507_14668_b200.geometry import TtShape
+    return TtEngine(TtShape(g.m, g.n, g.r), max(T, 16), max(B, 16), "cuda")
+
+
+def to_dev(cores32):
+    return [torch.from_numpy(np.ascontiguousarray(c, dtype=np.float32)).cuda() for c in cores32]
+
+
+def run_case(g, cores32, idx, off, gout=None):
+    eng = make_engine(g, idx.size, off.size - 1)
+    dc = to_dev(cores32)
+    eng.plan(torch.from_numpy(idx).cuda(), torch.from_numpy(off).cuda())
+    out = eng.forward(dc).cpu().numpy()
+    res = dict(out=out, eng=eng, dc=dc)
+    if gout is not None:
+        grads = eng.backward(dc, torch.from_numpy(gout.astype(np.float32)).cuda())
+        res["grads"] = [x.cpu().numpy() for x in grads]
+    return res
+
+
+# ------------------------------------------------------------------ golden
+def test_plan_bit_exact_golden(golden):
+    s = golden("forward")
+    ncheck = 0
+    for c in range(int(s["ncases"])):
+        p = f"case{c}"
+        g = golden_geom(s, p)
+        if g.d != 3:
+            continue
+        cores32 = [s[f"{p}.core{k}"].astype(np.float32) for k in range(3)]
+        r = run_case(g, cores32, s[f"{p}.idx"], s[f"{p}.off"])
+        ex = r["eng"].export_plan()
+        assert np.array_equal(ex["work"], s[f"{p}.work"]), p
+        assert np.array_equal(ex["slot_occ"], s[f"{p}.slot_occ"]), p
+        assert np.array_equal(ex["seg_ids"], s[f"{p}.seg_ids"]), p
+        assert np.array_equal(ex["seg_inv"], s[f"{p}.seg_inv"]), p
+        digits = np.stack(O.digits_of(s[f"{p}.idx"], g.m), axis=1)
+        assert np.array_equal(ex["digits"], digits)
+        ncheck += 1
+    assert ncheck >= 10
+
+
+def test_plan_frozen_known_answers(golden):
+    s = golden("forward")
+    g = O.Geometry((2, 2, 2), (2, 2, 2), (1, 2, 2, 1))
+    cores32 = [s[f"cube.core{k}"].astype(np.float32) for k in range(3)]
+    for j in range(4):
+        idx = s[f"frozen{j}.idx"].astype(np.int64)
+        off = np.array([0, idx.size], dtype=np.int64)
+        r = run_case(g, cores32, idx, off)
+        ex = r["eng"].export_plan()
+        assert np.array_equal(ex["work"], s[f"frozen{j}.work"])
+        hits, misses = s[f"frozen{j}.hits_misses"]
+        assert ex["P"] == misses and ex["T"] - ex["P"] == hits
+
+
+def test_forward_golden(golden):
+    s = golden("forward")
+    for c in range(int(s["ncases"])):
+        p = f"case{c}"
+        g = golden_geom(s, p)
+        cores32 = [s[f"{p}.core{k}"].astype(np.float32) for k in range(g.d)]
+        r = run_case(g, cores32, s[f"{p}.idx"], s[f"{p}.off"])
+        want = O.forward([x.astype(np.float64) for x in cores32], g, s[f"{p}.idx"], s[f"{p}.off"])
+        assert rel_err(r["out"], want) < FWD_TOL, p
+        if s[f"{p}.core0"].dtype == np.float32:  # the reference's own fp32 output
+            assert rel_err(r["out"], s[f"{p}.out"]) < FWD_TOL, p
+
+
+def test_backward_golden(golden):
+    s = golden("backward")
+    for c in range(int(s["ncases"])):
+        p = f"case{c}"
+        g = golden_geom(s, p)
+        cores32 = [s[f"{p}.core{k}"].astype(np.float32) for k in range(g.d)]
+        idx, off, gout = s[f"{p}.idx"], s[f"{p}.off"], s[f"{p}.gout"].astype(np.float32)
+        r = run_case(g, cores32, idx, off, gout)
+        per = np.repeat(gout.astype(np.float64), np.diff(off), axis=0)
+        ur, ug = O.unique_aggregate(idx, per)
+        want = O.core_grads([x.astype(np.float64) for x in cores32], g, ur, ug)
+        for k in range(g.d):
+            assert rel_err(r["grads"][k], want[k]) < GRAD_TOL, (p, k)
+        # unique rows: first-occurrence order, fp32 left-to-right sums, bit-exact
+        rows, grads = r["eng"].export_unique()
+        ur32, ug32 = O.unique_aggregate(idx, np.repeat(gout, np.diff(off), axis=0))
+        assert np.array_equal(rows.cpu().numpy(), ur32), p
+        assert np.array_equal(grads.cpu().numpy(), ug32), p
+
+
+# ------------------------------------------------------------------ random
+def random_batch(rng, rows, B, max_bag, skew=False):
+    sizes = rng.integers(1, max_bag + 1, size=B)
+    if skew:
+        p = 1.0 / np.arange(1, rows + 1) ** 1.05
+        idx = rng.choice(rows, size=int(sizes.sum()), p=p / p.sum())
+    else:
+        idx = rng.integers(0, rows, size=int(sizes.sum()))
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    return idx.astype(np.int64), off
+
+
+@pytest.mark.parametrize("m,n,r,B,max_bag,skew", [
+    ((10, 10, 10), (2, 2, 4), (1, 16, 16, 1), 300, 3, False),      # config-1 dims, small rows
+    ((20, 20, 25), (4, 4, 4), (1, 32, 32, 1), 500, 20, True),      # config-2/3 dims, Zipf, pooling 20
+    ((7, 11, 19), (4, 4, 4), (1, 32, 32, 1), 400, 5, False),       # Criteo-like small field
+    ((3, 5, 7), (2, 3, 2), (1, 5, 3, 1), 200, 4, False),           # run-time dims path
+    ((4, 6, 9), (1, 1, 7), (1, 3, 2, 1), 100, 40, True),           # n padded with 1s, long bags (> 32)
+    ((1, 30, 40), (1, 4, 4), (1, 1, 8, 1), 300, 6, True),          # d=2-shaped geometry
+])
+def test_random_parity(m, n, r, B, max_bag, skew):
+    rng = np.random.default_rng(hash((m, B)) % 2**32)
+    g = O.Geometry(m, n, r)
+    cores32 = [c.astype(np.float32) for c in O.init_cores(g, 3)]
+    idx, off = random_batch(rng, g.rows, B, max_bag, skew)
+    gout = rng.standard_normal((B, g.cols)).astype(np.float32)
+    res = run_case(g, cores32, idx, off, gout)
+    c64 = [c.astype(np.float64) for c in cores32]
+    out, plan = O.forward(c64, g, idx, off, want_plan=True)
+    assert rel_err(res["out"], out) < FWD_TOL
+    ex = res["eng"].export_plan()
+    assert np.array_equal(ex["work"], plan["work"])
+    assert np.array_equal(ex["slot_occ"], plan["slot_occ"])
+    assert np.array_equal(ex["seg_ids"], plan["seg_ids"])
+    assert np.array_equal(ex["seg_inv"], plan["seg_inv"])
+    ur, ug = O.unique_aggregate(idx, np.repeat(gout.astype(np.float64), np.diff(off), axis=0))
+    want = O.core_grads(c64, g, ur, ug)
+    for k in range(3):
+        assert rel_err(res["grads"][k], want[k]) < GRAD_TOL, k
+    assert res["eng"].status()["U"] == ur.size
+
+
+def test_d2_table_via_module():
+    from paper_2507_14668_b200.embedding_bag import TTEmbeddingBag
+    emb = TTEmbeddingBag(900, 12, (1, 6, 1), seed=4)
+    assert emb.shape.d == 2
+    rng = np.random.default_rng(5)
+    idx, off = random_batch(rng, 900, 64, 4)
+    out = emb(torch.from_numpy(idx).cuda(), torch.from_numpy(off[:-1]).cuda())
+    g = O.Geometry(emb.shape.m, emb.shape.n, emb.shape.ranks)
+    c64 = [c.detach().cpu().numpy().astype(np.float64) for c in emb.cores]
+    assert rel_err(out.detach().cpu().numpy(), O.forward(c64, g, idx, off)) < FWD_TOL
+    gout = torch.randn_like(out)
+    out.backward(gout)
+    ur, ug = O.unique_aggregate(idx, np.repeat(gout.cpu().numpy().astype(np.float64), np.diff(off), axis=0))
+    want = O.core_grads(c64, g, ur, ug)
+    for k in range(2):
+        assert rel_err(emb.cores[k].grad.cpu().numpy(), want[k]) < GRAD_TOL
+
+
+# ------------------------------------------------------------------ errors
+def test_errors_raise_value_error():
+    from paper_2507_14668_b200.embedding_bag import TTEmbeddingBag
+    emb = TTEmbeddingBag(1000, 16, (1, 4, 4, 1))
+    with pytest.raises(ValueError):
+        emb(torch.tensor([0, 1000], device="cuda"), torch.tensor([0, 1], device="cuda"))  # out of range
+    with pytest.raises(ValueError):
+        emb(torch.tensor([-1], device="cuda"), torch.tensor([0], device="cuda"))
+    with pytest.raises(ValueError):
+        emb(torch.tensor([1, 2], device="cuda"), torch.tensor([0, 0, 2], device="cuda"), )  # empty bag
+    with pytest.raises(ValueError):
+        emb(torch.tensor([], dtype=torch.int64, device="cuda"), torch.tensor([0], device="cuda"))
+    # still usable afterwards
+    out = emb(torch.tensor([3, 4, 999], device="cuda"), torch.tensor([0, 2], device="cuda"))
+    assert out.shape == (2, 16)
+
+
+# ------------------------------------------------------------------ update
+def test_sgd_update_bit_exact():
+    from paper_2507_14668_b200 import _native as nat
+    from paper_2507_14668_b200.engine import _ptr, _stream
+    lib = nat.load()
+    rng = np.random.default_rng(9)
+    p0 = rng.standard_normal(10_001).astype(np.float32)
+    g = rng.standard_normal(10_001).astype(np.float32)
+    for mu in (0.0, 0.9):
+        p = torch.from_numpy(p0.copy()).cuda()
+        gg = torch.from_numpy(g).cuda()
+        v = torch.zeros(p.numel(), dtype=torch.float64, device="cuda")
+        ref = p0.copy()
+        vel = None
+        for _ in range(3):
+            nat.check(lib.ttb_sgd_update(_ptr(p), _ptr(gg), _ptr(v) if mu else None, p.numel(), 0.05, mu, _stream()))
+            vel = O.sgd_step(ref, g.astype(np.float64), 0.05, mu, vel)
+        assert np.array_equal(p.cpu().numpy(), ref)
+
+
+def test_fused_sgd_module_matches_oracle():
+    from paper_2507_14668_b200.embedding_bag import TTEmbeddingBag
+    emb = TTEmbeddingBag(8000, 16, (1, 8, 8, 1), seed=2).enable_fused_sgd(0.05, 0.9)
+    g = O.Geometry(emb.shape.m, emb.shape.n, emb.shape.ranks)
+    ref = [c.detach().cpu().numpy().astype(np.float32).copy() for c in emb.cores]
+    vel = [None] * 3
+    rng = np.random.default_rng(11)
+    for step in range(3):
+        idx, off = random_batch(rng, 8000, 128, 3, skew=True)
+        out = emb(torch.from_numpy(idx).cuda(), torch.from_numpy(off[:-1]).cuda())
+        gout = torch.from_numpy(rng.standard_normal(out.shape).astype(np.float32)).cuda()
+        out.backward(gout)
+        c64 = [c.astype(np.float64) for c in ref]
+        ur, ug = O.unique_aggregate(idx, np.repeat(gout.cpu().numpy().astype(np.float64), np.diff(off), axis=0))
+        want = O.core_grads(c64, g, ur, ug)
+        for k in range(3):
+            vel[k] = O.sgd_step(ref[k], want[k], 0.05, 0.9, vel[k])
+    for k in range(3):
+        assert rel_err(emb.cores[k].detach().cpu().numpy(), ref[k]) < 1e-5, k
+
+
+# ------------------------------------------------------------------ full size
+def test_config2_full_size_properties():
+    """BASELINE config 2 (10M x 64, R=32, B=65536, pooling 1, uniform): plan
+    counts vs numpy, forward on a sample of bags vs the oracle's row
+    reconstruction, gradient determinism (two runs bitwise equal)."""
+    from paper_2507_14668_b200.embedding_bag import TTEmbeddingBag
+    emb = TTEmbeddingBag(10_000_000, 64, (1, 32, 32, 1), seed=0, max_indices=65536)
+    idx = np.random.default_rng(1).integers(0, 10_000_000, 65536)
+    off = np.arange(65537, dtype=np.int64)
+    gout = np.random.default_rng(2).standard_normal((65536, 64)).astype(np.float32)
+    ti, to = torch.from_numpy(idx).cuda(), torch.from_numpy(off).cuda()
+    eng = emb.engine
+    cores = [c.detach() for c in emb.cores]
+    eng.plan(ti, to)
+    out = eng.forward(cores)
+    st = eng.check_errors()
+    assert st["P"] == np.unique(idx // 250).size and st["S"] == 65536
+    g1 = [x.clone() for x in eng.backward(cores, torch.from_numpy(gout).cuda())]
+    assert eng.status()["U"] == np.unique(idx).size
+    g = O.Geometry(emb.shape.m, emb.shape.n, emb.shape.ranks)
+    c64 = [c.cpu().numpy().astype(np.float64) for c in cores]
+    sample = np.random.default_rng(3).choice(65536, 2000, replace=False)
+    want = O.reconstruct_rows(c64, g, idx[sample])
+    assert rel_err(out.cpu().numpy()[sample], want) < FWD_TOL
+    eng.plan(ti, to)
+    eng.forward(cores)
+    g2 = eng.backward(cores, torch.from_numpy(gout).cuda())
+    for a, b in zip(g1, g2):
+        assert torch.equal(a, b)
+    # gradients on a sub-batch against the oracle (fp64)
+    sub = 4096
+    eng.plan(ti[:sub], to[: sub + 1])
+    eng.forward(cores)
+    gs = eng.backward(cores, torch.from_numpy(gout[:sub]).cuda())
+    ur, ug = O.unique_aggregate(idx[:sub], gout[:sub].astype(np.float64))
+    want = O.core_grads(c64, g, ur, ug)
+    for k in range(3):
+        assert rel_err(gs[k].cpu().numpy(), want[k]) < GRAD_TOL
