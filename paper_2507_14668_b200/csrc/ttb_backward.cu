@@ -63,37 +63,40 @@ __global__ void __launch_bounds__(kBlock) k_runs(const unsigned* __restrict__ sk
 }
 
 // ---------------------------------------------------------------- reductions
-// dG2[:, i2] = sum over the CTA partials of group i2, in chunk order.
-__global__ void __launch_bounds__(kBlock) k_dg2_reduce(KGeom g, int C, int G2S, int cmax,
+// All three are deterministic: each output element is a sum in a fixed order
+// (warps own contiguous ranges of the summands; their partials are combined
+// in warp order), and the SGD(+momentum) step is applied by the thread that
+// produced the final gradient.
+constexpr int kRedWarps = kBlock / 32;
+
+// dG2[:, i2] = sum over the chunk partials of group i2, in chunk order.
+__global__ void __launch_bounds__(kBlock) k_dg2_reduce(KGeom g, int C, int G2S, int cmax, int ch,
                                                        const float* __restrict__ part, const int* __restrict__ grp_cnt,
                                                        const int* __restrict__ err, float* __restrict__ grad,
                                                        float* __restrict__ param, double* __restrict__ vel, double lr,
                                                        double mu, int do_update) {
   const unsigned i2 = blockIdx.x;
-  const int nch = (grp_cnt[i2] + kPrefixChunk - 1) / kPrefixChunk;
+  const int nch = (grp_cnt[i2] + ch - 1) / ch;
   const bool upd = do_update && ((*err & 8) == 0);
-  for (int e = threadIdx.x; e < G2S; e += kBlock) {
-    float acc = 0.f;
-    for (int c = 0; c < nch; ++c) acc += part[((size_t)i2 * cmax + c) * G2S + e];
-    const int r = e / C, cc = e - r * C;
-    const size_t gi = ((size_t)r * g.m2 + i2) * C + cc;
-    if (grad) grad[gi] = acc;
-    if (upd) param[gi] = sgd_apply(param[gi], acc, vel ? vel + gi : nullptr, lr, mu);
-  }
+  const int e = blockIdx.y * kBlock + threadIdx.x;
+  if (e >= G2S) return;
+  float acc = 0.f;
+  for (int c = 0; c < nch; ++c) acc += part[((size_t)i2 * cmax + c) * G2S + e];
+  const int r = e / C, cc = e - r * C;
+  const size_t gi = ((size_t)r * g.m2 + i2) * C + cc;
+  if (grad) grad[gi] = acc;
+  if (upd) param[gi] = sgd_apply(param[gi], acc, vel ? vel + gi : nullptr, lr, mu);
 }
 
-// i3_start[v] = first position of digit v among the i3-sorted rows
+// i3_start[v] = first position of digit v among the i3-sorted rows: every
+// boundary between consecutive sorted keys fills the digits it skips.
 __global__ void k_i3_bounds(const unsigned* __restrict__ k3, const int* __restrict__ counts, int m3,
                             int* __restrict__ i3_start) {
   const int U = counts[3];
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v <= m3; v += gridDim.x * blockDim.x) {
-    int lo = 0, hi = U;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (k3[mid] < (unsigned)v) lo = mid + 1;
-      else hi = mid;
-    }
-    i3_start[v] = lo;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q <= U; q += gridDim.x * blockDim.x) {
+    const int prev = q > 0 ? (int)k3[q - 1] : -1;
+    const int cur = q < U ? (int)k3[q] : m3;
+    for (int v = prev + 1; v <= cur; ++v) i3_start[v] = q;
   }
 }
 
@@ -103,13 +106,24 @@ __global__ void __launch_bounds__(kBlock) k_dg3_reduce(KGeom g, int N3, int G3S,
                                                        const int* __restrict__ err, float* __restrict__ grad,
                                                        float* __restrict__ param, double* __restrict__ vel, double lr,
                                                        double mu, int do_update) {
+  extern __shared__ float s_part[];  // kRedWarps x G3S
   const unsigned v = blockIdx.x;
   const int k0 = i3_start[v], k1 = i3_start[v + 1];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int per = (k1 - k0 + kRedWarps - 1) / kRedWarps;
+  const int a = k0 + w * per, b = min(k1, a + per);
+  for (int e = lane; e < G3S; e += 32) {
+    float acc = 0.f;
+    for (int k = a; k < b; ++k) acc += dH[(size_t)v3[k] * G3S + e];
+    s_part[w * G3S + e] = acc;
+  }
+  __syncthreads();
   const bool upd = do_update && ((*err & 8) == 0);
   const unsigned m3n3 = g.m3 * (unsigned)N3;
   for (int e = threadIdx.x; e < G3S; e += kBlock) {
     float acc = 0.f;
-    for (int k = k0; k < k1; ++k) acc += dH[(size_t)v3[k] * G3S + e];
+#pragma unroll
+    for (int ww = 0; ww < kRedWarps; ++ww) acc += s_part[ww * G3S + e];
     const int r = e / N3, j = e - r * N3;
     const size_t gi = (size_t)r * m3n3 + v * N3 + j;
     if (grad) grad[gi] = acc;
@@ -123,14 +137,25 @@ __global__ void __launch_bounds__(kBlock) k_dg1_reduce(KGeom g, int G1S, const u
                                                        const int* __restrict__ err, float* __restrict__ grad,
                                                        float* __restrict__ param, double* __restrict__ vel, double lr,
                                                        double mu, int do_update) {
+  extern __shared__ float s_part[];  // kRedWarps x G1S
   const unsigned i1 = blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int per = ((int)g.m2 + kRedWarps - 1) / kRedWarps;
+  const int a = w * per, b = min((int)g.m2, a + per);
+  for (int e = lane; e < G1S; e += 32) {
+    float acc = 0.f;
+    for (int i2 = a; i2 < b; ++i2) {
+      const unsigned key = i1 * g.m2 + (unsigned)i2;
+      if (pmap[key] != kEmpty) acc += E[(size_t)pslot[key] * G1S + e];
+    }
+    s_part[w * G1S + e] = acc;
+  }
+  __syncthreads();
   const bool upd = do_update && ((*err & 8) == 0);
   for (int e = threadIdx.x; e < G1S; e += kBlock) {
     float acc = 0.f;
-    for (unsigned i2 = 0; i2 < g.m2; ++i2) {
-      const unsigned key = i1 * g.m2 + i2;
-      if (pmap[key] != kEmpty) acc += E[(size_t)pslot[key] * G1S + e];
-    }
+#pragma unroll
+    for (int ww = 0; ww < kRedWarps; ++ww) acc += s_part[ww * G1S + e];
     const size_t gi = (size_t)i1 * G1S + e;
     if (grad) grad[gi] = acc;
     if (upd) param[gi] = sgd_apply(param[gi], acc, vel ? vel + gi : nullptr, lr, mu);
@@ -154,17 +179,17 @@ cudaError_t launch_sgd(float* p, const float* g, double* v, int64_t n, double lr
 
 // ---------------------------------------------------------------- dispatch
 template <class D>
-static size_t prefix_smem(const D& d) {
-  return sizeof(float) * ((size_t)dG2s(d) + (size_t)kPrefixChunk * dG1s(d));
+static size_t prefix_smem(const D& d, int ch) {
+  return sizeof(float) * ((size_t)d.r1 * dC(d) + (size_t)d.r1 * ch * d.n1);
 }
 template <class D>
 static size_t close_smem(const D& d) {
   return sizeof(float) * (kBlock / 32) * ((size_t)dX(d) * (d.r2 + 1) + dG3s(d) + dN(d));
 }
 template <class D>
-static size_t bwd_smem(const D& d) {
-  return sizeof(float) * (2 * (size_t)dG2s(d) + dG1s(d) + (size_t)dX(d) * (d.r2 + 1) + dSlot(d) +
-                          (size_t)kRowBatch * (dN(d) + dG3s(d)));
+static size_t bwd_smem(const D& d, int ch) {
+  const size_t M = (size_t)ch * d.n1, LZ = pad_ld(d);
+  return sizeof(float) * (M * LZ + (size_t)d.r1 * LZ + M * d.r1 + (kBlock / 32) * ((size_t)dN(d) + dG3s(d) + dSlot(d)));
 }
 
 template <class D>
@@ -173,12 +198,12 @@ static cudaError_t forward_impl(ttb_handle* h, const float* c0, const float* c1,
   const D d = make_dims<D>(h->dims);
   Workspace& w = h->w;
   cudaError_t e;
-  const size_t sm1 = prefix_smem(d);
+  const size_t sm1 = prefix_smem(d, h->chf);
   if ((e = cudaFuncSetAttribute(k_prefix_products<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1)))
     return e;
-  dim3 g1(h->kg.m2, (unsigned)h->cmax);
+  dim3 g1(h->kg.m2, (unsigned)h->cmaxf);
   { ProfScope _ps(h, s, "prefix_products");
-  k_prefix_products<D><<<g1, kBlock, sm1, s>>>(d, h->kg, c0, c1, w.pmap, w.pslot, w.slots);
+  k_prefix_products<D><<<g1, kBlock, sm1, s>>>(d, h->kg, h->chf, c0, c1, w.pmap, w.pslot, w.slots);
   }
   count_launch();
   const size_t sm2 = close_smem(d);
@@ -235,13 +260,13 @@ static cudaError_t backward_impl(ttb_handle* h, const float* c0, const float* c1
   cudaError_t e;
   if ((e = aggregate_impl<D>(h, gout, s))) return e;
   // 4. per-prefix contractions, grouped by i2
-  const size_t sm = bwd_smem(d);
+  const size_t sm = bwd_smem(d, h->chb);
   if ((e = cudaFuncSetAttribute(k_bwd_prefix<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm))) return e;
-  dim3 gp(h->kg.m2, (unsigned)h->cmax);
+  dim3 gp(h->kg.m2, (unsigned)h->cmaxb);
   { ProfScope _ps(h, s, "bwd_prefix");
-  k_bwd_prefix<D><<<gp, kBlock, sm, s>>>(d, h->kg, c0, c1, c2, w.pmap, w.pslot, w.slots, w.prow_begin, w.prow_end,
+  k_bwd_prefix<D><<<gp, kBlock, sm, s>>>(d, h->kg, h->chb, c0, c1, c2, w.pmap, w.pslot, w.slots, w.prow_begin, w.prow_end,
                                          w.urow_i3, w.gU, w.dH, w.E, w.dG2part, w.grp_cnt,
-                                         (int)h->cmax);
+                                         h->cmaxb);
   }
   count_launch();
   // 5. rows by last digit for the G3 reduction
@@ -250,22 +275,22 @@ static cudaError_t backward_impl(ttb_handle* h, const float* c0, const float* c1
                        s)))
     return e;
   { ProfScope _ps(h, s, "i3_bounds");
-  k_i3_bounds<<<(h->kg.m3 + kBlock) / kBlock, kBlock, 0, s>>>(k3, w.counts, (int)h->kg.m3, w.i3_start);
+  k_i3_bounds<<<(T + kBlock) / kBlock, kBlock, 0, s>>>(k3, w.counts, (int)h->kg.m3, w.i3_start);
   }
   count_launch();
   const bool upd = mode == 1;
   // 6. reductions (+ fused update)
   { ProfScope _ps(h, s, "dg1_reduce");
-  k_dg1_reduce<<<h->kg.m1, kBlock, 0, s>>>(h->kg, dG1s(d), w.pmap, w.pslot, w.E, w.err,
+  k_dg1_reduce<<<h->kg.m1, kBlock, sizeof(float) * kRedWarps * dG1s(d), s>>>(h->kg, dG1s(d), w.pmap, w.pslot, w.E, w.err,
                                            upd ? nullptr : g0, p0, v0, lr, mu, upd && (mask & 1));
   }
   { ProfScope _ps(h, s, "dg2_reduce");
-  k_dg2_reduce<<<h->kg.m2, kBlock, 0, s>>>(h->kg, dC(d), dG2s(d), (int)h->cmax, w.dG2part,
+  k_dg2_reduce<<<dim3(h->kg.m2, (dG2s(d) + kBlock - 1) / kBlock), kBlock, 0, s>>>(h->kg, dC(d), dG2s(d), h->cmaxb, h->chb, w.dG2part,
                                            w.grp_cnt, w.err, upd ? nullptr : g1, p1, v1, lr, mu,
                                            upd && (mask & 2));
   }
   { ProfScope _ps(h, s, "dg3_reduce");
-  k_dg3_reduce<<<h->kg.m3, kBlock, 0, s>>>(h->kg, d.n3, dG3s(d), w.i3_start, v3, w.dH, w.err,
+  k_dg3_reduce<<<h->kg.m3, kBlock, sizeof(float) * kRedWarps * dG3s(d), s>>>(h->kg, d.n3, dG3s(d), w.i3_start, v3, w.dH, w.err,
                                            upd ? nullptr : g2, p2, v2, lr, mu, upd && (mask & 4));
   }
   count_launch(3);
@@ -371,9 +396,16 @@ cudaError_t launch_export_unique(ttb_handle* h, int64_t* rows, float* grads, cud
 }  // namespace ttb
 
 namespace ttb {
-size_t max_smem_needed(const DynDims& d) {
-  size_t a = prefix_smem(d), b = close_smem(d), c = bwd_smem(d);
-  size_t m = a > b ? a : b;
-  return m > c ? m : c;
+// Picks the prefix chunk sizes (multiples of 8, <= kMaxChunk) that fit in
+// shared memory; false if even 8 does not fit.
+bool choose_chunks(const DynDims& d, int* chf, int* chb) {
+  const size_t cap = 227 * 1024;
+  *chf = *chb = 0;
+  for (int c : {32, 16, 8})
+    if (!*chf && prefix_smem(d, c) <= cap) *chf = c;
+  for (int c : {16, 8})
+    if (!*chb && bwd_smem(d, c) <= cap) *chb = c;
+  return *chf && *chb && close_smem(d) <= cap && sizeof(float) * kRedWarps * (size_t)dG1s(d) <= 48 * 1024 &&
+         sizeof(float) * kRedWarps * (size_t)dG3s(d) <= 48 * 1024;
 }
 }  // namespace ttb

@@ -6,7 +6,7 @@
 
 namespace ttb {
 long long g_launches = 0;
-size_t max_smem_needed(const DynDims& d);
+bool choose_chunks(const DynDims& d, int* chf, int* chb);
 }  // namespace ttb
 
 using namespace ttb;
@@ -51,7 +51,8 @@ void layout(ttb_handle& h, char* base) {
   const int64_t SL = (int64_t)d.n1 * d.n2 * d.r2, G1S = (int64_t)d.n1 * d.r1, G2S = (int64_t)d.r1 * d.n2 * d.r2,
                 G3S = (int64_t)d.r2 * d.n3;
   h.Pmax = T < m1m2 ? T : m1m2;
-  h.cmax = (g.m[0] + kPrefixChunk - 1) / kPrefixChunk;
+  h.cmaxf = (int)((g.m[0] + h.chf - 1) / h.chf);
+  h.cmaxb = (int)((g.m[0] + h.chb - 1) / h.chb);
   h.sort_tiles = (T + kTile - 1) / kTile + 1;
   int64_t st = (T + kTile - 1) / kTile;
   const int64_t bt = (B + 31) / 32;
@@ -88,7 +89,7 @@ void layout(ttb_handle& h, char* base) {
   w.gU = c.take<float>((size_t)T * N);
   w.dH = c.take<float>((size_t)T * G3S);
   w.E = c.take<float>((size_t)h.Pmax * G1S);
-  w.dG2part = c.take<float>((size_t)g.m[1] * h.cmax * G2S);
+  w.dG2part = c.take<float>((size_t)g.m[1] * h.cmaxb * G2S);
   w.i3_start = c.take<int>(g.m[2] + 1);
   w.grp_cnt = c.take<int>(g.m[1]);
   w.rkA = c.take<unsigned>(T);
@@ -112,7 +113,7 @@ bool init_handle(ttb_handle& h, const ttb_geom* g, int64_t max_T, int64_t max_B)
   h.kg.m1m2 = (unsigned)(g->m[0] * g->m[1]);
   h.kg.rows = (unsigned)(g->m[0] * g->m[1] * g->m[2]);
   h.dims = DynDims{g->n[0], g->n[1], g->n[2], g->r[1], g->r[2]};
-  if (max_smem_needed(h.dims) > 227 * 1024) return false;
+  if (!choose_chunks(h.dims, &h.chf, &h.chb)) return false;
   h.maxT = max_T;
   h.maxB = max_B;
   h.idx_bits = bits_for((uint64_t)h.kg.rows - 1);

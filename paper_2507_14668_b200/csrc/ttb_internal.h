@@ -8,8 +8,6 @@
 
 namespace ttb {
 
-// Prefixes handled per CTA in the i2-grouped prefix kernels.
-constexpr int kPrefixChunk = 32;
 
 struct Workspace {
   // error word + device counters: [0] err bits, [1] P, [2] S, [3] U
@@ -82,7 +80,8 @@ struct ttb_handle {
   ttb_geom geom;
   ttb::KGeom kg;
   ttb::DynDims dims;
-  int64_t maxT, maxB, Pmax, cmax, scan_tiles, sort_tiles;
+  int64_t maxT, maxB, Pmax, scan_tiles, sort_tiles;
+  int chf, chb, cmaxf, cmaxb;  // prefixes per CTA (forward / backward) and chunks per i2 group
   int idx_bits, i3_bits;
   char* base;
   size_t bytes;

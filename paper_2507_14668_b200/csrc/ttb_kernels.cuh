@@ -7,8 +7,15 @@
 
 namespace ttb {
 
+constexpr int kMaxChunk = 64;
+
 template <class D> struct IsFixed : std::false_type {};
 template <int A, int B, int C, int E, int F> struct IsFixed<FixDims<A, B, C, E, F>> : std::true_type {};
+// slot size n1 n2 r2 as a compile-time constant (1 for run-time dims)
+template <class D> struct FixSlot { static constexpr int value = 1; };
+template <int A, int B, int C, int E, int F> struct FixSlot<FixDims<A, B, C, E, F>> {
+  static constexpr int value = A * B * F;
+};
 
 // Enumerate the present prefixes of one group, in ascending order of the
 // free digit, and keep those whose ordinal falls in [chunk*CH, chunk*CH+CH).
@@ -59,45 +66,158 @@ __device__ inline int collect_chunk(const unsigned* __restrict__ pmap, const int
   return running;
 }
 
+// ------------------------------------------------------------ block GEMM helpers
+template <int V>
+__device__ __forceinline__ void lds_vec(float (&r)[V], const float* p) {
+  if constexpr (V % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < V; i += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(p + i);
+      r[i] = v.x; r[i + 1] = v.y; r[i + 2] = v.z; r[i + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i) r[i] = p[i];
+  }
+}
+
+// C[m][n] = sum_k At[k*lda + m] * B[k*ldb + n]   (both operands k-major in smem)
+// Thread tiles TM x TN, handed out n-fastest so a warp's B loads are one
+// contiguous run and its A loads broadcast. M % TM == 0, N % TN == 0.
+template <int TM, int TN, class Out>
+__device__ __forceinline__ void gemm_kk(int M, int N, int K, const float* At, int lda, const float* B, int ldb,
+                                        Out&& out) {
+  const int tn = N / TN, tiles = (M / TM) * tn;
+  for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
+    const int m0 = (t / tn) * TM, n0 = (t % tn) * TN;
+    float acc[TM][TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+#pragma unroll 4
+    for (int k = 0; k < K; ++k) {
+      float a[TM], b[TN];
+      lds_vec<TM>(a, At + k * lda + m0);
+      lds_vec<TN>(b, B + k * ldb + n0);
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    out(m0, n0, acc);
+  }
+}
+
+// C[m][n] = sum_k A[m*lda + k] * Bt[n*ldb + k]   (contraction contiguous in both)
+// K stepped by 4 with float4 loads when VEC (K % 4 == 0, 16-byte rows).
+template <int TM, int TN, bool VEC, class Out>
+__device__ __forceinline__ void gemm_nt(int M, int N, int K, const float* A, int lda, const float* Bt, int ldb,
+                                        Out&& out) {
+  const int tn = N / TN, tiles = (M / TM) * tn;
+  for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
+    const int m0 = (t / tn) * TM, n0 = (t % tn) * TN;
+    float acc[TM][TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+    if constexpr (VEC) {
+#pragma unroll 2
+      for (int k = 0; k < K; k += 4) {
+        float4 a[TM], b[TN];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) a[i] = *reinterpret_cast<const float4*>(A + (m0 + i) * lda + k);
+#pragma unroll
+        for (int j = 0; j < TN; ++j) b[j] = *reinterpret_cast<const float4*>(Bt + (n0 + j) * ldb + k);
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) {
+            float c = acc[i][j];
+            c = fmaf(a[i].x, b[j].x, c);
+            c = fmaf(a[i].y, b[j].y, c);
+            c = fmaf(a[i].z, b[j].z, c);
+            acc[i][j] = fmaf(a[i].w, b[j].w, c);
+          }
+      }
+    } else {
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(A[(m0 + i) * lda + k], Bt[(n0 + j) * ldb + k], acc[i][j]);
+    }
+    out(m0, n0, acc);
+  }
+}
+
+template <class D> struct Tiles {
+  // run-time dims: scalar tiles (always divisible)
+  static constexpr int FM = 1, FN = 1, BM = 1, BN = 1, CM = 1;
+  static constexpr bool VEC = false;
+};
+template <int A, int B_, int C_, int R1, int R2> struct Tiles<FixDims<A, B_, C_, R1, R2>> {
+  static constexpr int Cc = B_ * R2;
+  static constexpr int FM = 8;                                               // chunk rows (ch % 8 == 0)
+  static constexpr int FN = Cc % 8 == 0 ? 8 : (Cc % 4 == 0 ? 4 : 1);
+  static constexpr int BM = R1 % 4 == 0 ? 4 : 1;
+  static constexpr int BN = Cc % 4 == 0 ? 4 : 1;
+  static constexpr int CM = 8;
+  static constexpr bool VEC = Cc % 4 == 0;
+};
+
+template <class D> __host__ __device__ inline int pad_ld(const D& d) {
+  return dC(d) % 4 == 0 ? dC(d) + 4 : dC(d);
+}
+
 // ------------------------------------------------------------ K2: prefix products
-// slots[s] (n1 n2 x r2) = G1[i1] (n1 x r1) . G2[:, i2] (r1 x n2 r2), one CTA per
-// (i2, chunk of present prefixes): the G2 slice is read once per CTA.
-// Reference: lookup.py:138-146 (einsum "bxr,brys->bxys").
+// slots[s] (n1 n2 x r2) = G1[i1] (n1 x r1) . G2[:, i2] (r1 x n2 r2). One CTA per
+// (i2, chunk of <= ch present prefixes): a (ch n1) x (n2 r2) x r1 GEMM with the
+// G2 slice read once per CTA. Reference: lookup.py:138-146.
 template <class D>
-__global__ void __launch_bounds__(kBlock) k_prefix_products(D d, KGeom g, const float* __restrict__ G1,
+__global__ void __launch_bounds__(kBlock) k_prefix_products(D d, KGeom g, int ch, const float* __restrict__ G1,
                                                             const float* __restrict__ G2,
                                                             const unsigned* __restrict__ pmap,
                                                             const int* __restrict__ pslot, float* __restrict__ slots) {
-  extern __shared__ float smem[];
-  __shared__ int s_free[kPrefixChunk], s_slot[kPrefixChunk], s_w[kBlock / 32 + 2];
+  extern __shared__ __align__(16) float smem[];
+  __shared__ int s_free[kMaxChunk], s_slot[kMaxChunk], s_w[kBlock / 32 + 2];
   const int C = dC(d), R1 = d.r1, N1 = d.n1;
   const unsigned i2 = blockIdx.x;
   int np;
-  collect_chunk(pmap, pslot, g, true, i2, blockIdx.y, kPrefixChunk, s_free, s_slot, s_w, &np);
+  collect_chunk(pmap, pslot, g, true, i2, blockIdx.y, ch, s_free, s_slot, s_w, &np);
   if (np == 0) return;
-  float* s_g2 = smem;            // R1 x C
-  float* s_g1 = smem + R1 * C;   // np x R1 x N1 (transposed: [p][r][a])
+  const int M = ch * N1;   // padded rows (prefix, a)
+  float* s_g2 = smem;      // R1 x C   (k-major: [r1][c])
+  float* s_g1t = smem + R1 * C;  // R1 x M (k-major: [r1][p*N1 + a])
   for (int e = threadIdx.x; e < R1 * C; e += kBlock) {
     const int r = e / C, c = e - r * C;
     s_g2[e] = G2[((size_t)r * g.m2 + i2) * C + c];
   }
-  for (int e = threadIdx.x; e < np * R1 * N1; e += kBlock) {
-    const int p = e / (R1 * N1), rem = e - p * (R1 * N1);
-    const int a = rem / R1, r = rem - a * R1;
-    s_g1[(p * R1 + r) * N1 + a] = G1[((size_t)s_free[p] * N1 + a) * R1 + r];
+  for (int e = threadIdx.x; e < M * R1; e += kBlock) {
+    const int row = e / R1, r = e - row * R1;
+    const int p = row / N1, a = row - p * N1;
+    s_g1t[r * M + row] = p < np ? G1[((size_t)s_free[p] * N1 + a) * R1 + r] : 0.f;
   }
   __syncthreads();
+  using Tl = Tiles<D>;
   const int SL = dSlot(d);
-  // outputs (p, a, c): thread -> c fastest so the slot store is coalesced
-  for (int e = threadIdx.x; e < np * N1 * C; e += kBlock) {
-    const int p = e / (N1 * C), rem = e - p * (N1 * C);
-    const int a = rem / C, c = rem - a * C;
-    const float* g1 = s_g1 + p * R1 * N1 + a;
-    float acc = 0.f;
-#pragma unroll 8
-    for (int r = 0; r < R1; ++r) acc = fmaf(g1[r * N1], s_g2[r * C + c], acc);
-    slots[(size_t)s_slot[p] * SL + a * C + c] = acc;
-  }
+  gemm_kk<Tl::FM, Tl::FN>(M, C, R1, s_g1t, M, s_g2, C, [&](int m0, int n0, float (&acc)[Tl::FM][Tl::FN]) {
+#pragma unroll
+    for (int i = 0; i < Tl::FM; ++i) {
+      const int row = m0 + i, p = row / N1, a = row - p * N1;
+      if (p >= np) continue;
+      float* dst = slots + (size_t)s_slot[p] * SL + a * C + n0;
+      if constexpr (Tl::FN % 4 == 0) {
+#pragma unroll
+        for (int j = 0; j < Tl::FN; j += 4)
+          *reinterpret_cast<float4*>(dst + j) = make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < Tl::FN; ++j) dst[j] = acc[i][j];
+      }
+    }
+  });
 }
 
 // ------------------------------------------------------------ K3: close + pool
@@ -186,19 +306,17 @@ __global__ void __launch_bounds__(kBlock) k_row_agg(D d, const int* __restrict__
 }
 
 // ------------------------------------------------------------ backward: prefixes
-// One CTA per (i2, chunk). For each prefix p = (i1, i2) and each of its rows
-// u (contiguous in the row order):
-//   Z_p   += g_u (n1n2 x n3) . G3[i3_u]^T (n3 x r2)       -> dL/dslot_p
-//   dH_u   = slot_p^T (r2 x n1n2) . g_u                  -> G3 gradient block
-// then  dG2[:, i2] += G1[i1]^T . Z_p   (accumulated in the CTA)
-//       E_p         = Z_p . G2[:, i2]^T                  -> G1 gradient block
-// This regroups backward.py:152-178 (per-row left/right chains) so the two
-// r1 x n2 r2 products run once per distinct prefix instead of once per
-// distinct row; the sums are the same.
-constexpr int kRowBatch = 8;
-
+// One CTA per (i2, chunk of <= ch present prefixes).
+//  Phase A (warp per prefix): for each of the prefix's rows u (contiguous in
+//    the sorted row order)
+//      Z_p += g_u (n1n2 x n3) . G3[i3_u]^T      -> dL/dslot_p, kept in smem
+//      dH_u = slot_p^T . g_u (r2 x n3)          -> G3 gradient block, to HBM
+//  Phase B: dG2[:, i2] partial (r1 x n2r2) = G1_chunk^T . Z_chunk   (GEMM, K = np n1)
+//  Phase C: E_p (n1 x r1) = Z_p . G2[:, i2]^T                     (GEMM, K = n2 r2)
+// This regroups backward.py:152-178 (per-row chains) so the r1 x n2 r2
+// products run per distinct prefix; the sums are identical.
 template <class D>
-__global__ void __launch_bounds__(kBlock) k_bwd_prefix(D d, KGeom g, const float* __restrict__ G1,
+__global__ void __launch_bounds__(kBlock) k_bwd_prefix(D d, KGeom g, int ch, const float* __restrict__ G1,
                                                        const float* __restrict__ G2, const float* __restrict__ G3,
                                                        const unsigned* __restrict__ pmap, const int* __restrict__ pslot,
                                                        const float* __restrict__ slots,
@@ -208,97 +326,134 @@ __global__ void __launch_bounds__(kBlock) k_bwd_prefix(D d, KGeom g, const float
                                                        const float* __restrict__ gU, float* __restrict__ dH,
                                                        float* __restrict__ E, float* __restrict__ dG2part,
                                                        int* __restrict__ grp_cnt, int cmax) {
-  extern __shared__ float smem[];
-  __shared__ int s_free[kPrefixChunk], s_slot[kPrefixChunk], s_w[kBlock / 32 + 2];
-  const int C = dC(d), R1 = d.r1, R2 = d.r2, N1 = d.n1, N3 = d.n3, X = dX(d), N = dN(d);
-  const int SL = dSlot(d), G3S = dG3s(d), G2S = dG2s(d), G1S = dG1s(d);
+  extern __shared__ __align__(16) float smem[];
+  __shared__ int s_free[kMaxChunk], s_slot[kMaxChunk], s_w[kBlock / 32 + 2];
+  const int C = dC(d), R1 = d.r1, R2 = d.r2, N1 = d.n1, N2 = d.n2, N3 = d.n3, X = dX(d), N = dN(d);
+  const int SL = dSlot(d), G3S = dG3s(d), G1S = dG1s(d);
   const unsigned i2 = blockIdx.x;
   int np;
-  const int total = collect_chunk(pmap, pslot, g, true, i2, blockIdx.y, kPrefixChunk, s_free, s_slot, s_w, &np);
+  const int total = collect_chunk(pmap, pslot, g, true, i2, blockIdx.y, ch, s_free, s_slot, s_w, &np);
   if (blockIdx.y == 0 && threadIdx.x == 0) grp_cnt[i2] = total;
   if (np == 0) return;
-  const int RS = R2 + 1;
-  float* s_g2 = smem;                    // R1 x C
-  float* s_acc = s_g2 + G2S;             // R1 x C  (dG2 accumulator)
-  float* s_g1 = s_acc + G2S;             // N1 x R1
-  float* s_sb = s_g1 + G1S;              // X x RS
-  float* s_z = s_sb + X * RS;            // X x R2 == N1 x C
-  float* s_g = s_z + SL;                 // kRowBatch x N
-  float* s_g3 = s_g + kRowBatch * N;     // kRowBatch x G3S
-  for (int e = threadIdx.x; e < G2S; e += kBlock) {
+  const int M = ch * N1;
+  const int LZ = pad_ld(d);
+  float* s_z = smem;                 // M x LZ      Z rows (p, a), cols c = b r2 + r
+  float* s_g2 = s_z + M * LZ;        // R1 x LZ     G2 slice [r1][c]
+  float* s_g1 = s_g2 + R1 * LZ;      // M x R1      G1 chunk [(p, a)][r1]  (k-major for phase B)
+  float* s_wk = s_g1 + M * R1;       // per warp: g (N) + G3 slice (G3S) + slot (SL)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < R1 * C; e += kBlock) {
     const int r = e / C, c = e - r * C;
-    s_g2[e] = G2[((size_t)r * g.m2 + i2) * C + c];
-    s_acc[e] = 0.f;
+    s_g2[r * LZ + c] = G2[((size_t)r * g.m2 + i2) * C + c];
   }
-  const unsigned m3n3 = g.m3 * (unsigned)N3;
-  for (int pi = 0; pi < np; ++pi) {
-    const int slot = s_slot[pi];
-    const unsigned i1 = s_free[pi];
-    __syncthreads();
-    for (int e = threadIdx.x; e < G1S; e += kBlock) s_g1[e] = G1[(size_t)i1 * G1S + e];
-    const float* sb = slots + (size_t)slot * SL;
-    for (int e = threadIdx.x; e < SL; e += kBlock) {
-      const int x = e / R2, r = e - x * R2;
-      s_sb[x * RS + r] = sb[e];
-      s_z[e] = 0.f;
-    }
-    const int u0 = prow_begin[slot], u1 = prow_end[slot];
-    for (int ub = u0; ub < u1; ub += kRowBatch) {
-      const int nb = (u1 - ub) < kRowBatch ? (u1 - ub) : kRowBatch;
-      __syncthreads();
-      for (int e = threadIdx.x; e < nb * N; e += kBlock) s_g[e] = gU[(size_t)ub * N + e];
-      for (int e = threadIdx.x; e < nb * G3S; e += kBlock) {
-        const int k = e / G3S, rem = e - k * G3S;
-        const int r = rem / N3, j = rem - r * N3;
-        s_g3[e] = __ldg(&G3[(size_t)r * m3n3 + urow_i3[ub + k] * N3 + j]);
-      }
-      __syncthreads();
-      // Z (X x R2) += sum_k g_k (X x N3) . G3_k^T
-      for (int e = threadIdx.x; e < SL; e += kBlock) {
-        const int x = e / R2, r = e - x * R2;
-        float acc = s_z[e];
-        for (int k = 0; k < nb; ++k) {
-          const float* gk = s_g + k * N + x * N3;
-          const float* hk = s_g3 + k * G3S + r * N3;
+  for (int e = threadIdx.x; e < M * R1; e += kBlock) {
+    const int row = e / R1, r = e - row * R1;
+    const int p = row / N1, a = row - p * N1;
+    s_g1[e] = p < np ? G1[((size_t)s_free[p] * N1 + a) * R1 + r] : 0.f;
+  }
+  // ---- phase A
+  {
+    float* s_g = s_wk + w * (N + G3S + SL);
+    float* s_h = s_g + N;
+    float* s_sb = s_h + G3S;
+    const unsigned m3n3 = g.m3 * (unsigned)N3;
+    for (int pi = w; pi < np; pi += kBlock / 32) {
+      const int slot = s_slot[pi];
+      const float* sb = slots + (size_t)slot * SL;
+      for (int e = lane; e < SL; e += 32) s_sb[e] = sb[e];
+      constexpr int KZ = (FixSlot<D>::value + 31) / 32;
+      float zr[KZ];
 #pragma unroll
-          for (int j = 0; j < N3; ++j) acc = fmaf(gk[j], hk[j], acc);
+      for (int k = 0; k < KZ; ++k) zr[k] = 0.f;
+      if constexpr (!IsFixed<D>::value) {
+        for (int e = lane; e < SL; e += 32) {
+          const int x = e / R2, r = e - x * R2, a = x / N2, b = x - a * N2;
+          s_z[(pi * N1 + a) * LZ + b * R2 + r] = 0.f;
         }
-        s_z[e] = acc;
       }
-      // dH_k (R2 x N3) = slot^T . g_k
-      for (int e = threadIdx.x; e < nb * G3S; e += kBlock) {
-        const int k = e / G3S, rem = e - k * G3S;
-        const int r = rem / N3, j = rem - r * N3;
-        const float* gk = s_g + k * N + j;
-        float acc = 0.f;
-#pragma unroll 4
-        for (int x = 0; x < X; ++x) acc = fmaf(s_sb[x * RS + r], gk[x * N3], acc);
-        dH[(size_t)(ub + k) * G3S + rem] = acc;
-      }
-    }
-    __syncthreads();
-    // dG2 slice += G1^T . Z  (Z viewed as N1 x C)
-    for (int e = threadIdx.x; e < G2S; e += kBlock) {
-      const int r = e / C, c = e - r * C;
-      float acc = s_acc[e];
+      const int u0 = prow_begin[slot], u1 = prow_end[slot];
+      for (int u = u0; u < u1; ++u) {
+        __syncwarp();
+        const unsigned i3 = urow_i3[u];
+        for (int e = lane; e < N; e += 32) s_g[e] = gU[(size_t)u * N + e];
+        for (int e = lane; e < G3S; e += 32) {
+          const int r = e / N3, j = e - r * N3;
+          s_h[e] = __ldg(&G3[(size_t)r * m3n3 + i3 * N3 + j]);
+        }
+        __syncwarp();
+        // Z += g . G3^T
+        if constexpr (IsFixed<D>::value) {
 #pragma unroll
-      for (int a = 0; a < N1; ++a) acc = fmaf(s_g1[a * R1 + r], s_z[a * C + c], acc);
-      s_acc[e] = acc;
+          for (int k = 0; k < KZ; ++k) {
+            const int e = lane + 32 * k;
+            if (e < SL) {
+              const int x = e / R2, r = e - x * R2;
+              float acc = zr[k];
+#pragma unroll
+              for (int j = 0; j < N3; ++j) acc = fmaf(s_g[x * N3 + j], s_h[r * N3 + j], acc);
+              zr[k] = acc;
+            }
+          }
+        } else {
+          for (int e = lane; e < SL; e += 32) {
+            const int x = e / R2, r = e - x * R2, a = x / N2, b = x - a * N2;
+            float* zp = &s_z[(pi * N1 + a) * LZ + b * R2 + r];
+            float acc = *zp;
+            for (int j = 0; j < N3; ++j) acc = fmaf(s_g[x * N3 + j], s_h[r * N3 + j], acc);
+            *zp = acc;
+          }
+        }
+        // dH_u = slot^T . g
+        for (int e = lane; e < G3S; e += 32) {
+          const int r = e / N3, j = e - r * N3;
+          float acc = 0.f;
+#pragma unroll 4
+          for (int x = 0; x < X; ++x) acc = fmaf(s_sb[x * R2 + r], s_g[x * N3 + j], acc);
+          dH[(size_t)u * G3S + e] = acc;
+        }
+      }
+      if constexpr (IsFixed<D>::value) {
+#pragma unroll
+        for (int k = 0; k < KZ; ++k) {
+          const int e = lane + 32 * k;
+          if (e < SL) {
+            const int x = e / R2, r = e - x * R2, a = x / N2, b = x - a * N2;
+            s_z[(pi * N1 + a) * LZ + b * R2 + r] = zr[k];
+          }
+        }
+      }
     }
-    // E_p (N1 x R1) = Z . G2_slice^T
-    for (int e = threadIdx.x; e < G1S; e += kBlock) {
-      const int a = e / R1, r = e - a * R1;
-      const float* z = s_z + a * C;
-      const float* g2 = s_g2 + r * C;
-      float acc = 0.f;
-#pragma unroll 8
-      for (int c = 0; c < C; ++c) acc = fmaf(z[c], g2[c], acc);
-      E[(size_t)slot * G1S + e] = acc;
-    }
+    // rows of the padding prefixes: zero so the GEMMs stay finite
+    for (int e = np * N1 * LZ + threadIdx.x; e < M * LZ; e += kBlock) s_z[e] = 0.f;
   }
   __syncthreads();
-  float* part = dG2part + ((size_t)i2 * cmax + blockIdx.y) * G2S;
-  for (int e = threadIdx.x; e < G2S; e += kBlock) part[e] = s_acc[e];
+  using Tl = Tiles<D>;
+  // ---- phase B: dG2 partial = G1_chunk^T . Z_chunk
+  {
+    float* part = dG2part + ((size_t)i2 * cmax + blockIdx.y) * dG2s(d);
+    gemm_kk<Tl::BM, Tl::BN>(R1, C, np * N1, s_g1, R1, s_z, LZ, [&](int m0, int n0, float (&acc)[Tl::BM][Tl::BN]) {
+#pragma unroll
+      for (int i = 0; i < Tl::BM; ++i) {
+        float* dst = part + (size_t)(m0 + i) * C + n0;
+        if constexpr (Tl::BN % 4 == 0) {
+#pragma unroll
+          for (int j = 0; j < Tl::BN; j += 4)
+            *reinterpret_cast<float4*>(dst + j) = make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < Tl::BN; ++j) dst[j] = acc[i][j];
+        }
+      }
+    });
+  }
+  // ---- phase C: E = Z . G2_slice^T
+  gemm_nt<Tl::CM, 1, Tl::VEC>(M, R1, C, s_z, LZ, s_g2, LZ, [&](int m0, int n0, float (&acc)[Tl::CM][1]) {
+#pragma unroll
+    for (int i = 0; i < Tl::CM; ++i) {
+      const int row = m0 + i, p = row / N1, a = row - p * N1;
+      if (p < np) E[(size_t)s_slot[p] * G1S + a * R1 + n0] = acc[i][0];
+    }
+  });
 }
 
 }  // namespace ttb

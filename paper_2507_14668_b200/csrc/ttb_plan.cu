@@ -88,138 +88,164 @@ __global__ void __launch_bounds__(kBlock) k_plan_slots(const unsigned* __restric
 }
 
 // ---------------------------------------------------------------- P3: segments
-// One warp per bag; a tile is 8 warps x kBagsPerWarp bags. The distinct
-// slots of a bag, in ascending order, are its segments (np.unique sorts the
-// keys bag * P + slot). The bag's segment base comes from a look-back scan
-// of the per-bag distinct counts.
-constexpr int kBagsPerWarp = 4;
-constexpr int kBagsPerTile = (kBlock / 32) * kBagsPerWarp;
+// A tile is 256 consecutive bags, one thread each. The distinct slots of a
+// bag, in ascending order, are its segments (np.unique sorts bag * P + slot).
+// Bags of <= kShortBag indices are ranked in registers by their thread; longer
+// bags are handed to whole warps (O(L^2 / 32) through global scratch). The
+// bag's segment base comes from a look-back scan of the per-bag counts.
+constexpr int kShortBag = 8;
+constexpr int kBagsPerTile = kBlock;
+
+__device__ inline void long_bag_rank(int o0, int o1, const unsigned* __restrict__ keys32, unsigned m3,
+                                     const int* __restrict__ pslot, int* __restrict__ occ_slot,
+                                     int* __restrict__ occ_tmp, int* __restrict__ seg_inv, int* cnt_out) {
+  const int lane = threadIdx.x & 31;
+  for (int t = o0 + lane; t < o1; t += 32) occ_slot[t] = pslot[keys32[t] / m3];
+  __syncwarp();
+  for (int t = o0 + lane; t < o1; t += 32) {
+    const int sl = occ_slot[t];
+    int first = 1;
+    for (int u = o0; u < t; ++u)
+      if (occ_slot[u] == sl) {
+        first = 0;
+        break;
+      }
+    occ_tmp[t] = first;
+  }
+  __syncwarp();
+  int c = 0;
+  for (int t = o0 + lane; t < o1; t += 32) {
+    const int sl = occ_slot[t];
+    int r = 0;
+    for (int u = o0; u < o1; ++u) r += (occ_tmp[u] && occ_slot[u] < sl) ? 1 : 0;
+    seg_inv[t] = r;  // local rank for now
+    c += occ_tmp[t];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) *cnt_out = c;
+  __syncwarp();
+}
 
 __global__ void __launch_bounds__(kBlock) k_plan_segs(const unsigned* __restrict__ keys32,
-                                                      const int64_t* __restrict__ offsets, int T, int B, KGeom g,
+                                                      const int* __restrict__ bag_off, int T, int B, KGeom g,
                                                       const int* __restrict__ pslot, int* __restrict__ occ_slot,
                                                       int* __restrict__ occ_tmp, int* __restrict__ seg_inv,
                                                       int* __restrict__ seg_slot, int* __restrict__ seg_bag,
                                                       int* __restrict__ bag_seg, int* __restrict__ counts,
                                                       unsigned long long* status, unsigned* ctr) {
+  constexpr int NW = kBlock / 32;
   __shared__ int s_tile;
   __shared__ int s_cnt[kBagsPerTile];
-  __shared__ int s_base;
+  __shared__ int s_long[kBagsPerTile];
+  __shared__ int s_nlong, s_base, s_wsum[NW];
   const int tile = claim_tile(ctr, &s_tile);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const unsigned lt = lanemask_lt();
-
-  int my_slot[kBagsPerWarp], my_rank[kBagsPerWarp], o0s[kBagsPerWarp], lens[kBagsPerWarp];
-  bool my_first[kBagsPerWarp];
+  if (threadIdx.x == 0) s_nlong = 0;
+  __syncthreads();
+  const int b = tile * kBagsPerTile + threadIdx.x;
+  int o0 = 0, L = 0;
+  int sl[kShortBag], rk[kShortBag];
+  unsigned firstm = 0;
+  int cnt = 0;
+  if (b < B) {
+    o0 = bag_off[b];
+    const int o1 = bag_off[b + 1];
+    L = o1 > o0 ? o1 - o0 : 0;
+    if (L <= kShortBag) {
 #pragma unroll
-  for (int k = 0; k < kBagsPerWarp; ++k) {
-    const int b = tile * kBagsPerTile + w * kBagsPerWarp + k;
-    int cnt = 0;
-    my_slot[k] = 0x7fffffff;
-    my_rank[k] = 0;
-    my_first[k] = false;
-    o0s[k] = 0;
-    lens[k] = 0;
-    if (b < B) {
-      long long o0 = offsets[b], o1 = offsets[b + 1];
-      o0 = o0 < 0 ? 0 : (o0 > T ? T : o0);
-      o1 = o1 < o0 ? o0 : (o1 > T ? T : o1);
-      const int L = (int)(o1 - o0);
-      o0s[k] = (int)o0;
-      lens[k] = L;
-      if (L <= 32) {
-        const bool act = lane < L;
-        int s = 0x7fffffff;
-        if (act) {
-          s = pslot[keys32[o0 + lane] / g.m3];
-          occ_slot[o0 + lane] = s;
+      for (int i = 0; i < kShortBag; ++i) {
+        sl[i] = 0x7fffffff;
+        if (i < L) {
+          sl[i] = pslot[keys32[o0 + i] / g.m3];
+          occ_slot[o0 + i] = sl[i];
         }
-        const unsigned peers = __match_any_sync(0xffffffffu, s);
-        const bool first = act && ((peers & lt) == 0);
-        int r = 0;
-        for (int i = 0; i < 32; ++i) {
-          const int si = __shfl_sync(0xffffffffu, s, i);
-          const bool fi = __shfl_sync(0xffffffffu, first, i);
-          r += (fi && si < s) ? 1 : 0;
-        }
-        cnt = __popc(__ballot_sync(0xffffffffu, first));
-        my_slot[k] = s;
-        my_rank[k] = r;
-        my_first[k] = first;
-      } else {
-        // long bag: O(L^2 / 32) per warp, through global scratch
-        for (int t = (int)o0 + lane; t < (int)o1; t += 32) occ_slot[t] = pslot[keys32[t] / g.m3];
-        __syncwarp();
-        for (int t = (int)o0 + lane; t < (int)o1; t += 32) {
-          const int s = occ_slot[t];
-          int first = 1;
-          for (int u = (int)o0; u < t; ++u)
-            if (occ_slot[u] == s) {
-              first = 0;
-              break;
-            }
-          occ_tmp[t] = first;
-        }
-        __syncwarp();
-        int c = 0;
-        for (int t = (int)o0 + lane; t < (int)o1; t += 32) {
-          const int s = occ_slot[t];
-          int r = 0;
-          for (int u = (int)o0; u < (int)o1; ++u) r += (occ_tmp[u] && occ_slot[u] < s) ? 1 : 0;
-          seg_inv[t] = r;  // local rank for now
-          c += occ_tmp[t];
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        cnt = c;
       }
-    }
-    if (lane == 0) s_cnt[w * kBagsPerWarp + k] = cnt;
-  }
-  __syncthreads();
-  if (w == 0) {
-    const int v = s_cnt[lane];
-    int incl = v;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    s_cnt[lane] = incl - v;
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    if (lane == 0) s_base = (int)lookback_exclusive(status, tile, total);
-    const int ntiles = (B + kBagsPerTile - 1) / kBagsPerTile;
-    if (lane == 0 && tile == ntiles - 1) {
-      const int S = s_base + total;
-      bag_seg[B] = S;
-      counts[2] = S;
-    }
-  }
-  __syncthreads();
+      for (int i = 0; i < kShortBag; ++i) {
+        bool first = i < L;
 #pragma unroll
-  for (int k = 0; k < kBagsPerWarp; ++k) {
-    const int b = tile * kBagsPerTile + w * kBagsPerWarp + k;
-    if (b >= B) continue;
-    const int base = s_base + s_cnt[w * kBagsPerWarp + k];
-    if (lane == 0) bag_seg[b] = base;
-    const int o0 = o0s[k], L = lens[k];
-    if (L <= 32) {
-      if (lane < L) {
-        const int sg = base + my_rank[k];
-        seg_inv[o0 + lane] = sg;
-        if (my_first[k]) {
-          seg_slot[sg] = my_slot[k];
-          seg_bag[sg] = b;
-        }
+        for (int j = 0; j < i; ++j) first = first && (sl[j] != sl[i]);
+        if (first) firstm |= 1u << i;
+      }
+      cnt = __popc(firstm);
+#pragma unroll
+      for (int i = 0; i < kShortBag; ++i) {
+        int r = 0;
+#pragma unroll
+        for (int j = 0; j < kShortBag; ++j) r += ((firstm >> j) & 1u) && sl[j] < sl[i] ? 1 : 0;
+        rk[i] = r;
       }
     } else {
-      for (int t = o0 + lane; t < o0 + L; t += 32) {
-        const int sg = base + seg_inv[t];
-        seg_inv[t] = sg;
-        if (occ_tmp[t]) {
-          seg_slot[sg] = occ_slot[t];
-          seg_bag[sg] = b;
+      s_long[atomicAdd(&s_nlong, 1)] = threadIdx.x;
+    }
+  }
+  s_cnt[threadIdx.x] = cnt;
+  __syncthreads();
+  for (int i = w; i < s_nlong; i += NW) {
+    const int tb = s_long[i];
+    const int bb = tile * kBagsPerTile + tb;
+    long_bag_rank(bag_off[bb], bag_off[bb + 1], keys32, g.m3, pslot, occ_slot, occ_tmp, seg_inv, &s_cnt[tb]);
+  }
+  __syncthreads();
+  // block exclusive scan of the 256 counts + look-back across tiles
+  const int v = s_cnt[threadIdx.x];
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_wsum[w] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int i = 0; i < NW; ++i) {
+      const int c = s_wsum[i];
+      s_wsum[i] = acc;
+      acc += c;
+    }
+    s_base = (int)lookback_exclusive(status, tile, acc);
+    const int ntiles = (B + kBagsPerTile - 1) / kBagsPerTile;
+    if (tile == ntiles - 1) {
+      bag_seg[B] = s_base + acc;
+      counts[2] = s_base + acc;
+    }
+  }
+  __syncthreads();
+  const int base = s_base + s_wsum[w] + incl - v;
+  if (b < B) {
+    bag_seg[b] = base;
+    if (L <= kShortBag) {
+#pragma unroll
+      for (int i = 0; i < kShortBag; ++i) {
+        if (i < L) {
+          const int sg = base + rk[i];
+          seg_inv[o0 + i] = sg;
+          if ((firstm >> i) & 1u) {
+            seg_slot[sg] = sl[i];
+            seg_bag[sg] = b;
+          }
         }
+      }
+    }
+  }
+  // long bags: finish with their local ranks (warp per bag)
+  for (int i = w; i < s_nlong; i += NW) {
+    const int tb = s_long[i];
+    const int bb = tile * kBagsPerTile + tb;
+    // base of bag tb = its exclusive prefix within the tile, from s_cnt
+    int pre = 0;
+    for (int j = lane; j < tb; j += 32) pre += s_cnt[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    const int bbase = s_base + pre;
+    for (int t = bag_off[bb] + lane; t < bag_off[bb + 1]; t += 32) {
+      const int sg = bbase + seg_inv[t];
+      seg_inv[t] = sg;
+      if (occ_tmp[t]) {
+        seg_slot[sg] = occ_slot[t];
+        seg_bag[sg] = bb;
       }
     }
   }
@@ -257,7 +283,7 @@ cudaError_t launch_plan(ttb_handle* h, const void* idx, int idx64, const int64_t
   count_launch();
   const int btiles = (B + kBagsPerTile - 1) / kBagsPerTile;
   { ProfScope _ps(h, s, "plan_segs");
-  k_plan_segs<<<btiles, kBlock, 0, s>>>(w.keys32, offsets, T, B, h->kg, w.pslot, w.occ_slot, w.occ_tmp, w.seg_inv,
+  k_plan_segs<<<btiles, kBlock, 0, s>>>(w.keys32, w.bag_off, T, B, h->kg, w.pslot, w.occ_slot, w.occ_tmp, w.seg_inv,
                                         w.seg_slot, w.seg_bag, w.bag_seg, w.counts,
                                         w.scan_status + kScanSegs * h->scan_tiles, w.scan_ctr + kScanSegs);
   }
