@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip extras (for ncu launch lists)")
+    ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of replaying a CUDA graph")
     return ap.parse_args()
 
 
@@ -187,6 +188,26 @@ def run_ours(args):
     step()
     torch.cuda.synchronize()
     launches_per_step = nat.launch_count() - l0
+    eager_step = step
+    use_graph = not args.no_graph and world == 1
+    if use_graph:
+        # the whole step (plan + forward + backward + update: ~25 kernels and a
+        # few memsets) as one CUDA graph: no host round trips between kernels
+        graph = torch.cuda.CUDAGraph()
+        s_cap = torch.cuda.Stream()
+        s_cap.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s_cap):
+            step()
+            torch.cuda.synchronize()
+            with torch.cuda.graph(graph, stream=s_cap):
+                step()
+        torch.cuda.current_stream().wait_stream(s_cap)
+        torch.cuda.synchronize()
+        step = graph.replay
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        eng.check_errors()
 
     clocks = ClockSampler(local).start() if not args.quick else None
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -223,13 +244,14 @@ def run_ours(args):
             "batch_per_gpu": cfg["batch"], "pooling": cfg["pooling"],
             "parallelism": f"dp{world}" + (" (NCCL all-reduce of core grads)" if world > 1 else ""),
             "l2": "flushed between timed steps (512 MiB write, outside the timed events)",
+            "launch": "one CUDA graph per step" if use_graph else "eager launches",
         },
         "counts": {"T": st["T"], "B": st["B"], "P": st["P"], "S": st["S"], "U": eng.status()["U"]},
         "gpu_launches": int(launches_per_step * args.steps),
         "clocks": clk,
     }
     if rank == 0 and not args.quick:
-        result.update(profile_and_roofline(args, torch, eng, lib, emb, step, flush, st, dev))
+        result.update(profile_and_roofline(args, torch, eng, lib, emb, eager_step, flush, st, dev))
         if not args.no_e2e:
             result["e2e"] = e2e_run(args, torch, cfg, rank, dev, world)
         if world == 1 and not args.no_cpu_baseline:

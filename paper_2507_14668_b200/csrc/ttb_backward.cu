@@ -69,25 +69,6 @@ __global__ void __launch_bounds__(kBlock) k_runs(const unsigned* __restrict__ sk
 // produced the final gradient.
 constexpr int kRedWarps = kBlock / 32;
 
-// dG2[:, i2] = sum over the chunk partials of group i2, in chunk order.
-__global__ void __launch_bounds__(kBlock) k_dg2_reduce(KGeom g, int C, int G2S, int cmax, int ch,
-                                                       const float* __restrict__ part, const int* __restrict__ grp_cnt,
-                                                       const int* __restrict__ err, float* __restrict__ grad,
-                                                       float* __restrict__ param, double* __restrict__ vel, double lr,
-                                                       double mu, int do_update) {
-  const unsigned i2 = blockIdx.x;
-  const int nch = (grp_cnt[i2] + ch - 1) / ch;
-  const bool upd = do_update && ((*err & 8) == 0);
-  const int e = blockIdx.y * kBlock + threadIdx.x;
-  if (e >= G2S) return;
-  float acc = 0.f;
-  for (int c = 0; c < nch; ++c) acc += part[((size_t)i2 * cmax + c) * G2S + e];
-  const int r = e / C, cc = e - r * C;
-  const size_t gi = ((size_t)r * g.m2 + i2) * C + cc;
-  if (grad) grad[gi] = acc;
-  if (upd) param[gi] = sgd_apply(param[gi], acc, vel ? vel + gi : nullptr, lr, mu);
-}
-
 // i3_start[v] = first position of digit v among the i3-sorted rows: every
 // boundary between consecutive sorted keys fills the digits it skips.
 __global__ void k_i3_bounds(const unsigned* __restrict__ k3, const int* __restrict__ counts, int m3,
@@ -100,65 +81,230 @@ __global__ void k_i3_bounds(const unsigned* __restrict__ k3, const int* __restri
   }
 }
 
-// dG3[:, i3] = sum of dH over the rows with that last digit, in row order.
-__global__ void __launch_bounds__(kBlock) k_dg3_reduce(KGeom g, int N3, int G3S, const int* __restrict__ i3_start,
-                                                       const unsigned* __restrict__ v3, const float* __restrict__ dH,
-                                                       const int* __restrict__ err, float* __restrict__ grad,
-                                                       float* __restrict__ param, double* __restrict__ vel, double lr,
-                                                       double mu, int do_update) {
-  extern __shared__ float s_part[];  // kRedWarps x G3S
-  const unsigned v = blockIdx.x;
-  const int k0 = i3_start[v], k1 = i3_start[v + 1];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int per = (k1 - k0 + kRedWarps - 1) / kRedWarps;
-  const int a = k0 + w * per, b = min(k1, a + per);
-  for (int e = lane; e < G3S; e += 32) {
-    float acc = 0.f;
-    for (int k = a; k < b; ++k) acc += dH[(size_t)v3[k] * G3S + e];
-    s_part[w * G3S + e] = acc;
-  }
-  __syncthreads();
-  const bool upd = do_update && ((*err & 8) == 0);
-  const unsigned m3n3 = g.m3 * (unsigned)N3;
-  for (int e = threadIdx.x; e < G3S; e += kBlock) {
-    float acc = 0.f;
-#pragma unroll
-    for (int ww = 0; ww < kRedWarps; ++ww) acc += s_part[ww * G3S + e];
-    const int r = e / N3, j = e - r * N3;
-    const size_t gi = (size_t)r * m3n3 + v * N3 + j;
-    if (grad) grad[gi] = acc;
-    if (upd) param[gi] = sgd_apply(param[gi], acc, vel ? vel + gi : nullptr, lr, mu);
-  }
-}
 
-// dG1[i1] = sum of E over the present prefixes (i1, i2), ascending i2.
-__global__ void __launch_bounds__(kBlock) k_dg1_reduce(KGeom g, int G1S, const unsigned* __restrict__ pmap,
-                                                       const int* __restrict__ pslot, const float* __restrict__ E,
-                                                       const int* __restrict__ err, float* __restrict__ grad,
-                                                       float* __restrict__ param, double* __restrict__ vel, double lr,
-                                                       double mu, int do_update) {
-  extern __shared__ float s_part[];  // kRedWarps x G1S
-  const unsigned i1 = blockIdx.x;
+// One launch for the G1 and G3 reductions: blocks [0, m1) reduce dG1 rows,
+// blocks [m1, m1 + m3) reduce dG3 columns. Warp w owns a contiguous run of
+// the summands; warp partials are combined in warp order (deterministic), and
+// the SGD step is applied by the thread holding the final gradient.
+constexpr int kRedPerLane = 16;  // fallback: G1S, G3S <= 32 * kRedPerLane
+
+// dG1[i1] = sum of E over the present prefixes (i1, i2), ascending i2; the
+// block also resets its row of the prefix table for the next batch's plan.
+__device__ inline void dg1_block(KGeom g, int G1S, unsigned i1, unsigned* __restrict__ pmap,
+                                 const int* __restrict__ pslot, const float* __restrict__ E, float* s_part) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int per = ((int)g.m2 + kRedWarps - 1) / kRedWarps;
   const int a = w * per, b = min((int)g.m2, a + per);
-  for (int e = lane; e < G1S; e += 32) {
-    float acc = 0.f;
-    for (int i2 = a; i2 < b; ++i2) {
-      const unsigned key = i1 * g.m2 + (unsigned)i2;
-      if (pmap[key] != kEmpty) acc += E[(size_t)pslot[key] * G1S + e];
+  const bool vec = G1S == 128;
+  float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  float acc[kRedPerLane];
+#pragma unroll
+  for (int i = 0; i < kRedPerLane; ++i) acc[i] = 0.f;
+  for (int base = a; base < b; base += 32) {
+    const int i2 = base + lane;
+    int sl = -1;
+    unsigned key = 0;
+    if (i2 < b) {
+      key = i1 * g.m2 + (unsigned)i2;
+      if (pmap[key] != kEmpty) sl = pslot[key];
     }
-    s_part[w * G1S + e] = acc;
+    unsigned m = __ballot_sync(0xffffffffu, sl >= 0);
+    if (sl >= 0) pmap[key] = kEmpty;  // consumed: clean for the next plan
+    while (m) {
+      if (vec) {
+        float4 v[8];
+        int sls[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          sls[k] = -1;
+          if (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            sls[k] = __shfl_sync(0xffffffffu, sl, src);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (sls[k] >= 0) v[k] = reinterpret_cast<const float4*>(E + (size_t)sls[k] * 128)[lane];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (sls[k] >= 0) {
+            acc4.x += v[k].x;
+            acc4.y += v[k].y;
+            acc4.z += v[k].z;
+            acc4.w += v[k].w;
+          }
+      } else {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const int slot = __shfl_sync(0xffffffffu, sl, src);
+        const float* row = E + (size_t)slot * G1S;
+#pragma unroll
+        for (int q = 0; q < kRedPerLane; ++q)
+          if (lane + 32 * q < G1S) acc[q] += row[lane + 32 * q];
+      }
+    }
   }
-  __syncthreads();
+  if (vec) {
+    reinterpret_cast<float4*>(s_part + w * G1S)[lane] = acc4;
+  } else {
+#pragma unroll
+    for (int q = 0; q < kRedPerLane; ++q)
+      if (lane + 32 * q < G1S) s_part[w * G1S + lane + 32 * q] = acc[q];
+  }
+}
+
+// dG3[:, i3] = sum of dH over the rows with that last digit, in row order.
+__device__ inline void dg3_block(int G3S, unsigned v, const int* __restrict__ i3_start,
+                                 const unsigned* __restrict__ v3, const float* __restrict__ dH, float* s_part) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int k0 = i3_start[v], k1 = i3_start[v + 1];
+  const int per = (k1 - k0 + kRedWarps - 1) / kRedWarps;
+  const int a = k0 + w * per, b = min(k1, a + per);
+  const bool vec = G3S == 128;
+  float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  float acc[kRedPerLane];
+#pragma unroll
+  for (int i = 0; i < kRedPerLane; ++i) acc[i] = 0.f;
+  for (int base = a; base < b; base += 32) {
+    const int myk = base + lane;
+    const unsigned myu = myk < b ? v3[myk] : 0u;
+    const int cnt = min(32, b - base);
+    if (vec) {
+      for (int i0 = 0; i0 < cnt; i0 += 8) {
+        float4 r[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const unsigned u = __shfl_sync(0xffffffffu, myu, (i0 + k) & 31);
+          if (i0 + k < cnt) r[k] = reinterpret_cast<const float4*>(dH + (size_t)u * 128)[lane];
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (i0 + k < cnt) {
+            acc4.x += r[k].x;
+            acc4.y += r[k].y;
+            acc4.z += r[k].z;
+            acc4.w += r[k].w;
+          }
+      }
+    } else {
+      for (int i = 0; i < cnt; ++i) {
+        const unsigned u = __shfl_sync(0xffffffffu, myu, i);
+        const float* row = dH + (size_t)u * G3S;
+#pragma unroll
+        for (int q = 0; q < kRedPerLane; ++q)
+          if (lane + 32 * q < G3S) acc[q] += row[lane + 32 * q];
+      }
+    }
+  }
+  if (vec) {
+    reinterpret_cast<float4*>(s_part + w * G3S)[lane] = acc4;
+  } else {
+#pragma unroll
+    for (int q = 0; q < kRedPerLane; ++q)
+      if (lane + 32 * q < G3S) s_part[w * G3S + lane + 32 * q] = acc[q];
+  }
+}
+
+// dG2[:, i2] = sum of the group's chunk partials in chunk order; one thread
+// per 4 consecutive slice elements (float4), kBlock*4 elements per block.
+__device__ inline void dg2_part(KGeom g, int C, int G2S, int cmax, int ch, unsigned i2, int q,
+                                const float* __restrict__ part, const int* __restrict__ grp_cnt,
+                                const int* __restrict__ err, float* __restrict__ grad, float* __restrict__ param,
+                                double* __restrict__ vel, double lr, double mu, int do_update) {
+  const int nch = (grp_cnt[i2] + ch - 1) / ch;
   const bool upd = do_update && ((*err & 8) == 0);
-  for (int e = threadIdx.x; e < G1S; e += kBlock) {
+  const int e0 = (q * kBlock + threadIdx.x) * 4;
+  if (e0 >= G2S) return;
+  const float* base = part + (size_t)i2 * cmax * G2S;
+  if (G2S % 4 == 0 && C % 4 == 0) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int c = 0;
+    for (; c + 4 <= nch; c += 4) {
+      float4 v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = __ldcg(reinterpret_cast<const float4*>(base + (size_t)(c + k) * G2S + e0));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        acc.x += v[k].x;
+        acc.y += v[k].y;
+        acc.z += v[k].z;
+        acc.w += v[k].w;
+      }
+    }
+    for (; c < nch; ++c) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(base + (size_t)c * G2S + e0));
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    const int r = e0 / C, cc = e0 - r * C;
+    const size_t gi = ((size_t)r * g.m2 + i2) * C + cc;
+    const float a[4] = {acc.x, acc.y, acc.z, acc.w};
+    if (grad) *reinterpret_cast<float4*>(grad + gi) = acc;
+    if (upd) {
+      float4 p = *reinterpret_cast<const float4*>(param + gi);
+      float* pp = &p.x;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) pp[k] = sgd_apply(pp[k], a[k], vel ? vel + gi + k : nullptr, lr, mu);
+      *reinterpret_cast<float4*>(param + gi) = p;
+    }
+  } else {
+    for (int e = e0; e < e0 + 4 && e < G2S; ++e) {
+      float acc = 0.f;
+      for (int c = 0; c < nch; ++c) acc += base[(size_t)c * G2S + e];
+      const int r = e / C, cc = e - r * C;
+      const size_t gi = ((size_t)r * g.m2 + i2) * C + cc;
+      if (grad) grad[gi] = acc;
+      if (upd) param[gi] = sgd_apply(param[gi], acc, vel ? vel + gi : nullptr, lr, mu);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_dg13_reduce(KGeom g, int G1S, int N3, int G3S, unsigned* __restrict__ pmap,
+                                                        const int* __restrict__ pslot, const float* __restrict__ E,
+                                                        const int* __restrict__ i3_start,
+                                                        const unsigned* __restrict__ v3, const float* __restrict__ dH,
+                                                        const int* __restrict__ err, float* __restrict__ grad0,
+                                                        float* __restrict__ param0, double* __restrict__ vel0,
+                                                        int upd0, float* __restrict__ grad2,
+                                                        float* __restrict__ param2, double* __restrict__ vel2,
+                                                        int upd2, double lr, double mu, int C, int G2S, int cmax,
+                                                        int ch, const float* __restrict__ part,
+                                                        const int* __restrict__ grp_cnt, float* __restrict__ grad1,
+                                                        float* __restrict__ param1, double* __restrict__ vel1,
+                                                        int upd1) {
+  extern __shared__ __align__(16) float s_part[];  // kRedWarps x max(G1S, G3S)
+  if (blockIdx.x >= g.m1 + g.m3) {
+    const int qpb = (G2S + 4 * kBlock - 1) / (4 * kBlock);
+    const int k = blockIdx.x - (g.m1 + g.m3);
+    dg2_part(g, C, G2S, cmax, ch, (unsigned)(k / qpb), k % qpb, part, grp_cnt, err, grad1, param1, vel1, lr, mu,
+             upd1);
+    return;
+  }
+  const bool is1 = blockIdx.x < g.m1;
+  const int G = is1 ? G1S : G3S;
+  if (is1) dg1_block(g, G1S, blockIdx.x, pmap, pslot, E, s_part);
+  else dg3_block(G3S, blockIdx.x - g.m1, i3_start, v3, dH, s_part);
+  __syncthreads();
+  const bool ok = (*err & 8) == 0;
+  const unsigned v = blockIdx.x - g.m1;
+  const unsigned m3n3 = g.m3 * (unsigned)N3;
+  for (int e = threadIdx.x; e < G; e += kBlock) {
     float acc = 0.f;
 #pragma unroll
-    for (int ww = 0; ww < kRedWarps; ++ww) acc += s_part[ww * G1S + e];
-    const size_t gi = (size_t)i1 * G1S + e;
-    if (grad) grad[gi] = acc;
-    if (upd) param[gi] = sgd_apply(param[gi], acc, vel ? vel + gi : nullptr, lr, mu);
+    for (int ww = 0; ww < kRedWarps; ++ww) acc += s_part[ww * G + e];
+    if (is1) {
+      const size_t gi = (size_t)blockIdx.x * G1S + e;
+      if (grad0) grad0[gi] = acc;
+      if (upd0 && ok) param0[gi] = sgd_apply(param0[gi], acc, vel0 ? vel0 + gi : nullptr, lr, mu);
+    } else {
+      const int r = e / N3, j = e - r * N3;
+      const size_t gi = (size_t)r * m3n3 + v * N3 + j;
+      if (grad2) grad2[gi] = acc;
+      if (upd2 && ok) param2[gi] = sgd_apply(param2[gi], acc, vel2 ? vel2 + gi : nullptr, lr, mu);
+    }
   }
 }
 
@@ -184,12 +330,26 @@ static size_t prefix_smem(const D& d, int ch) {
 }
 template <class D>
 static size_t close_smem(const D& d) {
-  return sizeof(float) * (kBlock / 32) * ((size_t)dX(d) * (d.r2 + 1) + dG3s(d) + dN(d));
+  size_t per = (size_t)close_warp_floats(d);
+  if (kFastRows<D>) per = per > (size_t)(dX(d) + 4) * 36 ? per : (size_t)(dX(d) + 4) * 36;
+  return sizeof(float) * (kBlock / 32) * per;
 }
 template <class D>
 static size_t bwd_smem(const D& d, int ch) {
   const size_t M = (size_t)ch * d.n1, LZ = pad_ld(d);
-  return sizeof(float) * (M * LZ + (size_t)d.r1 * LZ + M * d.r1 + (kBlock / 32) * ((size_t)dN(d) + dG3s(d) + dSlot(d)));
+  const size_t per_warp = kFastRows<D> ? 2 * (size_t)dN(d) : (size_t)dN(d) + dG3s(d) + dSlot(d);
+  return sizeof(float) * (M * LZ + (size_t)d.r1 * LZ + M * d.r1 + (kBlock / 32) * per_warp);
+}
+
+// cudaFuncSetAttribute once per (kernel, size): it is a host-side call that
+// would otherwise sit on every launch path.
+template <class K>
+static cudaError_t ensure_smem(K kernel, size_t bytes) {
+  static size_t done = 0;
+  if (bytes <= done || bytes <= 48 * 1024) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done = bytes;
+  return e;
 }
 
 template <class D>
@@ -199,15 +359,14 @@ static cudaError_t forward_impl(ttb_handle* h, const float* c0, const float* c1,
   Workspace& w = h->w;
   cudaError_t e;
   const size_t sm1 = prefix_smem(d, h->chf);
-  if ((e = cudaFuncSetAttribute(k_prefix_products<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1)))
-    return e;
+  if ((e = ensure_smem(k_prefix_products<D>, sm1))) return e;
   dim3 g1(h->kg.m2, (unsigned)h->cmaxf);
   { ProfScope _ps(h, s, "prefix_products");
   k_prefix_products<D><<<g1, kBlock, sm1, s>>>(d, h->kg, h->chf, c0, c1, w.pmap, w.pslot, w.slots);
   }
   count_launch();
   const size_t sm2 = close_smem(d);
-  if ((e = cudaFuncSetAttribute(k_close_pool<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2))) return e;
+  if ((e = ensure_smem(k_close_pool<D>, sm2))) return e;
   const int B = (int)h->B;
   int grid = (B + kBlock / 32 - 1) / (kBlock / 32);
   if (grid > 148 * 32) grid = 148 * 32;
@@ -225,26 +384,24 @@ static cudaError_t aggregate_impl(ttb_handle* h, const float* gout, cudaStream_t
   Workspace& w = h->w;
   const int T = (int)h->T;
   cudaError_t e;
+  if (!h->bwd_zeroed && (e = cudaMemsetAsync(w.zeroB, 0, w.zeroB_bytes, s))) return e;
+  h->bwd_zeroed = 0;
   // 1. order the indices by row (stable: equal rows keep index order)
   unsigned *sk, *sv;
   if ((e = launch_sort(h, w.keys32, nullptr, w.skA, w.svA, w.skB, w.svB, nullptr, T, h->idx_bits, 0, &sk, &sv, s)))
     return e;
   // 2. row / prefix runs
-  if ((e = cudaMemsetAsync(w.scan_status + kScanRuns * h->scan_tiles, 0,
-                           sizeof(unsigned long long) * h->scan_tiles, s)))
-    return e;
-  if ((e = cudaMemsetAsync(w.scan_ctr + kScanRuns, 0, sizeof(unsigned), s))) return e;
   const int tiles = (T + kTile - 1) / kTile;
   { ProfScope _ps(h, s, "runs");
   k_runs<<<tiles, kBlock, 0, s>>>(sk, T, h->kg, w.pslot, w.urow, w.urow_start, w.urow_i3, w.prow_begin, w.prow_end,
-                                  w.counts, w.scan_status + kScanRuns * h->scan_tiles, w.scan_ctr + kScanRuns);
+                                  w.counts, w.runs_status, w.runs_ctr);
   }
   count_launch();
   // 3. aggregated row gradients
   int grid = (T + kBlock / 32 - 1) / (kBlock / 32);
   if (grid > 148 * 16) grid = 148 * 16;
   { ProfScope _ps(h, s, "row_agg");
-  k_row_agg<D><<<grid, kBlock, 0, s>>>(d, w.counts, w.urow_start, sv, w.bag_of, gout, w.gU, w.err);
+  k_row_agg<D><<<grid, kBlock, 0, s>>>(d, (int)h->B, w.counts, w.urow_start, sv, w.bag_of, gout, w.gU, w.err);
   }
   count_launch();
   return cudaGetLastError();
@@ -261,7 +418,7 @@ static cudaError_t backward_impl(ttb_handle* h, const float* c0, const float* c1
   if ((e = aggregate_impl<D>(h, gout, s))) return e;
   // 4. per-prefix contractions, grouped by i2
   const size_t sm = bwd_smem(d, h->chb);
-  if ((e = cudaFuncSetAttribute(k_bwd_prefix<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm))) return e;
+  if ((e = ensure_smem(k_bwd_prefix<D>, sm))) return e;
   dim3 gp(h->kg.m2, (unsigned)h->cmaxb);
   { ProfScope _ps(h, s, "bwd_prefix");
   k_bwd_prefix<D><<<gp, kBlock, sm, s>>>(d, h->kg, h->chb, c0, c1, c2, w.pmap, w.pslot, w.slots, w.prow_begin, w.prow_end,
@@ -280,20 +437,16 @@ static cudaError_t backward_impl(ttb_handle* h, const float* c0, const float* c1
   count_launch();
   const bool upd = mode == 1;
   // 6. reductions (+ fused update)
-  { ProfScope _ps(h, s, "dg1_reduce");
-  k_dg1_reduce<<<h->kg.m1, kBlock, sizeof(float) * kRedWarps * dG1s(d), s>>>(h->kg, dG1s(d), w.pmap, w.pslot, w.E, w.err,
-                                           upd ? nullptr : g0, p0, v0, lr, mu, upd && (mask & 1));
+  {
+    ProfScope _ps(h, s, "dg123_reduce");
+    const size_t smr = sizeof(float) * kRedWarps * (dG1s(d) > dG3s(d) ? dG1s(d) : dG3s(d));
+    const int qpb = (dG2s(d) + 4 * kBlock - 1) / (4 * kBlock);
+    k_dg13_reduce<<<h->kg.m1 + h->kg.m3 + h->kg.m2 * qpb, kBlock, smr, s>>>(
+        h->kg, dG1s(d), d.n3, dG3s(d), w.pmap, w.pslot, w.E, w.i3_start, v3, w.dH, w.err, upd ? nullptr : g0, p0, v0,
+        upd && (mask & 1), upd ? nullptr : g2, p2, v2, upd && (mask & 4), lr, mu, dC(d), dG2s(d), h->cmaxb, h->chb,
+        w.dG2part, w.grp_cnt, upd ? nullptr : g1, p1, v1, upd && (mask & 2));
   }
-  { ProfScope _ps(h, s, "dg2_reduce");
-  k_dg2_reduce<<<dim3(h->kg.m2, (dG2s(d) + kBlock - 1) / kBlock), kBlock, 0, s>>>(h->kg, dC(d), dG2s(d), h->cmaxb, h->chb, w.dG2part,
-                                           w.grp_cnt, w.err, upd ? nullptr : g1, p1, v1, lr, mu,
-                                           upd && (mask & 2));
-  }
-  { ProfScope _ps(h, s, "dg3_reduce");
-  k_dg3_reduce<<<h->kg.m3, kBlock, sizeof(float) * kRedWarps * dG3s(d), s>>>(h->kg, d.n3, dG3s(d), w.i3_start, v3, w.dH, w.err,
-                                           upd ? nullptr : g2, p2, v2, lr, mu, upd && (mask & 4));
-  }
-  count_launch(3);
+  count_launch(1);
   return cudaGetLastError();
 }
 
@@ -307,7 +460,8 @@ static cudaError_t backward_impl(ttb_handle* h, const float* c0, const float* c1
   X(4, 4, 8, 32, 32)
 
 template <class F>
-static cudaError_t dispatch(const DynDims& d, F&& f) {
+static cudaError_t dispatch(const DynDims& d, bool aligned, F&& f) {
+  if (!aligned) return f(d);
 #define TTB_TRY(A_, B_, C_, R1_, R2_) \
   if (d.n1 == A_ && d.n2 == B_ && d.n3 == C_ && d.r1 == R1_ && d.r2 == R2_) return f(FixDims<A_, B_, C_, R1_, R2_>{});
   TTB_FOR_SHAPES(TTB_TRY)
@@ -317,17 +471,21 @@ static cudaError_t dispatch(const DynDims& d, F&& f) {
 
 cudaError_t launch_forward(ttb_handle* h, const float* c0, const float* c1, const float* c2, float* out,
                            cudaStream_t s) {
-  return dispatch(h->dims, [&](auto d) { return forward_impl<decltype(d)>(h, c0, c1, c2, out, s); });
+  const bool al = (((uintptr_t)c0 | (uintptr_t)c1 | (uintptr_t)c2 | (uintptr_t)out) & 15) == 0;
+  return dispatch(h->dims, al, [&](auto d) { return forward_impl<decltype(d)>(h, c0, c1, c2, out, s); });
 }
 
 cudaError_t launch_aggregate(ttb_handle* h, const float* gout, cudaStream_t s) {
-  return dispatch(h->dims, [&](auto d) { return aggregate_impl<decltype(d)>(h, gout, s); });
+  const bool al = ((uintptr_t)gout & 15) == 0;
+  return dispatch(h->dims, al, [&](auto d) { return aggregate_impl<decltype(d)>(h, gout, s); });
 }
 
 cudaError_t launch_backward(ttb_handle* h, const float* c0, const float* c1, const float* c2, const float* gout,
                             float* g0, float* g1, float* g2, float* p0, float* p1, float* p2, double* v0, double* v1,
                             double* v2, double lr, double mu, int mask, int mode, cudaStream_t s) {
-  return dispatch(h->dims, [&](auto d) {
+  const bool al = (((uintptr_t)c0 | (uintptr_t)c1 | (uintptr_t)c2 | (uintptr_t)gout | (uintptr_t)g0 | (uintptr_t)g1 |
+                     (uintptr_t)g2 | (uintptr_t)p0 | (uintptr_t)p1 | (uintptr_t)p2) & 15) == 0;
+  return dispatch(h->dims, al, [&](auto d) {
     return backward_impl<decltype(d)>(h, c0, c1, c2, gout, g0, g1, g2, p0, p1, p2, v0, v1, v2, lr, mu, mask, mode,
                                       s);
   });
@@ -405,7 +563,6 @@ bool choose_chunks(const DynDims& d, int* chf, int* chb) {
     if (!*chf && prefix_smem(d, c) <= cap) *chf = c;
   for (int c : {16, 8})
     if (!*chb && bwd_smem(d, c) <= cap) *chb = c;
-  return *chf && *chb && close_smem(d) <= cap && sizeof(float) * kRedWarps * (size_t)dG1s(d) <= 48 * 1024 &&
-         sizeof(float) * kRedWarps * (size_t)dG3s(d) <= 48 * 1024;
+  return *chf && *chb && close_smem(d) <= cap && dG1s(d) <= 32 * kRedPerLane && dG3s(d) <= 32 * kRedPerLane;
 }
 }  // namespace ttb

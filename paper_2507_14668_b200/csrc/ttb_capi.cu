@@ -53,14 +53,32 @@ void layout(ttb_handle& h, char* base) {
   h.Pmax = T < m1m2 ? T : m1m2;
   h.cmaxf = (int)((g.m[0] + h.chf - 1) / h.chf);
   h.cmaxb = (int)((g.m[0] + h.chb - 1) / h.chb);
-  h.sort_tiles = (T + kTile - 1) / kTile + 1;
+  h.sort_tiles = (T + kSortTile - 1) / kSortTile + 1;
   int64_t st = (T + kTile - 1) / kTile;
   const int64_t bt = (B + 31) / 32;
   h.scan_tiles = (st > bt ? st : bt) + 1;
   Carver c{base};
   Workspace& w = h.w;
+  // zero block A
+  size_t a0 = c.off;
   w.err = c.take<int>(16);
-  w.counts = w.err ? w.err + 0 : nullptr;  // counts share the header block; index 1.. used
+  w.counts = w.err;  // [0] err bits, [1] P, [2] S, [3] U
+  w.scan_ctr = c.take<unsigned>(16);
+  w.scan_status = c.take<unsigned long long>((size_t)kNumScans * h.scan_tiles);
+  c.off = (c.off + 255) & ~(size_t)255;
+  w.zeroA = base ? base + a0 : nullptr;
+  w.zeroA_bytes = c.off - a0;
+  // zero block B
+  size_t b0 = c.off;
+  w.runs_ctr = c.take<unsigned>(16);
+  w.runs_status = c.take<unsigned long long>(h.scan_tiles);
+  w.sort_ctr = c.take<unsigned>(8);
+  w.sort_hist = c.take<unsigned>(2 * 4 * 256);
+  w.sort_status = c.take<unsigned>((size_t)2 * 4 * h.sort_tiles * 256);
+  c.off = (c.off + 255) & ~(size_t)255;
+  w.zeroB = base ? base + b0 : nullptr;
+  w.zeroB_bytes = c.off - b0;
+  w.grp_done = c.take<int>(g.m[1]);
   w.pmap = c.take<unsigned>(m1m2);
   w.pslot = c.take<int>(m1m2);
   w.work_key = c.take<unsigned>(h.Pmax);
@@ -78,9 +96,6 @@ void layout(ttb_handle& h, char* base) {
   w.svA = c.take<unsigned>(T);
   w.skB = c.take<unsigned>(T);
   w.svB = c.take<unsigned>(T);
-  w.sort_hist = c.take<unsigned>(2 * 4 * 256);
-  w.sort_status = c.take<unsigned>((size_t)2 * 4 * h.sort_tiles * 256);
-  w.sort_ctr = c.take<unsigned>(8);
   w.urow = c.take<unsigned>(T + 1);
   w.urow_start = c.take<int>(T + 1);
   w.urow_i3 = c.take<unsigned>(T);
@@ -97,8 +112,6 @@ void layout(ttb_handle& h, char* base) {
   w.rkB = c.take<unsigned>(T);
   w.rvB = c.take<unsigned>(T);
   w.uid_first = c.take<int>(T);
-  w.scan_status = c.take<unsigned long long>((size_t)kNumScans * h.scan_tiles);
-  w.scan_ctr = c.take<unsigned>(16);
   w.scratch1 = c.take<float>(16);
   h.bytes = c.off + 256;
 }
@@ -165,8 +178,10 @@ ttb_handle* ttb_create(const ttb_geom* g, int64_t max_T, int64_t max_B, void* wo
   char* base = (char*)(((uintptr_t)workspace + 255) & ~(uintptr_t)255);
   layout(*h, base);
   h->base = base;
+  h->pmap_clean = 1;
   cudaStream_t s = (cudaStream_t)stream;
-  if (cudaMemsetAsync(h->w.err, 0, sizeof(int) * 16, s) != cudaSuccess ||
+  if (cudaMemsetAsync(h->w.zeroA, 0, h->w.zeroA_bytes + h->w.zeroB_bytes, s) != cudaSuccess ||
+      cudaMemsetAsync(h->w.grp_done, 0, sizeof(int) * h->kg.m2, s) != cudaSuccess ||
       cudaMemsetAsync(h->w.pmap, 0xFF, sizeof(unsigned) * h->kg.m1m2, s) != cudaSuccess) {
     free(h);
     return nullptr;
@@ -195,7 +210,7 @@ int ttb_plan(ttb_handle* h, const void* indices, int idx_is_64, const int64_t* o
 
 int ttb_forward(ttb_handle* h, const float* c0, const float* c1, const float* c2, float* out, ttb_stream stream) {
   if (!h || !c0 || !c1 || !c2 || !out) return TTB_EINVAL;
-  if (!h->planned) return TTB_ESTATE;
+  if (!h->planned || h->pmap_clean) return TTB_ESTATE;  // a backward consumed this plan's prefix table
   cudaError_t e = launch_forward(h, c0, c1, c2, out, (cudaStream_t)stream);
   if (e != cudaSuccess) return TTB_ECUDA;
   h->forwarded = 1;
@@ -210,6 +225,7 @@ int ttb_backward(ttb_handle* h, const float* c0, const float* c1, const float* c
                                   nullptr, 0.0, 0.0, 0, 0, (cudaStream_t)stream);
   if (e != cudaSuccess) return TTB_ECUDA;
   h->backwarded = 1;
+  h->pmap_clean = 1;
   return TTB_OK;
 }
 
@@ -234,6 +250,7 @@ int ttb_backward_sgd(ttb_handle* h, float* c0, float* c1, float* c2, const float
                                   momentum, update_mask, 1, (cudaStream_t)stream);
   if (e != cudaSuccess) return TTB_ECUDA;
   h->backwarded = 1;
+  h->pmap_clean = 1;
   return TTB_OK;
 }
 

@@ -7,8 +7,10 @@ namespace ttb {
 
 constexpr unsigned kEmpty = 0xFFFFFFFFu;
 constexpr int kBlock = 256;  // threads per CTA for the streaming kernels
-constexpr int kItems = 8;    // items per thread for the scan / sort tiles
+constexpr int kItems = 2;    // items per thread for the scan tiles (many small tiles: latency)
 constexpr int kTile = kBlock * kItems;
+constexpr int kSortItems = 4;  // items per thread for the radix-sort tiles
+constexpr int kSortTile = kBlock * kSortItems;
 
 // Geometry as the kernels see it (d = 3; d = 2 tables arrive embedded).
 struct KGeom {
@@ -53,42 +55,55 @@ constexpr unsigned long long kFlagAgg = 1ull << 62;
 constexpr unsigned long long kFlagInc = 2ull << 62;
 constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+// The look-back status words carry their own payload (flag + count), so
+// relaxed gpu-scope accesses are sufficient; acquire loads would invalidate
+// L1 (CCTL.IVALL) on every probe of the spin loop.
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
   unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
   unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_u32(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // Called by ONE thread of the tile. Returns the exclusive prefix of `agg`
 // over all earlier tiles and publishes this tile's inclusive prefix.
 __device__ inline long long lookback_exclusive(unsigned long long* status, int tile, long long agg) {
   if (tile == 0) {
-    st_release_u64(&status[0], kFlagInc | (unsigned long long)agg);
+    st_relaxed_u64(&status[0], kFlagInc | (unsigned long long)agg);
     return 0;
   }
-  st_release_u64(&status[tile], kFlagAgg | (unsigned long long)agg);
+  st_relaxed_u64(&status[tile], kFlagAgg | (unsigned long long)agg);
   long long excl = 0;
   int j = tile - 1;
-  while (true) {
-    unsigned long long s = ld_acquire_u64(&status[j]);
-    unsigned long long f = s & ~kValMask;
-    if (f == 0) continue;
-    excl += (long long)(s & kValMask);
-    if (f == kFlagInc) break;
-    --j;
+  while (j >= 0) {  // windowed: 8 predecessors per round trip
+    unsigned long long sv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sv[i] = (j - i >= 0) ? ld_relaxed_u64(&status[j - i]) : 0ull;
+    bool done = false;
+    int used = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (done || used < i || j - i < 0) continue;
+      const unsigned long long f = sv[i] & ~kValMask;
+      if (f == 0) continue;
+      excl += (long long)(sv[i] & kValMask);
+      used = i + 1;
+      if (f == kFlagInc) done = true;
+    }
+    if (done) break;
+    j -= used;
   }
-  st_release_u64(&status[tile], kFlagInc | (unsigned long long)(excl + agg));
+  st_relaxed_u64(&status[tile], kFlagInc | (unsigned long long)(excl + agg));
   return excl;
 }
 
@@ -114,8 +129,8 @@ __device__ inline void tile_flag_scan(const bool (&f)[kItems], int (&rank)[kItem
                                       unsigned long long* status, int tile, int* s_tmp,
                                       long long* incl_out) {
   constexpr int NW = kBlock / 32;
-  constexpr int NV = kItems * NW;  // 64 values, in (k, warp) order
-  static_assert(NV % 32 == 0, "scan layout");
+  constexpr int NV = kItems * NW;  // values in (k, warp) order
+  static_assert(NV % 32 == 0 || NV < 32, "scan layout");
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned lt = lanemask_lt();
   int within[kItems];
@@ -127,12 +142,12 @@ __device__ inline void tile_flag_scan(const bool (&f)[kItems], int (&rank)[kItem
   }
   __syncthreads();
   if (w == 0) {
-    constexpr int PER = NV / 32;
+    constexpr int PER = NV >= 32 ? NV / 32 : 1;
     int v[PER];
     int sum = 0;
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
-      v[i] = s_tmp[lane * PER + i];
+      v[i] = (lane * PER + i < NV) ? s_tmp[lane * PER + i] : 0;
       sum += v[i];
     }
     int incl = sum;
@@ -144,7 +159,7 @@ __device__ inline void tile_flag_scan(const bool (&f)[kItems], int (&rank)[kItem
     int run = incl - sum;
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
-      s_tmp[lane * PER + i] = run;
+      if (lane * PER + i < NV) s_tmp[lane * PER + i] = run;
       run += v[i];
     }
     int total = __shfl_sync(0xffffffffu, incl, 31);

@@ -49,13 +49,23 @@ struct Workspace {
   int* grp_cnt;     // m2: present prefixes per i2
   unsigned *rkA, *rvA, *rkB, *rvB;  // rows-by-i3 sort buffers
   int* uid_first;   // T: first-occurrence rank flags / scratch
-  // look-back scan state, one region per scan kernel
-  unsigned long long* scan_status;  // kNumScans x scan_tiles
+  // look-back scan state. Zero block A (cleared by every plan) holds the
+  // error word / counts and the plan-scope scans; zero block B (cleared by
+  // the plan, and again if a second backward reuses the plan) holds the
+  // backward-scope scan and radix-sort state. A and B are contiguous.
+  char* zeroA;
+  size_t zeroA_bytes;
+  char* zeroB;
+  size_t zeroB_bytes;
+  unsigned long long* scan_status;  // kNumScans x scan_tiles (runs region lives in B)
   unsigned* scan_ctr;               // kNumScans counters
+  unsigned long long* runs_status;  // scan_tiles
+  unsigned* runs_ctr;
+  int* grp_done;                    // m2: finished chunk CTAs per i2 group (self-resetting)
   float* scratch1;                  // 1-float sink for the unit core of d = 2 tables
 };
 
-enum ScanId { kScanSlots = 0, kScanSegs = 1, kScanRuns = 2, kScanFirst = 3, kNumScans = 4 };
+enum ScanId { kScanSlots = 0, kScanSegs = 1, kScanFirst = 2, kNumScans = 3 };
 
 }  // namespace ttb
 
@@ -89,6 +99,8 @@ struct ttb_handle {
   // host-side state of the current plan
   int64_t T, B;
   int planned, forwarded, backwarded;
+  int pmap_clean;   // prefix table already reset (by the last backward)
+  int bwd_zeroed;   // zero block B is clear for the next backward
   int64_t gen;
   ttb::Profiler prof;
 };

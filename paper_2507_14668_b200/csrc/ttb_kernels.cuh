@@ -11,6 +11,17 @@ constexpr int kMaxChunk = 64;
 
 template <class D> struct IsFixed : std::false_type {};
 template <int A, int B, int C, int E, int F> struct IsFixed<FixDims<A, B, C, E, F>> : std::true_type {};
+// compile-time dims (zeros for run-time dims)
+template <class D> struct FixT { static constexpr int n1 = 0, n2 = 0, n3 = 0, r1 = 0, r2 = 0; };
+template <int A, int B, int C, int E, int F> struct FixT<FixDims<A, B, C, E, F>> {
+  static constexpr int n1 = A, n2 = B, n3 = C, r1 = E, r2 = F;
+};
+// warp-per-prefix backward fast path: lane <-> r2, float4 G3 slices
+template <class D> constexpr bool kFastRows = FixT<D>::r2 == 32 && FixT<D>::n3 == 4 &&
+                                              FixT<D>::n1 * FixT<D>::n2 * 4 <= 128;
+// vectorised operand staging: row lengths multiple of 4 floats
+template <class D> constexpr bool kVecStage = FixT<D>::r1 % 4 == 0 && FixT<D>::r1 > 0 &&
+                                              (FixT<D>::n2 * FixT<D>::r2) % 4 == 0;
 // slot size n1 n2 r2 as a compile-time constant (1 for run-time dims)
 template <class D> struct FixSlot { static constexpr int value = 1; };
 template <int A, int B, int C, int E, int F> struct FixSlot<FixDims<A, B, C, E, F>> {
@@ -84,12 +95,33 @@ __device__ __forceinline__ void lds_vec(float (&r)[V], const float* p) {
 // C[m][n] = sum_k At[k*lda + m] * B[k*ldb + n]   (both operands k-major in smem)
 // Thread tiles TM x TN, handed out n-fastest so a warp's B loads are one
 // contiguous run and its A loads broadcast. M % TM == 0, N % TN == 0.
+// A TM or TN of 8 is split into two float4 groups half the extent apart
+// (rows m0.., m0 + M/2..), which keeps a warp's 16-byte loads contiguous and
+// bank-conflict free; out() receives the row / column of each element.
+template <int V>
+__device__ __forceinline__ int split_index(int base, int half, int i) {
+  if constexpr (V == 8) return base + (i < 4 ? i : half + i - 4);
+  else return base + i;
+}
+template <int V>
+__device__ __forceinline__ void lds_split(float (&r)[V], const float* p, int half) {
+  if constexpr (V == 8) {
+    const float4 u = *reinterpret_cast<const float4*>(p);
+    const float4 v = *reinterpret_cast<const float4*>(p + half);
+    r[0] = u.x; r[1] = u.y; r[2] = u.z; r[3] = u.w;
+    r[4] = v.x; r[5] = v.y; r[6] = v.z; r[7] = v.w;
+  } else {
+    lds_vec<V>(r, p);
+  }
+}
+
 template <int TM, int TN, class Out>
 __device__ __forceinline__ void gemm_kk(int M, int N, int K, const float* At, int lda, const float* B, int ldb,
                                         Out&& out) {
   const int tn = N / TN, tiles = (M / TM) * tn;
+  const int hm = M / 2, hn = N / 2;
   for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
-    const int m0 = (t / tn) * TM, n0 = (t % tn) * TN;
+    const int m0 = (t / tn) * (TM == 8 ? 4 : TM), n0 = (t % tn) * (TN == 8 ? 4 : TN);
     float acc[TM][TN];
 #pragma unroll
     for (int i = 0; i < TM; ++i)
@@ -98,14 +130,14 @@ __device__ __forceinline__ void gemm_kk(int M, int N, int K, const float* At, in
 #pragma unroll 4
     for (int k = 0; k < K; ++k) {
       float a[TM], b[TN];
-      lds_vec<TM>(a, At + k * lda + m0);
-      lds_vec<TN>(b, B + k * ldb + n0);
+      lds_split<TM>(a, At + k * lda + m0, hm);
+      lds_split<TN>(b, B + k * ldb + n0, hn);
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
     }
-    out(m0, n0, acc);
+    out(m0, n0, hm, hn, acc);
   }
 }
 
@@ -190,40 +222,111 @@ __global__ void __launch_bounds__(kBlock) k_prefix_products(D d, KGeom g, int ch
   const int M = ch * N1;   // padded rows (prefix, a)
   float* s_g2 = smem;      // R1 x C   (k-major: [r1][c])
   float* s_g1t = smem + R1 * C;  // R1 x M (k-major: [r1][p*N1 + a])
-  for (int e = threadIdx.x; e < R1 * C; e += kBlock) {
-    const int r = e / C, c = e - r * C;
-    s_g2[e] = G2[((size_t)r * g.m2 + i2) * C + c];
-  }
-  for (int e = threadIdx.x; e < M * R1; e += kBlock) {
-    const int row = e / R1, r = e - row * R1;
-    const int p = row / N1, a = row - p * N1;
-    s_g1t[r * M + row] = p < np ? G1[((size_t)s_free[p] * N1 + a) * R1 + r] : 0.f;
+  if constexpr (kVecStage<D>) {
+    constexpr int C4 = FixT<D>::n2 * FixT<D>::r2 / 4, R1c = FixT<D>::r1, N1c = FixT<D>::n1;
+#pragma unroll 4
+    for (int e = threadIdx.x; e < R1c * C4; e += kBlock) {
+      const int r = e / C4, c4 = e - r * C4;
+      reinterpret_cast<float4*>(s_g2)[e] =
+          __ldg(reinterpret_cast<const float4*>(G2 + ((size_t)r * g.m2 + i2) * C) + c4);
+    }
+    constexpr int RQ = R1c / 4;  // float4 per G1 row
+#pragma unroll 4
+    for (int e = threadIdx.x; e < M * RQ; e += kBlock) {
+      const int row = e / RQ, q = e - row * RQ;
+      const int p = row / N1c, a = row - p * N1c;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (p < np) v = __ldg(reinterpret_cast<const float4*>(G1 + ((size_t)s_free[p] * N1c + a) * R1c) + q);
+      s_g1t[(4 * q + 0) * M + row] = v.x;
+      s_g1t[(4 * q + 1) * M + row] = v.y;
+      s_g1t[(4 * q + 2) * M + row] = v.z;
+      s_g1t[(4 * q + 3) * M + row] = v.w;
+    }
+  } else {
+    for (int e = threadIdx.x; e < R1 * C; e += kBlock) {
+      const int r = e / C, c = e - r * C;
+      s_g2[e] = G2[((size_t)r * g.m2 + i2) * C + c];
+    }
+    for (int e = threadIdx.x; e < M * R1; e += kBlock) {
+      const int row = e / R1, r = e - row * R1;
+      const int p = row / N1, a = row - p * N1;
+      s_g1t[r * M + row] = p < np ? G1[((size_t)s_free[p] * N1 + a) * R1 + r] : 0.f;
+    }
   }
   __syncthreads();
   using Tl = Tiles<D>;
   const int SL = dSlot(d);
-  gemm_kk<Tl::FM, Tl::FN>(M, C, R1, s_g1t, M, s_g2, C, [&](int m0, int n0, float (&acc)[Tl::FM][Tl::FN]) {
+  gemm_kk<Tl::FM, Tl::FN>(M, C, R1, s_g1t, M, s_g2, C,
+                          [&](int m0, int n0, int hm, int hn, float (&acc)[Tl::FM][Tl::FN]) {
 #pragma unroll
     for (int i = 0; i < Tl::FM; ++i) {
-      const int row = m0 + i, p = row / N1, a = row - p * N1;
+      const int row = split_index<Tl::FM>(m0, hm, i), p = row / N1, a = row - p * N1;
       if (p >= np) continue;
-      float* dst = slots + (size_t)s_slot[p] * SL + a * C + n0;
+      float* dst = slots + (size_t)s_slot[p] * SL + a * C;
       if constexpr (Tl::FN % 4 == 0) {
 #pragma unroll
         for (int j = 0; j < Tl::FN; j += 4)
-          *reinterpret_cast<float4*>(dst + j) = make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+          *reinterpret_cast<float4*>(dst + split_index<Tl::FN>(n0, hn, j)) =
+              make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
       } else {
 #pragma unroll
-        for (int j = 0; j < Tl::FN; ++j) dst[j] = acc[i][j];
+        for (int j = 0; j < Tl::FN; ++j) dst[n0 + j] = acc[i][j];
       }
     }
   });
 }
 
 // ------------------------------------------------------------ K3: close + pool
-// One warp per bag: for each segment (distinct prefix, ascending slot) sum the
-// G3 slices of its indices in index order, multiply by the slot, and add the
+// For each segment (distinct prefix of a bag, ascending slot) sum the G3
+// slices of its indices in index order, multiply by the slot, and add the
 // result to the bag in segment order. Reference: lookup.py:280-293.
+template <class D>
+__device__ __forceinline__ void close_bag_generic(const D& d, KGeom g, const float* __restrict__ G3,
+                                                  const float* __restrict__ slots, int b, int o0, int o1, int sg0,
+                                                  int sg1, const int* __restrict__ seg_slot,
+                                                  const int* __restrict__ occ_slot,
+                                                  const unsigned* __restrict__ keys32, float* s_sb, float* s_h,
+                                                  float* s_o, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int X = dX(d), R2 = d.r2, N3 = d.n3, N = dN(d), SL = dSlot(d), G3S = dG3s(d);
+  const int RS = R2 + 1;
+  const unsigned m3n3 = g.m3 * (unsigned)N3;
+  for (int o = lane; o < N; o += 32) s_o[o] = 0.f;
+  for (int sg = sg0; sg < sg1; ++sg) {
+    const int slot = seg_slot[sg];
+    for (int e = lane; e < G3S; e += 32) s_h[e] = 0.f;
+    for (int t = o0; t < o1; ++t) {
+      if (occ_slot[t] != slot) continue;
+      const unsigned i3 = keys32[t] % g.m3;
+      for (int e = lane; e < G3S; e += 32) {
+        const int r = e / N3, j = e - r * N3;
+        s_h[e] += __ldg(&G3[(size_t)r * m3n3 + i3 * N3 + j]);
+      }
+    }
+    const float* sb = slots + (size_t)slot * SL;
+    for (int e = lane; e < SL; e += 32) {
+      const int x = e / R2, r = e - x * R2;
+      s_sb[x * RS + r] = sb[e];
+    }
+    __syncwarp();
+    for (int o = lane; o < N; o += 32) {
+      const int x = o / N3, j = o - x * N3;
+      float acc = 0.f;
+#pragma unroll 8
+      for (int r = 0; r < R2; ++r) acc = fmaf(s_sb[x * RS + r], s_h[r * N3 + j], acc);
+      s_o[o] += acc;
+    }
+    __syncwarp();
+  }
+  for (int o = lane; o < N; o += 32) out[(size_t)b * N + o] = s_o[o];
+  __syncwarp();
+}
+
+template <class D>
+__host__ __device__ constexpr int close_warp_floats(const D& d) {
+  return dX(d) * (d.r2 + 1) + dG3s(d) + dN(d);
+}
+
 template <class D>
 __global__ void __launch_bounds__(kBlock) k_close_pool(D d, KGeom g, const float* __restrict__ G3,
                                                        const float* __restrict__ slots, const int* __restrict__ bag_off,
@@ -231,45 +334,100 @@ __global__ void __launch_bounds__(kBlock) k_close_pool(D d, KGeom g, const float
                                                        const int* __restrict__ occ_slot,
                                                        const unsigned* __restrict__ keys32, int B,
                                                        float* __restrict__ out) {
-  extern __shared__ float smem[];
+  extern __shared__ __align__(16) float smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int X = dX(d), R2 = d.r2, N3 = d.n3, N = dN(d), SL = dSlot(d), G3S = dG3s(d);
-  const int RS = R2 + 1;  // padded slot row stride (bank-conflict free)
-  float* s_sb = smem + w * (X * RS + G3S + N);
-  float* s_h = s_sb + X * RS;
-  float* s_o = s_h + G3S;
-  const unsigned m3n3 = g.m3 * (unsigned)N3;
-  for (int b = blockIdx.x * (kBlock / 32) + w; b < B; b += gridDim.x * (kBlock / 32)) {
-    const int o0 = bag_off[b], o1 = bag_off[b + 1];
-    for (int o = lane; o < N; o += 32) s_o[o] = 0.f;
-    for (int sg = bag_seg[b]; sg < bag_seg[b + 1]; ++sg) {
-      const int slot = seg_slot[sg];
-      for (int e = lane; e < G3S; e += 32) s_h[e] = 0.f;
-      for (int t = o0; t < o1; ++t) {
-        if (occ_slot[t] != slot) continue;
-        const unsigned i3 = keys32[t] % g.m3;
-        for (int e = lane; e < G3S; e += 32) {
-          const int r = e / N3, j = e - r * N3;
-          s_h[e] += __ldg(&G3[(size_t)r * m3n3 + i3 * N3 + j]);
+  const int WF = close_warp_floats(d);
+  float* s_sb = smem + w * WF;
+  float* s_h = s_sb + dX(d) * (d.r2 + 1);
+  float* s_o = s_h + dG3s(d);
+  const int gw = blockIdx.x * (kBlock / 32) + w, nw = gridDim.x * (kBlock / 32);
+  if constexpr (kFastRows<D>) {
+    // lane <-> r2 fast path for single-index bags (pooling 1), metadata for
+    // 32 bags fetched at once and the next bag's operands prefetched.
+    constexpr int Xc = FixT<D>::n1 * FixT<D>::n2, NN = Xc * 4, SLc = Xc * 32, LS = 36;
+    static_assert(NN == 64 || NN == 32 || NN == 128, "fast close layout");
+    float* f_sb = s_sb;          // Xc x LS (padded rows)
+    float* f_ht = s_sb + Xc * LS; // 4 x LS: H transposed [j][r2]
+    const unsigned m3n3 = g.m3 * 4u;
+    for (int b0 = gw * 32; b0 < B; b0 += nw * 32) {
+      const int b = b0 + lane;
+      int o0 = 0, o1 = 0, sg0 = 0, sg1 = 0, slot = 0;
+      unsigned i3 = 0;
+      if (b < B) {
+        o0 = bag_off[b];
+        o1 = bag_off[b + 1];
+        sg0 = bag_seg[b];
+        sg1 = bag_seg[b + 1];
+        if (o1 - o0 == 1) {
+          slot = occ_slot[o0];
+          i3 = keys32[o0] % g.m3;
         }
       }
-      const float* sb = slots + (size_t)slot * SL;
-      for (int e = lane; e < SL; e += 32) {
-        const int x = e / R2, r = e - x * R2;
-        s_sb[x * RS + r] = sb[e];
+      const int nb = min(32, B - b0);
+      const unsigned simple = __ballot_sync(0xffffffffu, b < B && o1 - o0 == 1);
+      // prefetch registers for the first simple bag
+      float4 pre_sb[SLc / 128], pre_h;
+      auto fetch = [&](int i) {
+        const int sl = __shfl_sync(0xffffffffu, slot, i);
+        const unsigned ii3 = __shfl_sync(0xffffffffu, i3, i);
+        const float4* src = reinterpret_cast<const float4*>(slots + (size_t)sl * SLc);
+#pragma unroll
+        for (int k = 0; k < SLc / 128; ++k) pre_sb[k] = src[lane + 32 * k];
+        pre_h = __ldg(reinterpret_cast<const float4*>(G3 + (size_t)lane * m3n3 + ii3 * 4u));
+      };
+      int next = simple ? __ffs(simple) - 1 : 32;
+      if (next < nb) fetch(next);
+      for (int i = 0; i < nb; ++i) {
+        if (!((simple >> i) & 1u)) {
+          const int bi = b0 + i;
+          close_bag_generic(d, g, G3, slots, bi, __shfl_sync(0xffffffffu, o0, i), __shfl_sync(0xffffffffu, o1, i),
+                            __shfl_sync(0xffffffffu, sg0, i), __shfl_sync(0xffffffffu, sg1, i), seg_slot, occ_slot,
+                            keys32, s_sb, s_h, s_o, out);
+          continue;
+        }
+        // stage the prefetched operands, then prefetch the next simple bag
+#pragma unroll
+        for (int k = 0; k < SLc / 128; ++k) {
+          const int e = 4 * (lane + 32 * k), x = e / 32, r = e - x * 32;
+          *reinterpret_cast<float4*>(f_sb + x * LS + r) = pre_sb[k];
+        }
+        f_ht[0 * LS + lane] = pre_h.x;
+        f_ht[1 * LS + lane] = pre_h.y;
+        f_ht[2 * LS + lane] = pre_h.z;
+        f_ht[3 * LS + lane] = pre_h.w;
+        const unsigned rest = simple & ~((2u << i) - 1u);
+        next = rest ? __ffs(rest) - 1 : 32;
+        if (next < nb) fetch(next);
+        __syncwarp();
+        // outputs: N = Xc * 4; each lane computes NN / 32 of them
+        constexpr int PER = NN / 32;
+        float res[PER];
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+          const int o = lane * PER + q, x = o / 4, j = o - x * 4;
+          float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;  // 4 independent chains
+#pragma unroll
+          for (int r = 0; r < 32; r += 4) {
+            const float4 sv = *reinterpret_cast<const float4*>(f_sb + x * LS + r);
+            const float4 hv = *reinterpret_cast<const float4*>(f_ht + j * LS + r);
+            a0 = fmaf(sv.x, hv.x, a0);
+            a1 = fmaf(sv.y, hv.y, a1);
+            a2 = fmaf(sv.z, hv.z, a2);
+            a3 = fmaf(sv.w, hv.w, a3);
+          }
+          res[q] = (a0 + a1) + (a2 + a3);
+        }
+        float* dst = out + (size_t)(b0 + i) * NN + lane * PER;
+        if constexpr (PER == 2) *reinterpret_cast<float2*>(dst) = make_float2(res[0], res[1]);
+        else if constexpr (PER == 4) *reinterpret_cast<float4*>(dst) = make_float4(res[0], res[1], res[2], res[3]);
+        else dst[0] = res[0];
+        __syncwarp();
       }
-      __syncwarp();
-      for (int o = lane; o < N; o += 32) {
-        const int x = o / N3, j = o - x * N3;
-        float acc = 0.f;
-#pragma unroll 8
-        for (int r = 0; r < R2; ++r) acc = fmaf(s_sb[x * RS + r], s_h[r * N3 + j], acc);
-        s_o[o] += acc;
-      }
-      __syncwarp();
     }
-    for (int o = lane; o < N; o += 32) out[(size_t)b * N + o] = s_o[o];
-    __syncwarp();
+  } else {
+    for (int b = gw; b < B; b += nw)
+      close_bag_generic(d, g, G3, slots, b, bag_off[b], bag_off[b + 1], bag_seg[b], bag_seg[b + 1], seg_slot,
+                        occ_slot, keys32, s_sb, s_h, s_o, out);
   }
 }
 
@@ -277,8 +435,10 @@ __global__ void __launch_bounds__(kBlock) k_close_pool(D d, KGeom g, const float
 // Aggregated row gradient g_u = sum of the bag gradients of the row's
 // occurrences, left to right in index order (backward.py:81-85 sums in the
 // gradient dtype in occurrence order; the stable sort preserves that order).
+// A warp takes 32 rows: lanes fetch their metadata at once, single-occurrence
+// rows (the common case) are copied 8 at a time with independent loads.
 template <class D>
-__global__ void __launch_bounds__(kBlock) k_row_agg(D d, const int* __restrict__ counts,
+__global__ void __launch_bounds__(kBlock) k_row_agg(D d, int B, const int* __restrict__ counts,
                                                     const int* __restrict__ urow_start,
                                                     const unsigned* __restrict__ svals, const int* __restrict__ bag_of,
                                                     const float* __restrict__ gout, float* __restrict__ gU,
@@ -287,18 +447,52 @@ __global__ void __launch_bounds__(kBlock) k_row_agg(D d, const int* __restrict__
   const int N = dN(d);
   const int U = counts[3];
   bool bad = false;
-  for (int u = blockIdx.x * (kBlock / 32) + w; u < U; u += gridDim.x * (kBlock / 32)) {
-    const int q0 = urow_start[u], q1 = urow_start[u + 1];
-    for (int o0 = 0; o0 < N; o0 += 32) {
-      const int o = o0 + lane;
-      float acc = 0.f;
-      if (o < N) {
-        for (int q = q0; q < q1; ++q) {
-          const float v = __ldg(&gout[(size_t)bag_of[svals[q]] * N + o]);
-          acc += v;
+  const int gw = blockIdx.x * (kBlock / 32) + w, nw = gridDim.x * (kBlock / 32);
+  for (int u0 = gw * 32; u0 < U; u0 += nw * 32) {
+    const int u = u0 + lane;
+    int q0 = 0, q1 = 0, bb = 0;
+    if (u < U) {
+      q0 = urow_start[u];
+      q1 = urow_start[u + 1];
+      if (q1 - q0 == 1) {
+        bb = bag_of[svals[q0]];
+        bb = bb < 0 ? 0 : (bb >= B ? B - 1 : bb);  // malformed offsets: garbage ids, never OOB
+      }
+    }
+    const int nr = min(32, U - u0);
+    const unsigned single = __ballot_sync(0xffffffffu, u < U && q1 - q0 == 1);
+    if constexpr (FixT<D>::n1 * FixT<D>::n2 * FixT<D>::n3 == 64) {
+      for (int i0 = 0; i0 < nr; i0 += 8) {
+        float2 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int bk = __shfl_sync(0xffffffffu, bb, (i0 + k) & 31);
+          if (i0 + k < nr && ((single >> (i0 + k)) & 1u))
+            v[k] = __ldg(reinterpret_cast<const float2*>(gout + (size_t)bk * 64) + lane);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (i0 + k < nr && ((single >> (i0 + k)) & 1u)) {
+            const float2 x = make_float2(0.f + v[k].x, 0.f + v[k].y);
+            if (!isfinite(x.x) || !isfinite(x.y)) bad = true;
+            reinterpret_cast<float2*>(gU + (size_t)(u0 + i0 + k) * 64)[lane] = x;
+          }
+      }
+    }
+    for (int i = 0; i < nr; ++i) {
+      if (FixT<D>::n1 * FixT<D>::n2 * FixT<D>::n3 == 64 && ((single >> i) & 1u)) continue;
+      const int a = __shfl_sync(0xffffffffu, q0, i), b = __shfl_sync(0xffffffffu, q1, i);
+      for (int o0 = 0; o0 < N; o0 += 32) {
+        const int o = o0 + lane;
+        if (o >= N) continue;
+        float acc = 0.f;
+        for (int q = a; q < b; ++q) {
+          int bq = bag_of[svals[q]];
+          bq = bq < 0 ? 0 : (bq >= B ? B - 1 : bq);
+          acc += __ldg(&gout[(size_t)bq * N + o]);
         }
         if (!isfinite(acc)) bad = true;
-        gU[(size_t)u * N + o] = acc;
+        gU[(size_t)(u0 + i) * N + o] = acc;
       }
     }
   }
@@ -342,17 +536,95 @@ __global__ void __launch_bounds__(kBlock) k_bwd_prefix(D d, KGeom g, int ch, con
   float* s_g1 = s_g2 + R1 * LZ;      // M x R1      G1 chunk [(p, a)][r1]  (k-major for phase B)
   float* s_wk = s_g1 + M * R1;       // per warp: g (N) + G3 slice (G3S) + slot (SL)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int e = threadIdx.x; e < R1 * C; e += kBlock) {
-    const int r = e / C, c = e - r * C;
-    s_g2[r * LZ + c] = G2[((size_t)r * g.m2 + i2) * C + c];
-  }
-  for (int e = threadIdx.x; e < M * R1; e += kBlock) {
-    const int row = e / R1, r = e - row * R1;
-    const int p = row / N1, a = row - p * N1;
-    s_g1[e] = p < np ? G1[((size_t)s_free[p] * N1 + a) * R1 + r] : 0.f;
+  if constexpr (kVecStage<D>) {
+    constexpr int C4 = FixT<D>::n2 * FixT<D>::r2 / 4, R1c = FixT<D>::r1, RQ = R1c / 4;
+#pragma unroll 4
+    for (int e = threadIdx.x; e < R1c * C4; e += kBlock) {
+      const int r = e / C4, c4 = e - r * C4;
+      *reinterpret_cast<float4*>(s_g2 + r * LZ + 4 * c4) =
+          __ldg(reinterpret_cast<const float4*>(G2 + ((size_t)r * g.m2 + i2) * C) + c4);
+    }
+#pragma unroll 4
+    for (int e = threadIdx.x; e < M * RQ; e += kBlock) {
+      const int row = e / RQ, q = e - row * RQ;
+      const int p = row / FixT<D>::n1, a = row - p * FixT<D>::n1;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (p < np) v = __ldg(reinterpret_cast<const float4*>(G1 + ((size_t)s_free[p] * FixT<D>::n1 + a) * R1c) + q);
+      reinterpret_cast<float4*>(s_g1)[e] = v;
+    }
+  } else {
+    for (int e = threadIdx.x; e < R1 * C; e += kBlock) {
+      const int r = e / C, c = e - r * C;
+      s_g2[r * LZ + c] = G2[((size_t)r * g.m2 + i2) * C + c];
+    }
+    for (int e = threadIdx.x; e < M * R1; e += kBlock) {
+      const int row = e / R1, r = e - row * R1;
+      const int p = row / N1, a = row - p * N1;
+      s_g1[e] = p < np ? G1[((size_t)s_free[p] * N1 + a) * R1 + r] : 0.f;
+    }
   }
   // ---- phase A
-  {
+  if constexpr (kFastRows<D>) {
+    // lane <-> r2; the slot column, Z column and one row's G3 slice live in
+    // registers; the row gradient is broadcast through a double-buffered
+    // per-warp smem line; the next row's loads are issued before the math.
+    constexpr int Xc = FixT<D>::n1 * FixT<D>::n2, NN = Xc * 4, N2c = FixT<D>::n2;
+    float* s_gw = s_wk + w * (2 * NN);
+    const unsigned m3n3 = g.m3 * 4u;
+    for (int pi = w; pi < np; pi += kBlock / 32) {
+      const int slot = s_slot[pi];
+      const float* sb = slots + (size_t)slot * (Xc * 32);
+      float sbc[Xc], zr[Xc];
+#pragma unroll
+      for (int x = 0; x < Xc; ++x) {
+        sbc[x] = sb[x * 32 + lane];
+        zr[x] = 0.f;
+      }
+      const int u0 = prow_begin[slot], u1 = prow_end[slot];
+      float ga = 0.f, gb = 0.f;
+      float4 hv = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (u0 < u1) {
+        ga = gU[(size_t)u0 * NN + lane];
+        if (NN > 32) gb = gU[(size_t)u0 * NN + 32 + lane];
+        hv = __ldg(reinterpret_cast<const float4*>(G3 + (size_t)lane * m3n3 + urow_i3[u0] * 4u));
+      }
+      int buf = 0;
+      for (int u = u0; u < u1; ++u) {
+        float* sg = s_gw + buf * NN;
+        if (lane < NN) sg[lane] = ga;
+        if (NN > 32) sg[32 + lane] = gb;
+        const float4 h = hv;
+        if (u + 1 < u1) {
+          ga = gU[(size_t)(u + 1) * NN + lane];
+          if (NN > 32) gb = gU[(size_t)(u + 1) * NN + 32 + lane];
+          hv = __ldg(reinterpret_cast<const float4*>(G3 + (size_t)lane * m3n3 + urow_i3[u + 1] * 4u));
+        }
+        __syncwarp();
+        float d0 = 0.f, d1 = 0.f, d2 = 0.f, d3 = 0.f;
+#pragma unroll
+        for (int x = 0; x < Xc; ++x) {
+          const float4 gx = *reinterpret_cast<const float4*>(sg + 4 * x);
+          float z = zr[x];
+          z = fmaf(gx.x, h.x, z);
+          z = fmaf(gx.y, h.y, z);
+          z = fmaf(gx.z, h.z, z);
+          zr[x] = fmaf(gx.w, h.w, z);
+          d0 = fmaf(sbc[x], gx.x, d0);
+          d1 = fmaf(sbc[x], gx.y, d1);
+          d2 = fmaf(sbc[x], gx.z, d2);
+          d3 = fmaf(sbc[x], gx.w, d3);
+        }
+        *reinterpret_cast<float4*>(dH + (size_t)u * 128 + lane * 4) = make_float4(d0, d1, d2, d3);
+        buf ^= 1;
+      }
+#pragma unroll
+      for (int x = 0; x < Xc; ++x) {
+        const int a = x / N2c, b = x - a * N2c;
+        s_z[(pi * FixT<D>::n1 + a) * LZ + b * 32 + lane] = zr[x];
+      }
+    }
+    for (int e = np * N1 * LZ + threadIdx.x; e < M * LZ; e += kBlock) s_z[e] = 0.f;
+  } else {
     float* s_g = s_wk + w * (N + G3S + SL);
     float* s_h = s_g + N;
     float* s_sb = s_h + G3S;
@@ -431,17 +703,19 @@ __global__ void __launch_bounds__(kBlock) k_bwd_prefix(D d, KGeom g, int ch, con
   // ---- phase B: dG2 partial = G1_chunk^T . Z_chunk
   {
     float* part = dG2part + ((size_t)i2 * cmax + blockIdx.y) * dG2s(d);
-    gemm_kk<Tl::BM, Tl::BN>(R1, C, np * N1, s_g1, R1, s_z, LZ, [&](int m0, int n0, float (&acc)[Tl::BM][Tl::BN]) {
+    gemm_kk<Tl::BM, Tl::BN>(R1, C, np * N1, s_g1, R1, s_z, LZ,
+                            [&](int m0, int n0, int hm, int hn, float (&acc)[Tl::BM][Tl::BN]) {
 #pragma unroll
       for (int i = 0; i < Tl::BM; ++i) {
-        float* dst = part + (size_t)(m0 + i) * C + n0;
+        float* dst = part + (size_t)split_index<Tl::BM>(m0, hm, i) * C;
         if constexpr (Tl::BN % 4 == 0) {
 #pragma unroll
           for (int j = 0; j < Tl::BN; j += 4)
-            *reinterpret_cast<float4*>(dst + j) = make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+            *reinterpret_cast<float4*>(dst + split_index<Tl::BN>(n0, hn, j)) =
+                make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
         } else {
 #pragma unroll
-          for (int j = 0; j < Tl::BN; ++j) dst[j] = acc[i][j];
+          for (int j = 0; j < Tl::BN; ++j) dst[n0 + j] = acc[i][j];
         }
       }
     });

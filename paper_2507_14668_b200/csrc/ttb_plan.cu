@@ -30,6 +30,9 @@ __global__ void __launch_bounds__(kBlock) k_plan_mark(const IdxT* __restrict__ i
       const int64_t on = offsets[b + 1];
       if (on == ob) bits |= 2;
       else if (on < ob) bits |= 4;
+      // bag id of each index (clamped so malformed offsets cannot write out of range)
+      const int lo = (int)(ob < 0 ? 0 : (ob > T ? T : ob)), hi = (int)(on < lo ? lo : (on > T ? T : on));
+      for (int t = lo; t < hi; ++t) bag_of[t] = b;
     }
   }
   for (int t = tid; t < T; t += stride) {
@@ -41,14 +44,6 @@ __global__ void __launch_bounds__(kBlock) k_plan_mark(const IdxT* __restrict__ i
     const unsigned i = (unsigned)v;
     keys32[t] = i;
     atomicMin(&pmap[i / g.m3], (unsigned)t);
-    // bag id: last b with offsets[b] <= t
-    int lo = 0, hi = B - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (offsets[mid] <= (int64_t)t) lo = mid;
-      else hi = mid - 1;
-    }
-    bag_of[t] = lo;
   }
   if (bits) atomicOr(err, bits);
 }
@@ -257,10 +252,12 @@ cudaError_t launch_plan(ttb_handle* h, const void* idx, int idx64, const int64_t
   const int T = (int)h->T, B = (int)h->B;
   cudaError_t e;
   // fresh prefix table, error word/counters and look-back state
-  if ((e = cudaMemsetAsync(w.pmap, 0xFF, sizeof(unsigned) * h->kg.m1m2, s))) return e;
-  if ((e = cudaMemsetAsync(w.err, 0, sizeof(int) * 8, s))) return e;
-  if ((e = cudaMemsetAsync(w.scan_status, 0, sizeof(unsigned long long) * h->scan_tiles * kNumScans, s))) return e;
-  if ((e = cudaMemsetAsync(w.scan_ctr, 0, sizeof(unsigned) * 16, s))) return e;
+  // one memset for all per-batch state (zero blocks A and B are contiguous);
+  // the prefix table is reset by the previous backward unless it was skipped
+  if (!h->pmap_clean && (e = cudaMemsetAsync(w.pmap, 0xFF, sizeof(unsigned) * h->kg.m1m2, s))) return e;
+  h->pmap_clean = 0;
+  if ((e = cudaMemsetAsync(w.zeroA, 0, w.zeroA_bytes + w.zeroB_bytes, s))) return e;
+  h->bwd_zeroed = 1;
 
   const int work = T > B + 1 ? T : B + 1;
   int grid = (work + kBlock - 1) / kBlock;

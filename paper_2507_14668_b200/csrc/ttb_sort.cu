@@ -69,18 +69,18 @@ __global__ void __launch_bounds__(kBlock) k_sort_pass(const unsigned* __restrict
   __shared__ unsigned s_goff[kRadix];
   const int n = sort_count(d_count, max_n);
   const int tile = claim_tile(ctr, &s_tile);
-  const int base = tile * kTile;
+  const int base = tile * kSortTile;
   if (base >= n) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned lt = lanemask_lt();
   for (int i = threadIdx.x; i < NW * kRadix; i += kBlock) (&whist[0][0])[i] = 0;
   __syncthreads();
 
-  unsigned key[kItems], val[kItems];
-  int rank[kItems];
+  unsigned key[kSortItems], val[kSortItems];
+  int rank[kSortItems];
 #pragma unroll
-  for (int k = 0; k < kItems; ++k) {
-    const int pos = base + w * (32 * kItems) + k * 32 + lane;
+  for (int k = 0; k < kSortItems; ++k) {
+    const int pos = base + w * (32 * kSortItems) + k * 32 + lane;
     const bool ok = pos < n;
     key[k] = ok ? kin[pos] : 0u;
     val[k] = ok ? (vin ? vin[pos] : (unsigned)pos) : 0u;
@@ -106,26 +106,37 @@ __global__ void __launch_bounds__(kBlock) k_sort_pass(const unsigned* __restrict
     unsigned* st = status + (size_t)tile * kRadix + d;
     unsigned excl = 0;
     if (tile == 0) {
-      st_release_u32(st, kSFlagInc | run);
+      st_relaxed_u32(st, kSFlagInc | run);
     } else {
-      st_release_u32(st, kSFlagAgg | run);
+      st_relaxed_u32(st, kSFlagAgg | run);
+      // windowed look-back: 8 predecessors per round trip instead of 1
       int j = tile - 1;
-      while (true) {
-        const unsigned sv = ld_acquire_u32(status + (size_t)j * kRadix + d);
-        const unsigned f = sv & ~kSValMask;
-        if (f == 0) continue;
-        excl += sv & kSValMask;
-        if (f == kSFlagInc) break;
-        --j;
+      while (j >= 0) {
+        unsigned sv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sv[i] = (j - i >= 0) ? ld_relaxed_u32(status + (size_t)(j - i) * kRadix + d) : 0u;
+        bool done = false;
+        int used = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (done || used < i || j - i < 0) continue;
+          const unsigned f = sv[i] & ~kSValMask;
+          if (f == 0) continue;
+          excl += sv[i] & kSValMask;
+          used = i + 1;
+          if (f == kSFlagInc) done = true;
+        }
+        if (done) break;
+        j -= used;
       }
-      st_release_u32(st, kSFlagInc | (excl + run));
+      st_relaxed_u32(st, kSFlagInc | (excl + run));
     }
     s_goff[d] = goff[d] + excl;
   }
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < kItems; ++k) {
-    const int pos = base + w * (32 * kItems) + k * 32 + lane;
+  for (int k = 0; k < kSortItems; ++k) {
+    const int pos = base + w * (32 * kSortItems) + k * 32 + lane;
     if (pos < n) {
       const unsigned d = (key[k] >> shift) & 255u;
       const unsigned o = s_goff[d] + whist[w][d] + (unsigned)rank[k];
@@ -147,10 +158,7 @@ cudaError_t launch_sort(ttb_handle* h, const unsigned* keys_in, const unsigned* 
   unsigned* hist = w.sort_hist + (size_t)region * 4 * kRadix;
   unsigned* status = w.sort_status + (size_t)region * 4 * h->sort_tiles * kRadix;
   unsigned* ctr = w.sort_ctr + region * 4;
-  cudaError_t e;
-  if ((e = cudaMemsetAsync(hist, 0, sizeof(unsigned) * 4 * kRadix, s))) return e;
-  if ((e = cudaMemsetAsync(status, 0, sizeof(unsigned) * 4 * h->sort_tiles * kRadix, s))) return e;
-  if ((e = cudaMemsetAsync(ctr, 0, sizeof(unsigned) * 4, s))) return e;
+  // hist / status / counters live in zero block B, cleared before the backward
   int hgrid = (max_n + kBlock * 4 - 1) / (kBlock * 4);
   if (hgrid > 148 * 4) hgrid = 148 * 4;
   if (hgrid < 1) hgrid = 1;
@@ -160,7 +168,7 @@ cudaError_t launch_sort(ttb_handle* h, const unsigned* keys_in, const unsigned* 
     k_sort_scan<<<1, kRadix, 0, s>>>(hist, passes);
   }
   count_launch(2);
-  const int tiles = (max_n + kTile - 1) / kTile;
+  const int tiles = (max_n + kSortTile - 1) / kSortTile;
   const unsigned* ki = keys_in;
   const unsigned* vi = vals_in;
   for (int p = 0; p < passes; ++p) {
