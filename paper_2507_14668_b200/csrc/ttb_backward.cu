@@ -208,15 +208,15 @@ __device__ inline void dg3_block(int G3S, unsigned v, const int* __restrict__ i3
 
 // dG2[:, i2] = sum of the group's chunk partials in chunk order; one thread
 // per 4 consecutive slice elements (float4), kBlock*4 elements per block.
-__device__ inline void dg2_part(KGeom g, int C, int G2S, int cmax, int ch, unsigned i2, int q,
+__device__ inline void dg2_part(KGeom g, int C, int G2S, int nsplit, int ch, unsigned i2, int q,
                                 const float* __restrict__ part, const int* __restrict__ grp_cnt,
                                 const int* __restrict__ err, float* __restrict__ grad, float* __restrict__ param,
                                 double* __restrict__ vel, double lr, double mu, int do_update) {
-  const int nch = (grp_cnt[i2] + ch - 1) / ch;
+  const int nch = (grp_cnt[i2] + ch - 1) / ch;  // chunks that wrote a partial
   const bool upd = do_update && ((*err & 8) == 0);
   const int e0 = (q * kBlock + threadIdx.x) * 4;
   if (e0 >= G2S) return;
-  const float* base = part + (size_t)i2 * cmax * G2S;
+  const float* base = part + (size_t)i2 * nsplit * G2S;
   if (G2S % 4 == 0 && C % 4 == 0) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     int c = 0;
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kBlock) k_dg13_reduce(KGeom g, int G1S, int N3
                                                         float* __restrict__ param0, double* __restrict__ vel0,
                                                         int upd0, float* __restrict__ grad2,
                                                         float* __restrict__ param2, double* __restrict__ vel2,
-                                                        int upd2, double lr, double mu, int C, int G2S, int cmax,
+                                                        int upd2, double lr, double mu, int C, int G2S, int nsplit,
                                                         int ch, const float* __restrict__ part,
                                                         const int* __restrict__ grp_cnt, float* __restrict__ grad1,
                                                         float* __restrict__ param1, double* __restrict__ vel1,
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(kBlock) k_dg13_reduce(KGeom g, int G1S, int N3
   if (blockIdx.x >= g.m1 + g.m3) {
     const int qpb = (G2S + 4 * kBlock - 1) / (4 * kBlock);
     const int k = blockIdx.x - (g.m1 + g.m3);
-    dg2_part(g, C, G2S, cmax, ch, (unsigned)(k / qpb), k % qpb, part, grp_cnt, err, grad1, param1, vel1, lr, mu,
+    dg2_part(g, C, G2S, nsplit, ch, (unsigned)(k / qpb), k % qpb, part, grp_cnt, err, grad1, param1, vel1, lr, mu,
              upd1);
     return;
   }
@@ -331,7 +331,7 @@ static size_t prefix_smem(const D& d, int ch) {
 template <class D>
 static size_t close_smem(const D& d) {
   size_t per = (size_t)close_warp_floats(d);
-  if (kFastRows<D>) per = per > (size_t)(dX(d) + 4) * 36 ? per : (size_t)(dX(d) + 4) * 36;
+  if (kFastRows<D>) per = per > (size_t)136 ? per : (size_t)136;
   return sizeof(float) * (kBlock / 32) * per;
 }
 template <class D>
@@ -360,7 +360,7 @@ static cudaError_t forward_impl(ttb_handle* h, const float* c0, const float* c1,
   cudaError_t e;
   const size_t sm1 = prefix_smem(d, h->chf);
   if ((e = ensure_smem(k_prefix_products<D>, sm1))) return e;
-  dim3 g1(h->kg.m2, (unsigned)h->cmaxf);
+  dim3 g1(h->kg.m2, (unsigned)h->nsplitf);
   { ProfScope _ps(h, s, "prefix_products");
   k_prefix_products<D><<<g1, kBlock, sm1, s>>>(d, h->kg, h->chf, c0, c1, w.pmap, w.pslot, w.slots);
   }
@@ -419,7 +419,7 @@ static cudaError_t backward_impl(ttb_handle* h, const float* c0, const float* c1
   // 4. per-prefix contractions, grouped by i2
   const size_t sm = bwd_smem(d, h->chb);
   if ((e = ensure_smem(k_bwd_prefix<D>, sm))) return e;
-  dim3 gp(h->kg.m2, (unsigned)h->cmaxb);
+  dim3 gp(h->kg.m2, (unsigned)h->nsplitb);
   { ProfScope _ps(h, s, "bwd_prefix");
   k_bwd_prefix<D><<<gp, kBlock, sm, s>>>(d, h->kg, h->chb, c0, c1, c2, w.pmap, w.pslot, w.slots, w.prow_begin, w.prow_end,
                                          w.urow_i3, w.gU, w.dH, w.E, w.dG2part, w.grp_cnt,

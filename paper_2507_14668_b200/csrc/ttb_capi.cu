@@ -51,8 +51,12 @@ void layout(ttb_handle& h, char* base) {
   const int64_t SL = (int64_t)d.n1 * d.n2 * d.r2, G1S = (int64_t)d.n1 * d.r1, G2S = (int64_t)d.r1 * d.n2 * d.r2,
                 G3S = (int64_t)d.r2 * d.n3;
   h.Pmax = T < m1m2 ? T : m1m2;
-  h.cmaxf = (int)((g.m[0] + h.chf - 1) / h.chf);
-  h.cmaxb = (int)((g.m[0] + h.chb - 1) / h.chb);
+  // one CTA per chunk: the prefix kernels are latency bound and gain from
+  // many co-resident CTAs overlapping their gather / GEMM phases (measured:
+  // fewer, longer CTAs that loop over chunks were 25% slower)
+  h.nsplitf = (int)((g.m[0] + h.chf - 1) / h.chf);
+  h.nsplitb = (int)((g.m[0] + h.chb - 1) / h.chb);
+  h.cmaxb = h.nsplitb;
   h.sort_tiles = (T + kSortTile - 1) / kSortTile + 1;
   int64_t st = (T + kTile - 1) / kTile;
   const int64_t bt = (B + 31) / 32;

@@ -91,7 +91,9 @@ struct ttb_handle {
   ttb::KGeom kg;
   ttb::DynDims dims;
   int64_t maxT, maxB, Pmax, scan_tiles, sort_tiles;
-  int chf, chb, cmaxf, cmaxb;  // prefixes per CTA (forward / backward) and chunks per i2 group
+  int chf, chb;          // prefixes per chunk (forward / backward kernels)
+  int nsplitf, nsplitb;  // CTAs per i2 group (forward / backward)
+  int cmaxb;             // chunks per i2 group in the backward (dG2 partials)
   int idx_bits, i3_bits;
   char* base;
   size_t bytes;

@@ -141,6 +141,23 @@ __device__ __forceinline__ void gemm_kk(int M, int N, int K, const float* At, in
   }
 }
 
+// One thread tile of gemm_kk accumulated into a caller-held register array
+// (used when the tile grid equals the block: acc persists across sub-batches).
+template <int TM, int TN>
+__device__ __forceinline__ void gemm_kk_tile(int K, const float* At, int lda, const float* B, int ldb, int m0,
+                                             int n0, int hm, int hn, float (&acc)[TM][TN]) {
+#pragma unroll 4
+  for (int k = 0; k < K; ++k) {
+    float a[TM], b[TN];
+    lds_split<TM>(a, At + k * lda + m0, hm);
+    lds_split<TN>(b, B + k * ldb + n0, hn);
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+  }
+}
+
 // C[m][n] = sum_k A[m*lda + k] * Bt[n*ldb + k]   (contraction contiguous in both)
 // K stepped by 4 with float4 loads when VEC (K % 4 == 0, 16-byte rows).
 template <int TM, int TN, bool VEC, class Out>
@@ -199,6 +216,13 @@ template <int A, int B_, int C_, int R1, int R2> struct Tiles<FixDims<A, B_, C_,
   static constexpr bool VEC = Cc % 4 == 0;
 };
 
+// the phase-B tile grid of k_bwd_prefix equals the block: the dG2 partial
+// can live in registers across the CTA's chunks
+template <class D> struct RegAcc {
+  static constexpr bool value = IsFixed<D>::value && FixT<D>::r1 > 0 &&
+                                (FixT<D>::r1 / Tiles<D>::BM) * (FixT<D>::n2 * FixT<D>::r2 / Tiles<D>::BN) == kBlock;
+};
+
 template <class D> __host__ __device__ inline int pad_ld(const D& d) {
   return dC(d) % 4 == 0 ? dC(d) + 4 : dC(d);
 }
@@ -216,64 +240,76 @@ __global__ void __launch_bounds__(kBlock) k_prefix_products(D d, KGeom g, int ch
   __shared__ int s_free[kMaxChunk], s_slot[kMaxChunk], s_w[kBlock / 32 + 2];
   const int C = dC(d), R1 = d.r1, N1 = d.n1;
   const unsigned i2 = blockIdx.x;
+  const int split = blockIdx.y, nsplit = gridDim.y;
   int np;
-  collect_chunk(pmap, pslot, g, true, i2, blockIdx.y, ch, s_free, s_slot, s_w, &np);
-  if (np == 0) return;
+  const int total = collect_chunk(pmap, pslot, g, true, i2, split, ch, s_free, s_slot, s_w, &np);
+  const int nchunks = (total + ch - 1) / ch;
+  if (split >= nchunks) return;
   const int M = ch * N1;   // padded rows (prefix, a)
   float* s_g2 = smem;      // R1 x C   (k-major: [r1][c])
   float* s_g1t = smem + R1 * C;  // R1 x M (k-major: [r1][p*N1 + a])
+  // the G2 slice is staged once per CTA and reused by all its chunks
   if constexpr (kVecStage<D>) {
-    constexpr int C4 = FixT<D>::n2 * FixT<D>::r2 / 4, R1c = FixT<D>::r1, N1c = FixT<D>::n1;
+    constexpr int C4 = FixT<D>::n2 * FixT<D>::r2 / 4, R1c = FixT<D>::r1;
 #pragma unroll 4
     for (int e = threadIdx.x; e < R1c * C4; e += kBlock) {
       const int r = e / C4, c4 = e - r * C4;
       reinterpret_cast<float4*>(s_g2)[e] =
           __ldg(reinterpret_cast<const float4*>(G2 + ((size_t)r * g.m2 + i2) * C) + c4);
     }
-    constexpr int RQ = R1c / 4;  // float4 per G1 row
-#pragma unroll 4
-    for (int e = threadIdx.x; e < M * RQ; e += kBlock) {
-      const int row = e / RQ, q = e - row * RQ;
-      const int p = row / N1c, a = row - p * N1c;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (p < np) v = __ldg(reinterpret_cast<const float4*>(G1 + ((size_t)s_free[p] * N1c + a) * R1c) + q);
-      s_g1t[(4 * q + 0) * M + row] = v.x;
-      s_g1t[(4 * q + 1) * M + row] = v.y;
-      s_g1t[(4 * q + 2) * M + row] = v.z;
-      s_g1t[(4 * q + 3) * M + row] = v.w;
-    }
   } else {
     for (int e = threadIdx.x; e < R1 * C; e += kBlock) {
       const int r = e / C, c = e - r * C;
       s_g2[e] = G2[((size_t)r * g.m2 + i2) * C + c];
     }
-    for (int e = threadIdx.x; e < M * R1; e += kBlock) {
-      const int row = e / R1, r = e - row * R1;
-      const int p = row / N1, a = row - p * N1;
-      s_g1t[r * M + row] = p < np ? G1[((size_t)s_free[p] * N1 + a) * R1 + r] : 0.f;
-    }
   }
-  __syncthreads();
   using Tl = Tiles<D>;
   const int SL = dSlot(d);
-  gemm_kk<Tl::FM, Tl::FN>(M, C, R1, s_g1t, M, s_g2, C,
-                          [&](int m0, int n0, int hm, int hn, float (&acc)[Tl::FM][Tl::FN]) {
-#pragma unroll
-    for (int i = 0; i < Tl::FM; ++i) {
-      const int row = split_index<Tl::FM>(m0, hm, i), p = row / N1, a = row - p * N1;
-      if (p >= np) continue;
-      float* dst = slots + (size_t)s_slot[p] * SL + a * C;
-      if constexpr (Tl::FN % 4 == 0) {
-#pragma unroll
-        for (int j = 0; j < Tl::FN; j += 4)
-          *reinterpret_cast<float4*>(dst + split_index<Tl::FN>(n0, hn, j)) =
-              make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < Tl::FN; ++j) dst[n0 + j] = acc[i][j];
+  for (int chunk = split; chunk < nchunks; chunk += nsplit) {
+    if (chunk != split) {
+      __syncthreads();  // previous chunk's GEMM done with s_g1t / s_slot
+      collect_chunk(pmap, pslot, g, true, i2, chunk, ch, s_free, s_slot, s_w, &np);
+    }
+    if constexpr (kVecStage<D>) {
+      constexpr int R1c = FixT<D>::r1, N1c = FixT<D>::n1, RQ = R1c / 4;  // float4 per G1 row
+#pragma unroll 4
+      for (int e = threadIdx.x; e < M * RQ; e += kBlock) {
+        const int row = e / RQ, q = e - row * RQ;
+        const int p = row / N1c, a = row - p * N1c;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (p < np) v = __ldg(reinterpret_cast<const float4*>(G1 + ((size_t)s_free[p] * N1c + a) * R1c) + q);
+        s_g1t[(4 * q + 0) * M + row] = v.x;
+        s_g1t[(4 * q + 1) * M + row] = v.y;
+        s_g1t[(4 * q + 2) * M + row] = v.z;
+        s_g1t[(4 * q + 3) * M + row] = v.w;
+      }
+    } else {
+      for (int e = threadIdx.x; e < M * R1; e += kBlock) {
+        const int row = e / R1, r = e - row * R1;
+        const int p = row / N1, a = row - p * N1;
+        s_g1t[r * M + row] = p < np ? G1[((size_t)s_free[p] * N1 + a) * R1 + r] : 0.f;
       }
     }
-  });
+    __syncthreads();
+    gemm_kk<Tl::FM, Tl::FN>(M, C, R1, s_g1t, M, s_g2, C,
+                            [&](int m0, int n0, int hm, int hn, float (&acc)[Tl::FM][Tl::FN]) {
+#pragma unroll
+      for (int i = 0; i < Tl::FM; ++i) {
+        const int row = split_index<Tl::FM>(m0, hm, i), p = row / N1, a = row - p * N1;
+        if (p >= np) continue;
+        float* dst = slots + (size_t)s_slot[p] * SL + a * C;
+        if constexpr (Tl::FN % 4 == 0) {
+#pragma unroll
+          for (int j = 0; j < Tl::FN; j += 4)
+            *reinterpret_cast<float4*>(dst + split_index<Tl::FN>(n0, hn, j)) =
+                make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < Tl::FN; ++j) dst[n0 + j] = acc[i][j];
+        }
+      }
+    });
+  }
 }
 
 // ------------------------------------------------------------ K3: close + pool
@@ -341,19 +377,22 @@ __global__ void __launch_bounds__(kBlock) k_close_pool(D d, KGeom g, const float
   float* s_h = s_sb + dX(d) * (d.r2 + 1);
   float* s_o = s_h + dG3s(d);
   const int gw = blockIdx.x * (kBlock / 32) + w, nw = gridDim.x * (kBlock / 32);
-  if constexpr (kFastRows<D>) {
-    // lane <-> r2 fast path for single-index bags (pooling 1), metadata for
-    // 32 bags fetched at once and the next bag's operands prefetched.
-    constexpr int Xc = FixT<D>::n1 * FixT<D>::n2, NN = Xc * 4, SLc = Xc * 32, LS = 36;
-    static_assert(NN == 64 || NN == 32 || NN == 128, "fast close layout");
-    float* f_sb = s_sb;          // Xc x LS (padded rows)
-    float* f_ht = s_sb + Xc * LS; // 4 x LS: H transposed [j][r2]
+  if constexpr (kFastRows<D> && FixT<D>::n1 * FixT<D>::n2 == 16) {
+    // Single-index bags (pooling 1): out[x][j] = sum_r slot[x][r] G3[r][j].
+    // Lane pair (x, h) owns slot row x, half h of r: its 16 slot values come
+    // straight from global (2 KB per bag, one coalesced sweep), the 32 x 4 G3
+    // slice is staged once in smem and read as broadcast float4s, and the two
+    // halves are combined with one shuffle. Bag metadata is fetched 32 bags at
+    // a time and the next bag's operands are prefetched.
+    float* f_h = s_sb;  // 32 r x 4 j, the r >= 16 half shifted by 4 floats (bank split)
     const unsigned m3n3 = g.m3 * 4u;
-    for (int b0 = gw * 32; b0 < B; b0 += nw * 32) {
+    const int x = lane >> 1, hf = lane & 1;
+    constexpr int kGrp = 8;  // bags per warp iteration: many warps in flight
+    for (int b0 = gw * kGrp; b0 < B; b0 += nw * kGrp) {
       const int b = b0 + lane;
       int o0 = 0, o1 = 0, sg0 = 0, sg1 = 0, slot = 0;
       unsigned i3 = 0;
-      if (b < B) {
+      if (lane < kGrp && b < B) {
         o0 = bag_off[b];
         o1 = bag_off[b + 1];
         sg0 = bag_seg[b];
@@ -363,17 +402,16 @@ __global__ void __launch_bounds__(kBlock) k_close_pool(D d, KGeom g, const float
           i3 = keys32[o0] % g.m3;
         }
       }
-      const int nb = min(32, B - b0);
-      const unsigned simple = __ballot_sync(0xffffffffu, b < B && o1 - o0 == 1);
-      // prefetch registers for the first simple bag
-      float4 pre_sb[SLc / 128], pre_h;
+      const int nb = min(kGrp, B - b0);
+      const unsigned simple = __ballot_sync(0xffffffffu, lane < kGrp && b < B && o1 - o0 == 1);
+      float4 psb[4], ph;
       auto fetch = [&](int i) {
         const int sl = __shfl_sync(0xffffffffu, slot, i);
         const unsigned ii3 = __shfl_sync(0xffffffffu, i3, i);
-        const float4* src = reinterpret_cast<const float4*>(slots + (size_t)sl * SLc);
+        const float4* src = reinterpret_cast<const float4*>(slots + (size_t)sl * 512 + x * 32 + hf * 16);
 #pragma unroll
-        for (int k = 0; k < SLc / 128; ++k) pre_sb[k] = src[lane + 32 * k];
-        pre_h = __ldg(reinterpret_cast<const float4*>(G3 + (size_t)lane * m3n3 + ii3 * 4u));
+        for (int k = 0; k < 4; ++k) psb[k] = src[k];
+        ph = __ldg(reinterpret_cast<const float4*>(G3 + (size_t)lane * m3n3 + ii3 * 4u));
       };
       int next = simple ? __ffs(simple) - 1 : 32;
       if (next < nb) fetch(next);
@@ -385,42 +423,35 @@ __global__ void __launch_bounds__(kBlock) k_close_pool(D d, KGeom g, const float
                             keys32, s_sb, s_h, s_o, out);
           continue;
         }
-        // stage the prefetched operands, then prefetch the next simple bag
+        float sv[16];
 #pragma unroll
-        for (int k = 0; k < SLc / 128; ++k) {
-          const int e = 4 * (lane + 32 * k), x = e / 32, r = e - x * 32;
-          *reinterpret_cast<float4*>(f_sb + x * LS + r) = pre_sb[k];
+        for (int k = 0; k < 4; ++k) {
+          sv[4 * k] = psb[k].x;
+          sv[4 * k + 1] = psb[k].y;
+          sv[4 * k + 2] = psb[k].z;
+          sv[4 * k + 3] = psb[k].w;
         }
-        f_ht[0 * LS + lane] = pre_h.x;
-        f_ht[1 * LS + lane] = pre_h.y;
-        f_ht[2 * LS + lane] = pre_h.z;
-        f_ht[3 * LS + lane] = pre_h.w;
+        // lane r2 = lane stages its G3 row
+        *reinterpret_cast<float4*>(f_h + lane * 4 + (lane >= 16 ? 4 : 0)) = ph;
         const unsigned rest = simple & ~((2u << i) - 1u);
         next = rest ? __ffs(rest) - 1 : 32;
         if (next < nb) fetch(next);
         __syncwarp();
-        // outputs: N = Xc * 4; each lane computes NN / 32 of them
-        constexpr int PER = NN / 32;
-        float res[PER];
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
-        for (int q = 0; q < PER; ++q) {
-          const int o = lane * PER + q, x = o / 4, j = o - x * 4;
-          float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;  // 4 independent chains
-#pragma unroll
-          for (int r = 0; r < 32; r += 4) {
-            const float4 sv = *reinterpret_cast<const float4*>(f_sb + x * LS + r);
-            const float4 hv = *reinterpret_cast<const float4*>(f_ht + j * LS + r);
-            a0 = fmaf(sv.x, hv.x, a0);
-            a1 = fmaf(sv.y, hv.y, a1);
-            a2 = fmaf(sv.z, hv.z, a2);
-            a3 = fmaf(sv.w, hv.w, a3);
-          }
-          res[q] = (a0 + a1) + (a2 + a3);
+        for (int k = 0; k < 16; ++k) {
+          const int r = hf * 16 + k;
+          const float4 hv = *reinterpret_cast<const float4*>(f_h + r * 4 + hf * 4);
+          a0 = fmaf(sv[k], hv.x, a0);
+          a1 = fmaf(sv[k], hv.y, a1);
+          a2 = fmaf(sv[k], hv.z, a2);
+          a3 = fmaf(sv[k], hv.w, a3);
         }
-        float* dst = out + (size_t)(b0 + i) * NN + lane * PER;
-        if constexpr (PER == 2) *reinterpret_cast<float2*>(dst) = make_float2(res[0], res[1]);
-        else if constexpr (PER == 4) *reinterpret_cast<float4*>(dst) = make_float4(res[0], res[1], res[2], res[3]);
-        else dst[0] = res[0];
+        // combine the two r halves: lane h keeps outputs j = 2h, 2h + 1
+        const float s0 = hf ? a0 : a2, s1 = hf ? a1 : a3;
+        const float r0 = __shfl_xor_sync(0xffffffffu, s0, 1), r1 = __shfl_xor_sync(0xffffffffu, s1, 1);
+        const float o_0 = (hf ? a2 : a0) + r0, o_1 = (hf ? a3 : a1) + r1;
+        *reinterpret_cast<float2*>(out + (size_t)(b0 + i) * 64 + x * 4 + hf * 2) = make_float2(o_0, o_1);
         __syncwarp();
       }
     }
@@ -448,10 +479,11 @@ __global__ void __launch_bounds__(kBlock) k_row_agg(D d, int B, const int* __res
   const int U = counts[3];
   bool bad = false;
   const int gw = blockIdx.x * (kBlock / 32) + w, nw = gridDim.x * (kBlock / 32);
-  for (int u0 = gw * 32; u0 < U; u0 += nw * 32) {
+  constexpr int kGrp = 8;  // rows per warp iteration: many warps in flight
+  for (int u0 = gw * kGrp; u0 < U; u0 += nw * kGrp) {
     const int u = u0 + lane;
     int q0 = 0, q1 = 0, bb = 0;
-    if (u < U) {
+    if (lane < kGrp && u < U) {
       q0 = urow_start[u];
       q1 = urow_start[u + 1];
       if (q1 - q0 == 1) {
@@ -459,8 +491,8 @@ __global__ void __launch_bounds__(kBlock) k_row_agg(D d, int B, const int* __res
         bb = bb < 0 ? 0 : (bb >= B ? B - 1 : bb);  // malformed offsets: garbage ids, never OOB
       }
     }
-    const int nr = min(32, U - u0);
-    const unsigned single = __ballot_sync(0xffffffffu, u < U && q1 - q0 == 1);
+    const int nr = min(kGrp, U - u0);
+    const unsigned single = __ballot_sync(0xffffffffu, lane < kGrp && u < U && q1 - q0 == 1);
     if constexpr (FixT<D>::n1 * FixT<D>::n2 * FixT<D>::n3 == 64) {
       for (int i0 = 0; i0 < nr; i0 += 8) {
         float2 v[8];
@@ -510,7 +542,7 @@ __global__ void __launch_bounds__(kBlock) k_row_agg(D d, int B, const int* __res
 // This regroups backward.py:152-178 (per-row chains) so the r1 x n2 r2
 // products run per distinct prefix; the sums are identical.
 template <class D>
-__global__ void __launch_bounds__(kBlock) k_bwd_prefix(D d, KGeom g, int ch, const float* __restrict__ G1,
+__global__ void __launch_bounds__(kBlock, 3) k_bwd_prefix(D d, KGeom g, int ch, const float* __restrict__ G1,
                                                        const float* __restrict__ G2, const float* __restrict__ G3,
                                                        const unsigned* __restrict__ pmap, const int* __restrict__ pslot,
                                                        const float* __restrict__ slots,
@@ -522,13 +554,16 @@ __global__ void __launch_bounds__(kBlock) k_bwd_prefix(D d, KGeom g, int ch, con
                                                        int* __restrict__ grp_cnt, int cmax) {
   extern __shared__ __align__(16) float smem[];
   __shared__ int s_free[kMaxChunk], s_slot[kMaxChunk], s_w[kBlock / 32 + 2];
+  __shared__ int s_next;
   const int C = dC(d), R1 = d.r1, R2 = d.r2, N1 = d.n1, N2 = d.n2, N3 = d.n3, X = dX(d), N = dN(d);
-  const int SL = dSlot(d), G3S = dG3s(d), G1S = dG1s(d);
+  const int SL = dSlot(d), G3S = dG3s(d), G1S = dG1s(d), G2S = dG2s(d);
   const unsigned i2 = blockIdx.x;
+  const int split = blockIdx.y, nsplit = gridDim.y;
   int np;
-  const int total = collect_chunk(pmap, pslot, g, true, i2, blockIdx.y, ch, s_free, s_slot, s_w, &np);
-  if (blockIdx.y == 0 && threadIdx.x == 0) grp_cnt[i2] = total;
-  if (np == 0) return;
+  const int total = collect_chunk(pmap, pslot, g, true, i2, split, ch, s_free, s_slot, s_w, &np);
+  if (split == 0 && threadIdx.x == 0) grp_cnt[i2] = total;
+  const int nchunks = (total + ch - 1) / ch;
+  if (split >= nchunks) return;
   const int M = ch * N1;
   const int LZ = pad_ld(d);
   float* s_z = smem;                 // M x LZ      Z rows (p, a), cols c = b r2 + r
@@ -536,14 +571,30 @@ __global__ void __launch_bounds__(kBlock) k_bwd_prefix(D d, KGeom g, int ch, con
   float* s_g1 = s_g2 + R1 * LZ;      // M x R1      G1 chunk [(p, a)][r1]  (k-major for phase B)
   float* s_wk = s_g1 + M * R1;       // per warp: g (N) + G3 slice (G3S) + slot (SL)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  using Tl = Tiles<D>;
+  // G2 slice: staged once per CTA
   if constexpr (kVecStage<D>) {
-    constexpr int C4 = FixT<D>::n2 * FixT<D>::r2 / 4, R1c = FixT<D>::r1, RQ = R1c / 4;
+    constexpr int C4 = FixT<D>::n2 * FixT<D>::r2 / 4, R1c = FixT<D>::r1;
 #pragma unroll 4
     for (int e = threadIdx.x; e < R1c * C4; e += kBlock) {
       const int r = e / C4, c4 = e - r * C4;
       *reinterpret_cast<float4*>(s_g2 + r * LZ + 4 * c4) =
           __ldg(reinterpret_cast<const float4*>(G2 + ((size_t)r * g.m2 + i2) * C) + c4);
     }
+  } else {
+    for (int e = threadIdx.x; e < R1 * C; e += kBlock) {
+      const int r = e / C, c = e - r * C;
+      s_g2[r * LZ + c] = G2[((size_t)r * g.m2 + i2) * C + c];
+    }
+  }
+  for (int chunk = split; chunk < nchunks; chunk += nsplit) {
+  if (chunk != split) {
+    __syncthreads();  // previous chunk's phases done with s_z / s_g1 / s_slot
+    collect_chunk(pmap, pslot, g, true, i2, chunk, ch, s_free, s_slot, s_w, &np);
+  }
+  if (threadIdx.x == 0) s_next = 0;
+  if constexpr (kVecStage<D>) {
+    constexpr int R1c = FixT<D>::r1, RQ = R1c / 4;
 #pragma unroll 4
     for (int e = threadIdx.x; e < M * RQ; e += kBlock) {
       const int row = e / RQ, q = e - row * RQ;
@@ -553,16 +604,13 @@ __global__ void __launch_bounds__(kBlock) k_bwd_prefix(D d, KGeom g, int ch, con
       reinterpret_cast<float4*>(s_g1)[e] = v;
     }
   } else {
-    for (int e = threadIdx.x; e < R1 * C; e += kBlock) {
-      const int r = e / C, c = e - r * C;
-      s_g2[r * LZ + c] = G2[((size_t)r * g.m2 + i2) * C + c];
-    }
     for (int e = threadIdx.x; e < M * R1; e += kBlock) {
       const int row = e / R1, r = e - row * R1;
       const int p = row / N1, a = row - p * N1;
       s_g1[e] = p < np ? G1[((size_t)s_free[p] * N1 + a) * R1 + r] : 0.f;
     }
   }
+  __syncthreads();  // s_next visible before the dynamic prefix hand-out
   // ---- phase A
   if constexpr (kFastRows<D>) {
     // lane <-> r2; the slot column, Z column and one row's G3 slice live in
@@ -571,7 +619,12 @@ __global__ void __launch_bounds__(kBlock) k_bwd_prefix(D d, KGeom g, int ch, con
     constexpr int Xc = FixT<D>::n1 * FixT<D>::n2, NN = Xc * 4, N2c = FixT<D>::n2;
     float* s_gw = s_wk + w * (2 * NN);
     const unsigned m3n3 = g.m3 * 4u;
-    for (int pi = w; pi < np; pi += kBlock / 32) {
+    // prefixes are handed to warps dynamically (row counts differ per prefix)
+    for (;;) {
+      int pi = 0;
+      if (lane == 0) pi = atomicAdd(&s_next, 1);
+      pi = __shfl_sync(0xffffffffu, pi, 0);
+      if (pi >= np) break;
       const int slot = s_slot[pi];
       const float* sb = slots + (size_t)slot * (Xc * 32);
       float sbc[Xc], zr[Xc];
@@ -699,10 +752,9 @@ __global__ void __launch_bounds__(kBlock) k_bwd_prefix(D d, KGeom g, int ch, con
     for (int e = np * N1 * LZ + threadIdx.x; e < M * LZ; e += kBlock) s_z[e] = 0.f;
   }
   __syncthreads();
-  using Tl = Tiles<D>;
-  // ---- phase B: dG2 partial = G1_chunk^T . Z_chunk
+  // ---- phase B: this chunk's dG2 partial = G1_chunk^T . Z_chunk
   {
-    float* part = dG2part + ((size_t)i2 * cmax + blockIdx.y) * dG2s(d);
+    float* part = dG2part + ((size_t)i2 * cmax + chunk) * G2S;
     gemm_kk<Tl::BM, Tl::BN>(R1, C, np * N1, s_g1, R1, s_z, LZ,
                             [&](int m0, int n0, int hm, int hn, float (&acc)[Tl::BM][Tl::BN]) {
 #pragma unroll
@@ -728,6 +780,7 @@ __global__ void __launch_bounds__(kBlock) k_bwd_prefix(D d, KGeom g, int ch, con
       if (p < np) E[(size_t)s_slot[p] * G1S + a * R1 + n0] = acc[i][0];
     }
   });
+  }  // chunk loop
 }
 
 }  // namespace ttb
