@@ -154,13 +154,10 @@ def run_ours(args):
                          max_bags=cfg["batch"], device=dev, check_errors=False)
     shape, eng = emb.shape, emb.engine
     # flat parameter / grad / velocity buffers (cores are views) for the DP path
-    sizes = [math.prod(shape.core_extent(k)) for k in range(3)]
-    flat_p = torch.cat([c.detach().reshape(-1) for c in emb.cores]).contiguous()
-    cores = [v.view(shape.core_extent(k)) for k, v in enumerate(torch.split(flat_p, sizes))]
-    flat_g = torch.zeros_like(flat_p)
-    grads = [v.view(shape.core_extent(k)) for k, v in enumerate(torch.split(flat_g, sizes))]
-    flat_v = torch.zeros(flat_p.numel(), dtype=torch.float64, device=dev)
-    vel = [v.view(shape.core_extent(k)) for k, v in enumerate(torch.split(flat_v, sizes))]
+    from paper_2507_14668_b200 import dp
+    flat = dp.FlatCores(emb.cores, device=dev)
+    cores, grads, vel = flat.cores, flat.grads, flat.velocities
+    flat_p, flat_g, flat_v = flat.param, flat.grad, flat.velocity
 
     idx_h, off_h, gout_h = synthetic_batch(rank, cfg)
     idx = torch.from_numpy(idx_h).to(dev)
@@ -176,7 +173,7 @@ def run_ours(args):
             eng.backward_sgd(cores, gout, LR, MU, vel)
         else:
             eng.backward(cores, gout, grads=grads)
-            dist.all_reduce(flat_g)
+            dp.allreduce_grads(flat_g)  # NCCL SUM over ranks: the DP exchange step
             nat.check(lib.ttb_sgd_update(_ptr(flat_p), _ptr(flat_g), _ptr(flat_v), flat_p.numel(), LR, MU,
                                          _stream()))
 
@@ -297,11 +294,16 @@ def profile_and_roofline(args, torch, eng, lib, emb, step, flush, st, dev):
     hbm = peaks["hbm_gbs"]
     step_us = sum(v["us_per_step"] for v in kernels.values())
     dk = kernels[dominant]
+    traffic = None
+    tp = ROOT / "profiles" / "ncu_traffic.json"
+    if tp.exists():  # from one committed `ncu --set full` capture (profiles/summarize.py traffic)
+        traffic = json.loads(tp.read_text())["bytes_per_launch"].get(dominant)
     if dominant in fl:
         achieved = fl[dominant] / (dk["avg_us"] * 1e-6) / 1e12
         roof = {"bound": "fp32", "kernel": dominant, "achieved": achieved, "peak": best, "unit": "TFLOP/s",
                 "frac": achieved / best, "peak_source": "measured FP32 FMA probe (ttb_fma_peak) on this GPU",
-                "algorithmic_flops_per_launch": fl[dominant], "traffic": None}
+                "algorithmic_flops_per_launch": fl[dominant], "traffic": traffic,
+                "traffic_unit": "bytes/launch (DRAM read+write, ncu --set full, cold cache)"}
     else:
         # integer / sort kernels: bytes moved per launch (keys+values read and written)
         T = st["T"]
@@ -310,7 +312,7 @@ def profile_and_roofline(args, torch, eng, lib, emb, step, flush, st, dev):
         achieved = nbytes / (dk["avg_us"] * 1e-6) / 1e9
         roof = {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                "algorithmic_bytes_per_launch": nbytes, "traffic": None}
+                "algorithmic_bytes_per_launch": nbytes, "traffic": traffic}
     t_flop = (fwd + bwd) / (best * 1e12)
     t_mem = step_bytes / (hbm * 1e9)
     t_roof = max(t_flop, t_mem)

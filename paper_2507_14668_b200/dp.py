@@ -1,0 +1,90 @@
+"""Data-parallel TT-EmbeddingBag training (Rec-AD DP).
+
+One process per GPU, `torch.distributed` with NCCL. TT cores are replicated;
+the batch is sharded by contiguous bag ranges; every rank computes its core
+gradients into ONE flat fp32 buffer, the buffer is all-reduced (SUM), and
+every rank applies the same SGD(+momentum) step (fp64 velocity, one rounding:
+backward.py:186-204), so replicas stay bitwise identical.
+
+The host-side pieces (sharding, flat buffers, the all-reduce) are plain
+torch and are exercised on CPU with the gloo backend (tests/test_dp.py); the
+compute runs through TtEngine (CUDA only).
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+import torch.distributed as dist
+
+
+def shard_bags(offsets: torch.Tensor, rank: int, world: int):
+    """Contiguous bag range [b0, b1) of `rank` and its index range [t0, t1)
+    for (B+1)-style offsets. Bags are split as evenly as possible."""
+    B = offsets.numel() - 1
+    b0 = (B * rank) // world
+    b1 = (B * (rank + 1)) // world
+    t0, t1 = int(offsets[b0]), int(offsets[b1])
+    return b0, b1, t0, t1
+
+
+def local_batch(indices: torch.Tensor, offsets: torch.Tensor, rank: int, world: int):
+    """This rank's (indices, offsets) slice, offsets rebased to 0."""
+    b0, b1, t0, t1 = shard_bags(offsets, rank, world)
+    return indices[t0:t1], offsets[b0:b1 + 1] - offsets[b0], (b0, b1)
+
+
+class FlatCores:
+    """Flat fp32 parameter and gradient buffers and an fp64 velocity buffer,
+    with per-core views in the reference layout (r_{k-1}, m_k n_k, r_k)."""
+
+    def __init__(self, cores, device=None):
+        cores = [c.detach() for c in cores]
+        dev = device if device is not None else cores[0].device
+        self.shapes = [tuple(c.shape) for c in cores]
+        self.sizes = [math.prod(s) for s in self.shapes]
+        self.param = torch.cat([c.reshape(-1).to(dev, torch.float32) for c in cores]).contiguous()
+        self.grad = torch.zeros_like(self.param)
+        self.velocity = torch.zeros(self.param.numel(), dtype=torch.float64, device=dev)
+
+    def _views(self, flat):
+        return [v.view(s) for v, s in zip(torch.split(flat, self.sizes), self.shapes)]
+
+    @property
+    def cores(self):
+        return self._views(self.param)
+
+    @property
+    def grads(self):
+        return self._views(self.grad)
+
+    @property
+    def velocities(self):
+        return self._views(self.velocity)
+
+
+def allreduce_grads(flat_grad: torch.Tensor, group=None, scale: float | None = None) -> torch.Tensor:
+    """SUM all-reduce of the flat gradient buffer (in place). `scale` (e.g.
+    local_B / global_B for a batch-mean loss, model.py:85-86) is applied on
+    the local contribution before the reduction."""
+    if scale is not None and scale != 1.0:
+        flat_grad.mul_(scale)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(flat_grad, op=dist.ReduceOp.SUM, group=group)
+    return flat_grad
+
+
+def dp_step(engine, flat: FlatCores, indices, offsets, grad_out, lr: float, momentum: float = 0.0, group=None):
+    """One data-parallel step on this rank's shard: plan, forward (returned),
+    core gradients, all-reduce, SGD(+momentum) on the flat buffers."""
+    from . import _native as nat
+    from .engine import _ptr, _stream
+
+    engine.plan(indices, offsets)
+    out = engine.forward(flat.cores)
+    engine.backward(flat.cores, grad_out, grads=flat.grads)
+    allreduce_grads(flat.grad, group)
+    lib = nat.load()
+    nat.check(lib.ttb_sgd_update(_ptr(flat.param), _ptr(flat.grad), _ptr(flat.velocity) if momentum > 0 else None,
+                                 flat.param.numel(), float(lr), float(momentum), _stream()), "sgd_update")
+    return out

@@ -274,3 +274,28 @@ def test_config2_full_size_properties():
     want = O.core_grads(c64, g, ur, ug)
     for k in range(3):
         assert rel_err(gs[k].cpu().numpy(), want[k]) < GRAD_TOL
+
+
+def test_dp_step_matches_fused_update():
+    """dp.dp_step (gradients -> flat all-reduce -> ttb_sgd_update), here on
+    one process, lands on the same bits as the fused backward + SGD path."""
+    from paper_2507_14668_b200 import dp
+    from paper_2507_14668_b200.engine import TtEngine
+    from paper_2507_14668_b200.geometry import TtShape, init_random_cores
+    shape = TtShape((20, 20, 25), (4, 4, 4), (1, 32, 32, 1))
+    host = init_random_cores(shape, 7)
+    rng = np.random.default_rng(8)
+    idx, off = random_batch(rng, shape.rows, 256, 3, skew=True)
+    ti, to = torch.from_numpy(idx).cuda(), torch.from_numpy(off).cuda()
+    gout = torch.from_numpy(rng.standard_normal((256, 64)).astype(np.float32)).cuda()
+    e1, e2 = TtEngine(shape, 4096, 4096), TtEngine(shape, 4096, 4096)
+    flat = dp.FlatCores([torch.from_numpy(c).cuda() for c in host])
+    fused = dp.FlatCores([torch.from_numpy(c).cuda() for c in host])
+    for _ in range(3):
+        dp.dp_step(e1, flat, ti, to, gout, 0.05, 0.9)
+        e2.plan(ti, to)
+        e2.forward(fused.cores)
+        e2.backward_sgd(fused.cores, gout, 0.05, 0.9, fused.velocities)
+    torch.cuda.synchronize()
+    assert torch.equal(flat.param, fused.param)
+    assert torch.equal(flat.velocity, fused.velocity)
