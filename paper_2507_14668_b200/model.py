@@ -1,0 +1,218 @@
+"""DLRM-style model with TT-EmbeddingBag fields, on the GPU.
+
+Mirrors the reference's model module (pkg/src/ttemb/model.py):
+
+    ModelConfig            model.py:34-65
+    loss / logit gradient  model.py:68-86   (BCE on the sigmoid, MSE)
+    feature_interaction    model.py:106-112 (concat(v0, pairwise dots, lexicographic))
+    Mlp                    model.py:134-173 (ReLU between, linear output)
+    FieldTable             model.py:179-243 (TT above tt_threshold, dense below)
+    DlrmModel              model.py:249-365 (init order, forward, train_step)
+
+The TT fields run on the CUDA TT-EmbeddingBag (TTEmbeddingBag); the dense
+MLPs, the interaction and the small dense fields stay in PyTorch (north star
+item 4). Initialisation draws from ONE seeded numpy stream in the reference's
+order, so a model built here starts from the reference's exact parameters;
+train_step applies the reference's SGD(+momentum) — fp64 velocity, one
+rounding into fp32 — through the library's ttb_sgd_update kernel (the TT cores
+take the same step inside their backward kernels).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+from torch import nn
+
+from . import _native as nat
+from .embedding_bag import TTEmbeddingBag
+from .engine import _ptr, _stream, require_cuda, to_offsets
+from .geometry import factorize_dims
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    n_dense: int
+    rows_per_field: tuple
+    emb_dim: int = 16
+    ranks: tuple = (1, 8, 8, 1)
+    tt_threshold: int = 1000
+    bottom_sizes: tuple = (64,)
+    top_sizes: tuple = (64, 32)
+    loss: str = "bce"
+    seed: int = 0
+
+    def validate(self) -> None:
+        if self.n_dense < 1 or self.emb_dim < 1 or not self.rows_per_field:
+            raise ValueError("need dense features, an embedding dim, and fields")
+        if any(r < 1 for r in self.rows_per_field):
+            raise ValueError("every field needs at least one row")
+        if self.loss not in ("bce", "mse"):
+            raise ValueError(f"unknown loss {self.loss!r}")
+        if self.tt_threshold < 1:
+            raise ValueError("tt_threshold must be positive")
+        if len(self.ranks) < 3 or self.ranks[0] != 1 or self.ranks[-1] != 1:
+            raise ValueError("ranks must be (1, r_1, .., 1) with d >= 2 cores")
+
+    @property
+    def n_sparse(self) -> int:
+        return len(self.rows_per_field)
+
+    @property
+    def interaction_dim(self) -> int:
+        v = self.n_sparse + 1
+        return self.emb_dim + v * (v - 1) // 2
+
+
+def feature_interaction(vectors: Sequence[torch.Tensor]) -> torch.Tensor:
+    """concat(vectors[0], all pairwise dots), pairs (0,1), (0,2), .., (1,2).."""
+    stack = torch.stack(list(vectors), dim=1)  # (B, v, D)
+    gram = torch.bmm(stack, stack.transpose(1, 2))
+    iu = torch.triu_indices(stack.shape[1], stack.shape[1], offset=1, device=stack.device)
+    return torch.cat([vectors[0], gram[:, iu[0], iu[1]]], dim=1)
+
+
+class Mlp(nn.Module):
+    def __init__(self, sizes: Sequence[int], rng: np.random.Generator, device):
+        super().__init__()
+        if len(sizes) < 2 or any(s < 1 for s in sizes):
+            raise ValueError("MLP needs positive layer sizes, input to output")
+        self.sizes = tuple(int(s) for s in sizes)
+        last = len(sizes) - 2
+        ws, bs = [], []
+        for i, (fin, fout) in enumerate(zip(sizes[:-1], sizes[1:])):
+            scale = math.sqrt((2.0 if i < last else 1.0) / fin)
+            w = (rng.standard_normal((fin, fout)) * scale).astype(np.float32)
+            ws.append(nn.Parameter(torch.from_numpy(w).to(device)))
+            bs.append(nn.Parameter(torch.zeros(fout, dtype=torch.float32, device=device)))
+        self.weights = nn.ParameterList(ws)
+        self.biases = nn.ParameterList(bs)
+
+    def forward(self, x):
+        n = len(self.weights)
+        for i in range(n):
+            x = torch.addmm(self.biases[i], x, self.weights[i])
+            if i < n - 1:
+                x = torch.relu(x)
+        return x
+
+
+class DenseField(nn.Module):
+    """Small field below tt_threshold: plain (rows, dim) table, sum pooling."""
+
+    def __init__(self, rows: int, dim: int, seed: int, device):
+        super().__init__()
+        rng = np.random.default_rng(seed)
+        w = (rng.standard_normal((rows, dim)) * 0.1).astype(np.float32)
+        self.rows = nn.Parameter(torch.from_numpy(w).to(device))
+
+    def forward(self, indices, offsets):
+        if indices.numel() and (int(indices.min()) < 0 or int(indices.max()) >= self.rows.shape[0]):
+            raise ValueError(f"index outside [0, {self.rows.shape[0]})")
+        return torch.nn.functional.embedding_bag(indices, self.rows, offsets[:-1], mode="sum")
+
+
+class DlrmModel(nn.Module):
+    def __init__(self, config: ModelConfig, device=None, max_indices: int = 1 << 16, check_errors: bool = True):
+        super().__init__()
+        config.validate()
+        self.config = config
+        dev = require_cuda(device)
+        self.device = dev
+        rng = np.random.default_rng(config.seed)
+        fields = []
+        for rows in config.rows_per_field:
+            seed = int(rng.integers(2 ** 31))
+            if rows >= config.tt_threshold:
+                fields.append(TTEmbeddingBag(rows, config.emb_dim, config.ranks, seed=seed, device=dev,
+                                             include_last_offset=True, max_indices=max_indices,
+                                             check_errors=check_errors))
+            else:
+                fields.append(DenseField(rows, config.emb_dim, seed, dev))
+        self.fields = nn.ModuleList(fields)
+        self.bottom = Mlp((config.n_dense, *config.bottom_sizes, config.emb_dim), rng, dev)
+        self.top = Mlp((config.interaction_dim, *config.top_sizes, 1), rng, dev)
+        self._velocity: dict = {}
+
+    # ------------------------------------------------------------ parameters
+    def named_ref_params(self):
+        """(reference name, tensor) in DlrmModel.named_params order (model.py:272-282)."""
+        out = []
+        for f, fld in enumerate(self.fields):
+            if isinstance(fld, TTEmbeddingBag):
+                out.extend((f"field_{f}.core{k}", c) for k, c in enumerate(fld.cores))
+            else:
+                out.append((f"field_{f}.rows", fld.rows))
+        for i in range(len(self.bottom.weights)):
+            out.append((f"bottom.{i}.w", self.bottom.weights[i]))
+            out.append((f"bottom.{i}.b", self.bottom.biases[i]))
+        for i in range(len(self.top.weights)):
+            out.append((f"top.{i}.w", self.top.weights[i]))
+            out.append((f"top.{i}.b", self.top.biases[i]))
+        return out
+
+    # ------------------------------------------------------------ forward
+    def forward(self, dense: torch.Tensor, sparse) -> torch.Tensor:
+        """dense (B, n_dense) fp32; sparse: per field (indices, offsets (B+1))."""
+        if len(sparse) != self.config.n_sparse:
+            raise ValueError("batch field count != model field count")
+        v0 = self.bottom(dense)
+        vectors = [v0]
+        for fld, (idx, off) in zip(self.fields, sparse):
+            vectors.append(fld(idx, off))
+        inter = feature_interaction(vectors)
+        return self.top(inter).reshape(-1)
+
+    def loss_and_logit_grad(self, z: torch.Tensor, y: torch.Tensor):
+        """model.py:77-86: loss value (fp64) and dL/dz = (sigmoid(z) - y) / B."""
+        z64, y64 = z.detach().double(), y.double()
+        if self.config.loss == "bce":
+            p = torch.sigmoid(z64)
+            pc = p.clamp(1e-7, 1.0 - 1e-7)
+            loss = -(y64 * torch.log(pc) + (1.0 - y64) * torch.log(1.0 - pc)).mean()
+            gz = (p - y64) / z.numel()
+        else:
+            loss = ((z64 - y64) ** 2).mean()
+            gz = 2.0 * (z64 - y64) / z.numel()
+        return loss, gz.to(torch.float32)
+
+    # ------------------------------------------------------------ train step
+    def train_step(self, dense, sparse, labels, lr: float, momentum: float = 0.0, sync_loss: bool = True):
+        """One SGD(+momentum) step over every parameter (model.py:347-365).
+        TT cores are updated inside their backward kernels; everything else by
+        ttb_sgd_update (fp64 velocity, one rounding)."""
+        if lr < 0 or not 0.0 <= momentum < 1.0:
+            raise ValueError("need lr >= 0 and 0 <= momentum < 1")
+        for fld in self.fields:
+            if isinstance(fld, TTEmbeddingBag):
+                fld.enable_fused_sgd(lr, momentum)
+        for p in self.parameters():
+            p.grad = None
+        z = self.forward(dense, sparse)
+        loss, gz = self.loss_and_logit_grad(z, labels)
+        z.backward(gz)
+        lib = nat.load()
+        with torch.no_grad():
+            for name, p in self.named_ref_params():
+                if ".core" in name:
+                    continue  # TT cores: fused update already applied
+                g = p.grad if p.grad is not None else torch.zeros_like(p)
+                g = g.contiguous()
+                v = None
+                if momentum > 0.0:
+                    v = self._velocity.get(name)
+                    if v is None:
+                        v = torch.zeros(p.shape, dtype=torch.float64, device=p.device)
+                        self._velocity[name] = v
+                nat.check(lib.ttb_sgd_update(_ptr(p), _ptr(g), _ptr(v), p.numel(), float(lr), float(momentum),
+                                             _stream()), "sgd_update")
+        return float(loss) if sync_loss else loss
+
+
+def bags_field_tensors(bags_per_field, device):
+    """Reference Dataset.bags (field -> sample -> bag) -> [(indices, offsets)]."""
+    from .engine import bags_to_tensors
+    return [bags_to_tensors(bags, device) for bags in bags_per_field]

@@ -1,0 +1,38 @@
+"""DLRM with TT fields on the GPU vs the unmodified reference's DlrmModel
+(golden run in tests/golden/dlrm.npz: fp32 model, 3 SGD+momentum steps)."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def test_dlrm_matches_reference_run(golden):
+    from paper_2507_14668_b200.model import DlrmModel, ModelConfig, bags_field_tensors
+    torch.backends.cuda.matmul.allow_tf32 = False
+    s = golden("dlrm")
+    cfg = ModelConfig(n_dense=6, rows_per_field=(4000, 500, 118), emb_dim=16, ranks=(1, 4, 4, 1), tt_threshold=1000,
+                      bottom_sizes=(32,), top_sizes=(32, 16), loss="bce", seed=5)
+    model = DlrmModel(cfg)
+    params = dict(model.named_ref_params())
+    # initialisation: same seeded stream, same order -> identical bits
+    for name, p in params.items():
+        assert np.array_equal(p.detach().cpu().numpy(), s[f"init.{name}"]), name
+    dense = torch.from_numpy(s["data.dense"].astype(np.float32)).cuda()
+    labels = torch.from_numpy(s["data.labels"]).cuda()
+    bs = 32
+    for step in range(3):
+        lo, hi = step * bs, (step + 1) * bs
+        sparse = []
+        for f in range(3):
+            idx, off = s[f"data.idx{f}"], s[f"data.off{f}"]
+            sub_idx = idx[off[lo]:off[hi]]
+            sub_off = off[lo:hi + 1] - off[lo]
+            sparse.append((torch.from_numpy(sub_idx).cuda(), torch.from_numpy(sub_off).cuda()))
+        loss = model.train_step(dense[lo:hi], sparse, labels[lo:hi], lr=0.05, momentum=0.9)
+        assert abs(loss - s["losses"][step]) <= 1e-5 * max(1.0, abs(s["losses"][step])), (step, loss)
+        for name, p in params.items():
+            got = p.detach().cpu().numpy().astype(np.float64)
+            want = s[f"step{step}.{name}"].astype(np.float64)
+            err = np.abs(got - want).max() / max(1e-3, np.abs(want).max())
+            assert err < 1e-4, (step, name, err)
