@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=8192, help="lookups in the CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip configs 1/3/4 (reported under extras)")
     ap.add_argument("--quick", action="store_true", help="skip extras (for ncu launch lists)")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of replaying a CUDA graph")
     return ap.parse_args()
@@ -253,6 +254,9 @@ def run_ours(args):
             result["e2e"] = e2e_run(args, torch, cfg, rank, dev, world)
         if world == 1 and not args.no_cpu_baseline:
             result["cpu_baseline"] = cpu_baseline(args, cfg)
+        if world == 1 and not args.no_extras:
+            import bench_extras
+            result["extras"] = bench_extras.run_all(dev)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -1,0 +1,152 @@
+"""Secondary BASELINE configs measured by bench.py (reported under "extras").
+
+    cfg1  Reference CPU Rec-AD DLRM: one TT field 1M x 16, ranks 16, batch 256,
+          FDIA-style bags of 1-3 Zipf(1.05) indices             -> samples/s
+    cfg3  26 TT tables 10M x 64, ranks 32, Zipf(1.05), pooling 20,
+          B = 65,536 bags per table, native and permuted ids     -> lookups/s
+    cfg4  Criteo-Kaggle-shaped TT-DLRM (13 dense, 26 sparse, 15 TT fields at
+          tt_threshold 1000), bottom 512-256-64, top 512-256-1,
+          B = 65,536, fp32 MLPs (TF32 off)                       -> samples/s
+
+Every step runs through the public API (TTEmbeddingBag / DlrmModel) and is
+replayed as one CUDA graph; timings are CUDA events over the timed steps.
+Synthetic data: Zipf by inverse CDF (same law as the reference's
+rng.choice(p=zipf_probs), data.py:103-108, 164; different random stream).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+KAGGLE_ROWS = (1460, 583, 10131227, 2202608, 305, 24, 12517, 633, 3, 93145, 5683, 8351593, 3194, 27, 14992,
+               5461306, 10, 5652, 2173, 4, 7046547, 18, 15, 286181, 105, 142572)
+
+_cdf_cache: dict = {}
+
+
+def zipf(rows: int, n: int, rng, s: float = 1.05) -> np.ndarray:
+    key = (rows, s)
+    if key not in _cdf_cache:
+        p = np.arange(1, rows + 1, dtype=np.float64) ** -s
+        c = np.cumsum(p)
+        _cdf_cache[key] = c / c[-1]
+    return np.minimum(np.searchsorted(_cdf_cache[key], rng.random(n), side="right"), rows - 1).astype(np.int64)
+
+
+def _time_graph(fn, steps: int, warmup: int = 3) -> float:
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    for _ in range(2):
+        g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / steps
+
+
+def _dlrm_batch(cfg, B, rng, dev, bag_lo, bag_hi):
+    dense = torch.from_numpy(rng.standard_normal((B, cfg.n_dense)).astype(np.float32)).to(dev)
+    labels = torch.from_numpy((rng.random(B) < 0.19).astype(np.float64)).to(dev)
+    sparse = []
+    for rows in cfg.rows_per_field:
+        sizes = rng.integers(bag_lo, bag_hi + 1, size=B)
+        idx = zipf(rows, int(sizes.sum()), rng)
+        off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        sparse.append((torch.from_numpy(idx).to(dev), torch.from_numpy(off).to(dev)))
+    return dense, sparse, labels
+
+
+def dlrm_samples_per_s(cfg, B, bag_lo, bag_hi, steps, dev):
+    from paper_2507_14668_b200.model import DlrmModel
+    torch.backends.cuda.matmul.allow_tf32 = False
+    rng = np.random.default_rng(11)
+    model = DlrmModel(cfg, device=dev, max_indices=B * bag_hi, check_errors=False)
+    dense, sparse, labels = _dlrm_batch(cfg, B, rng, dev, bag_lo, bag_hi)
+    ms = _time_graph(lambda: model.train_step(dense, sparse, labels, 0.05, 0.9, sync_loss=False), steps)
+    ntt = sum(1 for r in cfg.rows_per_field if r >= cfg.tt_threshold)
+    return {"value": B / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms, "batch": B, "tt_fields": ntt,
+            "fields": cfg.n_sparse}
+
+
+def cfg1(dev, steps=50):
+    from paper_2507_14668_b200.model import ModelConfig
+    cfg = ModelConfig(n_dense=6, rows_per_field=(1_000_000,), emb_dim=16, ranks=(1, 16, 16, 1), tt_threshold=1000,
+                      bottom_sizes=(64,), top_sizes=(64, 32), loss="bce", seed=0)
+    r = dlrm_samples_per_s(cfg, 256, 1, 3, steps, dev)
+    r["workload"] = "cfg1: DLRM, 1 TT field 1M x 16 ranks 16, bags 1-3 Zipf(1.05), batch 256, SGD momentum 0.9"
+    return r
+
+
+def cfg4(dev, steps=5, B=65536):
+    from paper_2507_14668_b200.model import ModelConfig
+    cfg = ModelConfig(n_dense=13, rows_per_field=KAGGLE_ROWS, emb_dim=64, ranks=(1, 32, 32, 1), tt_threshold=1000,
+                      bottom_sizes=(512, 256), top_sizes=(512, 256), loss="bce", seed=0)
+    r = dlrm_samples_per_s(cfg, B, 1, 1, steps, dev)
+    r["workload"] = (f"cfg4: Criteo-Kaggle-shaped TT-DLRM, 26 fields (15 TT, tt_threshold 1000), emb 64, ranks 32, "
+                     f"bottom 512-256-64, top 512-256-1, batch {B}, fp32 MLPs")
+    return r
+
+
+def cfg3(dev, steps=3, B=65536, pooling=20, permuted=False, tables=26):
+    from paper_2507_14668_b200.engine import TtEngine
+    from paper_2507_14668_b200.geometry import TtShape, factorize_dims, init_random_cores
+    M = 10_000_000
+    m, n = factorize_dims(M, 64, 3)
+    shape = TtShape(m, n, (1, 32, 32, 1))
+    T = B * pooling
+    eng = TtEngine(shape, T, B, dev)  # one workspace, tables stepped in turn
+    rng = np.random.default_rng(3)
+    perm = np.random.default_rng(123).permutation(M) if permuted else None
+    cores, vel, idxs = [], [], []
+    for t in range(tables):
+        cores.append([torch.from_numpy(c).to(dev) for c in init_random_cores(shape, t)])
+        vel.append([torch.zeros(c.shape, dtype=torch.float64, device=dev) for c in cores[-1]])
+        ids = zipf(M, T, rng)
+        if perm is not None:
+            ids = perm[ids]
+        idxs.append(torch.from_numpy(ids).to(dev))
+    off = torch.arange(0, T + 1, pooling, dtype=torch.int64, device=dev)
+    gout = torch.randn((B, 64), device=dev)
+    out = torch.empty((B, 64), device=dev)
+
+    def step():
+        for t in range(tables):
+            eng.plan(idxs[t], off)
+            eng.forward(cores[t], out=out)
+            eng.backward_sgd(cores[t], gout, 0.05, 0.9, vel[t])
+
+    step()
+    torch.cuda.synchronize()
+    st = eng.check_errors()
+    st["U"] = eng.status()["U"]
+    ms = _time_graph(step, steps, warmup=1)
+    return {"value": tables * T / (ms / 1e3), "unit": "lookups/s", "ms_per_step": ms, "tables": tables,
+            "lookups_per_table": T, "last_table_counts": {k: st[k] for k in ("P", "S", "U")},
+            "workload": f"cfg3: {tables} TT tables 10M x 64 ranks 32, Zipf(1.05) {'permuted' if permuted else 'native'} "
+                        f"ids, pooling {pooling}, {B} bags/table, plan+fwd+bwd+SGD per table"}
+
+
+def run_all(dev) -> dict:
+    res = {}
+    for name, fn in (("cfg1_dlrm", lambda: cfg1(dev)), ("cfg3_native", lambda: cfg3(dev)),
+                     ("cfg3_permuted", lambda: cfg3(dev, permuted=True)), ("cfg4_dlrm", lambda: cfg4(dev))):
+        try:
+            res[name] = fn()
+        except Exception as e:  # report, do not hide: an extra that fails is listed with its error
+            res[name] = {"error": f"{type(e).__name__}: {e}"}
+        torch.cuda.empty_cache()
+    return res

@@ -10,8 +10,8 @@ __global__ void __launch_bounds__(kBlock) k_runs(const unsigned* __restrict__ sk
                                                  const int* __restrict__ pslot, unsigned* __restrict__ urow,
                                                  int* __restrict__ urow_start, unsigned* __restrict__ urow_i3,
                                                  int* __restrict__ prow_begin, int* __restrict__ prow_end,
-                                                 int* __restrict__ counts, unsigned long long* status,
-                                                 unsigned* ctr) {
+                                                 int* __restrict__ qrow, int* __restrict__ counts,
+                                                 unsigned long long* status, unsigned* ctr) {
   __shared__ int s_tile;
   __shared__ int s_tmp[kItems * (kBlock / 32) + 2];
   const int tile = claim_tile(ctr, &s_tile);
@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(kBlock) k_runs(const unsigned* __restrict__ sk
     const int q = base + k * kBlock + threadIdx.x;
     if (q >= T) continue;
     const int u = rank[k] + (f[k] ? 1 : 0) - 1;
+    qrow[q] = u;
     if (f[k]) {
       urow[u] = key[k];
       urow_start[u] = q;
@@ -331,7 +332,8 @@ static size_t prefix_smem(const D& d, int ch) {
 template <class D>
 static size_t close_smem(const D& d) {
   size_t per = (size_t)close_warp_floats(d);
-  if (kFastRows<D>) per = per > (size_t)136 ? per : (size_t)136;
+  const size_t fast = 136 + (size_t)kMultiSeg * 128;  // G3 staging + per-segment H sums
+  if (kFastRows<D>) per = per > fast ? per : fast;
   return sizeof(float) * (kBlock / 32) * per;
 }
 template <class D>
@@ -371,7 +373,7 @@ static cudaError_t forward_impl(ttb_handle* h, const float* c0, const float* c1,
   int grid = (B + kBlock / 32 - 1) / (kBlock / 32);
   if (grid > 148 * 32) grid = 148 * 32;
   { ProfScope _ps(h, s, "close_pool");
-  k_close_pool<D><<<grid, kBlock, sm2, s>>>(d, h->kg, c2, w.slots, w.bag_off, w.bag_seg, w.seg_slot, w.occ_slot,
+  k_close_pool<D><<<grid, kBlock, sm2, s>>>(d, h->kg, c2, w.slots, w.bag_off, w.bag_seg, w.seg_slot, w.seg_inv, w.occ_slot,
                                             w.keys32, B, out);
   }
   count_launch();
@@ -394,16 +396,26 @@ static cudaError_t aggregate_impl(ttb_handle* h, const float* gout, cudaStream_t
   const int tiles = (T + kTile - 1) / kTile;
   { ProfScope _ps(h, s, "runs");
   k_runs<<<tiles, kBlock, 0, s>>>(sk, T, h->kg, w.pslot, w.urow, w.urow_start, w.urow_i3, w.prow_begin, w.prow_end,
-                                  w.counts, w.runs_status, w.runs_ctr);
+                                  w.qrow, w.counts, w.runs_status, w.runs_ctr);
   }
   count_launch();
-  // 3. aggregated row gradients
-  int grid = (T + kBlock / 32 - 1) / (kBlock / 32);
-  if (grid > 148 * 16) grid = 148 * 16;
-  { ProfScope _ps(h, s, "row_agg");
-  k_row_agg<D><<<grid, kBlock, 0, s>>>(d, (int)h->B, w.counts, w.urow_start, sv, w.bag_of, gout, w.gU, w.err);
+  // 3. aggregated row gradients (two-level segmented reduction)
+  {
+    const int nblk = (T + kAggBlock - 1) / kAggBlock;
+    int grid = (nblk + kBlock / 32 - 1) / (kBlock / 32);
+    if (grid > 148 * 16) grid = 148 * 16;
+    ProfScope _ps(h, s, "row_agg");
+    k_row_agg<D><<<grid, kBlock, 0, s>>>(d, (int)h->B, T, w.counts, w.urow_start, w.qrow, sv, w.bag_of, gout, w.gU,
+                                         w.agg_hp, w.agg_tp, w.span_list, reinterpret_cast<int*>(w.runs_ctr + 8), w.err);
   }
-  count_launch();
+  {
+    int grid = (T / kAggBlock) + 1;
+    if (grid > 148 * 8) grid = 148 * 8;
+    ProfScope _ps(h, s, "row_agg_span");
+    k_row_agg_span<D><<<grid, kBlock, sizeof(float) * (kBlock / 32) * dN(d), s>>>(
+        d, w.urow_start, w.span_list, reinterpret_cast<int*>(w.runs_ctr + 8), w.agg_hp, w.agg_tp, w.gU, w.err);
+  }
+  count_launch(2);
   return cudaGetLastError();
 }
 
@@ -563,6 +575,7 @@ bool choose_chunks(const DynDims& d, int* chf, int* chb) {
     if (!*chf && prefix_smem(d, c) <= cap) *chf = c;
   for (int c : {16, 8})
     if (!*chb && bwd_smem(d, c) <= cap) *chb = c;
-  return *chf && *chb && close_smem(d) <= cap && dG1s(d) <= 32 * kRedPerLane && dG3s(d) <= 32 * kRedPerLane;
+  return *chf && *chb && close_smem(d) <= cap && dG1s(d) <= 32 * kRedPerLane && dG3s(d) <= 32 * kRedPerLane &&
+         dN(d) <= 32 * kMaxPerLane;
 }
 }  // namespace ttb

@@ -116,6 +116,10 @@ void layout(ttb_handle& h, char* base) {
   w.rkB = c.take<unsigned>(T);
   w.rvB = c.take<unsigned>(T);
   w.uid_first = c.take<int>(T);
+  w.qrow = c.take<int>(T);
+  w.agg_hp = c.take<float>((size_t)(T / 64 + 2) * N);
+  w.agg_tp = c.take<float>((size_t)(T / 64 + 2) * N);
+  w.span_list = c.take<int>(T / 64 + 2);
   w.scratch1 = c.take<float>(16);
   h.bytes = c.off + 256;
 }

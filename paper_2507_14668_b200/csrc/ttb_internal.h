@@ -49,6 +49,10 @@ struct Workspace {
   int* grp_cnt;     // m2: present prefixes per i2
   unsigned *rkA, *rvA, *rkB, *rvB;  // rows-by-i3 sort buffers
   int* uid_first;   // T: first-occurrence rank flags / scratch
+  int* qrow;        // T: row ordinal of each sorted position
+  float* agg_hp;    // (T / 64 + 1) x N: per-block head partial row sums
+  float* agg_tp;    // (T / 64 + 1) x N: per-block tail partial row sums
+  int* span_list;   // rows spanning aggregation blocks
   // look-back scan state. Zero block A (cleared by every plan) holds the
   // error word / counts and the plan-scope scans; zero block B (cleared by
   // the plan, and again if a second backward reuses the plan) holds the

@@ -358,6 +358,8 @@ __device__ __forceinline__ void close_bag_generic(const D& d, KGeom g, const flo
   __syncwarp();
 }
 
+constexpr int kMultiSeg = 24;  // segments per bag handled by the register close path
+
 template <class D>
 __host__ __device__ constexpr int close_warp_floats(const D& d) {
   return dX(d) * (d.r2 + 1) + dG3s(d) + dN(d);
@@ -367,12 +369,14 @@ template <class D>
 __global__ void __launch_bounds__(kBlock) k_close_pool(D d, KGeom g, const float* __restrict__ G3,
                                                        const float* __restrict__ slots, const int* __restrict__ bag_off,
                                                        const int* __restrict__ bag_seg, const int* __restrict__ seg_slot,
+                                                       const int* __restrict__ seg_inv,
                                                        const int* __restrict__ occ_slot,
                                                        const unsigned* __restrict__ keys32, int B,
                                                        float* __restrict__ out) {
   extern __shared__ __align__(16) float smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int WF = close_warp_floats(d);
+  // per-warp smem stride: the fast path also keeps per-segment H sums
+  const int WF = kFastRows<D> ? max(close_warp_floats(d), 136 + kMultiSeg * 128) : close_warp_floats(d);
   float* s_sb = smem + w * WF;
   float* s_h = s_sb + dX(d) * (d.r2 + 1);
   float* s_o = s_h + dG3s(d);
@@ -418,9 +422,85 @@ __global__ void __launch_bounds__(kBlock) k_close_pool(D d, KGeom g, const float
       for (int i = 0; i < nb; ++i) {
         if (!((simple >> i) & 1u)) {
           const int bi = b0 + i;
-          close_bag_generic(d, g, G3, slots, bi, __shfl_sync(0xffffffffu, o0, i), __shfl_sync(0xffffffffu, o1, i),
-                            __shfl_sync(0xffffffffu, sg0, i), __shfl_sync(0xffffffffu, sg1, i), seg_slot, occ_slot,
-                            keys32, s_sb, s_h, s_o, out);
+          const int a0i = __shfl_sync(0xffffffffu, o0, i), a1i = __shfl_sync(0xffffffffu, o1, i);
+          const int s0i = __shfl_sync(0xffffffffu, sg0, i), s1i = __shfl_sync(0xffffffffu, sg1, i);
+          const int L = a1i - a0i, S = s1i - s0i;
+          if (L > 32 || S > kMultiSeg) {
+            close_bag_generic(d, g, G3, slots, bi, a0i, a1i, s0i, s1i, seg_slot, occ_slot, keys32, s_sb, s_h, s_o,
+                              out);
+            continue;
+          }
+          // pass 1: H_s for every segment of the bag. Lane r2 fetches its
+          // float4 of every index's G3 slice (all loads in flight at once) and
+          // adds them into the segment's row in index order.
+          float* f_hs = s_sb + 136;  // S x 32 x 4 (r2-major per segment)
+          const int myseg = lane < L ? seg_inv[a0i + lane] - s0i : 0;
+          const unsigned myi3 = lane < L ? keys32[a0i + lane] % g.m3 : 0u;
+          const int myslot = lane < S ? seg_slot[s0i + lane] : 0;
+          for (int e = lane; e < S * 32; e += 32) reinterpret_cast<float4*>(f_hs)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+          __syncwarp();
+          for (int t0 = 0; t0 < L; t0 += 8) {
+            float4 gv[8];
+            int sj[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const unsigned ii3 = __shfl_sync(0xffffffffu, myi3, (t0 + k) & 31);
+              sj[k] = __shfl_sync(0xffffffffu, myseg, (t0 + k) & 31);
+              if (t0 + k < L) gv[k] = __ldg(reinterpret_cast<const float4*>(G3 + (size_t)lane * m3n3 + ii3 * 4u));
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (t0 + k < L) {
+                float4* hp4 = reinterpret_cast<float4*>(f_hs) + sj[k] * 32 + lane;
+                float4 hv = *hp4;
+                hv.x += gv[k].x;
+                hv.y += gv[k].y;
+                hv.z += gv[k].z;
+                hv.w += gv[k].w;
+                *hp4 = hv;
+              }
+          }
+          __syncwarp();
+          // pass 2: close each segment (ascending slot) and add to the bag in
+          // segment order; the next segment's slot row halves are prefetched
+          float2 ob = make_float2(0.f, 0.f);
+          float4 cur4[4], nxt4[4];
+          {
+            const int sl = __shfl_sync(0xffffffffu, myslot, 0);
+            const float4* src = reinterpret_cast<const float4*>(slots + (size_t)sl * 512 + x * 32 + hf * 16);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) cur4[k] = src[k];
+          }
+          for (int j = 0; j < S; ++j) {
+            const int sln = __shfl_sync(0xffffffffu, myslot, (j + 1) & 31);
+            if (j + 1 < S) {
+              const float4* src = reinterpret_cast<const float4*>(slots + (size_t)sln * 512 + x * 32 + hf * 16);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) nxt4[k] = src[k];
+            }
+            const float* hseg = f_hs + j * 128;  // [r2][j4]
+            float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float sv4[4] = {cur4[k].x, cur4[k].y, cur4[k].z, cur4[k].w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float4 hv = *reinterpret_cast<const float4*>(hseg + (hf * 16 + 4 * k + q) * 4);
+                c0 = fmaf(sv4[q], hv.x, c0);
+                c1 = fmaf(sv4[q], hv.y, c1);
+                c2 = fmaf(sv4[q], hv.z, c2);
+                c3 = fmaf(sv4[q], hv.w, c3);
+              }
+            }
+            const float e0 = hf ? c0 : c2, e1 = hf ? c1 : c3;
+            const float r0 = __shfl_xor_sync(0xffffffffu, e0, 1), r1 = __shfl_xor_sync(0xffffffffu, e1, 1);
+            ob.x += (hf ? c2 : c0) + r0;
+            ob.y += (hf ? c3 : c1) + r1;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) cur4[k] = nxt4[k];
+          }
+          *reinterpret_cast<float2*>(out + (size_t)bi * 64 + x * 4 + hf * 2) = ob;
+          __syncwarp();
           continue;
         }
         float sv[16];
@@ -464,71 +544,168 @@ __global__ void __launch_bounds__(kBlock) k_close_pool(D d, KGeom g, const float
 
 // ------------------------------------------------------------ backward: rows
 // Aggregated row gradient g_u = sum of the bag gradients of the row's
-// occurrences, left to right in index order (backward.py:81-85 sums in the
-// gradient dtype in occurrence order; the stable sort preserves that order).
-// A warp takes 32 rows: lanes fetch their metadata at once, single-occurrence
-// rows (the common case) are copied 8 at a time with independent loads.
+// occurrences (backward.py:81-85: occurrence order, gradient dtype). The
+// sorted occurrence array is cut into fixed blocks of kAggBlock positions,
+// one warp each, summed strictly left to right:
+//   * a row that starts and ends inside a block is final (bit-exact with the
+//     reference's left-to-right sum);
+//   * a row crossing block boundaries leaves a tail partial in its first
+//     block and head partials in the following blocks; level 2 adds them in
+//     block order (deterministic; the association differs from a single
+//     left-to-right chain only for such rows).
+// Work per warp is bounded, so hot Zipf rows (1e5 occurrences) cost the same
+// as cold ones.
+constexpr int kAggBlock = 64;
+constexpr int kMaxPerLane = 16;  // N <= 512
+
+template <class D> constexpr int agg_per_lane() {
+  return IsFixed<D>::value ? (FixT<D>::n1 * FixT<D>::n2 * FixT<D>::n3 + 31) / 32 : kMaxPerLane;
+}
+
 template <class D>
-__global__ void __launch_bounds__(kBlock) k_row_agg(D d, int B, const int* __restrict__ counts,
-                                                    const int* __restrict__ urow_start,
+__global__ void __launch_bounds__(kBlock) k_row_agg(D d, int B, int T, const int* __restrict__ counts,
+                                                    const int* __restrict__ urow_start, const int* __restrict__ qrow,
                                                     const unsigned* __restrict__ svals, const int* __restrict__ bag_of,
                                                     const float* __restrict__ gout, float* __restrict__ gU,
+                                                    float* __restrict__ hp, float* __restrict__ tp,
+                                                    int* __restrict__ span_list, int* __restrict__ span_count,
                                                     int* __restrict__ err) {
+  constexpr int PL = agg_per_lane<D>();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int N = dN(d);
-  const int U = counts[3];
+  const int nblk = (T + kAggBlock - 1) / kAggBlock;
   bool bad = false;
-  const int gw = blockIdx.x * (kBlock / 32) + w, nw = gridDim.x * (kBlock / 32);
-  constexpr int kGrp = 8;  // rows per warp iteration: many warps in flight
-  for (int u0 = gw * kGrp; u0 < U; u0 += nw * kGrp) {
-    const int u = u0 + lane;
-    int q0 = 0, q1 = 0, bb = 0;
-    if (lane < kGrp && u < U) {
-      q0 = urow_start[u];
-      q1 = urow_start[u + 1];
-      if (q1 - q0 == 1) {
-        bb = bag_of[svals[q0]];
-        bb = bb < 0 ? 0 : (bb >= B ? B - 1 : bb);  // malformed offsets: garbage ids, never OOB
+  for (int blk = blockIdx.x * (kBlock / 32) + w; blk < nblk; blk += gridDim.x * (kBlock / 32)) {
+    const int q0 = blk * kAggBlock, q1 = min(T, q0 + kAggBlock);
+    // lanes prefetch bag id and row of 2 x 32 positions
+    int bq[kAggBlock / 32], uq[kAggBlock / 32], kq[kAggBlock / 32];
+#pragma unroll
+    for (int k = 0; k < kAggBlock / 32; ++k) {
+      const int q = q0 + 32 * k + lane;
+      bq[k] = 0;
+      uq[k] = -1;
+      kq[k] = 0;
+      if (q < q1) {
+        int b = bag_of[svals[q]];
+        bq[k] = b < 0 ? 0 : (b >= B ? B - 1 : b);  // malformed offsets: garbage ids, never OOB
+        const int u = qrow[q];
+        uq[k] = u;
+        // where this position's row lives: 0 inside the block, 1 entered
+        // from the left (head partial), 2 starts here and leaves right (tail)
+        const int head = urow_start[u], tail = urow_start[u + 1];
+        kq[k] = head < q0 ? 1 : (tail > q1 ? 2 : 0);
       }
     }
-    const int nr = min(kGrp, U - u0);
-    const unsigned single = __ballot_sync(0xffffffffu, lane < kGrp && u < U && q1 - q0 == 1);
-    if constexpr (FixT<D>::n1 * FixT<D>::n2 * FixT<D>::n3 == 64) {
-      for (int i0 = 0; i0 < nr; i0 += 8) {
-        float2 v[8];
+    float acc[PL];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int bk = __shfl_sync(0xffffffffu, bb, (i0 + k) & 31);
-          if (i0 + k < nr && ((single >> (i0 + k)) & 1u))
-            v[k] = __ldg(reinterpret_cast<const float2*>(gout + (size_t)bk * 64) + lane);
+    for (int i = 0; i < PL; ++i) acc[i] = 0.f;
+    int cur = __shfl_sync(0xffffffffu, uq[0], 0);
+    int cur_kind = __shfl_sync(0xffffffffu, kq[0], 0);
+    auto flush = [&](int u, bool at_block_end) {
+      float* dst;
+      if (cur_kind == 0) dst = gU + (size_t)u * N;       // whole row inside the block
+      else if (cur_kind == 1) dst = hp + (size_t)blk * N;  // row entered from the left
+      else dst = tp + (size_t)blk * N;                     // row starts here, leaves right
+      if (cur_kind == 2 && lane == 0) span_list[atomicAdd(span_count, 1)] = u;
+#pragma unroll
+      for (int i = 0; i < PL; ++i) {
+        const int o = lane + 32 * i;
+        if (o < N) {
+          if (!isfinite(acc[i])) bad = true;
+          dst[o] = acc[i];
+        }
+        acc[i] = 0.f;
+      }
+      (void)at_block_end;
+    };
+    const int n = q1 - q0;
+    for (int i0 = 0; i0 < n; i0 += 8) {
+      float v[8][PL];
+      int uu[8], kk[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int i = i0 + k;
+        const int src = i & 31;
+        const int b = __shfl_sync(0xffffffffu, (i >> 5) ? bq[1] : bq[0], src);
+        uu[k] = __shfl_sync(0xffffffffu, (i >> 5) ? uq[1] : uq[0], src);
+        kk[k] = __shfl_sync(0xffffffffu, (i >> 5) ? kq[1] : kq[0], src);
+#pragma unroll
+        for (int j = 0; j < PL; ++j) {
+          const int o = lane + 32 * j;
+          v[k][j] = (i < n && o < N) ? __ldg(&gout[(size_t)b * N + o]) : 0.f;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (i0 + k >= n) break;
+        if (uu[k] != cur) {
+          flush(cur, false);
+          cur = uu[k];
+          cur_kind = kk[k];
         }
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (i0 + k < nr && ((single >> (i0 + k)) & 1u)) {
-            const float2 x = make_float2(0.f + v[k].x, 0.f + v[k].y);
-            if (!isfinite(x.x) || !isfinite(x.y)) bad = true;
-            reinterpret_cast<float2*>(gU + (size_t)(u0 + i0 + k) * 64)[lane] = x;
-          }
+        for (int j = 0; j < PL; ++j) acc[j] += v[k][j];
       }
     }
-    for (int i = 0; i < nr; ++i) {
-      if (FixT<D>::n1 * FixT<D>::n2 * FixT<D>::n3 == 64 && ((single >> i) & 1u)) continue;
-      const int a = __shfl_sync(0xffffffffu, q0, i), b = __shfl_sync(0xffffffffu, q1, i);
-      for (int o0 = 0; o0 < N; o0 += 32) {
-        const int o = o0 + lane;
-        if (o >= N) continue;
-        float acc = 0.f;
-        for (int q = a; q < b; ++q) {
-          int bq = bag_of[svals[q]];
-          bq = bq < 0 ? 0 : (bq >= B ? B - 1 : bq);
-          acc += __ldg(&gout[(size_t)bq * N + o]);
-        }
-        if (!isfinite(acc)) bad = true;
-        gU[(size_t)(u0 + i) * N + o] = acc;
-      }
-    }
+    flush(cur, true);
   }
   if (bad) atomicOr(err, 8);
+}
+
+// Level 2: rows spanning blocks: g_u = tp[first block] + hp[next blocks...],
+// in block order. One CTA per listed row; warps own contiguous block ranges.
+template <class D>
+__global__ void __launch_bounds__(kBlock) k_row_agg_span(D d, const int* __restrict__ urow_start,
+                                                         const int* __restrict__ span_list,
+                                                         const int* __restrict__ span_count,
+                                                         const float* __restrict__ hp, const float* __restrict__ tp,
+                                                         float* __restrict__ gU, int* __restrict__ err) {
+  constexpr int PL = agg_per_lane<D>();
+  extern __shared__ float s_part[];  // (kBlock/32) x N
+  const int N = dN(d);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nspan = *span_count;
+  for (int it = blockIdx.x; it < nspan; it += gridDim.x) {
+    const int u = span_list[it];
+    const int head = urow_start[u], tail = urow_start[u + 1];
+    const int bs = head / kAggBlock, be = (tail - 1) / kAggBlock;
+    const int nmid = be - bs;  // head partials of blocks bs+1 .. be
+    const int per = (nmid + kBlock / 32 - 1) / (kBlock / 32);
+    const int a = bs + 1 + w * per, b = min(be + 1, a + per);
+    float acc[PL];
+#pragma unroll
+    for (int i = 0; i < PL; ++i) acc[i] = 0.f;
+    for (int k0 = a; k0 < b; k0 += 8) {
+      float v[8][PL];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+#pragma unroll
+        for (int j = 0; j < PL; ++j) {
+          const int o = lane + 32 * j;
+          v[k][j] = (k0 + k < b && o < N) ? hp[(size_t)(k0 + k) * N + o] : 0.f;
+        }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k0 + k < b)
+#pragma unroll
+          for (int j = 0; j < PL; ++j) acc[j] += v[k][j];
+    }
+#pragma unroll
+    for (int j = 0; j < PL; ++j) {
+      const int o = lane + 32 * j;
+      if (o < N) s_part[w * N + o] = acc[j];
+    }
+    __syncthreads();
+    bool bad = false;
+    for (int o = threadIdx.x; o < N; o += kBlock) {
+      float t = tp[(size_t)bs * N + o];
+      for (int ww = 0; ww < kBlock / 32; ++ww) t += s_part[ww * N + o];
+      if (!isfinite(t)) bad = true;
+      gU[(size_t)u * N + o] = t;
+    }
+    if (bad) atomicOr(err, 8);
+    __syncthreads();
+  }
 }
 
 // ------------------------------------------------------------ backward: prefixes

@@ -43,7 +43,14 @@ __global__ void __launch_bounds__(kBlock) k_plan_mark(const IdxT* __restrict__ i
     }
     const unsigned i = (unsigned)v;
     keys32[t] = i;
-    atomicMin(&pmap[i / g.m3], (unsigned)t);
+    // warp-aggregated: one atomic per distinct prefix per warp (hot Zipf
+    // prefixes would otherwise serialise thousands of atomics on one word);
+    // the lowest lane of a peer group holds the smallest position
+    const unsigned key = i / g.m3;
+    const unsigned peers = __match_any_sync(__activemask(), key);
+    // (a plain read first: once a hot prefix holds a small position most
+    // later candidates see it and skip the atomic entirely)
+    if ((peers & lanemask_lt()) == 0 && pmap[key] > (unsigned)t) atomicMin(&pmap[key], (unsigned)t);
   }
   if (bits) atomicOr(err, bits);
 }
@@ -180,7 +187,32 @@ __global__ void __launch_bounds__(kBlock) k_plan_segs(const unsigned* __restrict
   for (int i = w; i < s_nlong; i += NW) {
     const int tb = s_long[i];
     const int bb = tile * kBagsPerTile + tb;
-    long_bag_rank(bag_off[bb], bag_off[bb + 1], keys32, g.m3, pslot, occ_slot, occ_tmp, seg_inv, &s_cnt[tb]);
+    const int lo = bag_off[bb], hi = bag_off[bb + 1];
+    if (hi - lo <= 32) {
+      // one index per lane: first occurrences by match_any, ranks by shuffles
+      const bool act = lane < hi - lo;
+      int sl = 0x7fffffff;
+      if (act) {
+        sl = pslot[keys32[lo + lane] / g.m3];
+        occ_slot[lo + lane] = sl;
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, sl);
+      const bool first = act && ((peers & lanemask_lt()) == 0);
+      int r = 0;
+      for (int j = 0; j < 32; ++j) {
+        const int sj = __shfl_sync(0xffffffffu, sl, j);
+        const bool fj = __shfl_sync(0xffffffffu, first, j);
+        r += (fj && sj < sl) ? 1 : 0;
+      }
+      if (act) {
+        seg_inv[lo + lane] = r;  // local rank for now
+        occ_tmp[lo + lane] = first ? 1 : 0;
+      }
+      const int c = __popc(__ballot_sync(0xffffffffu, first));
+      if (lane == 0) s_cnt[tb] = c;
+    } else {
+      long_bag_rank(lo, hi, keys32, g.m3, pslot, occ_slot, occ_tmp, seg_inv, &s_cnt[tb]);
+    }
   }
   __syncthreads();
   // block exclusive scan of the 256 counts + look-back across tiles

@@ -103,14 +103,16 @@ class Mlp(nn.Module):
 class DenseField(nn.Module):
     """Small field below tt_threshold: plain (rows, dim) table, sum pooling."""
 
-    def __init__(self, rows: int, dim: int, seed: int, device):
+    def __init__(self, rows: int, dim: int, seed: int, device, check_errors: bool = True):
         super().__init__()
+        self.check_errors = check_errors
         rng = np.random.default_rng(seed)
         w = (rng.standard_normal((rows, dim)) * 0.1).astype(np.float32)
         self.rows = nn.Parameter(torch.from_numpy(w).to(device))
 
     def forward(self, indices, offsets):
-        if indices.numel() and (int(indices.min()) < 0 or int(indices.max()) >= self.rows.shape[0]):
+        if self.check_errors and indices.numel() and (
+                int(indices.min()) < 0 or int(indices.max()) >= self.rows.shape[0]):
             raise ValueError(f"index outside [0, {self.rows.shape[0]})")
         return torch.nn.functional.embedding_bag(indices, self.rows, offsets[:-1], mode="sum")
 
@@ -131,7 +133,7 @@ class DlrmModel(nn.Module):
                                              include_last_offset=True, max_indices=max_indices,
                                              check_errors=check_errors))
             else:
-                fields.append(DenseField(rows, config.emb_dim, seed, dev))
+                fields.append(DenseField(rows, config.emb_dim, seed, dev, check_errors))
         self.fields = nn.ModuleList(fields)
         self.bottom = Mlp((config.n_dense, *config.bottom_sizes, config.emb_dim), rng, dev)
         self.top = Mlp((config.interaction_dim, *config.top_sizes, 1), rng, dev)
