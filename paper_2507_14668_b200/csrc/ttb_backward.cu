@@ -332,7 +332,7 @@ static size_t prefix_smem(const D& d, int ch) {
 template <class D>
 static size_t close_smem(const D& d) {
   size_t per = (size_t)close_warp_floats(d);
-  const size_t fast = 136 + (size_t)kMultiSeg * 128;  // G3 staging + per-segment H sums
+  const size_t fast = 136 + (size_t)kSegGroup * 128;  // G3 staging + per-segment H sums (k_close_multi)
   if (kFastRows<D>) per = per > fast ? per : fast;
   return sizeof(float) * (kBlock / 32) * per;
 }
@@ -377,6 +377,15 @@ static cudaError_t forward_impl(ttb_handle* h, const float* c0, const float* c1,
                                             w.keys32, B, out);
   }
   count_launch();
+  if (kFastRows<D> && FixT<D>::n1 * FixT<D>::n2 == 16) {
+    if ((e = ensure_smem(k_close_multi<D>, sm2))) return e;
+    int gridm = (B + kBlock / 32 - 1) / (kBlock / 32);
+    if (gridm > 148 * 16) gridm = 148 * 16;
+    ProfScope _ps(h, s, "close_multi");
+    k_close_multi<D><<<gridm, kBlock, sm2, s>>>(d, h->kg, c2, w.slots, w.bag_off, w.bag_seg, w.seg_slot, w.seg_inv,
+                                                w.occ_slot, w.keys32, B, w.counts, out);
+    count_launch();
+  }
   return cudaGetLastError();
 }
 

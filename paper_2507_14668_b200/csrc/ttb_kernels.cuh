@@ -358,7 +358,8 @@ __device__ __forceinline__ void close_bag_generic(const D& d, KGeom g, const flo
   __syncwarp();
 }
 
-constexpr int kMultiSeg = 24;  // segments per bag handled by the register close path
+constexpr int kMultiSeg = 32;  // segments per bag handled by the register close path
+constexpr int kSegGroup = 8;   // segments whose H sums are staged at once (smem per warp)
 
 template <class D>
 __host__ __device__ constexpr int close_warp_floats(const D& d) {
@@ -376,7 +377,7 @@ __global__ void __launch_bounds__(kBlock) k_close_pool(D d, KGeom g, const float
   extern __shared__ __align__(16) float smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   // per-warp smem stride: the fast path also keeps per-segment H sums
-  const int WF = kFastRows<D> ? max(close_warp_floats(d), 136 + kMultiSeg * 128) : close_warp_floats(d);
+  const int WF = kFastRows<D> ? max(close_warp_floats(d), 136 + kSegGroup * 128) : close_warp_floats(d);
   float* s_sb = smem + w * WF;
   float* s_h = s_sb + dX(d) * (d.r2 + 1);
   float* s_o = s_h + dG3s(d);
@@ -420,89 +421,7 @@ __global__ void __launch_bounds__(kBlock) k_close_pool(D d, KGeom g, const float
       int next = simple ? __ffs(simple) - 1 : 32;
       if (next < nb) fetch(next);
       for (int i = 0; i < nb; ++i) {
-        if (!((simple >> i) & 1u)) {
-          const int bi = b0 + i;
-          const int a0i = __shfl_sync(0xffffffffu, o0, i), a1i = __shfl_sync(0xffffffffu, o1, i);
-          const int s0i = __shfl_sync(0xffffffffu, sg0, i), s1i = __shfl_sync(0xffffffffu, sg1, i);
-          const int L = a1i - a0i, S = s1i - s0i;
-          if (L > 32 || S > kMultiSeg) {
-            close_bag_generic(d, g, G3, slots, bi, a0i, a1i, s0i, s1i, seg_slot, occ_slot, keys32, s_sb, s_h, s_o,
-                              out);
-            continue;
-          }
-          // pass 1: H_s for every segment of the bag. Lane r2 fetches its
-          // float4 of every index's G3 slice (all loads in flight at once) and
-          // adds them into the segment's row in index order.
-          float* f_hs = s_sb + 136;  // S x 32 x 4 (r2-major per segment)
-          const int myseg = lane < L ? seg_inv[a0i + lane] - s0i : 0;
-          const unsigned myi3 = lane < L ? keys32[a0i + lane] % g.m3 : 0u;
-          const int myslot = lane < S ? seg_slot[s0i + lane] : 0;
-          for (int e = lane; e < S * 32; e += 32) reinterpret_cast<float4*>(f_hs)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
-          __syncwarp();
-          for (int t0 = 0; t0 < L; t0 += 8) {
-            float4 gv[8];
-            int sj[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const unsigned ii3 = __shfl_sync(0xffffffffu, myi3, (t0 + k) & 31);
-              sj[k] = __shfl_sync(0xffffffffu, myseg, (t0 + k) & 31);
-              if (t0 + k < L) gv[k] = __ldg(reinterpret_cast<const float4*>(G3 + (size_t)lane * m3n3 + ii3 * 4u));
-            }
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-              if (t0 + k < L) {
-                float4* hp4 = reinterpret_cast<float4*>(f_hs) + sj[k] * 32 + lane;
-                float4 hv = *hp4;
-                hv.x += gv[k].x;
-                hv.y += gv[k].y;
-                hv.z += gv[k].z;
-                hv.w += gv[k].w;
-                *hp4 = hv;
-              }
-          }
-          __syncwarp();
-          // pass 2: close each segment (ascending slot) and add to the bag in
-          // segment order; the next segment's slot row halves are prefetched
-          float2 ob = make_float2(0.f, 0.f);
-          float4 cur4[4], nxt4[4];
-          {
-            const int sl = __shfl_sync(0xffffffffu, myslot, 0);
-            const float4* src = reinterpret_cast<const float4*>(slots + (size_t)sl * 512 + x * 32 + hf * 16);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) cur4[k] = src[k];
-          }
-          for (int j = 0; j < S; ++j) {
-            const int sln = __shfl_sync(0xffffffffu, myslot, (j + 1) & 31);
-            if (j + 1 < S) {
-              const float4* src = reinterpret_cast<const float4*>(slots + (size_t)sln * 512 + x * 32 + hf * 16);
-#pragma unroll
-              for (int k = 0; k < 4; ++k) nxt4[k] = src[k];
-            }
-            const float* hseg = f_hs + j * 128;  // [r2][j4]
-            float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const float sv4[4] = {cur4[k].x, cur4[k].y, cur4[k].z, cur4[k].w};
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const float4 hv = *reinterpret_cast<const float4*>(hseg + (hf * 16 + 4 * k + q) * 4);
-                c0 = fmaf(sv4[q], hv.x, c0);
-                c1 = fmaf(sv4[q], hv.y, c1);
-                c2 = fmaf(sv4[q], hv.z, c2);
-                c3 = fmaf(sv4[q], hv.w, c3);
-              }
-            }
-            const float e0 = hf ? c0 : c2, e1 = hf ? c1 : c3;
-            const float r0 = __shfl_xor_sync(0xffffffffu, e0, 1), r1 = __shfl_xor_sync(0xffffffffu, e1, 1);
-            ob.x += (hf ? c2 : c0) + r0;
-            ob.y += (hf ? c3 : c1) + r1;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) cur4[k] = nxt4[k];
-          }
-          *reinterpret_cast<float2*>(out + (size_t)bi * 64 + x * 4 + hf * 2) = ob;
-          __syncwarp();
-          continue;
-        }
+        if (!((simple >> i) & 1u)) continue;  // multi-index bags: k_close_multi
         float sv[16];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -539,6 +458,129 @@ __global__ void __launch_bounds__(kBlock) k_close_pool(D d, KGeom g, const float
     for (int b = gw; b < B; b += nw)
       close_bag_generic(d, g, G3, slots, b, bag_off[b], bag_off[b + 1], bag_seg[b], bag_seg[b + 1], seg_slot,
                         occ_slot, keys32, s_sb, s_h, s_o, out);
+  }
+}
+
+
+// Multi-index bags (pooling > 1) of the lane <-> r2 fast shape; single-index
+// bags are done by k_close_pool. One warp per bag.
+template <class D>
+__global__ void __launch_bounds__(kBlock) k_close_multi(D d, KGeom g, const float* __restrict__ G3,
+                                                        const float* __restrict__ slots,
+                                                        const int* __restrict__ bag_off,
+                                                        const int* __restrict__ bag_seg,
+                                                        const int* __restrict__ seg_slot,
+                                                        const int* __restrict__ seg_inv,
+                                                        const int* __restrict__ occ_slot,
+                                                        const unsigned* __restrict__ keys32, int B,
+                                                        const int* __restrict__ counts, float* __restrict__ out) {
+  if constexpr (kFastRows<D> && FixT<D>::n1 * FixT<D>::n2 == 16) {
+    if (counts[4] == 0) return;  // no bag has more than one index
+    extern __shared__ __align__(16) float smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int WF = max(close_warp_floats(d), 136 + kSegGroup * 128);
+    float* s_sb = smem + w * WF;
+    float* s_h = s_sb + dX(d) * (d.r2 + 1);
+    float* s_o = s_h + dG3s(d);
+    const unsigned m3n3 = g.m3 * 4u;
+    const int x = lane >> 1, hf = lane & 1;
+    const int gw = blockIdx.x * (kBlock / 32) + w, nw = gridDim.x * (kBlock / 32);
+    for (int b = gw; b < B; b += nw) {
+      const int o0 = bag_off[b], o1 = bag_off[b + 1];
+      if (o1 - o0 <= 1) continue;
+      const int sg0 = bag_seg[b], sg1 = bag_seg[b + 1];
+        {
+          const int bi = b;
+          const int a0i = o0, a1i = o1, s0i = sg0, s1i = sg1;
+          const int L = a1i - a0i, S = s1i - s0i;
+          if (L > 32 || S > kMultiSeg) {
+            close_bag_generic(d, g, G3, slots, bi, a0i, a1i, s0i, s1i, seg_slot, occ_slot, keys32, s_sb, s_h, s_o,
+                              out);
+            continue;
+          }
+          // Segments are closed in groups of kSegGroup (ascending slot). Pass 1
+          // builds the group's H_s sums: lane r2 fetches its float4 of every
+          // index's G3 slice (8 loads in flight) and adds those of the group's
+          // segments in index order. Pass 2 closes each segment with the
+          // slot's row halves (next segment's halves prefetched) and adds it
+          // to the bag in segment order.
+          float* f_hs = s_sb + 136;  // kSegGroup x 32 x 4 (r2-major per segment)
+          const int myseg = lane < L ? seg_inv[a0i + lane] - s0i : 0;
+          const unsigned myi3 = lane < L ? keys32[a0i + lane] % g.m3 : 0u;
+          const int myslot = lane < S ? seg_slot[s0i + lane] : 0;
+          float2 ob = make_float2(0.f, 0.f);
+          float4 cur4[4], nxt4[4];
+          {
+            const int sl = __shfl_sync(0xffffffffu, myslot, 0);
+            const float4* src = reinterpret_cast<const float4*>(slots + (size_t)sl * 512 + x * 32 + hf * 16);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) cur4[k] = src[k];
+          }
+          for (int g0 = 0; g0 < S; g0 += kSegGroup) {
+            const int gn = min(kSegGroup, S - g0);
+#pragma unroll
+            for (int e = lane; e < kSegGroup * 32; e += 32)
+              reinterpret_cast<float4*>(f_hs)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+            __syncwarp();
+            for (int t0 = 0; t0 < L; t0 += 8) {
+              float4 gv[8];
+              int sj[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const unsigned ii3 = __shfl_sync(0xffffffffu, myi3, (t0 + k) & 31);
+                sj[k] = __shfl_sync(0xffffffffu, myseg, (t0 + k) & 31) - g0;
+                if (t0 + k < L && sj[k] >= 0 && sj[k] < gn)
+                  gv[k] = __ldg(reinterpret_cast<const float4*>(G3 + (size_t)lane * m3n3 + ii3 * 4u));
+              }
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                if (t0 + k < L && sj[k] >= 0 && sj[k] < gn) {
+                  float4* hp4 = reinterpret_cast<float4*>(f_hs) + sj[k] * 32 + lane;
+                  float4 hv = *hp4;
+                  hv.x += gv[k].x;
+                  hv.y += gv[k].y;
+                  hv.z += gv[k].z;
+                  hv.w += gv[k].w;
+                  *hp4 = hv;
+                }
+            }
+            __syncwarp();
+            for (int jj = 0; jj < gn; ++jj) {
+              const int j = g0 + jj;
+              const int sln = __shfl_sync(0xffffffffu, myslot, (j + 1) & 31);
+              if (j + 1 < S) {
+                const float4* src = reinterpret_cast<const float4*>(slots + (size_t)sln * 512 + x * 32 + hf * 16);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) nxt4[k] = src[k];
+              }
+              const float* hseg = f_hs + jj * 128;  // [r2][j4]
+              float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const float sv4[4] = {cur4[k].x, cur4[k].y, cur4[k].z, cur4[k].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const float4 hv = *reinterpret_cast<const float4*>(hseg + (hf * 16 + 4 * k + q) * 4);
+                  c0 = fmaf(sv4[q], hv.x, c0);
+                  c1 = fmaf(sv4[q], hv.y, c1);
+                  c2 = fmaf(sv4[q], hv.z, c2);
+                  c3 = fmaf(sv4[q], hv.w, c3);
+                }
+              }
+              const float e0 = hf ? c0 : c2, e1 = hf ? c1 : c3;
+              const float r0 = __shfl_xor_sync(0xffffffffu, e0, 1), r1 = __shfl_xor_sync(0xffffffffu, e1, 1);
+              ob.x += (hf ? c2 : c0) + r0;
+              ob.y += (hf ? c3 : c1) + r1;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) cur4[k] = nxt4[k];
+            }
+            __syncwarp();
+          }
+          *reinterpret_cast<float2*>(out + (size_t)bi * 64 + x * 4 + hf * 2) = ob;
+          __syncwarp();
+          continue;
+        }
+    }
   }
 }
 

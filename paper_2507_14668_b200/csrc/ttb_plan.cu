@@ -20,7 +20,7 @@ __global__ void __launch_bounds__(kBlock) k_plan_mark(const IdxT* __restrict__ i
                                                       int* __restrict__ bag_off, int* __restrict__ err) {
   const int stride = gridDim.x * blockDim.x;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-  int bits = 0;
+  int bits = 0, multi = 0;
   for (int b = tid; b <= B; b += stride) {
     const int64_t ob = offsets[b];
     bag_off[b] = (int)(ob < 0 ? 0 : (ob > T ? T : ob));
@@ -33,6 +33,7 @@ __global__ void __launch_bounds__(kBlock) k_plan_mark(const IdxT* __restrict__ i
       // bag id of each index (clamped so malformed offsets cannot write out of range)
       const int lo = (int)(ob < 0 ? 0 : (ob > T ? T : ob)), hi = (int)(on < lo ? lo : (on > T ? T : on));
       for (int t = lo; t < hi; ++t) bag_of[t] = b;
+      if (hi - lo > 1) multi = 1;
     }
   }
   for (int t = tid; t < T; t += stride) {
@@ -53,6 +54,7 @@ __global__ void __launch_bounds__(kBlock) k_plan_mark(const IdxT* __restrict__ i
     if ((peers & lanemask_lt()) == 0 && pmap[key] > (unsigned)t) atomicMin(&pmap[key], (unsigned)t);
   }
   if (bits) atomicOr(err, bits);
+  if (multi) err[4] = 1;  // counts[4]: some bag holds more than one index
 }
 
 // ---------------------------------------------------------------- P2: slots
