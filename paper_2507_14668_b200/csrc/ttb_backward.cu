@@ -360,10 +360,21 @@ static cudaError_t forward_impl(ttb_handle* h, const float* c0, const float* c1,
   const D d = make_dims<D>(h->dims);
   Workspace& w = h->w;
   cudaError_t e;
-  const size_t sm1 = prefix_smem(d, h->chf);
+  if constexpr (kTcPrefix<D>) {
+    // tensor-core path (tcgen05 kind::tf32, 3xTF32)
+    constexpr int R1 = FixT<D>::r1, C = FixT<D>::n2 * FixT<D>::r2;
+    const size_t smt = sizeof(float) * ((size_t)2 * 128 * R1 + (size_t)2 * C * R1);
+    const size_t sms = sizeof(float) * (size_t)128 * (C + 4);
+    const size_t smtc = smt > sms ? smt : sms;
+    if ((e = ensure_smem(k_prefix_products_tc<D>, smtc))) return e;
+    dim3 gt(h->kg.m2, (unsigned)((h->kg.m1 + kTcChunk - 1) / kTcChunk));
+    ProfScope _ps(h, s, "prefix_products_tc");
+    k_prefix_products_tc<D><<<gt, kBlock, smtc, s>>>(d, h->kg, c0, c1, w.pmap, w.pslot, w.slots);
+  } else
+  { const size_t sm1 = prefix_smem(d, h->chf);
   if ((e = ensure_smem(k_prefix_products<D>, sm1))) return e;
   dim3 g1(h->kg.m2, (unsigned)h->nsplitf);
-  { ProfScope _ps(h, s, "prefix_products");
+  ProfScope _ps(h, s, "prefix_products");
   k_prefix_products<D><<<g1, kBlock, sm1, s>>>(d, h->kg, h->chf, c0, c1, w.pmap, w.pslot, w.slots);
   }
   count_launch();

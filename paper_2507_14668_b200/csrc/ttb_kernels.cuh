@@ -4,6 +4,7 @@
 #include <type_traits>
 
 #include "ttb_internal.h"
+#include "ttb_umma.cuh"
 
 namespace ttb {
 
@@ -309,6 +310,124 @@ __global__ void __launch_bounds__(kBlock) k_prefix_products(D d, KGeom g, int ch
         }
       }
     });
+  }
+}
+
+// ------------------------------------------------------------ K2 on the tensor cores
+// Same product as k_prefix_products, issued as tcgen05.mma kind::tf32 with a
+// 3xTF32 split (a = hi + lo, a.b ~ hi.hi + hi.lo + lo.hi in fp32 TMEM
+// accumulators; measured 4e-7 relative vs 3e-4 for plain TF32), so the slots
+// keep fp32-level accuracy. One CTA per (i2, chunk of 32 prefixes): the
+// (32 n1 = 128) x (n2 r2) x r1 GEMM is one M=128 UMMA tile. Operands are
+// staged K-major (SWIZZLE_NONE core matrices) by all threads, one thread issues
+// the 3 * r1/8 MMAs, and the accumulator is read back by 8 warps (lane quarter
+// = warp % 4, column half = warp / 4) and written through smem as full rows.
+template <class D> constexpr bool kTcPrefix = FixT<D>::n1 == 4 && FixT<D>::r1 % 8 == 0 && FixT<D>::r1 >= 8 &&
+                                              (FixT<D>::n2 * FixT<D>::r2) % 64 == 0 &&
+                                              FixT<D>::n2 * FixT<D>::r2 <= 256;
+constexpr int kTcChunk = 32;  // prefixes per CTA: M = 32 * n1 = 128
+
+template <class D>
+__global__ void __launch_bounds__(kBlock) k_prefix_products_tc(D d, KGeom g, const float* __restrict__ G1,
+                                                               const float* __restrict__ G2,
+                                                               const unsigned* __restrict__ pmap,
+                                                               const int* __restrict__ pslot,
+                                                               float* __restrict__ slots) {
+  if constexpr (kTcPrefix<D>) {
+    constexpr int R1 = FixT<D>::r1, C = FixT<D>::n2 * FixT<D>::r2, M = 128, N1 = 4;
+    extern __shared__ __align__(128) float smem[];
+    __shared__ int s_free[kMaxChunk], s_slot[kMaxChunk], s_w[kBlock / 32 + 2];
+    __shared__ uint64_t s_mbar;
+    __shared__ uint32_t s_tmem;
+    const unsigned i2 = blockIdx.x;
+    int np;
+    collect_chunk(pmap, pslot, g, true, i2, blockIdx.y, kTcChunk, s_free, s_slot, s_w, &np);
+    if (np == 0) return;
+    float* a_hi = smem;             // K-major [(r1/4)][row][4], M rows
+    float* a_lo = a_hi + M * R1;
+    float* b_hi = a_lo + M * R1;    // K-major [(r1/4)][c][4], C rows
+    float* b_lo = b_hi + C * R1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0) umma::tmem_alloc(&s_tmem, C <= 128 ? 128 : 256);
+    if (threadIdx.x == 32) umma::mbar_init(&s_mbar, 1);
+    // A: G1 rows (prefix, a) hold r1 contiguous: one float4 = one 16-byte unit
+    for (int e = threadIdx.x; e < M * (R1 / 4); e += kBlock) {
+      const int row = e % M, q = e / M;  // consecutive threads -> consecutive rows (conflict-free STS.128)
+      const int p = row / N1, a = row - p * N1;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (p < np) v = __ldg(reinterpret_cast<const float4*>(G1 + ((size_t)s_free[p] * N1 + a) * R1) + q);
+      float4 h, l;
+      umma::split3(v.x, h.x, l.x);
+      umma::split3(v.y, h.y, l.y);
+      umma::split3(v.z, h.z, l.z);
+      umma::split3(v.w, h.w, l.w);
+      reinterpret_cast<float4*>(a_hi)[q * M + row] = h;
+      reinterpret_cast<float4*>(a_lo)[q * M + row] = l;
+    }
+    // B: G2 slice [r1][c] -> K-major over r1: gather 4 consecutive r1 of one c
+    for (int e = threadIdx.x; e < C * (R1 / 4); e += kBlock) {
+      const int c = e % C, q = e / C;
+      float4 v;
+      v.x = __ldg(&G2[((size_t)(4 * q + 0) * g.m2 + i2) * C + c]);
+      v.y = __ldg(&G2[((size_t)(4 * q + 1) * g.m2 + i2) * C + c]);
+      v.z = __ldg(&G2[((size_t)(4 * q + 2) * g.m2 + i2) * C + c]);
+      v.w = __ldg(&G2[((size_t)(4 * q + 3) * g.m2 + i2) * C + c]);
+      float4 h, l;
+      umma::split3(v.x, h.x, l.x);
+      umma::split3(v.y, h.y, l.y);
+      umma::split3(v.z, h.z, l.z);
+      umma::split3(v.w, h.w, l.w);
+      reinterpret_cast<float4*>(b_hi)[q * C + c] = h;
+      reinterpret_cast<float4*>(b_lo)[q * C + c] = l;
+    }
+    umma::fence_smem_to_async();
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    const uint32_t tmem = s_tmem;
+    if (threadIdx.x == 0) {
+      constexpr uint32_t idesc = umma::idesc_tf32(M, C, false, false);
+      const float* as[3] = {a_hi, a_hi, a_lo};
+      const float* bs[3] = {b_hi, b_lo, b_hi};
+#pragma unroll
+      for (int s = 0; s < R1 / 8; ++s)
+#pragma unroll
+        for (int v = 0; v < 3; ++v) {
+          const uint64_t ad = umma::desc(umma::smem_u32(as[v]) + s * 2 * M * 16, M * 16, 128);
+          const uint64_t bd = umma::desc(umma::smem_u32(bs[v]) + s * 2 * C * 16, C * 16, 128);
+          umma::mma_tf32(tmem, ad, bd, idesc, (s > 0 || v > 0) ? 1u : 0u);
+        }
+      umma::commit(&s_mbar);
+    }
+    umma::mbar_wait(&s_mbar, 0);
+    umma::fence_after_sync();
+    // epilogue: warp -> (lane quarter, column half); rows staged in smem (the
+    // operand buffers are free now) then written out as whole slot rows
+    float* stage = smem;  // M x (C + 4) floats
+    constexpr int LS = C + 4;
+    {
+      const int quarter = warp & 3, half = warp >> 2;
+      const int row = 32 * quarter + lane;
+#pragma unroll
+      for (int c0 = 0; c0 < C / 2; c0 += 32) {
+        float v[32];
+        umma::tmem_ld32(tmem + ((uint32_t)(32 * quarter) << 16) + half * (C / 2) + c0, v);
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          *reinterpret_cast<float4*>(stage + row * LS + half * (C / 2) + c0 + i) =
+              make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      }
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) umma::tmem_free(tmem, C <= 128 ? 128 : 256);
+    constexpr int SL = N1 * C;  // slot = n1 rows (a) x C
+    for (int row = warp; row < np * N1; row += kBlock / 32) {
+      const int p = row / N1, a = row - p * N1;
+      float* dst = slots + (size_t)s_slot[p] * SL + a * C;
+      for (int c = 4 * lane; c < C; c += 128)
+        *reinterpret_cast<float4*>(dst + c) = *reinterpret_cast<const float4*>(stage + row * LS + c);
+    }
   }
 }
 
