@@ -12,6 +12,7 @@ __global__ void __launch_bounds__(kBlock) k_runs(const unsigned* __restrict__ sk
                                                  int* __restrict__ prow_begin, int* __restrict__ prow_end,
                                                  int* __restrict__ qrow, int* __restrict__ counts,
                                                  unsigned long long* status, unsigned* ctr) {
+  pdl_enter();
   __shared__ int s_tile;
   __shared__ int s_tmp[kItems * (kBlock / 32) + 2];
   const int tile = claim_tile(ctr, &s_tile);
@@ -74,6 +75,7 @@ constexpr int kRedWarps = kBlock / 32;
 // boundary between consecutive sorted keys fills the digits it skips.
 __global__ void k_i3_bounds(const unsigned* __restrict__ k3, const int* __restrict__ counts, int m3,
                             int* __restrict__ i3_start) {
+  pdl_enter();
   const int U = counts[3];
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q <= U; q += gridDim.x * blockDim.x) {
     const int prev = q > 0 ? (int)k3[q - 1] : -1;
@@ -276,6 +278,7 @@ __global__ void __launch_bounds__(kBlock) k_dg13_reduce(KGeom g, int G1S, int N3
                                                         const int* __restrict__ grp_cnt, float* __restrict__ grad1,
                                                         float* __restrict__ param1, double* __restrict__ vel1,
                                                         int upd1) {
+  pdl_enter();
   extern __shared__ __align__(16) float s_part[];  // kRedWarps x max(G1S, G3S)
   if (blockIdx.x >= g.m1 + g.m3) {
     const int qpb = (G2S + 4 * kBlock - 1) / (4 * kBlock);
@@ -311,6 +314,7 @@ __global__ void __launch_bounds__(kBlock) k_dg13_reduce(KGeom g, int G1S, int N3
 
 __global__ void k_sgd(float* __restrict__ p, const float* __restrict__ gr, double* __restrict__ v, int64_t n,
                       double lr, double mu) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = sgd_apply(p[i], gr[i], v ? v + i : nullptr, lr, mu);
 }
@@ -319,7 +323,7 @@ cudaError_t launch_sgd(float* p, const float* g, double* v, int64_t n, double lr
   if (n <= 0) return cudaSuccess;
   int64_t grid = (n + kBlock - 1) / kBlock;
   if (grid > 148 * 8) grid = 148 * 8;
-  k_sgd<<<(int)grid, kBlock, 0, s>>>(p, g, v, n, lr, mu);
+  launch_pdl(k_sgd, dim3((int)grid), dim3(kBlock), 0, s, p, g, v, n, lr, mu);
   count_launch();
   return cudaGetLastError();
 }
@@ -369,13 +373,13 @@ static cudaError_t forward_impl(ttb_handle* h, const float* c0, const float* c1,
     if ((e = ensure_smem(k_prefix_products_tc<D>, smtc))) return e;
     dim3 gt(h->kg.m2, (unsigned)((h->kg.m1 + kTcChunk - 1) / kTcChunk));
     ProfScope _ps(h, s, "prefix_products_tc");
-    k_prefix_products_tc<D><<<gt, kBlock, smtc, s>>>(d, h->kg, c0, c1, w.pmap, w.pslot, w.slots);
+    launch_pdl(k_prefix_products_tc<D>, dim3(gt), dim3(kBlock), smtc, s, d, h->kg, c0, c1, w.pmap, w.pslot, w.slots);
   } else
   { const size_t sm1 = prefix_smem(d, h->chf);
   if ((e = ensure_smem(k_prefix_products<D>, sm1))) return e;
   dim3 g1(h->kg.m2, (unsigned)h->nsplitf);
   ProfScope _ps(h, s, "prefix_products");
-  k_prefix_products<D><<<g1, kBlock, sm1, s>>>(d, h->kg, h->chf, c0, c1, w.pmap, w.pslot, w.slots);
+  launch_pdl(k_prefix_products<D>, dim3(g1), dim3(kBlock), sm1, s, d, h->kg, h->chf, c0, c1, w.pmap, w.pslot, w.slots);
   }
   count_launch();
   const size_t sm2 = close_smem(d);
@@ -384,7 +388,7 @@ static cudaError_t forward_impl(ttb_handle* h, const float* c0, const float* c1,
   int grid = (B + kBlock / 32 - 1) / (kBlock / 32);
   if (grid > 148 * 32) grid = 148 * 32;
   { ProfScope _ps(h, s, "close_pool");
-  k_close_pool<D><<<grid, kBlock, sm2, s>>>(d, h->kg, c2, w.slots, w.bag_off, w.bag_seg, w.seg_slot, w.seg_inv, w.occ_slot,
+  launch_pdl(k_close_pool<D>, dim3(grid), dim3(kBlock), sm2, s, d, h->kg, c2, w.slots, w.bag_off, w.bag_seg, w.seg_slot, w.seg_inv, w.occ_slot,
                                             w.keys32, B, out);
   }
   count_launch();
@@ -393,7 +397,7 @@ static cudaError_t forward_impl(ttb_handle* h, const float* c0, const float* c1,
     int gridm = (B + kBlock / 32 - 1) / (kBlock / 32);
     if (gridm > 148 * 16) gridm = 148 * 16;
     ProfScope _ps(h, s, "close_multi");
-    k_close_multi<D><<<gridm, kBlock, sm2, s>>>(d, h->kg, c2, w.slots, w.bag_off, w.bag_seg, w.seg_slot, w.seg_inv,
+    launch_pdl(k_close_multi<D>, dim3(gridm), dim3(kBlock), sm2, s, d, h->kg, c2, w.slots, w.bag_off, w.bag_seg, w.seg_slot, w.seg_inv,
                                                 w.occ_slot, w.keys32, B, w.counts, out);
     count_launch();
   }
@@ -415,7 +419,7 @@ static cudaError_t aggregate_impl(ttb_handle* h, const float* gout, cudaStream_t
   // 2. row / prefix runs
   const int tiles = (T + kTile - 1) / kTile;
   { ProfScope _ps(h, s, "runs");
-  k_runs<<<tiles, kBlock, 0, s>>>(sk, T, h->kg, w.pslot, w.urow, w.urow_start, w.urow_i3, w.prow_begin, w.prow_end,
+  launch_pdl(k_runs, dim3(tiles), dim3(kBlock), 0, s, sk, T, h->kg, w.pslot, w.urow, w.urow_start, w.urow_i3, w.prow_begin, w.prow_end,
                                   w.qrow, w.counts, w.runs_status, w.runs_ctr);
   }
   count_launch();
@@ -425,14 +429,14 @@ static cudaError_t aggregate_impl(ttb_handle* h, const float* gout, cudaStream_t
     int grid = (nblk + kBlock / 32 - 1) / (kBlock / 32);
     if (grid > 148 * 16) grid = 148 * 16;
     ProfScope _ps(h, s, "row_agg");
-    k_row_agg<D><<<grid, kBlock, 0, s>>>(d, (int)h->B, T, w.counts, w.urow_start, w.qrow, sv, w.bag_of, gout, w.gU,
+    launch_pdl(k_row_agg<D>, dim3(grid), dim3(kBlock), 0, s, d, (int)h->B, T, w.counts, w.urow_start, w.qrow, sv, w.bag_of, gout, w.gU,
                                          w.agg_hp, w.agg_tp, w.span_list, reinterpret_cast<int*>(w.runs_ctr + 8), w.err);
   }
   {
     int grid = (T / kAggBlock) + 1;
     if (grid > 148 * 8) grid = 148 * 8;
     ProfScope _ps(h, s, "row_agg_span");
-    k_row_agg_span<D><<<grid, kBlock, sizeof(float) * (kBlock / 32) * dN(d), s>>>(
+    launch_pdl(k_row_agg_span<D>, dim3(grid), dim3(kBlock), sizeof(float) * (kBlock / 32) * dN(d), s, 
         d, w.urow_start, w.span_list, reinterpret_cast<int*>(w.runs_ctr + 8), w.agg_hp, w.agg_tp, w.gU, w.err);
   }
   count_launch(2);
@@ -453,7 +457,7 @@ static cudaError_t backward_impl(ttb_handle* h, const float* c0, const float* c1
   if ((e = ensure_smem(k_bwd_prefix<D>, sm))) return e;
   dim3 gp(h->kg.m2, (unsigned)h->nsplitb);
   { ProfScope _ps(h, s, "bwd_prefix");
-  k_bwd_prefix<D><<<gp, kBlock, sm, s>>>(d, h->kg, h->chb, c0, c1, c2, w.pmap, w.pslot, w.slots, w.prow_begin, w.prow_end,
+  launch_pdl(k_bwd_prefix<D>, dim3(gp), dim3(kBlock), sm, s, d, h->kg, h->chb, c0, c1, c2, w.pmap, w.pslot, w.slots, w.prow_begin, w.prow_end,
                                          w.urow_i3, w.gU, w.dH, w.E, w.dG2part, w.grp_cnt,
                                          h->cmaxb);
   }
@@ -464,7 +468,7 @@ static cudaError_t backward_impl(ttb_handle* h, const float* c0, const float* c1
                        s)))
     return e;
   { ProfScope _ps(h, s, "i3_bounds");
-  k_i3_bounds<<<(T + kBlock) / kBlock, kBlock, 0, s>>>(k3, w.counts, (int)h->kg.m3, w.i3_start);
+  launch_pdl(k_i3_bounds, dim3((T + kBlock) / kBlock), dim3(kBlock), 0, s, k3, w.counts, (int)h->kg.m3, w.i3_start);
   }
   count_launch();
   const bool upd = mode == 1;
@@ -473,7 +477,7 @@ static cudaError_t backward_impl(ttb_handle* h, const float* c0, const float* c1
     ProfScope _ps(h, s, "dg123_reduce");
     const size_t smr = sizeof(float) * kRedWarps * (dG1s(d) > dG3s(d) ? dG1s(d) : dG3s(d));
     const int qpb = (dG2s(d) + 4 * kBlock - 1) / (4 * kBlock);
-    k_dg13_reduce<<<h->kg.m1 + h->kg.m3 + h->kg.m2 * qpb, kBlock, smr, s>>>(
+    launch_pdl(k_dg13_reduce, dim3(h->kg.m1 + h->kg.m3 + h->kg.m2 * qpb), dim3(kBlock), smr, s,
         h->kg, dG1s(d), d.n3, dG3s(d), w.pmap, w.pslot, w.E, w.i3_start, v3, w.dH, w.err, upd ? nullptr : g0, p0, v0,
         upd && (mask & 1), upd ? nullptr : g2, p2, v2, upd && (mask & 4), lr, mu, dC(d), dG2s(d), h->cmaxb, h->chb,
         w.dG2part, w.grp_cnt, upd ? nullptr : g1, p1, v1, upd && (mask & 2));
@@ -528,6 +532,7 @@ cudaError_t launch_backward(ttb_handle* h, const float* c0, const float* c1, con
 // index position, then a flag scan over positions numbers them.
 __global__ void k_mark_first(const int* __restrict__ counts, const int* __restrict__ urow_start,
                              const unsigned* __restrict__ sv, int* __restrict__ first_of) {
+  pdl_enter();
   const int U = counts[3];
   for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x)
     first_of[sv[urow_start[u]]] = u + 1;
@@ -537,6 +542,7 @@ __global__ void __launch_bounds__(kBlock) k_first_scan(const int* __restrict__ f
                                                        const unsigned* __restrict__ urow, const float* __restrict__ gU,
                                                        int64_t* __restrict__ rows, float* __restrict__ grads,
                                                        unsigned long long* status, unsigned* ctr) {
+  pdl_enter();
   __shared__ int s_tile;
   __shared__ int s_tmp[kItems * (kBlock / 32) + 2];
   const int tile = claim_tile(ctr, &s_tile);

@@ -75,6 +75,16 @@ __device__ __forceinline__ void st_relaxed_u32(unsigned* p, unsigned v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Programmatic dependent launch: every kernel of the step waits for its
+// predecessor grid (and its memory) here, and immediately allows its own
+// dependent to be scheduled, so launch latency overlaps the previous tail.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+constexpr int kLookWindow = 16;  // predecessors probed per look-back round trip
+
 // Called by ONE thread of the tile. Returns the exclusive prefix of `agg`
 // over all earlier tiles and publishes this tile's inclusive prefix.
 __device__ inline long long lookback_exclusive(unsigned long long* status, int tile, long long agg) {
@@ -85,14 +95,14 @@ __device__ inline long long lookback_exclusive(unsigned long long* status, int t
   st_relaxed_u64(&status[tile], kFlagAgg | (unsigned long long)agg);
   long long excl = 0;
   int j = tile - 1;
-  while (j >= 0) {  // windowed: 8 predecessors per round trip
-    unsigned long long sv[8];
+  while (j >= 0) {  // windowed: kLookWindow predecessors per round trip
+    unsigned long long sv[kLookWindow];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) sv[i] = (j - i >= 0) ? ld_relaxed_u64(&status[j - i]) : 0ull;
+    for (int i = 0; i < kLookWindow; ++i) sv[i] = (j - i >= 0) ? ld_relaxed_u64(&status[j - i]) : 0ull;
     bool done = false;
     int used = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < kLookWindow; ++i) {
       if (done || used < i || j - i < 0) continue;
       const unsigned long long f = sv[i] & ~kValMask;
       if (f == 0) continue;

@@ -237,6 +237,7 @@ __global__ void __launch_bounds__(kBlock) k_prefix_products(D d, KGeom g, int ch
                                                             const float* __restrict__ G2,
                                                             const unsigned* __restrict__ pmap,
                                                             const int* __restrict__ pslot, float* __restrict__ slots) {
+  pdl_enter();
   extern __shared__ __align__(16) float smem[];
   __shared__ int s_free[kMaxChunk], s_slot[kMaxChunk], s_w[kBlock / 32 + 2];
   const int C = dC(d), R1 = d.r1, N1 = d.n1;
@@ -333,6 +334,7 @@ __global__ void __launch_bounds__(kBlock) k_prefix_products_tc(D d, KGeom g, con
                                                                const unsigned* __restrict__ pmap,
                                                                const int* __restrict__ pslot,
                                                                float* __restrict__ slots) {
+  pdl_enter();
   if constexpr (kTcPrefix<D>) {
     constexpr int R1 = FixT<D>::r1, C = FixT<D>::n2 * FixT<D>::r2, M = 128, N1 = 4;
     extern __shared__ __align__(128) float smem[];
@@ -350,33 +352,49 @@ __global__ void __launch_bounds__(kBlock) k_prefix_products_tc(D d, KGeom g, con
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == 0) umma::tmem_alloc(&s_tmem, C <= 128 ? 128 : 256);
     if (threadIdx.x == 32) umma::mbar_init(&s_mbar, 1);
-    // A: G1 rows (prefix, a) hold r1 contiguous: one float4 = one 16-byte unit
-    for (int e = threadIdx.x; e < M * (R1 / 4); e += kBlock) {
-      const int row = e % M, q = e / M;  // consecutive threads -> consecutive rows (conflict-free STS.128)
+    // Operand staging. All global loads of this thread are issued first (so
+    // they are in flight together), then split into hi / lo and stored.
+    // A: G1 rows (prefix, a) hold r1 contiguous: one float4 = one 16-byte unit.
+    // B: G2 slice [r1][c] -> K-major over r1: 4 consecutive r1 of one c.
+    constexpr int NA = M * (R1 / 4) / kBlock, NB = C * (R1 / 4) / kBlock;
+    static_assert(NA * kBlock == M * (R1 / 4) && NB * kBlock == C * (R1 / 4), "staging split");
+    float4 va[NA], vb[NB];
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const int e = threadIdx.x + i * kBlock, row = e % M, q = e / M;
       const int p = row / N1, a = row - p * N1;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (p < np) v = __ldg(reinterpret_cast<const float4*>(G1 + ((size_t)s_free[p] * N1 + a) * R1) + q);
-      float4 h, l;
+      va[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (p < np) va[i] = __ldg(reinterpret_cast<const float4*>(G1 + ((size_t)s_free[p] * N1 + a) * R1) + q);
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const int e = threadIdx.x + i * kBlock, c = e % C, q = e / C;
+      const float* src = G2 + ((size_t)(4 * q) * g.m2 + i2) * C + c;
+      const size_t rs = (size_t)g.m2 * C;
+      vb[i].x = __ldg(src);
+      vb[i].y = __ldg(src + rs);
+      vb[i].z = __ldg(src + 2 * rs);
+      vb[i].w = __ldg(src + 3 * rs);
+    }
+    auto split4 = [](const float4& v, float4& h, float4& l) {
       umma::split3(v.x, h.x, l.x);
       umma::split3(v.y, h.y, l.y);
       umma::split3(v.z, h.z, l.z);
       umma::split3(v.w, h.w, l.w);
+    };
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const int e = threadIdx.x + i * kBlock, row = e % M, q = e / M;
+      float4 h, l;
+      split4(va[i], h, l);
       reinterpret_cast<float4*>(a_hi)[q * M + row] = h;
       reinterpret_cast<float4*>(a_lo)[q * M + row] = l;
     }
-    // B: G2 slice [r1][c] -> K-major over r1: gather 4 consecutive r1 of one c
-    for (int e = threadIdx.x; e < C * (R1 / 4); e += kBlock) {
-      const int c = e % C, q = e / C;
-      float4 v;
-      v.x = __ldg(&G2[((size_t)(4 * q + 0) * g.m2 + i2) * C + c]);
-      v.y = __ldg(&G2[((size_t)(4 * q + 1) * g.m2 + i2) * C + c]);
-      v.z = __ldg(&G2[((size_t)(4 * q + 2) * g.m2 + i2) * C + c]);
-      v.w = __ldg(&G2[((size_t)(4 * q + 3) * g.m2 + i2) * C + c]);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const int e = threadIdx.x + i * kBlock, c = e % C, q = e / C;
       float4 h, l;
-      umma::split3(v.x, h.x, l.x);
-      umma::split3(v.y, h.y, l.y);
-      umma::split3(v.z, h.z, l.z);
-      umma::split3(v.w, h.w, l.w);
+      split4(vb[i], h, l);
       reinterpret_cast<float4*>(b_hi)[q * C + c] = h;
       reinterpret_cast<float4*>(b_lo)[q * C + c] = l;
     }
@@ -493,6 +511,7 @@ __global__ void __launch_bounds__(kBlock) k_close_pool(D d, KGeom g, const float
                                                        const int* __restrict__ occ_slot,
                                                        const unsigned* __restrict__ keys32, int B,
                                                        float* __restrict__ out) {
+  pdl_enter();
   extern __shared__ __align__(16) float smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   // per-warp smem stride: the fast path also keeps per-segment H sums
@@ -593,6 +612,7 @@ __global__ void __launch_bounds__(kBlock) k_close_multi(D d, KGeom g, const floa
                                                         const int* __restrict__ occ_slot,
                                                         const unsigned* __restrict__ keys32, int B,
                                                         const int* __restrict__ counts, float* __restrict__ out) {
+  pdl_enter();
   if constexpr (kFastRows<D> && FixT<D>::n1 * FixT<D>::n2 == 16) {
     if (counts[4] == 0) return;  // no bag has more than one index
     extern __shared__ __align__(16) float smem[];
@@ -731,6 +751,7 @@ __global__ void __launch_bounds__(kBlock) k_row_agg(D d, int B, int T, const int
                                                     float* __restrict__ hp, float* __restrict__ tp,
                                                     int* __restrict__ span_list, int* __restrict__ span_count,
                                                     int* __restrict__ err) {
+  pdl_enter();
   constexpr int PL = agg_per_lane<D>();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int N = dN(d);
@@ -821,6 +842,7 @@ __global__ void __launch_bounds__(kBlock) k_row_agg_span(D d, const int* __restr
                                                          const int* __restrict__ span_count,
                                                          const float* __restrict__ hp, const float* __restrict__ tp,
                                                          float* __restrict__ gU, int* __restrict__ err) {
+  pdl_enter();
   constexpr int PL = agg_per_lane<D>();
   extern __shared__ float s_part[];  // (kBlock/32) x N
   const int N = dN(d);
@@ -890,6 +912,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_bwd_prefix(D d, KGeom g, int ch, 
                                                        const float* __restrict__ gU, float* __restrict__ dH,
                                                        float* __restrict__ E, float* __restrict__ dG2part,
                                                        int* __restrict__ grp_cnt, int cmax) {
+  pdl_enter();
   extern __shared__ __align__(16) float smem[];
   __shared__ int s_free[kMaxChunk], s_slot[kMaxChunk], s_w[kBlock / 32 + 2];
   __shared__ int s_next;

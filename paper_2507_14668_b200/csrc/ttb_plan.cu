@@ -18,6 +18,7 @@ __global__ void __launch_bounds__(kBlock) k_plan_mark(const IdxT* __restrict__ i
                                                       KGeom g, unsigned* __restrict__ pmap,
                                                       unsigned* __restrict__ keys32, int* __restrict__ bag_of,
                                                       int* __restrict__ bag_off, int* __restrict__ err) {
+  pdl_enter();
   const int stride = gridDim.x * blockDim.x;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   int bits = 0, multi = 0;
@@ -62,6 +63,7 @@ __global__ void __launch_bounds__(kBlock) k_plan_slots(const unsigned* __restric
                                                        const unsigned* __restrict__ pmap, int* __restrict__ pslot,
                                                        unsigned* __restrict__ work_key, int* __restrict__ counts,
                                                        unsigned long long* status, unsigned* ctr) {
+  pdl_enter();
   __shared__ int s_tile;
   __shared__ int s_tmp[kItems * (kBlock / 32) + 2];
   const int tile = claim_tile(ctr, &s_tile);
@@ -138,6 +140,7 @@ __global__ void __launch_bounds__(kBlock) k_plan_segs(const unsigned* __restrict
                                                       int* __restrict__ seg_slot, int* __restrict__ seg_bag,
                                                       int* __restrict__ bag_seg, int* __restrict__ counts,
                                                       unsigned long long* status, unsigned* ctr) {
+  pdl_enter();
   constexpr int NW = kBlock / 32;
   __shared__ int s_tile;
   __shared__ int s_cnt[kBagsPerTile];
@@ -299,22 +302,22 @@ cudaError_t launch_plan(ttb_handle* h, const void* idx, int idx64, const int64_t
   {
   ProfScope _ps(h, s, "plan_mark");
   if (idx64)
-    k_plan_mark<long long><<<grid, kBlock, 0, s>>>((const long long*)idx, offsets, T, B, h->kg, w.pmap, w.keys32,
+    launch_pdl(k_plan_mark<long long>, dim3(grid), dim3(kBlock), 0, s, (const long long*)idx, offsets, T, B, h->kg, w.pmap, w.keys32,
                                                    w.bag_of, w.bag_off, w.err);
   else
-    k_plan_mark<int><<<grid, kBlock, 0, s>>>((const int*)idx, offsets, T, B, h->kg, w.pmap, w.keys32, w.bag_of,
+    launch_pdl(k_plan_mark<int>, dim3(grid), dim3(kBlock), 0, s, (const int*)idx, offsets, T, B, h->kg, w.pmap, w.keys32, w.bag_of,
                                              w.bag_off, w.err);
   }
   count_launch();
   const int tiles = (T + kTile - 1) / kTile;
   { ProfScope _ps(h, s, "plan_slots");
-  k_plan_slots<<<tiles, kBlock, 0, s>>>(w.keys32, T, h->kg, w.pmap, w.pslot, w.work_key, w.counts,
+  launch_pdl(k_plan_slots, dim3(tiles), dim3(kBlock), 0, s, w.keys32, T, h->kg, w.pmap, w.pslot, w.work_key, w.counts,
                                         w.scan_status + kScanSlots * h->scan_tiles, w.scan_ctr + kScanSlots);
   }
   count_launch();
   const int btiles = (B + kBagsPerTile - 1) / kBagsPerTile;
   { ProfScope _ps(h, s, "plan_segs");
-  k_plan_segs<<<btiles, kBlock, 0, s>>>(w.keys32, w.bag_off, T, B, h->kg, w.pslot, w.occ_slot, w.occ_tmp, w.seg_inv,
+  launch_pdl(k_plan_segs, dim3(btiles), dim3(kBlock), 0, s, w.keys32, w.bag_off, T, B, h->kg, w.pslot, w.occ_slot, w.occ_tmp, w.seg_inv,
                                         w.seg_slot, w.seg_bag, w.bag_seg, w.counts,
                                         w.scan_status + kScanSegs * h->scan_tiles, w.scan_ctr + kScanSegs);
   }
@@ -325,6 +328,7 @@ cudaError_t launch_plan(ttb_handle* h, const void* idx, int idx64, const int64_t
 // ---------------------------------------------------------------- export
 __global__ void k_export_plan(const Workspace w, KGeom g, int T, int64_t* work, int64_t* slot_occ, int64_t* seg_ids,
                               int64_t* seg_invo, int64_t* digits) {
+  pdl_enter();
   const int P = w.counts[1], S = w.counts[2];
   const int stride = gridDim.x * blockDim.x;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < T; i += stride) {

@@ -23,6 +23,7 @@ __device__ __forceinline__ int sort_count(const int* d_count, int max_n) {
 // global digit histograms for every pass at once
 __global__ void __launch_bounds__(kBlock) k_sort_hist(const unsigned* __restrict__ keys, const int* d_count,
                                                       int max_n, int passes, unsigned* __restrict__ hist) {
+  pdl_enter();
   __shared__ unsigned sh[4][kRadix];
   for (int i = threadIdx.x; i < 4 * kRadix; i += blockDim.x) (&sh[0][0])[i] = 0;
   __syncthreads();
@@ -38,24 +39,6 @@ __global__ void __launch_bounds__(kBlock) k_sort_hist(const unsigned* __restrict
   }
 }
 
-// exclusive scan of each pass's 256 counts (in place); one CTA of 256
-__global__ void k_sort_scan(unsigned* hist, int passes) {
-  __shared__ unsigned s[kRadix];
-  for (int p = 0; p < passes; ++p) {
-    const unsigned v = hist[p * kRadix + threadIdx.x];
-    s[threadIdx.x] = v;
-    __syncthreads();
-    for (int o = 1; o < kRadix; o <<= 1) {
-      const unsigned y = threadIdx.x >= (unsigned)o ? s[threadIdx.x - o] : 0u;
-      __syncthreads();
-      s[threadIdx.x] += y;
-      __syncthreads();
-    }
-    hist[p * kRadix + threadIdx.x] = s[threadIdx.x] - v;
-    __syncthreads();
-  }
-}
-
 // one digit pass; items of a tile are laid out warp-blocked so that
 // (warp, round, lane) order equals input order (stability)
 __global__ void __launch_bounds__(kBlock) k_sort_pass(const unsigned* __restrict__ kin,
@@ -63,6 +46,7 @@ __global__ void __launch_bounds__(kBlock) k_sort_pass(const unsigned* __restrict
                                                       unsigned* __restrict__ vout, const int* d_count, int max_n,
                                                       int shift, const unsigned* __restrict__ goff,
                                                       unsigned* status, unsigned* ctr) {
+  pdl_enter();
   constexpr int NW = kBlock / 32;
   __shared__ int s_tile;
   __shared__ unsigned whist[NW][kRadix];
@@ -71,10 +55,29 @@ __global__ void __launch_bounds__(kBlock) k_sort_pass(const unsigned* __restrict
   const int tile = claim_tile(ctr, &s_tile);
   const int base = tile * kSortTile;
   if (base >= n) return;
+  // global digit offsets: exclusive scan of this pass's 256-bin histogram
+  // (every tile recomputes it: 256 values, no extra kernel)
+  {
+    __shared__ unsigned s_wsum[NW];
+    const unsigned v = goff[threadIdx.x];
+    unsigned incl = v;
+    const int ln = threadIdx.x & 31, wi = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (ln >= o) incl += y;
+    }
+    if (ln == 31) s_wsum[wi] = incl;
+    __syncthreads();
+    unsigned wbase = 0;
+    for (int i = 0; i < wi; ++i) wbase += s_wsum[i];
+    s_goff[threadIdx.x] = wbase + incl - v;
+  }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned lt = lanemask_lt();
   for (int i = threadIdx.x; i < NW * kRadix; i += kBlock) (&whist[0][0])[i] = 0;
   __syncthreads();
+
 
   unsigned key[kSortItems], val[kSortItems];
   int rank[kSortItems];
@@ -131,7 +134,7 @@ __global__ void __launch_bounds__(kBlock) k_sort_pass(const unsigned* __restrict
       }
       st_relaxed_u32(st, kSFlagInc | (excl + run));
     }
-    s_goff[d] = goff[d] + excl;
+    s_goff[d] += excl;
   }
   __syncthreads();
 #pragma unroll
@@ -159,15 +162,16 @@ cudaError_t launch_sort(ttb_handle* h, const unsigned* keys_in, const unsigned* 
   unsigned* status = w.sort_status + (size_t)region * 4 * h->sort_tiles * kRadix;
   unsigned* ctr = w.sort_ctr + region * 4;
   // hist / status / counters live in zero block B, cleared before the backward
+  cudaError_t e;
   int hgrid = (max_n + kBlock * 4 - 1) / (kBlock * 4);
   if (hgrid > 148 * 4) hgrid = 148 * 4;
   if (hgrid < 1) hgrid = 1;
   {
     ProfScope _ps(h, s, region ? "sort_i3_hist" : "sort_rows_hist");
-    k_sort_hist<<<hgrid, kBlock, 0, s>>>(keys_in, d_count, max_n, passes, hist);
-    k_sort_scan<<<1, kRadix, 0, s>>>(hist, passes);
+    e = launch_pdl(k_sort_hist, dim3(hgrid), dim3(kBlock), 0, s, keys_in, d_count, max_n, passes, hist);
+    if (e) return e;
   }
-  count_launch(2);
+  count_launch(1);
   const int tiles = (max_n + kSortTile - 1) / kSortTile;
   const unsigned* ki = keys_in;
   const unsigned* vi = vals_in;
@@ -176,8 +180,9 @@ cudaError_t launch_sort(ttb_handle* h, const unsigned* keys_in, const unsigned* 
     unsigned* vo = (p & 1) ? vB : vA;
     {
       ProfScope _ps(h, s, region ? "sort_i3_pass" : "sort_rows_pass");
-      k_sort_pass<<<tiles, kBlock, 0, s>>>(ki, vi, ko, vo, d_count, max_n, 8 * p, hist + p * kRadix,
-                                           status + (size_t)p * h->sort_tiles * kRadix, ctr + p);
+      e = launch_pdl(k_sort_pass, dim3(tiles), dim3(kBlock), 0, s, ki, vi, ko, vo, d_count, max_n, 8 * p,
+                     (const unsigned*)(hist + p * kRadix), status + (size_t)p * h->sort_tiles * kRadix, ctr + p);
+      if (e) return e;
     }
     count_launch();
     ki = ko;
