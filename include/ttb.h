@@ -162,6 +162,12 @@ int ttb_export_slots(ttb_handle *h, float *slots, ttb_stream stream);
 int ttb_profile_enable(ttb_handle *h, int on);
 int ttb_profile_read(ttb_handle *h, char *names, double *ms, int64_t *calls,
                      int cap, int *count);
+/* Kernel-path options (defaults are the fastest measured):
+ *   TTB_OPT_BWD_SPLIT (1): 1 = backward as a warp-per-prefix rows kernel plus
+ *   an i2-chunk GEMM kernel (tcgen05 3xTF32 where the shape allows) instead
+ *   of the fused backward kernel. */
+#define TTB_OPT_BWD_SPLIT 1
+int ttb_set_option(ttb_handle *h, int option, int value);
 /* FP32 FMA throughput probe: blocks x 256 threads x iters x 16 flops; the
  * caller times it with CUDA events to get the measured FP32 peak. */
 int ttb_fma_peak(float *sink, int iters, int blocks, ttb_stream stream);

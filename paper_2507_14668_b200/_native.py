@@ -32,7 +32,7 @@ EXPORTS = [
     "ttb_abi_version", "ttb_strerror", "ttb_launch_count", "ttb_workspace_bytes", "ttb_create",
     "ttb_destroy", "ttb_plan", "ttb_forward", "ttb_backward", "ttb_aggregate", "ttb_backward_sgd", "ttb_sgd_update",
     "ttb_read_status", "ttb_export_plan", "ttb_export_unique", "ttb_export_slots",
-    "ttb_profile_enable", "ttb_profile_read", "ttb_fma_peak",
+    "ttb_profile_enable", "ttb_profile_read", "ttb_set_option", "ttb_fma_peak",
 ]
 
 
@@ -64,6 +64,7 @@ _PROTOS = {
     "ttb_export_slots": (_int, [_vp, _vp, _vp]),
     "ttb_profile_enable": (_int, [_vp, _int]),
     "ttb_profile_read": (_int, [_vp, _vp, _vp, _vp, _int, C.POINTER(_int)]),
+    "ttb_set_option": (_int, [_vp, _int, _int]),
     "ttb_fma_peak": (_int, [_vp, _int, _int, _vp]),
 }
 

@@ -215,7 +215,8 @@ __device__ inline void dg2_part(KGeom g, int C, int G2S, int nsplit, int ch, uns
                                 const float* __restrict__ part, const int* __restrict__ grp_cnt,
                                 const int* __restrict__ err, float* __restrict__ grad, float* __restrict__ param,
                                 double* __restrict__ vel, double lr, double mu, int do_update) {
-  const int nch = (grp_cnt[i2] + ch - 1) / ch;  // chunks that wrote a partial
+  int nch = (grp_cnt[i2] + ch - 1) / ch;  // chunks (or CTAs) that wrote a partial
+  if (nch > nsplit) nch = nsplit;
   const bool upd = do_update && ((*err & 8) == 0);
   const int e0 = (q * kBlock + threadIdx.x) * 4;
   if (e0 >= G2S) return;
@@ -453,6 +454,44 @@ static cudaError_t backward_impl(ttb_handle* h, const float* c0, const float* c1
   cudaError_t e;
   if ((e = aggregate_impl<D>(h, gout, s))) return e;
   // 4. per-prefix contractions, grouped by i2
+  h->dg2_slots = h->cmaxb;
+  // The split form (k_bwd_rows + k_bwd_gemm[_tc2]) is kept selectable: on
+  // B200 at config 2 it measured 42 + 105 us (SIMT GEMM) / 42 + 156 us
+  // (tcgen05, unpipelined) against 125 us for the fused k_bwd_prefix, so the
+  // fused kernel is the default until the tensor-core GEMM is pipelined.
+  if (h->bwd_split && kFastRows<D> && kVecStage<D> && FixT<D>::n1 == 4) {
+    // split form: warp-per-prefix Z / dH, then the i2-chunk GEMMs
+    {
+      int grid = (int)((h->Pmax + kBlock / 32 - 1) / (kBlock / 32));
+      if (grid > 148 * 8) grid = 148 * 8;
+      ProfScope _ps(h, s, "bwd_rows");
+      launch_pdl(k_bwd_rows<D>, dim3(grid), dim3(kBlock), 0, s, d, h->kg, (const int*)w.counts, c2,
+                 (const float*)w.slots, (const int*)w.prow_begin, (const int*)w.prow_end,
+                 (const unsigned*)w.urow_i3, (const float*)w.gU, w.dH, w.zbuf);
+    }
+    if (kTcBwd<D> && h->chb == kTcBwdChunk && h->kg.m1 <= (unsigned)kMaxGroup) {
+      // persistent tensor-core form: ~2 CTAs per SM across the i2 groups
+      const size_t smt = (size_t)2 * 64 * 128 * 4 + (size_t)2 * 64 * 32 * 4 + (size_t)2 * 32 * 128 * 4;
+      if ((e = ensure_smem(k_bwd_gemm_tc2<D>, smt))) return e;
+      int ns = (int)((2 * 148 + h->kg.m2 - 1) / h->kg.m2);
+      if (ns > h->cmaxb) ns = h->cmaxb;
+      if (ns < 1) ns = 1;
+      h->dg2_slots = ns;
+      dim3 gp(h->kg.m2, (unsigned)ns);
+      ProfScope _ps(h, s, "bwd_gemm_tc");
+      launch_pdl(k_bwd_gemm_tc2<D>, gp, dim3(kBlock), smt, s, d, h->kg, c0, c1, (const unsigned*)w.pmap,
+                 (const int*)w.pslot, (const float*)w.zbuf, w.E, w.dG2part, w.grp_cnt);
+    } else {
+      const size_t smg = sizeof(float) * ((size_t)h->chb * d.n1 * (dC(d) + 4) + (size_t)d.r1 * (dC(d) + 4) +
+                                          (size_t)h->chb * d.n1 * d.r1);
+      if ((e = ensure_smem(k_bwd_gemm<D>, smg))) return e;
+      dim3 gp(h->kg.m2, (unsigned)h->nsplitb);
+      ProfScope _ps(h, s, "bwd_gemm");
+      launch_pdl(k_bwd_gemm<D>, gp, dim3(kBlock), smg, s, d, h->kg, h->chb, c0, c1, (const unsigned*)w.pmap,
+                 (const int*)w.pslot, (const float*)w.zbuf, w.E, w.dG2part, w.grp_cnt, h->cmaxb);
+    }
+    count_launch(2);
+  } else {
   const size_t sm = bwd_smem(d, h->chb);
   if ((e = ensure_smem(k_bwd_prefix<D>, sm))) return e;
   dim3 gp(h->kg.m2, (unsigned)h->nsplitb);
@@ -462,6 +501,7 @@ static cudaError_t backward_impl(ttb_handle* h, const float* c0, const float* c1
                                          h->cmaxb);
   }
   count_launch();
+  }
   // 5. rows by last digit for the G3 reduction
   unsigned *k3, *v3;
   if ((e = launch_sort(h, w.urow_i3, nullptr, w.rkA, w.rvA, w.rkB, w.rvB, w.counts + 3, T, h->i3_bits, 1, &k3, &v3,
@@ -479,7 +519,7 @@ static cudaError_t backward_impl(ttb_handle* h, const float* c0, const float* c1
     const int qpb = (dG2s(d) + 4 * kBlock - 1) / (4 * kBlock);
     launch_pdl(k_dg13_reduce, dim3(h->kg.m1 + h->kg.m3 + h->kg.m2 * qpb), dim3(kBlock), smr, s,
         h->kg, dG1s(d), d.n3, dG3s(d), w.pmap, w.pslot, w.E, w.i3_start, v3, w.dH, w.err, upd ? nullptr : g0, p0, v0,
-        upd && (mask & 1), upd ? nullptr : g2, p2, v2, upd && (mask & 4), lr, mu, dC(d), dG2s(d), h->cmaxb, h->chb,
+        upd && (mask & 1), upd ? nullptr : g2, p2, v2, upd && (mask & 4), lr, mu, dC(d), dG2s(d), h->dg2_slots, h->chb,
         w.dG2part, w.grp_cnt, upd ? nullptr : g1, p1, v1, upd && (mask & 2));
   }
   count_launch(1);

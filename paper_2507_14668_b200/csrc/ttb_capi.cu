@@ -108,6 +108,7 @@ void layout(ttb_handle& h, char* base) {
   w.gU = c.take<float>((size_t)T * N);
   w.dH = c.take<float>((size_t)T * G3S);
   w.E = c.take<float>((size_t)h.Pmax * G1S);
+  w.zbuf = c.take<float>((size_t)h.Pmax * SL);
   w.dG2part = c.take<float>((size_t)g.m[1] * h.cmaxb * G2S);
   w.i3_start = c.take<int>(g.m[2] + 1);
   w.grp_cnt = c.take<int>(g.m[1]);

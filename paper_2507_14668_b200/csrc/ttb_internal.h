@@ -44,6 +44,7 @@ struct Workspace {
   float* gU;        // U x N aggregated row gradients
   float* dH;        // U x (r2 n3) per-row G3 gradient blocks
   float* E;         // Pmax x (n1 r1) per-prefix G1 gradient blocks
+  float* zbuf;      // Pmax x slot: dL/dslot per prefix (split backward)
   float* dG2part;   // m2 x cmax x G2 slice
   int* i3_start;    // m3 + 1
   int* grp_cnt;     // m2: present prefixes per i2
@@ -98,6 +99,8 @@ struct ttb_handle {
   int chf, chb;          // prefixes per chunk (forward / backward kernels)
   int nsplitf, nsplitb;  // CTAs per i2 group (forward / backward)
   int cmaxb;             // chunks per i2 group in the backward (dG2 partials)
+  int dg2_slots;         // dG2 partial slots per i2 written by the last backward
+  int bwd_split;         // use the split backward (rows kernel + tensor-core GEMM kernel)
   int idx_bits, i3_bits;
   char* base;
   size_t bytes;

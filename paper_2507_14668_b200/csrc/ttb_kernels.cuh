@@ -916,6 +916,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_bwd_prefix(D d, KGeom g, int ch, 
   extern __shared__ __align__(16) float smem[];
   __shared__ int s_free[kMaxChunk], s_slot[kMaxChunk], s_w[kBlock / 32 + 2];
   __shared__ int s_next;
+  __shared__ int s_u0[kMaxChunk], s_u1[kMaxChunk];
   const int C = dC(d), R1 = d.r1, R2 = d.r2, N1 = d.n1, N2 = d.n2, N3 = d.n3, X = dX(d), N = dN(d);
   const int SL = dSlot(d), G3S = dG3s(d), G1S = dG1s(d), G2S = dG2s(d);
   const unsigned i2 = blockIdx.x;
@@ -954,6 +955,12 @@ __global__ void __launch_bounds__(kBlock, 3) k_bwd_prefix(D d, KGeom g, int ch, 
     collect_chunk(pmap, pslot, g, true, i2, chunk, ch, s_free, s_slot, s_w, &np);
   }
   if (threadIdx.x == 0) s_next = 0;
+  // row ranges of the chunk's prefixes, one round trip for all of them
+  if (threadIdx.x < np) {
+    const int sl = s_slot[threadIdx.x];
+    s_u0[threadIdx.x] = prow_begin[sl];
+    s_u1[threadIdx.x] = prow_end[sl];
+  }
   if constexpr (kVecStage<D>) {
     constexpr int R1c = FixT<D>::r1, RQ = R1c / 4;
 #pragma unroll 4
@@ -994,7 +1001,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_bwd_prefix(D d, KGeom g, int ch, 
         sbc[x] = sb[x * 32 + lane];
         zr[x] = 0.f;
       }
-      const int u0 = prow_begin[slot], u1 = prow_end[slot];
+      const int u0 = s_u0[pi], u1 = s_u1[pi];
       float ga = 0.f, gb = 0.f;
       float4 hv = make_float4(0.f, 0.f, 0.f, 0.f);
       if (u0 < u1) {
@@ -1142,6 +1149,519 @@ __global__ void __launch_bounds__(kBlock, 3) k_bwd_prefix(D d, KGeom g, int ch, 
     }
   });
   }  // chunk loop
+}
+
+// ------------------------------------------------------------ backward, split form
+// k_bwd_rows: one warp per distinct prefix (any order, high occupancy):
+//   Z_p = sum_u g_u . G3[i3_u]^T  (kept in registers, lane <-> r2) -> Zbuf[slot]
+//   dH_u = slot_p^T . g_u                                          -> dH[u]
+// k_bwd_gemm: one CTA per (i2, chunk of prefixes): loads the chunk's Z rows
+// and runs phases B / C of k_bwd_prefix (dG2 partial, E) without the gather
+// phase, so neither kernel's occupancy is set by the other's needs.
+template <class D>
+__global__ void __launch_bounds__(kBlock) k_bwd_rows(D d, KGeom g, const int* __restrict__ counts,
+                                                     const float* __restrict__ G3, const float* __restrict__ slots,
+                                                     const int* __restrict__ prow_begin,
+                                                     const int* __restrict__ prow_end,
+                                                     const unsigned* __restrict__ urow_i3,
+                                                     const float* __restrict__ gU, float* __restrict__ dH,
+                                                     float* __restrict__ Zbuf) {
+  pdl_enter();
+  if constexpr (kFastRows<D>) {
+    constexpr int Xc = FixT<D>::n1 * FixT<D>::n2, NN = Xc * 4;
+    __shared__ __align__(16) float s_g[kBlock / 32][2 * NN];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    float* s_gw = s_g[w];
+    const unsigned m3n3 = g.m3 * 4u;
+    const int P = counts[1];
+    for (int slot = blockIdx.x * (kBlock / 32) + w; slot < P; slot += gridDim.x * (kBlock / 32)) {
+      const int u0 = prow_begin[slot], u1 = prow_end[slot];
+      const float* sb = slots + (size_t)slot * (Xc * 32);
+      float sbc[Xc], zr[Xc];
+#pragma unroll
+      for (int x = 0; x < Xc; ++x) {
+        sbc[x] = sb[x * 32 + lane];
+        zr[x] = 0.f;
+      }
+      float ga = 0.f, gb = 0.f;
+      float4 hv = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (u0 < u1) {
+        ga = gU[(size_t)u0 * NN + lane];
+        if (NN > 32) gb = gU[(size_t)u0 * NN + 32 + lane];
+        hv = __ldg(reinterpret_cast<const float4*>(G3 + (size_t)lane * m3n3 + urow_i3[u0] * 4u));
+      }
+      int buf = 0;
+      for (int u = u0; u < u1; ++u) {
+        float* sg = s_gw + buf * NN;
+        if (lane < NN) sg[lane] = ga;
+        if (NN > 32) sg[32 + lane] = gb;
+        const float4 h = hv;
+        if (u + 1 < u1) {
+          ga = gU[(size_t)(u + 1) * NN + lane];
+          if (NN > 32) gb = gU[(size_t)(u + 1) * NN + 32 + lane];
+          hv = __ldg(reinterpret_cast<const float4*>(G3 + (size_t)lane * m3n3 + urow_i3[u + 1] * 4u));
+        }
+        __syncwarp();
+        float d0 = 0.f, d1 = 0.f, d2 = 0.f, d3 = 0.f;
+#pragma unroll
+        for (int x = 0; x < Xc; ++x) {
+          const float4 gx = *reinterpret_cast<const float4*>(sg + 4 * x);
+          float z = zr[x];
+          z = fmaf(gx.x, h.x, z);
+          z = fmaf(gx.y, h.y, z);
+          z = fmaf(gx.z, h.z, z);
+          zr[x] = fmaf(gx.w, h.w, z);
+          d0 = fmaf(sbc[x], gx.x, d0);
+          d1 = fmaf(sbc[x], gx.y, d1);
+          d2 = fmaf(sbc[x], gx.z, d2);
+          d3 = fmaf(sbc[x], gx.w, d3);
+        }
+        *reinterpret_cast<float4*>(dH + (size_t)u * 128 + lane * 4) = make_float4(d0, d1, d2, d3);
+        buf ^= 1;
+      }
+      // Z stored column-major per prefix: [c = b r2 + r][a] (the n1 = 4 values
+      // of a column form one 16-byte unit: a K-major UMMA core-matrix row)
+      float4* zo = reinterpret_cast<float4*>(Zbuf + (size_t)slot * (Xc * 32));
+      constexpr int N2c = FixT<D>::n2;
+      static_assert(FixT<D>::n1 == 4, "Z unit layout assumes n1 = 4");
+#pragma unroll
+      for (int b = 0; b < N2c; ++b)
+        zo[b * 32 + lane] = make_float4(zr[0 * N2c + b], zr[1 * N2c + b], zr[2 * N2c + b], zr[3 * N2c + b]);
+    }
+  }
+}
+
+template <class D>
+__global__ void __launch_bounds__(kBlock) k_bwd_gemm(D d, KGeom g, int ch, const float* __restrict__ G1,
+                                                     const float* __restrict__ G2, const unsigned* __restrict__ pmap,
+                                                     const int* __restrict__ pslot, const float* __restrict__ Zbuf,
+                                                     float* __restrict__ E, float* __restrict__ dG2part,
+                                                     int* __restrict__ grp_cnt, int cmax) {
+  pdl_enter();
+  if constexpr (kFastRows<D> && kVecStage<D> && FixT<D>::n1 == 4) {
+    extern __shared__ __align__(16) float smem[];
+    __shared__ int s_free[kMaxChunk], s_slot[kMaxChunk], s_w[kBlock / 32 + 2];
+    constexpr int C = FixT<D>::n2 * FixT<D>::r2, R1 = FixT<D>::r1, N1 = FixT<D>::n1, G1S = N1 * R1;
+    constexpr int LZ = C + 4, C4 = C / 4, RQ = R1 / 4, G2S = R1 * C;
+    const unsigned i2 = blockIdx.x;
+    int np;
+    const int total = collect_chunk(pmap, pslot, g, true, i2, blockIdx.y, ch, s_free, s_slot, s_w, &np);
+    if (blockIdx.y == 0 && threadIdx.x == 0) grp_cnt[i2] = total;
+    if (np == 0) return;
+    const int M = ch * N1;
+    float* s_z = smem;            // M x LZ
+    float* s_g2 = s_z + M * LZ;   // R1 x LZ
+    float* s_g1 = s_g2 + R1 * LZ; // M x R1
+#pragma unroll 4
+    for (int e = threadIdx.x; e < R1 * C4; e += kBlock) {
+      const int r = e / C4, c4 = e - r * C4;
+      *reinterpret_cast<float4*>(s_g2 + r * LZ + 4 * c4) =
+          __ldg(reinterpret_cast<const float4*>(G2 + ((size_t)r * g.m2 + i2) * C) + c4);
+    }
+#pragma unroll 4
+    for (int e = threadIdx.x; e < M * RQ; e += kBlock) {
+      const int row = e / RQ, q = e - row * RQ;
+      const int p = row / N1, a = row - p * N1;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (p < np) v = __ldg(reinterpret_cast<const float4*>(G1 + ((size_t)s_free[p] * N1 + a) * R1) + q);
+      reinterpret_cast<float4*>(s_g1)[e] = v;
+    }
+    // Z rows: Zbuf[slot] is [c][a] (16-byte unit per column)
+#pragma unroll 4
+    for (int e = threadIdx.x; e < ch * C; e += kBlock) {
+      const int p = e / C, c = e - p * C;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (p < np) v = __ldcg(reinterpret_cast<const float4*>(Zbuf + (size_t)s_slot[p] * (N1 * C)) + c);
+      s_z[(p * N1 + 0) * LZ + c] = v.x;
+      s_z[(p * N1 + 1) * LZ + c] = v.y;
+      s_z[(p * N1 + 2) * LZ + c] = v.z;
+      s_z[(p * N1 + 3) * LZ + c] = v.w;
+    }
+    __syncthreads();
+    using Tl = Tiles<D>;
+    {
+      float* part = dG2part + ((size_t)i2 * cmax + blockIdx.y) * G2S;
+      gemm_kk<Tl::BM, Tl::BN>(R1, C, np * N1, s_g1, R1, s_z, LZ,
+                              [&](int m0, int n0, int hm, int hn, float (&acc)[Tl::BM][Tl::BN]) {
+#pragma unroll
+        for (int i = 0; i < Tl::BM; ++i) {
+          float* dst = part + (size_t)split_index<Tl::BM>(m0, hm, i) * C;
+#pragma unroll
+          for (int j = 0; j < Tl::BN; j += 4)
+            *reinterpret_cast<float4*>(dst + split_index<Tl::BN>(n0, hn, j)) =
+                make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+        }
+      });
+    }
+    gemm_nt<Tl::CM, 1, Tl::VEC>(M, R1, C, s_z, LZ, s_g2, LZ, [&](int m0, int n0, float (&acc)[Tl::CM][1]) {
+#pragma unroll
+      for (int i = 0; i < Tl::CM; ++i) {
+        const int row = m0 + i, p = row / N1, a = row - p * N1;
+        if (p < np) E[(size_t)s_slot[p] * G1S + a * R1 + n0] = acc[i][0];
+      }
+    });
+  }
+}
+
+// k_bwd_gemm on the tensor cores (tcgen05 kind::tf32, 3xTF32), for the
+// shape with n1 = 4, r1 = 32, n2 r2 = 128 and 16-prefix chunks (64 Z rows):
+//   phase B: dG2^T (M = n2 r2 = 128, N = r1, K = 64 rows)  = Z^T . G1_chunk
+//   phase C: E     (M = 64 rows,   N = r1, K = n2 r2)      = Z . G2_slice^T
+// Both read Z (loaded once into registers) in a different K-major layout, so
+// the operands are staged, multiplied and then re-staged in the same smem.
+template <class D> constexpr bool kTcBwd = FixT<D>::n1 == 4 && FixT<D>::r1 == 32 && FixT<D>::n2 * FixT<D>::r2 == 128;
+constexpr int kTcBwdChunk = 16;
+
+template <class D>
+__global__ void __launch_bounds__(kBlock) k_bwd_gemm_tc(D d, KGeom g, const float* __restrict__ G1,
+                                                        const float* __restrict__ G2,
+                                                        const unsigned* __restrict__ pmap,
+                                                        const int* __restrict__ pslot, const float* __restrict__ Zbuf,
+                                                        float* __restrict__ E, float* __restrict__ dG2part,
+                                                        int* __restrict__ grp_cnt, int cmax) {
+  pdl_enter();
+  if constexpr (kTcBwd<D>) {
+    constexpr int C = 128, R1 = 32, N1 = 4, ROWS = kTcBwdChunk * N1;  // 64
+    extern __shared__ __align__(128) float smem[];
+    __shared__ int s_free[kMaxChunk], s_slot[kMaxChunk], s_w[kBlock / 32 + 2];
+    __shared__ uint64_t s_mbar;
+    __shared__ uint32_t s_tmem;
+    const unsigned i2 = blockIdx.x;
+    int np;
+    const int total = collect_chunk(pmap, pslot, g, true, i2, blockIdx.y, kTcBwdChunk, s_free, s_slot, s_w, &np);
+    if (blockIdx.y == 0 && threadIdx.x == 0) grp_cnt[i2] = total;
+    if (np == 0) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0) umma::tmem_alloc(&s_tmem, 64);
+    if (threadIdx.x == 32) umma::mbar_init(&s_mbar, 1);
+    char* za_hi = reinterpret_cast<char*>(smem);            // Z operand (32 KB) x2
+    char* za_lo = za_hi + ROWS * C * 4;
+    char* ob_hi = za_lo + ROWS * C * 4;                      // G1 / G2 operand (<= 16 KB) x2
+    char* ob_lo = ob_hi + R1 * C * 4;
+    // ---- loads, all issued up front. A thread owns (prefix p, column group
+    // cg) units: 4 consecutive columns c = 4 cg .. 4 cg + 3, each a float4 of
+    // the 4 rows a of prefix p (Zbuf layout [c][a]).
+    constexpr int NGZ = kTcBwdChunk * (C / 4) / kBlock;  // 2 (p, cg) groups per thread
+    float4 vz[NGZ][4];
+#pragma unroll
+    for (int i = 0; i < NGZ; ++i) {
+      const int e = threadIdx.x + i * kBlock, p = e % kTcBwdChunk, cg = e / kTcBwdChunk;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        vz[i][j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (p < np) vz[i][j] = __ldcg(reinterpret_cast<const float4*>(Zbuf + (size_t)s_slot[p] * (N1 * C)) + 4 * cg + j);
+      }
+    }
+    // G1 chunk: a thread owns (p, r1 group rg): 4 rows a x 4 r1
+    constexpr int NG1 = kTcBwdChunk * (R1 / 4) / kBlock;  // 0.5 -> threads < 128 only
+    float4 vg1[4];
+    const bool own_g1 = threadIdx.x < kTcBwdChunk * (R1 / 4);
+    const int g1p = threadIdx.x % kTcBwdChunk, g1r = threadIdx.x / kTcBwdChunk;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      vg1[a] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (own_g1 && g1p < np)
+        vg1[a] = __ldg(reinterpret_cast<const float4*>(G1 + ((size_t)s_free[g1p] * N1 + a) * R1) + g1r);
+    }
+    (void)NG1;
+    constexpr int NG2 = R1 * C / 4 / kBlock;  // 4 float4 of the G2 slice
+    float4 vg2[NG2];
+#pragma unroll
+    for (int i = 0; i < NG2; ++i) {
+      const int e = threadIdx.x + i * kBlock, r = e % R1, c4 = e / R1;
+      vg2[i] = __ldg(reinterpret_cast<const float4*>(G2 + ((size_t)r * g.m2 + i2) * C) + c4);
+    }
+    auto put4 = [](char* hi, char* lo, uint32_t off, const float4& v) {
+      float4 h, l;
+      umma::split3(v.x, h.x, l.x);
+      umma::split3(v.y, h.y, l.y);
+      umma::split3(v.z, h.z, l.z);
+      umma::split3(v.w, h.w, l.w);
+      *reinterpret_cast<float4*>(hi + off) = h;
+      *reinterpret_cast<float4*>(lo + off) = l;
+    };
+    // ---- phase B operands (K = Z row = 4 p + a):
+    //   A[c][4p + a] : 16-byte unit (k-block p, row c) = the Zbuf unit of column c
+    //   B[r][4p + a] : unit (p, r) = G1[p][0..3][r] (register transpose)
+#pragma unroll
+    for (int i = 0; i < NGZ; ++i) {
+      const int e = threadIdx.x + i * kBlock, p = e % kTcBwdChunk, cg = e / kTcBwdChunk;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) put4(za_hi, za_lo, (uint32_t)((p * C + 4 * cg + j) * 16), vz[i][j]);
+    }
+    if (own_g1) {
+      const float4 t0 = make_float4(vg1[0].x, vg1[1].x, vg1[2].x, vg1[3].x);
+      const float4 t1 = make_float4(vg1[0].y, vg1[1].y, vg1[2].y, vg1[3].y);
+      const float4 t2 = make_float4(vg1[0].z, vg1[1].z, vg1[2].z, vg1[3].z);
+      const float4 t3 = make_float4(vg1[0].w, vg1[1].w, vg1[2].w, vg1[3].w);
+      put4(ob_hi, ob_lo, (uint32_t)((g1p * R1 + 4 * g1r + 0) * 16), t0);
+      put4(ob_hi, ob_lo, (uint32_t)((g1p * R1 + 4 * g1r + 1) * 16), t1);
+      put4(ob_hi, ob_lo, (uint32_t)((g1p * R1 + 4 * g1r + 2) * 16), t2);
+      put4(ob_hi, ob_lo, (uint32_t)((g1p * R1 + 4 * g1r + 3) * 16), t3);
+    }
+    umma::fence_smem_to_async();
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    const uint32_t tmem = s_tmem;
+    if (threadIdx.x == 0) {
+      constexpr uint32_t idB = umma::idesc_tf32(128, R1, false, false);
+      const char* as[3] = {za_hi, za_hi, za_lo};
+      const char* bs[3] = {ob_hi, ob_lo, ob_hi};
+#pragma unroll
+      for (int s = 0; s < ROWS / 8; ++s)
+#pragma unroll
+        for (int v = 0; v < 3; ++v)
+          umma::mma_tf32(tmem, umma::desc(umma::smem_u32(as[v]) + s * 2 * C * 16, C * 16, 128),
+                         umma::desc(umma::smem_u32(bs[v]) + s * 2 * R1 * 16, R1 * 16, 128), idB,
+                         (s > 0 || v > 0) ? 1u : 0u);
+      umma::commit(&s_mbar);
+    }
+    umma::mbar_wait(&s_mbar, 0);  // phase B done reading smem
+    umma::fence_after_sync();
+    // ---- phase C operands (K = column c):
+    //   A[4p + a][c] : unit (k-block cg, row 4p + a) = Z[4p + a][4cg .. 4cg + 3]
+    //   B[r][c]      : unit (cg, r) = G2[r][4cg .. 4cg + 3]
+#pragma unroll
+    for (int i = 0; i < NGZ; ++i) {
+      const int e = threadIdx.x + i * kBlock, p = e % kTcBwdChunk, cg = e / kTcBwdChunk;
+      const float4 a0 = make_float4(vz[i][0].x, vz[i][1].x, vz[i][2].x, vz[i][3].x);
+      const float4 a1 = make_float4(vz[i][0].y, vz[i][1].y, vz[i][2].y, vz[i][3].y);
+      const float4 a2 = make_float4(vz[i][0].z, vz[i][1].z, vz[i][2].z, vz[i][3].z);
+      const float4 a3 = make_float4(vz[i][0].w, vz[i][1].w, vz[i][2].w, vz[i][3].w);
+      put4(za_hi, za_lo, (uint32_t)((cg * ROWS + 4 * p + 0) * 16), a0);
+      put4(za_hi, za_lo, (uint32_t)((cg * ROWS + 4 * p + 1) * 16), a1);
+      put4(za_hi, za_lo, (uint32_t)((cg * ROWS + 4 * p + 2) * 16), a2);
+      put4(za_hi, za_lo, (uint32_t)((cg * ROWS + 4 * p + 3) * 16), a3);
+    }
+#pragma unroll
+    for (int i = 0; i < NG2; ++i) {
+      const int e = threadIdx.x + i * kBlock, r = e % R1, c4 = e / R1;
+      put4(ob_hi, ob_lo, (uint32_t)((c4 * R1 + r) * 16), vg2[i]);
+    }
+    umma::fence_smem_to_async();
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    if (threadIdx.x == 0) {
+      constexpr uint32_t idC = umma::idesc_tf32(ROWS, R1, false, false);
+      const char* as[3] = {za_hi, za_hi, za_lo};
+      const char* bs[3] = {ob_hi, ob_lo, ob_hi};
+#pragma unroll
+      for (int s = 0; s < C / 8; ++s)
+#pragma unroll
+        for (int v = 0; v < 3; ++v)
+          umma::mma_tf32(tmem + 32, umma::desc(umma::smem_u32(as[v]) + s * 2 * ROWS * 16, ROWS * 16, 128),
+                         umma::desc(umma::smem_u32(bs[v]) + s * 2 * R1 * 16, R1 * 16, 128), idC,
+                         (s > 0 || v > 0) ? 1u : 0u);
+      umma::commit(&s_mbar);
+    }
+    umma::mbar_wait(&s_mbar, 1);
+    umma::fence_after_sync();
+    // ---- epilogue: warps 0-3 drain dG2^T (lane = c), warps 4-7 drain E
+    // (M = 64: rows 16q .. 16q + 15 sit in lanes 0..15 of lane quarter q)
+    const int q = warp & 3;
+    if (warp < 4) {
+      float v[32];
+      umma::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16), v);
+      float* part = dG2part + ((size_t)i2 * cmax + blockIdx.y) * (R1 * C);
+      const int c = 32 * q + lane;
+#pragma unroll
+      for (int r = 0; r < R1; ++r) part[r * C + c] = v[r];
+    } else {
+      float v[32];
+      umma::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 32, v);
+      const int zrow = 16 * q + lane, p = zrow / N1, a = zrow % N1;
+      if (lane < 16 && p < np) {
+        float* dst = E + (size_t)s_slot[p] * (N1 * R1) + a * R1;
+#pragma unroll
+        for (int r = 0; r < R1; r += 4)
+          *reinterpret_cast<float4*>(dst + r) = make_float4(v[r], v[r + 1], v[r + 2], v[r + 3]);
+      }
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) umma::tmem_free(tmem, 64);
+  }
+}
+
+// Persistent form of k_bwd_gemm_tc: one CTA per (i2, split). The group's
+// present prefixes are enumerated once, the G2 slice (phase C B operand) is
+// staged once, and dG2^T accumulates in TMEM over all of the CTA's chunks
+// (chunks split, split + nsplit, ...), so each CTA writes ONE dG2 partial.
+constexpr int kMaxGroup = 512;  // prefixes per i2 group enumerated in smem (m1 <= 512)
+
+template <class D>
+__global__ void __launch_bounds__(kBlock) k_bwd_gemm_tc2(D d, KGeom g, const float* __restrict__ G1,
+                                                         const float* __restrict__ G2,
+                                                         const unsigned* __restrict__ pmap,
+                                                         const int* __restrict__ pslot,
+                                                         const float* __restrict__ Zbuf, float* __restrict__ E,
+                                                         float* __restrict__ dG2part, int* __restrict__ grp_cnt) {
+  pdl_enter();
+  if constexpr (kTcBwd<D>) {
+    constexpr int C = 128, R1 = 32, N1 = 4, CH = kTcBwdChunk, ROWS = CH * N1;  // 64
+    extern __shared__ __align__(128) float smem[];
+    __shared__ int s_free[kMaxGroup], s_slot[kMaxGroup], s_w[kBlock / 32 + 2];
+    __shared__ uint64_t s_mbar;
+    __shared__ uint32_t s_tmem;
+    const unsigned i2 = blockIdx.x;
+    const int split = blockIdx.y, nsplit = gridDim.y;
+    int dummy;
+    const int total = collect_chunk(pmap, pslot, g, true, i2, 0, kMaxGroup, s_free, s_slot, s_w, &dummy);
+    if (split == 0 && threadIdx.x == 0) grp_cnt[i2] = total;
+    const int nch = (total + CH - 1) / CH;
+    if (split >= nch) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0) umma::tmem_alloc(&s_tmem, 64);
+    if (threadIdx.x == 32) umma::mbar_init(&s_mbar, 1);
+    char* za_hi = reinterpret_cast<char*>(smem);  // Z operand, 32 KB each
+    char* za_lo = za_hi + ROWS * C * 4;
+    char* g1_hi = za_lo + ROWS * C * 4;           // G1 chunk operand, 8 KB each
+    char* g1_lo = g1_hi + ROWS * R1 * 4;
+    char* g2_hi = g1_lo + ROWS * R1 * 4;          // G2 slice operand, 16 KB each
+    char* g2_lo = g2_hi + R1 * C * 4;
+    auto put4 = [](char* hi, char* lo, uint32_t off, const float4& v) {
+      float4 h, l;
+      umma::split3(v.x, h.x, l.x);
+      umma::split3(v.y, h.y, l.y);
+      umma::split3(v.z, h.z, l.z);
+      umma::split3(v.w, h.w, l.w);
+      *reinterpret_cast<float4*>(hi + off) = h;
+      *reinterpret_cast<float4*>(lo + off) = l;
+    };
+    {  // G2 slice, once: B[r][c] unit (cg, r) = G2[r][4cg .. 4cg + 3]
+      constexpr int NG2 = R1 * C / 4 / kBlock;
+#pragma unroll
+      for (int i = 0; i < NG2; ++i) {
+        const int e = threadIdx.x + i * kBlock, r = e % R1, c4 = e / R1;
+        put4(g2_hi, g2_lo, (uint32_t)((c4 * R1 + r) * 16),
+             __ldg(reinterpret_cast<const float4*>(G2 + ((size_t)r * g.m2 + i2) * C) + c4));
+      }
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    const uint32_t tmem = s_tmem;
+    uint32_t phase = 0;
+    constexpr int NGZ = CH * (C / 4) / kBlock;  // 2 (p, cg) groups per thread
+    const bool own_g1 = threadIdx.x < CH * (R1 / 4);
+    const int g1p = threadIdx.x % CH, g1r = threadIdx.x / CH;
+    bool first = true;
+    for (int chunk = split; chunk < nch; chunk += nsplit) {
+      const int p0 = chunk * CH, np = min(CH, total - p0);
+      // ---- loads for this chunk
+      float4 vz[NGZ][4], vg1[4];
+#pragma unroll
+      for (int i = 0; i < NGZ; ++i) {
+        const int e = threadIdx.x + i * kBlock, p = e % CH, cg = e / CH;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          vz[i][j] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (p < np)
+            vz[i][j] = __ldcg(reinterpret_cast<const float4*>(Zbuf + (size_t)s_slot[p0 + p] * (N1 * C)) + 4 * cg + j);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        vg1[a] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (own_g1 && g1p < np)
+          vg1[a] = __ldg(reinterpret_cast<const float4*>(G1 + ((size_t)s_free[p0 + g1p] * N1 + a) * R1) + g1r);
+      }
+      // ---- phase B operands
+#pragma unroll
+      for (int i = 0; i < NGZ; ++i) {
+        const int e = threadIdx.x + i * kBlock, p = e % CH, cg = e / CH;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) put4(za_hi, za_lo, (uint32_t)((p * C + 4 * cg + j) * 16), vz[i][j]);
+      }
+      if (own_g1) {
+        put4(g1_hi, g1_lo, (uint32_t)((g1p * R1 + 4 * g1r + 0) * 16), make_float4(vg1[0].x, vg1[1].x, vg1[2].x, vg1[3].x));
+        put4(g1_hi, g1_lo, (uint32_t)((g1p * R1 + 4 * g1r + 1) * 16), make_float4(vg1[0].y, vg1[1].y, vg1[2].y, vg1[3].y));
+        put4(g1_hi, g1_lo, (uint32_t)((g1p * R1 + 4 * g1r + 2) * 16), make_float4(vg1[0].z, vg1[1].z, vg1[2].z, vg1[3].z));
+        put4(g1_hi, g1_lo, (uint32_t)((g1p * R1 + 4 * g1r + 3) * 16), make_float4(vg1[0].w, vg1[1].w, vg1[2].w, vg1[3].w));
+      }
+      umma::fence_smem_to_async();
+      umma::fence_before_sync();
+      __syncthreads();
+      umma::fence_after_sync();
+      if (threadIdx.x == 0) {
+        constexpr uint32_t idB = umma::idesc_tf32(128, R1, false, false);
+        const char* as[3] = {za_hi, za_hi, za_lo};
+        const char* bs[3] = {g1_hi, g1_lo, g1_hi};
+#pragma unroll
+        for (int s = 0; s < ROWS / 8; ++s)
+#pragma unroll
+          for (int v = 0; v < 3; ++v)
+            umma::mma_tf32(tmem, umma::desc(umma::smem_u32(as[v]) + s * 2 * C * 16, C * 16, 128),
+                           umma::desc(umma::smem_u32(bs[v]) + s * 2 * R1 * 16, R1 * 16, 128), idB,
+                           (!first || s > 0 || v > 0) ? 1u : 0u);
+        umma::commit(&s_mbar);
+      }
+      first = false;
+      umma::mbar_wait(&s_mbar, phase);
+      phase ^= 1u;
+      umma::fence_after_sync();
+      // ---- phase C operand (Z with K = c); G2 operand is resident
+#pragma unroll
+      for (int i = 0; i < NGZ; ++i) {
+        const int e = threadIdx.x + i * kBlock, p = e % CH, cg = e / CH;
+        put4(za_hi, za_lo, (uint32_t)((cg * ROWS + 4 * p + 0) * 16), make_float4(vz[i][0].x, vz[i][1].x, vz[i][2].x, vz[i][3].x));
+        put4(za_hi, za_lo, (uint32_t)((cg * ROWS + 4 * p + 1) * 16), make_float4(vz[i][0].y, vz[i][1].y, vz[i][2].y, vz[i][3].y));
+        put4(za_hi, za_lo, (uint32_t)((cg * ROWS + 4 * p + 2) * 16), make_float4(vz[i][0].z, vz[i][1].z, vz[i][2].z, vz[i][3].z));
+        put4(za_hi, za_lo, (uint32_t)((cg * ROWS + 4 * p + 3) * 16), make_float4(vz[i][0].w, vz[i][1].w, vz[i][2].w, vz[i][3].w));
+      }
+      umma::fence_smem_to_async();
+      umma::fence_before_sync();
+      __syncthreads();
+      umma::fence_after_sync();
+      if (threadIdx.x == 0) {
+        constexpr uint32_t idC = umma::idesc_tf32(ROWS, R1, false, false);
+        const char* as[3] = {za_hi, za_hi, za_lo};
+        const char* bs[3] = {g2_hi, g2_lo, g2_hi};
+#pragma unroll
+        for (int s = 0; s < C / 8; ++s)
+#pragma unroll
+          for (int v = 0; v < 3; ++v)
+            umma::mma_tf32(tmem + 32, umma::desc(umma::smem_u32(as[v]) + s * 2 * ROWS * 16, ROWS * 16, 128),
+                           umma::desc(umma::smem_u32(bs[v]) + s * 2 * R1 * 16, R1 * 16, 128), idC,
+                           (s > 0 || v > 0) ? 1u : 0u);
+        umma::commit(&s_mbar);
+      }
+      umma::mbar_wait(&s_mbar, phase);
+      phase ^= 1u;
+      umma::fence_after_sync();
+      // ---- E rows of this chunk (M = 64: rows 16q .. 16q + 15 in lanes 0..15 of quarter q)
+      if (warp >= 4) {
+        const int q = warp & 3;
+        float v[32];
+        umma::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 32, v);
+        const int zrow = 16 * q + lane, p = zrow / N1, a = zrow % N1;
+        if (lane < 16 && p < np) {
+          float* dst = E + (size_t)s_slot[p0 + p] * (N1 * R1) + a * R1;
+#pragma unroll
+          for (int r = 0; r < R1; r += 4)
+            *reinterpret_cast<float4*>(dst + r) = make_float4(v[r], v[r + 1], v[r + 2], v[r + 3]);
+        }
+      }
+      umma::fence_before_sync();
+      __syncthreads();  // E drained before the next chunk's MMA C; smem free for restaging
+      umma::fence_after_sync();
+    }
+    // ---- this CTA's dG2 partial (accumulated over its chunks): lane = c
+    if (warp < 4) {
+      const int q = warp;
+      float v[32];
+      umma::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16), v);
+      float* part = dG2part + ((size_t)i2 * nsplit + split) * (R1 * C);
+      const int c = 32 * q + lane;
+#pragma unroll
+      for (int r = 0; r < R1; ++r) part[r * C + c] = v[r];
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) umma::tmem_free(tmem, 64);
+  }
 }
 
 }  // namespace ttb

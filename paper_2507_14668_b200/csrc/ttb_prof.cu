@@ -94,6 +94,14 @@ int ttb_profile_read(ttb_handle* h, char* names, double* ms, int64_t* calls, int
   return TTB_OK;
 }
 
+int ttb_set_option(ttb_handle* h, int option, int value) {
+  if (!h) return TTB_EINVAL;
+  switch (option) {
+    case 1: h->bwd_split = value ? 1 : 0; return TTB_OK;  // TTB_OPT_BWD_SPLIT
+    default: return TTB_EINVAL;
+  }
+}
+
 int ttb_fma_peak(float* sink, int iters, int blocks, ttb_stream stream) {
   if (!sink || iters < 1 || blocks < 1) return TTB_EINVAL;
   k_fma_peak<<<blocks, 256, 0, (cudaStream_t)stream>>>(sink, iters, 0.999999f, 1e-7f);

@@ -171,6 +171,9 @@ class TtEngine:
     def aggregate(self, grad_out: torch.Tensor) -> None:
         nat.check(self.lib.ttb_aggregate(self._handle, _ptr(self._gout(grad_out)), _stream()), "aggregate")
 
+    def set_option(self, option: int, value: int) -> None:
+        nat.check(self.lib.ttb_set_option(self._handle, int(option), int(value)), "set_option")
+
     # ------------------------------------------------------------ profiling
     def profile(self, on: bool = True) -> None:
         nat.check(self.lib.ttb_profile_enable(self._handle, int(bool(on))), "profile")

@@ -299,3 +299,23 @@ def test_dp_step_matches_fused_update():
     torch.cuda.synchronize()
     assert torch.equal(flat.param, fused.param)
     assert torch.equal(flat.velocity, fused.velocity)
+
+
+def test_split_backward_paths_match_oracle():
+    """The split backward (rows kernel + tcgen05 3xTF32 GEMM kernel) is
+    selectable (TTB_OPT_BWD_SPLIT); it must meet the same gradient bar."""
+    g = O.Geometry((40, 60, 25), (4, 4, 4), (1, 32, 32, 1))
+    cores32 = [c.astype(np.float32) for c in O.init_cores(g, 6)]
+    rng = np.random.default_rng(12)
+    idx, off = random_batch(rng, g.rows, 3000, 3, skew=True)
+    gout = rng.standard_normal((3000, g.cols)).astype(np.float32)
+    eng = make_engine(g, idx.size, 3000)
+    eng.set_option(1, 1)
+    dc = to_dev(cores32)
+    eng.plan(torch.from_numpy(idx).cuda(), torch.from_numpy(off).cuda())
+    eng.forward(dc)
+    grads = eng.backward(dc, torch.from_numpy(gout).cuda())
+    ur, ug = O.unique_aggregate(idx, np.repeat(gout.astype(np.float64), np.diff(off), axis=0))
+    want = O.core_grads([c.astype(np.float64) for c in cores32], g, ur, ug)
+    for k in range(3):
+        assert rel_err(grads[k].cpu().numpy(), want[k]) < GRAD_TOL, k
