@@ -155,6 +155,23 @@ int ttb_export_unique(ttb_handle *h, int64_t *rows, float *grads,
  * order (ReuseBuffer.slots, lookup.py:79-85). After ttb_forward. */
 int ttb_export_slots(ttb_handle *h, float *slots, ttb_stream stream);
 
+/* ---- offline index reordering (reference reorder.py) -------------------
+ * ttb_count_frequencies  reorder.py:90-104   counts[table_len] (u64) of all
+ *                        indices; *err != 0 if one lies outside [0, table_len)
+ * ttb_rank_rows          reorder.py:100-104  rows by (count desc, id asc):
+ *                        row_of_rank and rank_of (int64, either nullable);
+ *                        workspace of ttb_rank_workspace_bytes(table_len)
+ * ttb_apply_bijection    reorder.py:286-296  out[i] = forward[in[i]]; *err set
+ *                        (and out = -1) for indices outside [0, table_len)
+ * Community detection (reorder.py:176-236) stays on the host. */
+int ttb_count_frequencies(const int64_t *indices, int64_t n, int64_t table_len,
+                          uint64_t *counts, int *err, ttb_stream stream);
+int ttb_rank_workspace_bytes(int64_t table_len, size_t *bytes);
+int ttb_rank_rows(const uint64_t *counts, int64_t table_len, int64_t *row_of_rank,
+                  int64_t *rank_of, void *workspace, size_t bytes, ttb_stream stream);
+int ttb_apply_bijection(const int64_t *forward, int64_t table_len, const int64_t *in,
+                        int64_t *out, int64_t n, int *err, ttb_stream stream);
+
 /* ---- measurement hooks (not part of the reference interface) ----------
  * Per-kernel CUDA-event timing of one handle's launches: enable, run, then
  * read the accumulated milliseconds and launch counts per kernel name

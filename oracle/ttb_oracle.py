@@ -26,6 +26,7 @@ __all__ = [
     "Geometry", "factorize", "digits_of", "init_cores", "reuse_plan", "segments",
     "forward", "forward_direct", "unique_aggregate", "core_grads", "sgd_step",
     "counters_forward", "counters_backward", "reconstruct_rows",
+    "count_frequencies", "build_bijection", "apply_bijection",
 ]
 
 
@@ -318,3 +319,53 @@ def counters_backward(T, U, d=3, with_buffer=True):
     reuse buffer, 8U without, for d=3; 4U for d=2."""
     per = {3: 7 if with_buffer else 8, 2: 4}[d]
     return dict(slice_mults=per * U, row_adds=T - U, buffer_hits=0, buffer_misses=0)
+
+
+# ------------------------------------------------------------ reordering
+def count_frequencies(batches, table_len):
+    """(counts, row_of_rank, rank_of): bincount over all batches, rows ranked
+    by count descending then id ascending (reorder.py:90-104)."""
+    counts = np.zeros(table_len, dtype=np.int64)
+    for b in batches:
+        a = np.asarray(b, dtype=np.int64)
+        if a.size == 0:
+            continue
+        if (a < 0).any() or (a >= table_len).any():
+            raise ValueError(f"batch index outside [0, {table_len})")
+        counts += np.bincount(a, minlength=table_len)
+    row_of_rank = np.array(sorted(range(table_len), key=lambda r: (-int(counts[r]), r)), dtype=np.int64)
+    rank_of = np.empty(table_len, dtype=np.int64)
+    rank_of[row_of_rank] = np.arange(table_len)
+    return counts, row_of_rank, rank_of
+
+
+def build_bijection(community_of, hot_rows, counts, rank_of, table_len):
+    """forward map: hot rows fixed, cold rows grouped by community, communities
+    by (-total count, min member), members by (-count, id), placed on the free
+    positions in ascending order (reorder.py:239-283)."""
+    thr = len(hot_rows)
+    groups = {}
+    for row in range(table_len):
+        if row not in hot_rows:
+            groups.setdefault(int(community_of[int(rank_of[row]) - thr]), []).append(row)
+    comms = sorted(groups.values(), key=lambda rows: (-sum(int(counts[r]) for r in rows), min(rows)))
+    forward = np.full(table_len, -1, dtype=np.int64)
+    for row in hot_rows:
+        forward[row] = row
+    free = iter(sorted(set(range(table_len)) - set(hot_rows)))
+    for rows in comms:
+        for row in sorted(rows, key=lambda r: (-int(counts[r]), r)):
+            forward[row] = next(free)
+    return forward
+
+
+def apply_bijection(forward, batches):
+    """Relabel every index through forward (reorder.py:286-296)."""
+    out = []
+    n = len(forward)
+    for b in batches:
+        a = np.asarray(b, dtype=np.int64)
+        if a.size and ((a < 0).any() or (a >= n).any()):
+            raise ValueError(f"batch index outside [0, {n})")
+        out.append(np.asarray(forward)[a].tolist())
+    return out

@@ -33,6 +33,7 @@ EXPORTS = [
     "ttb_destroy", "ttb_plan", "ttb_forward", "ttb_backward", "ttb_aggregate", "ttb_backward_sgd", "ttb_sgd_update",
     "ttb_read_status", "ttb_export_plan", "ttb_export_unique", "ttb_export_slots",
     "ttb_profile_enable", "ttb_profile_read", "ttb_set_option", "ttb_fma_peak",
+    "ttb_count_frequencies", "ttb_rank_workspace_bytes", "ttb_rank_rows", "ttb_apply_bijection",
 ]
 
 
@@ -65,6 +66,10 @@ _PROTOS = {
     "ttb_profile_enable": (_int, [_vp, _int]),
     "ttb_profile_read": (_int, [_vp, _vp, _vp, _vp, _int, C.POINTER(_int)]),
     "ttb_set_option": (_int, [_vp, _int, _int]),
+    "ttb_count_frequencies": (_int, [_vp, _i64, _i64, _vp, _vp, _vp]),
+    "ttb_rank_workspace_bytes": (_int, [_i64, C.POINTER(C.c_size_t)]),
+    "ttb_rank_rows": (_int, [_vp, _i64, _vp, _vp, _vp, C.c_size_t, _vp]),
+    "ttb_apply_bijection": (_int, [_vp, _i64, _vp, _vp, _i64, _vp, _vp]),
     "ttb_fma_peak": (_int, [_vp, _int, _int, _vp]),
 }
 

@@ -159,6 +159,9 @@ cudaError_t launch_backward(ttb_handle* h, const float* c0, const float* c1, con
 cudaError_t launch_sort(ttb_handle* h, const unsigned* keys_in, const unsigned* vals_in, unsigned* kA,
                         unsigned* vA, unsigned* kB, unsigned* vB, const int* d_count, int max_n,
                         int bits, int region, unsigned** keys_out, unsigned** vals_out, cudaStream_t s);
+cudaError_t launch_sort_raw(const unsigned* keys_in, const unsigned* vals_in, unsigned* kA, unsigned* vA, unsigned* kB,
+                            unsigned* vB, int n, int bits, unsigned* hist, unsigned* status, int tiles_cap,
+                            unsigned* ctr, unsigned** keys_out, unsigned** vals_out, cudaStream_t s);
 cudaError_t launch_sgd(float* p, const float* g, double* v, int64_t n, double lr, double mu, cudaStream_t s);
 cudaError_t launch_export_plan(ttb_handle* h, int64_t* work, int64_t* slot_occ, int64_t* seg_ids,
                                int64_t* seg_inv, int64_t* digits, cudaStream_t s);

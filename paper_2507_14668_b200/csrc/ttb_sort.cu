@@ -193,4 +193,38 @@ cudaError_t launch_sort(ttb_handle* h, const unsigned* keys_in, const unsigned* 
   return cudaGetLastError();
 }
 
+// Sort with caller-provided state (no handle): used by the offline reorder
+// passes. status: 4 x tiles x 256 u32, hist: 4 x 256 u32, ctr: 4 u32, all
+// zero on entry.
+cudaError_t launch_sort_raw(const unsigned* keys_in, const unsigned* vals_in, unsigned* kA, unsigned* vA, unsigned* kB,
+                            unsigned* vB, int n, int bits, unsigned* hist, unsigned* status, int tiles_cap,
+                            unsigned* ctr, unsigned** keys_out, unsigned** vals_out, cudaStream_t s) {
+  int passes = (bits + 7) / 8;
+  if (passes < 1) passes = 1;
+  if (passes > 4) return cudaErrorInvalidValue;
+  cudaError_t e;
+  int hgrid = (n + kBlock * 4 - 1) / (kBlock * 4);
+  if (hgrid > 148 * 4) hgrid = 148 * 4;
+  if (hgrid < 1) hgrid = 1;
+  if ((e = launch_pdl(k_sort_hist, dim3(hgrid), dim3(kBlock), 0, s, keys_in, (const int*)nullptr, n, passes, hist)))
+    return e;
+  count_launch();
+  const int tiles = (n + kSortTile - 1) / kSortTile;
+  const unsigned* ki = keys_in;
+  const unsigned* vi = vals_in;
+  for (int p = 0; p < passes; ++p) {
+    unsigned* ko = (p & 1) ? kB : kA;
+    unsigned* vo = (p & 1) ? vB : vA;
+    if ((e = launch_pdl(k_sort_pass, dim3(tiles), dim3(kBlock), 0, s, ki, vi, ko, vo, (const int*)nullptr, n, 8 * p,
+                        (const unsigned*)(hist + p * kRadix), status + (size_t)p * tiles_cap * kRadix, ctr + p)))
+      return e;
+    count_launch();
+    ki = ko;
+    vi = vo;
+  }
+  *keys_out = const_cast<unsigned*>(ki);
+  *vals_out = const_cast<unsigned*>(vi);
+  return cudaGetLastError();
+}
+
 }  // namespace ttb

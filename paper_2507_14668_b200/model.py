@@ -8,6 +8,8 @@ Mirrors the reference's model module (pkg/src/ttemb/model.py):
     Mlp                    model.py:134-173 (ReLU between, linear output)
     FieldTable             model.py:179-243 (TT above tt_threshold, dense below)
     DlrmModel              model.py:249-365 (init order, forward, train_step)
+    checkpoint_bytes / save_checkpoint / load_checkpoint / read_checkpoint_records
+                           model.py:388-520 (TTCKPT1 records, byte-compatible)
 
 The TT fields run on the CUDA TT-EmbeddingBag (TTEmbeddingBag); the dense
 MLPs, the interaction and the small dense fields stay in PyTorch (north star
@@ -19,7 +21,9 @@ take the same step inside their backward kernels).
 """
 from __future__ import annotations
 
+import json
 import math
+import struct
 from dataclasses import dataclass
 from typing import Optional, Sequence
 
@@ -30,7 +34,9 @@ from torch import nn
 from . import _native as nat
 from .embedding_bag import TTEmbeddingBag
 from .engine import _ptr, _stream, require_cuda, to_offsets
-from .geometry import factorize_dims
+from .geometry import bytes_to_table, factorize_dims, table_to_bytes
+
+CKPT_MAGIC = b"TTCKPT1\n"
 
 
 @dataclass(frozen=True)
@@ -218,3 +224,128 @@ def bags_field_tensors(bags_per_field, device):
     """Reference Dataset.bags (field -> sample -> bag) -> [(indices, offsets)]."""
     from .engine import bags_to_tensors
     return [bags_to_tensors(bags, device) for bags in bags_per_field]
+
+
+# -------------------------------------------------------------- checkpoint
+def _tensor_payload(t: torch.Tensor) -> bytes:
+    """u64 ndim, u64 dims, fp32 LE data (model.py:388-391)."""
+    arr = t.detach().cpu().numpy()
+    head = struct.pack("<Q", arr.ndim) + b"".join(struct.pack("<Q", s) for s in arr.shape)
+    return head + np.ascontiguousarray(arr, dtype="<f4").tobytes()
+
+
+def _tensor_from_payload(payload: bytes, name: str) -> np.ndarray:
+    if len(payload) < 8:
+        raise ValueError(f"record {name}: truncated tensor header")
+    ndim = struct.unpack_from("<Q", payload, 0)[0]
+    if len(payload) < 8 + 8 * ndim:
+        raise ValueError(f"record {name}: truncated tensor dims")
+    shape = struct.unpack_from(f"<{ndim}Q", payload, 8) if ndim else ()
+    body = payload[8 + 8 * ndim:]
+    count = int(np.prod(shape, dtype=np.int64)) if ndim else 1
+    if len(body) != 4 * count:
+        raise ValueError(f"record {name}: payload size != declared shape")
+    return np.frombuffer(body, dtype="<f4").reshape(shape)
+
+
+def _config_payload(c: ModelConfig) -> bytes:
+    doc = {"n_dense": c.n_dense, "rows_per_field": list(c.rows_per_field), "emb_dim": c.emb_dim,
+           "ranks": list(c.ranks), "tt_threshold": c.tt_threshold, "bottom_sizes": list(c.bottom_sizes),
+           "top_sizes": list(c.top_sizes), "loss": c.loss, "seed": c.seed}
+    return json.dumps(doc, sort_keys=True, separators=(",", ":")).encode("ascii")
+
+
+def _config_from_payload(payload: bytes) -> ModelConfig:
+    d = json.loads(payload.decode("ascii"))
+    return ModelConfig(n_dense=d["n_dense"], rows_per_field=tuple(d["rows_per_field"]), emb_dim=d["emb_dim"],
+                       ranks=tuple(d["ranks"]), tt_threshold=d["tt_threshold"],
+                       bottom_sizes=tuple(d["bottom_sizes"]), top_sizes=tuple(d["top_sizes"]), loss=d["loss"],
+                       seed=d["seed"])
+
+
+def checkpoint_bytes(model: DlrmModel) -> bytes:
+    """TTCKPT1: magic, then records (u64 name len, name, u64 payload len,
+    payload): config JSON, per field a TTEMB1 blob or a dense tensor, then
+    the MLP tensors in named_params order (model.py:436-460)."""
+    records = [("config", _config_payload(model.config))]
+    for f, fld in enumerate(model.fields):
+        if isinstance(fld, TTEmbeddingBag):
+            records.append((f"field_{f}.tt", table_to_bytes(fld.shape, [c.detach().cpu().numpy()
+                                                                         for c in fld.cores])))
+        else:
+            records.append((f"field_{f}.rows", _tensor_payload(fld.rows)))
+    for name, t in model.named_ref_params():
+        if not name.startswith("field_"):
+            records.append((name, _tensor_payload(t)))
+    out = [CKPT_MAGIC]
+    for name, payload in records:
+        raw = name.encode("ascii")
+        out += [struct.pack("<Q", len(raw)), raw, struct.pack("<Q", len(payload)), payload]
+    return b"".join(out)
+
+
+def save_checkpoint(model: DlrmModel, path) -> None:
+    with open(path, "wb") as fh:
+        fh.write(checkpoint_bytes(model))
+
+
+def parse_checkpoint(buf: bytes) -> list:
+    """[(name, payload)] of a TTCKPT1 buffer (model.py:468-490)."""
+    if buf[:len(CKPT_MAGIC)] != CKPT_MAGIC:
+        raise ValueError("not a checkpoint file (bad magic)")
+    pos, records = len(CKPT_MAGIC), []
+    while pos < len(buf):
+        if pos + 8 > len(buf):
+            raise ValueError("truncated record header")
+        (nlen,) = struct.unpack_from("<Q", buf, pos)
+        pos += 8
+        if pos + nlen + 8 > len(buf):
+            raise ValueError("truncated record name or length")
+        name = buf[pos:pos + nlen].decode("ascii")
+        pos += nlen
+        (size,) = struct.unpack_from("<Q", buf, pos)
+        pos += 8
+        if pos + size > len(buf):
+            raise ValueError(f"record {name}: truncated payload")
+        records.append((name, buf[pos:pos + size]))
+        pos += size
+    return records
+
+
+def read_checkpoint_records(path) -> list:
+    with open(path, "rb") as fh:
+        return parse_checkpoint(fh.read())
+
+
+def load_checkpoint(path, device=None, **model_kwargs) -> DlrmModel:
+    """Rebuild the model from its config record, then overwrite every
+    parameter from the records (model.py:493-520); strict about missing,
+    mismatched and unknown records."""
+    records = dict(read_checkpoint_records(path))
+    if "config" not in records:
+        raise ValueError("checkpoint has no config record")
+    model = DlrmModel(_config_from_payload(records.pop("config")), device=device, **model_kwargs)
+    with torch.no_grad():
+        for f, fld in enumerate(model.fields):
+            if not isinstance(fld, TTEmbeddingBag):
+                continue
+            name = f"field_{f}.tt"
+            if name not in records:
+                raise ValueError(f"checkpoint missing record {name}")
+            shape, cores = bytes_to_table(records.pop(name))
+            if shape != fld.shape:
+                raise ValueError(f"record {name}: table shape mismatch")
+            for dst, src in zip(fld.cores, cores):
+                dst.copy_(torch.from_numpy(np.ascontiguousarray(src, dtype=np.float32)))
+        for name, param in model.named_ref_params():
+            if ".core" in name:
+                continue
+            if name not in records:
+                raise ValueError(f"checkpoint missing record {name}")
+            arr = _tensor_from_payload(records.pop(name), name)
+            if tuple(arr.shape) != tuple(param.shape):
+                raise ValueError(f"record {name}: shape mismatch")
+            param.copy_(torch.from_numpy(arr.copy()))
+    if records:
+        raise ValueError(f"checkpoint has unknown records: {', '.join(sorted(records))}")
+    return model

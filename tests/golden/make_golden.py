@@ -191,6 +191,7 @@ def gen_dlrm():
     model = md.DlrmModel(cfg, dtype=np.float32)
     for name, arr in model.named_params():
         s[f"init.{name}"] = arr.copy()
+    s["ckpt_init"] = np.frombuffer(md.checkpoint_bytes(model), dtype=np.uint8)
     s["data.labels"] = ds.labels
     s["data.dense"] = ds.dense
     for f in range(3):
@@ -205,7 +206,43 @@ def gen_dlrm():
             s[f"step{step}.{name}"] = arr.copy()
     s["losses"] = np.array(losses)
     s["config"] = np.array([6, 16, 4, 1000, 5])
+    s["ckpt_final"] = np.frombuffer(md.checkpoint_bytes(model), dtype=np.uint8)
     np.savez_compressed(OUT / "dlrm.npz", **s)
+
+
+def gen_reorder():
+    """Frequencies, hot rows, communities and the bijection of the reference's
+    reorder pipeline on a skewed synthetic trace with planted clusters."""
+    from ttemb import reorder as ro
+    s = {}
+    rng = np.random.default_rng(41)
+    table_len = 600
+    perm = rng.permutation(table_len)
+    batches = []
+    for _ in range(80):
+        c = int(rng.integers(0, 12))
+        members = perm[c * 50:(c + 1) * 50]
+        size = int(rng.integers(1, 9))
+        b = rng.choice(members, size=size).tolist()
+        if rng.random() < 0.3:
+            b.append(int(rng.integers(0, 5)))  # hot head
+        batches.append(b)
+    freq = ro.count_frequencies(batches, table_len)
+    graph, hot = ro.build_index_graph(batches, freq, 0.02)
+    comm = ro.detect_communities(graph)
+    bij = ro.build_bijection(comm, hot, freq, table_len)
+    idx, off = batch_arrays(batches)
+    s["idx"], s["off"] = idx, off
+    s["table_len"] = np.array([table_len])
+    s["counts"], s["row_of_rank"], s["rank_of"] = freq.counts, freq.row_of_rank, freq.rank_of
+    s["hot"] = np.array(sorted(hot), dtype=np.int64)
+    s["community_of"] = comm.community_of.astype(np.int64)
+    s["forward"], s["inverse"] = bij.forward, bij.inverse
+    rel = ro.apply_bijection(bij, batches)
+    s["relabeled"] = np.concatenate([np.asarray(b, dtype=np.int64) for b in rel])
+    s["mdp_before"] = np.array([ro.mean_distinct_prefixes(batches, 8)])
+    s["mdp_after"] = np.array([ro.mean_distinct_prefixes(rel, 8)])
+    np.savez_compressed(OUT / "reorder.npz", **s)
 
 
 if __name__ == "__main__":
@@ -214,5 +251,6 @@ if __name__ == "__main__":
     gen_plans_forward()
     gen_backward()
     gen_dlrm()
+    gen_reorder()
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size)

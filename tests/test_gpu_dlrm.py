@@ -36,3 +36,31 @@ def test_dlrm_matches_reference_run(golden):
             want = s[f"step{step}.{name}"].astype(np.float64)
             err = np.abs(got - want).max() / max(1e-3, np.abs(want).max())
             assert err < 1e-4, (step, name, err)
+
+
+def test_checkpoint_bytes_match_reference(golden, tmp_path):
+    """TTCKPT1 of the freshly initialised model == the reference's bytes;
+    save -> load round trip restores every parameter; corrupt files raise."""
+    from paper_2507_14668_b200 import model as M
+    s = golden("dlrm")
+    cfg = M.ModelConfig(n_dense=6, rows_per_field=(4000, 500, 118), emb_dim=16, ranks=(1, 4, 4, 1),
+                        tt_threshold=1000, bottom_sizes=(32,), top_sizes=(32, 16), loss="bce", seed=5)
+    model = M.DlrmModel(cfg)
+    assert M.checkpoint_bytes(model) == s["ckpt_init"].tobytes()
+    # the reference's post-training checkpoint loads here with the same tensors
+    path = tmp_path / "ref.ckpt"
+    path.write_bytes(s["ckpt_final"].tobytes())
+    loaded = M.load_checkpoint(path)
+    for name, p in loaded.named_ref_params():
+        assert np.array_equal(p.detach().cpu().numpy(), s[f"step2.{name}"]), name
+    assert M.checkpoint_bytes(loaded) == s["ckpt_final"].tobytes()
+    M.save_checkpoint(loaded, tmp_path / "mine.ckpt")
+    assert (tmp_path / "mine.ckpt").read_bytes() == s["ckpt_final"].tobytes()
+    # corruption
+    bad = tmp_path / "bad.ckpt"
+    bad.write_bytes(b"NOTCKPT" + s["ckpt_final"].tobytes()[7:])
+    with pytest.raises(ValueError):
+        M.load_checkpoint(bad)
+    bad.write_bytes(s["ckpt_final"].tobytes()[:-3])
+    with pytest.raises(ValueError):
+        M.load_checkpoint(bad)
