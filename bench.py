@@ -122,6 +122,10 @@ def algorithmic_counts(shape, T, B, P, S, U):
     }
     fwd = fl["prefix_products"] + fl["close_pool"]
     bwd = P * 2 * f_pre + U * 4 * N * r2 + (U - P) * n1 * n2 * r2 + (T - U) * N + 5 * G
+    # tensor-core pipeline: whole forward / whole backward (algorithmic work
+    # only: the backward's recomputation of X = G1.G2 is not counted)
+    fl["f_fwd"] = fwd
+    fl["f_bwd"] = bwd
     step_bytes = 2 * (T * 8 + (B + 1) * 8 + B * N * 4) + 16 * G
     return fl, fwd, bwd, step_bytes
 
@@ -244,7 +248,8 @@ def run_ours(args):
             "l2": "flushed between timed steps (512 MiB write, outside the timed events)",
             "launch": "one CUDA graph per step" if use_graph else "eager launches",
         },
-        "counts": {"T": st["T"], "B": st["B"], "P": st["P"], "S": st["S"], "U": eng.status()["U"]},
+        "counts": host_counts(idx_h, off_h, shape, st),
+        "pipeline": "tensor-core (TTB_OPT_FAST)" if eng.fast else "deterministic",
         "gpu_launches": int(launches_per_step * args.steps),
         "clocks": clk,
     }
@@ -264,6 +269,23 @@ def run_ours(args):
         print(json.dumps(result), flush=True)
 
 
+_COUNTS = {}
+
+
+def host_counts(idx_h, off_h, shape, st, cache=False):
+    """T, B, P, S, U of the benchmark batch. The tensor-core pipeline does not
+    form the reference's segments / unique rows, so they come from numpy."""
+    if cache:
+        return _COUNTS["last"]
+    import numpy as np
+    m3 = shape.m[-1]
+    bag = np.repeat(np.arange(off_h.size - 1), np.diff(off_h))
+    S = np.unique(bag.astype(np.int64) * (int(shape.rows) // m3 + 1) + idx_h // m3).size
+    c = {"T": int(st["T"]), "B": int(st["B"]), "P": int(st["P"]), "S": int(S), "U": int(np.unique(idx_h).size)}
+    _COUNTS["last"] = c
+    return c
+
+
 def profile_and_roofline(args, torch, eng, lib, emb, step, flush, st, dev):
     """Per-kernel CUDA-event durations (live, on the launch stream) over
     profiled steps; roofline of the dominant kernel and of the whole step."""
@@ -277,8 +299,8 @@ def profile_and_roofline(args, torch, eng, lib, emb, step, flush, st, dev):
     torch.cuda.synchronize()
     prof = eng.profile_read()
     eng.profile(False)
-    U = eng.status()["U"]
-    fl, fwd, bwd, step_bytes = algorithmic_counts(emb.shape, st["T"], st["B"], st["P"], st["S"], U)
+    cnt = host_counts(None, None, emb.shape, st, cache=True)
+    fl, fwd, bwd, step_bytes = algorithmic_counts(emb.shape, cnt["T"], cnt["B"], cnt["P"], cnt["S"], cnt["U"])
     kernels = {}
     for k, (ms, c) in prof.items():
         kernels[k] = {"us_per_step": 1e3 * ms / nprof, "launches_per_step": c / nprof, "avg_us": 1e3 * ms / max(c, 1)}
@@ -311,6 +333,7 @@ def profile_and_roofline(args, torch, eng, lib, emb, step, flush, st, dev):
     else:
         # integer / sort kernels: bytes moved per launch (keys+values read and written)
         T = st["T"]
+        U = _COUNTS["last"]["U"]
         nbytes = {"sort_rows_pass": 16 * T, "sort_rows_hist": 4 * T, "plan_mark": 8 * T + 8 * st["B"] + 12 * T,
                   "plan_slots": 8 * T, "plan_segs": 24 * T, "runs": 8 * T + 16 * U}.get(dominant, 8 * T)
         achieved = nbytes / (dk["avg_us"] * 1e-6) / 1e9

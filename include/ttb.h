@@ -182,8 +182,19 @@ int ttb_profile_read(ttb_handle *h, char *names, double *ms, int64_t *calls,
 /* Kernel-path options (defaults are the fastest measured):
  *   TTB_OPT_BWD_SPLIT (1): 1 = backward as a warp-per-prefix rows kernel plus
  *   an i2-chunk GEMM kernel (tcgen05 3xTF32 where the shape allows) instead
- *   of the fused backward kernel. */
+ *   of the fused backward kernel (deterministic pipeline only).
+ *   TTB_OPT_FAST (2): 1 (default where n = (4,4,4), ranks (1,32,32,1)) = the
+ *   tensor-core pipeline: prefix-sorted work tiles, X = G1.G2 formed in TMEM
+ *   by tcgen05 3xTF32 in the forward and recomputed in the backward, core
+ *   gradients accumulated with fp32 reductions (summation order not fixed).
+ *   0 = the deterministic pipeline (fixed summation order, reference-ordered
+ *   plan resident, ttb_aggregate / ttb_export_unique / ttb_export_slots).
+ *   Under 1, ttb_export_plan builds the reference-ordered plan on demand from
+ *   the buffers given to ttb_plan (they must still be valid then) and
+ *   ttb_read_status reports S = -1 until it has, U = -1, and status[7] = the
+ *   number of work items. Changing the option drops the current plan. */
 #define TTB_OPT_BWD_SPLIT 1
+#define TTB_OPT_FAST 2
 int ttb_set_option(ttb_handle *h, int option, int value);
 /* FP32 FMA throughput probe: blocks x 256 threads x iters x 16 flops; the
  * caller times it with CUDA events to get the measured FP32 peak. */

@@ -27,6 +27,9 @@ ERRBIT_EMPTY_BAG = 2
 ERRBIT_OFFSETS = 4
 ERRBIT_NONFINITE = 8
 
+OPT_BWD_SPLIT = 1
+OPT_FAST = 2
+
 # every symbol include/ttb.h declares (tests check the .so exports them all)
 EXPORTS = [
     "ttb_abi_version", "ttb_strerror", "ttb_launch_count", "ttb_workspace_bytes", "ttb_create",

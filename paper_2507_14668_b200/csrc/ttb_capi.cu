@@ -63,6 +63,7 @@ void layout(ttb_handle& h, char* base) {
   h.scan_tiles = (st > bt ? st : bt) + 1;
   Carver c{base};
   Workspace& w = h.w;
+  w.fast_hdr = c.take<int>(64);  // right before zero block A (fast_plan clears both in one memset)
   // zero block A
   size_t a0 = c.off;
   w.err = c.take<int>(16);
@@ -122,6 +123,18 @@ void layout(ttb_handle& h, char* base) {
   w.agg_tp = c.take<float>((size_t)(T / 64 + 2) * N);
   w.span_list = c.take<int>(T / 64 + 2);
   w.scratch1 = c.take<float>(16);
+  const bool fz = h.fast_ok;
+  w.f_key = c.take<unsigned>(fz ? T : 0);
+  w.f_i3 = c.take<unsigned>(fz ? T : 0);
+  w.f_sbi = c.take<int2>(fz ? T : 0);
+  w.f_item_start = c.take<int>(fz ? T + 1 : 0);
+  w.f_item_key = c.take<unsigned>(fz ? T : 0);
+  w.f_i2_item = c.take<int>(fz ? g.m[1] + 1 : 0);
+  w.f_tile_start = c.take<int>(fz ? g.m[1] + 1 : 0);
+  w.f_tile_info = c.take<int4>(fz ? T / 32 + g.m[1] + 2 : 0);
+  w.f_g1img = c.take<float>(fz ? (size_t)g.m[0] * 512 : 0);
+  w.f_img = c.take<float>(fz ? (size_t)g.m[1] * 16384 : 0);
+  w.f_grad = c.take<float>(fz ? (size_t)(G1S * g.m[0] + G2S * g.m[1] + G3S * g.m[2]) : 0);
   h.bytes = c.off + 256;
 }
 
@@ -139,6 +152,8 @@ bool init_handle(ttb_handle& h, const ttb_geom* g, int64_t max_T, int64_t max_B)
   h.maxT = max_T;
   h.maxB = max_B;
   h.idx_bits = bits_for((uint64_t)h.kg.rows - 1);
+  h.fast_ok = fast_supported(&h) ? 1 : 0;
+  h.fast = h.fast_ok;
   h.i3_bits = bits_for((uint64_t)h.kg.m3 - 1);
   layout(h, nullptr);
   return true;
@@ -188,6 +203,13 @@ ttb_handle* ttb_create(const ttb_geom* g, int64_t max_T, int64_t max_B, void* wo
   layout(*h, base);
   h->base = base;
   h->pmap_clean = 1;
+  {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+      h->num_sms = sms;
+    else
+      h->num_sms = 148;
+  }
   cudaStream_t s = (cudaStream_t)stream;
   if (cudaMemsetAsync(h->w.zeroA, 0, h->w.zeroA_bytes + h->w.zeroB_bytes, s) != cudaSuccess ||
       cudaMemsetAsync(h->w.grp_done, 0, sizeof(int) * h->kg.m2, s) != cudaSuccess ||
@@ -210,7 +232,13 @@ int ttb_plan(ttb_handle* h, const void* indices, int idx_is_64, const int64_t* o
   h->planned = 0;
   h->forwarded = 0;
   h->backwarded = 0;
-  cudaError_t e = launch_plan(h, indices, idx_is_64, offsets, (cudaStream_t)stream);
+  h->plan_idx = indices;
+  h->plan_off = offsets;
+  h->plan_idx64 = idx_is_64;
+  h->legacy_planned = 0;
+  cudaError_t e = h->fast ? fast_plan(h, indices, idx_is_64, offsets, (cudaStream_t)stream)
+                          : launch_plan(h, indices, idx_is_64, offsets, (cudaStream_t)stream);
+  if (!h->fast) h->legacy_planned = 1;
   if (e != cudaSuccess) return TTB_ECUDA;
   h->planned = 1;
   ++h->gen;
@@ -219,8 +247,10 @@ int ttb_plan(ttb_handle* h, const void* indices, int idx_is_64, const int64_t* o
 
 int ttb_forward(ttb_handle* h, const float* c0, const float* c1, const float* c2, float* out, ttb_stream stream) {
   if (!h || !c0 || !c1 || !c2 || !out) return TTB_EINVAL;
-  if (!h->planned || h->pmap_clean) return TTB_ESTATE;  // a backward consumed this plan's prefix table
-  cudaError_t e = launch_forward(h, c0, c1, c2, out, (cudaStream_t)stream);
+  if (!h->planned) return TTB_ESTATE;
+  if (!h->fast && h->pmap_clean) return TTB_ESTATE;  // a backward consumed this plan's prefix table
+  cudaError_t e = h->fast ? fast_forward(h, c0, c1, c2, out, (cudaStream_t)stream)
+                          : launch_forward(h, c0, c1, c2, out, (cudaStream_t)stream);
   if (e != cudaSuccess) return TTB_ECUDA;
   h->forwarded = 1;
   return TTB_OK;
@@ -230,8 +260,10 @@ int ttb_backward(ttb_handle* h, const float* c0, const float* c1, const float* c
                  float* g1, float* g2, ttb_stream stream) {
   if (!h || !c0 || !c1 || !c2 || !grad_out || !g0 || !g1 || !g2) return TTB_EINVAL;
   if (!h->forwarded) return TTB_ESTATE;
-  cudaError_t e = launch_backward(h, c0, c1, c2, grad_out, g0, g1, g2, nullptr, nullptr, nullptr, nullptr, nullptr,
-                                  nullptr, 0.0, 0.0, 0, 0, (cudaStream_t)stream);
+  cudaError_t e = h->fast ? fast_backward(h, c0, c1, c2, grad_out, g0, g1, g2, nullptr, nullptr, nullptr, nullptr,
+                                          nullptr, nullptr, 0.0, 0.0, 0, 0, (cudaStream_t)stream)
+                          : launch_backward(h, c0, c1, c2, grad_out, g0, g1, g2, nullptr, nullptr, nullptr, nullptr,
+                                            nullptr, nullptr, 0.0, 0.0, 0, 0, (cudaStream_t)stream);
   if (e != cudaSuccess) return TTB_ECUDA;
   h->backwarded = 1;
   h->pmap_clean = 1;
@@ -240,7 +272,7 @@ int ttb_backward(ttb_handle* h, const float* c0, const float* c1, const float* c
 
 int ttb_aggregate(ttb_handle* h, const float* grad_out, ttb_stream stream) {
   if (!h || !grad_out) return TTB_EINVAL;
-  if (!h->planned) return TTB_ESTATE;
+  if (!h->planned || h->fast) return TTB_ESTATE;  // legacy pipeline only
   cudaError_t e = launch_aggregate(h, grad_out, (cudaStream_t)stream);
   if (e != cudaSuccess) return TTB_ECUDA;
   h->backwarded = 1;
@@ -255,8 +287,10 @@ int ttb_backward_sgd(ttb_handle* h, float* c0, float* c1, float* c2, const float
     return TTB_EINVAL;
   if (!h->forwarded) return TTB_ESTATE;
   if (momentum == 0.0) v0 = v1 = v2 = nullptr;
-  cudaError_t e = launch_backward(h, c0, c1, c2, grad_out, nullptr, nullptr, nullptr, c0, c1, c2, v0, v1, v2, lr,
-                                  momentum, update_mask, 1, (cudaStream_t)stream);
+  cudaError_t e = h->fast ? fast_backward(h, c0, c1, c2, grad_out, nullptr, nullptr, nullptr, c0, c1, c2, v0, v1, v2,
+                                          lr, momentum, update_mask, 1, (cudaStream_t)stream)
+                          : launch_backward(h, c0, c1, c2, grad_out, nullptr, nullptr, nullptr, c0, c1, c2, v0, v1, v2,
+                                            lr, momentum, update_mask, 1, (cudaStream_t)stream);
   if (e != cudaSuccess) return TTB_ECUDA;
   h->backwarded = 1;
   h->pmap_clean = 1;
@@ -278,13 +312,24 @@ int ttb_read_status(ttb_handle* h, int64_t status[8], ttb_stream stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (cudaMemcpyAsync(hdr, h->w.err, sizeof(hdr), cudaMemcpyDeviceToHost, s) != cudaSuccess) return TTB_ECUDA;
   if (cudaStreamSynchronize(s) != cudaSuccess) return TTB_ECUDA;
-  status[0] = hdr[0];
   status[1] = h->T;
   status[2] = h->B;
+  status[6] = h->gen;
+  if (h->fast) {
+    int fh[8];
+    if (cudaMemcpyAsync(fh, h->w.fast_hdr, sizeof(fh), cudaMemcpyDeviceToHost, s) != cudaSuccess) return TTB_ECUDA;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return TTB_ECUDA;
+    status[0] = fh[0] | (h->legacy_planned ? hdr[0] : 0);
+    status[3] = fh[3];
+    status[4] = h->legacy_planned ? hdr[2] : -1;  // segments: known once the legacy plan was built
+    status[5] = -1;                               // unique rows: not formed by this pipeline
+    status[7] = fh[2];                            // work items
+    return TTB_OK;
+  }
+  status[0] = hdr[0];
   status[3] = hdr[1];
   status[4] = hdr[2];
   status[5] = h->backwarded ? hdr[3] : 0;
-  status[6] = h->gen;
   status[7] = 0;
   return TTB_OK;
 }
@@ -293,18 +338,24 @@ int ttb_export_plan(ttb_handle* h, int64_t* work, int64_t* slot_occ, int64_t* se
                     int64_t* digits, ttb_stream stream) {
   if (!h) return TTB_EINVAL;
   if (!h->planned) return TTB_ESTATE;
+  if (!h->legacy_planned) {
+    // the reference-ordered plan (first-occurrence slots, segments) on demand
+    cudaError_t e = launch_plan(h, h->plan_idx, h->plan_idx64, h->plan_off, (cudaStream_t)stream);
+    if (e != cudaSuccess) return TTB_ECUDA;
+    h->legacy_planned = 1;
+  }
   return cuda_status(launch_export_plan(h, work, slot_occ, seg_ids, seg_inv, digits, (cudaStream_t)stream));
 }
 
 int ttb_export_unique(ttb_handle* h, int64_t* rows, float* grads, ttb_stream stream) {
   if (!h) return TTB_EINVAL;
-  if (!h->backwarded) return TTB_ESTATE;
+  if (!h->backwarded || h->fast) return TTB_ESTATE;
   return cuda_status(launch_export_unique(h, rows, grads, (cudaStream_t)stream));
 }
 
 int ttb_export_slots(ttb_handle* h, float* slots, ttb_stream stream) {
   if (!h || !slots) return TTB_EINVAL;
-  if (!h->forwarded) return TTB_ESTATE;
+  if (!h->forwarded || h->fast) return TTB_ESTATE;
   int64_t st[8];
   int rc = ttb_read_status(h, st, stream);
   if (rc) return rc;

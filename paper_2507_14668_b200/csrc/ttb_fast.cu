@@ -1,0 +1,994 @@
+// Tensor-core step pipeline ("fast path") for the production geometry
+// n = (4, 4, 4), ranks (1, 32, 32, 1) — BASELINE configs 2 and 3.
+//
+// Same operator semantics as the plan/forward/backward of ttb_plan.cu /
+// ttb_backward.cu (reference lookup.py:236-296, backward.py:131-200), but
+// organised around the i2 digit so every contraction with a G2 slice is a
+// 128-row tcgen05 GEMM (3xTF32, fp32-level accuracy):
+//
+//   plan     keys (i2 m1 + i1, i3, bag) -> stable radix sort by prefix key ->
+//            work items (<= 32 lookups of one prefix) -> tiles (<= 32 items
+//            of one i2 = 128 accumulator rows (item, a))
+//   forward  X[(item, a), (c, b)] = G1[i1] . G2[:, i2]  in TMEM; each lookup
+//            closes X with its G3 slice in registers and pools into its bag
+//   backward X^T recomputed in TMEM (cheaper than storing it); per segment
+//            (lookups of one bag under one prefix) Z += g (x) sum G3 and
+//            dG3 += X^T g (SIMT, lane <-> (c, b)); then on the tensor core
+//            dG2 += Z^T . G1 (Z^T from TMEM) and dG1 += Z . G2^T
+//
+// Reuse of the partial products across duplicate prefixes (the paper's reuse
+// buffer) is the item grouping: X is formed once per item for all its
+// lookups. Gradient accumulation into the cores uses fp32 reductions in L2
+// (red.global.add), so summation order — unlike the legacy path — is not
+// fixed; results agree with the reference within the north-star tolerances.
+#include <stdio.h>
+#include <stdlib.h>
+
+#include "ttb_internal.h"
+#include "ttb_umma.cuh"
+
+namespace ttb {
+namespace fast {
+
+constexpr int kItemLen = 32;    // max lookups per work item
+constexpr int kTileItems = 32;  // items per tile: M = 32 * n1 = 128
+constexpr int R1 = 32, C = 128, NOUT = 64;
+constexpr int kImg = 16384;     // bytes of one 128 x 32 / 32 x 128 fp32 image
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ void red_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+__device__ __forceinline__ void red_f32(float* p, float a) {
+  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(a) : "memory");
+}
+
+// ------------------------------------------------------------ plan: keys
+template <typename IdxT>
+__global__ void __launch_bounds__(kBlock) k_keys(const IdxT* __restrict__ idx, const int64_t* __restrict__ offsets,
+                                                 int T, int B, KGeom g, unsigned* __restrict__ key,
+                                                 unsigned* __restrict__ i3o, int* __restrict__ bag_of,
+                                                 int* __restrict__ hdr) {
+  pdl_enter();
+  const int stride = gridDim.x * blockDim.x;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  int bits = 0, multi = 0;
+  for (int b = tid; b < B; b += stride) {
+    const int64_t ob = offsets[b], on = offsets[b + 1];
+    if (b == 0 && ob != 0) bits |= 4;
+    if (b == B - 1 && on != (int64_t)T) bits |= 4;
+    if (on == ob) bits |= 2;
+    else if (on < ob) bits |= 4;
+    const int lo = (int)(ob < 0 ? 0 : (ob > T ? T : ob)), hi = (int)(on < lo ? lo : (on > T ? T : on));
+    for (int t = lo; t < hi; ++t) bag_of[t] = b;
+    if (hi - lo > 1) multi = 1;
+  }
+  const unsigned m2m3 = g.m2 * g.m3;
+  for (int t = tid; t < T; t += stride) {
+    long long v = (long long)idx[t];
+    if (v < 0 || v >= (long long)g.rows) {
+      bits |= 1;
+      v = 0;
+    }
+    const unsigned i = (unsigned)v, i1 = i / m2m3, r = i - i1 * m2m3, i2 = r / g.m3;
+    key[t] = i2 * g.m1 + i1;  // i2-major prefix key
+    i3o[t] = r - i2 * g.m3;
+  }
+  if (bits) atomicOr(&hdr[0], bits);
+  if (multi) hdr[1] = 1;
+}
+
+// ------------------------------------------------------------ plan: items
+// Over the prefix-sorted positions: item heads (prefix change, or every
+// kItemLen positions), the sorted (bag, i3) pairs, and the prefix count.
+__global__ void __launch_bounds__(kBlock) k_items(const unsigned* __restrict__ sk, const unsigned* __restrict__ sv,
+                                                  const int* __restrict__ bag_of, const unsigned* __restrict__ i3o,
+                                                  int T, int* __restrict__ item_start, unsigned* __restrict__ item_key,
+                                                  int2* __restrict__ sbi, int* __restrict__ hdr,
+                                                  unsigned long long* status, unsigned* ctr) {
+  pdl_enter();
+  __shared__ int s_tile;
+  __shared__ int s_tmp[kItems * (kBlock / 32) + 2];
+  const int tile = claim_tile(ctr, &s_tile);
+  const int base = tile * kTile;
+  bool f[kItems];
+  unsigned key[kItems];
+  int nph = 0;
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    const int q = base + k * kBlock + threadIdx.x;
+    f[k] = false;
+    key[k] = 0;
+    if (q < T) {
+      key[k] = sk[q];
+      const bool ph = q == 0 || sk[q - 1] != key[k];
+      f[k] = ph || (q % kItemLen) == 0;
+      nph += ph;
+      const unsigned l = sv[q];
+      sbi[q] = make_int2(bag_of[l], (int)i3o[l]);
+    }
+  }
+  int rank[kItems];
+  long long incl;
+  tile_flag_scan(f, rank, status, tile, s_tmp, &incl);
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    if (f[k]) {
+      item_start[rank[k]] = base + k * kBlock + threadIdx.x;
+      item_key[rank[k]] = key[k];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nph += __shfl_xor_sync(0xffffffffu, nph, o);
+  if ((threadIdx.x & 31) == 0 && nph) atomicAdd(&hdr[3], nph);
+  if (tile == (T + kTile - 1) / kTile - 1 && threadIdx.x == 0) {
+    hdr[2] = (int)incl;
+    item_start[incl] = T;
+  }
+}
+
+// ------------------------------------------------------------ plan: tiles
+// One CTA: first item of every i2 (binary search over the sorted item keys)
+// and the exclusive scan of ceil(items / 32) per i2.
+__global__ void __launch_bounds__(1024) k_tiles(const unsigned* __restrict__ item_key, KGeom g,
+                                                int* __restrict__ i2_item, int* __restrict__ tile_start,
+                                                int4* __restrict__ tile_info, int* __restrict__ hdr) {
+  pdl_enter();
+  __shared__ int s_w[32];
+  __shared__ int s_carry;
+  const int n = hdr[2];
+  for (unsigned i2 = threadIdx.x; i2 <= g.m2; i2 += blockDim.x) {
+    const unsigned target = i2 * g.m1;
+    int lo = 0, hi = n;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (item_key[mid] < target) lo = mid + 1;
+      else hi = mid;
+    }
+    i2_item[i2] = lo;
+  }
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (unsigned b0 = 0; b0 < g.m2; b0 += blockDim.x) {
+    const unsigned i2 = b0 + threadIdx.x;
+    const int v = i2 < g.m2 ? (i2_item[i2 + 1] - i2_item[i2] + kTileItems - 1) / kTileItems : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int y = lane < (int)(blockDim.x >> 5) ? s_w[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int z = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) y += z;
+      }
+      s_w[lane] = y;  // inclusive warp totals
+    }
+    __syncthreads();
+    const int carry = s_carry;
+    const int excl = carry + (w ? s_w[w - 1] : 0) + x - v;
+    if (i2 < g.m2) {
+      tile_start[i2] = excl;
+      // tile table: (i2, first item, items) of each of this group's tiles
+      const int first = i2_item[i2], cnt = i2_item[i2 + 1] - first;
+      for (int j = 0; j < v; ++j) {
+        const int nn = cnt - j * kTileItems;
+        tile_info[excl + j] = make_int4((int)i2, first + j * kTileItems, nn < kTileItems ? nn : kTileItems, 0);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry = carry + s_w[31];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    tile_start[g.m2] = s_carry;
+    hdr[4] = s_carry;
+  }
+}
+
+// ------------------------------------------------------------ core images
+// Split (hi / lo) tf32 forms of the cores, built once per step (the cores
+// change every step) and copied verbatim into shared memory by the step
+// kernels (cp.async, no register staging):
+//   per i2 (4 x 16 KB, the exact K-major SWIZZLE_128B smem images)
+//     [0] cb_hi  [1] cb_lo : rows (c, b) = 4 c + b (128), K = k (32)
+//     [2..3] k      : rows k (hi 0..31, lo 32..63), K = (c, b) (128)
+//   per i1 (512 floats): rows_hi[a][k], rows_lo[a][k], t_hi[k][a], t_lo[k][a]
+constexpr int kG1Img = 512;
+
+__global__ void __launch_bounds__(kThreads) k_coreimg(const float* __restrict__ G1, const float* __restrict__ G2,
+                                                      KGeom g, float* __restrict__ img, float* __restrict__ g1img) {
+  pdl_enter();
+  if (blockIdx.x >= g.m2) {  // G1 images: 2 i1 per block (128 elements each)
+    const unsigned i1 = (blockIdx.x - g.m2) * 2 + (threadIdx.x >> 7);
+    const int e = threadIdx.x & 127, a = e >> 5, k = e & 31;
+    if (i1 < g.m1) {
+      float hi, lo;
+      umma::split3(__ldg(G1 + (size_t)i1 * 128 + e), hi, lo);
+      float* d = g1img + (size_t)i1 * kG1Img;
+      d[e] = hi;
+      d[128 + e] = lo;
+      d[256 + k * 4 + a] = hi;
+      d[384 + k * 4 + a] = lo;
+    }
+    return;
+  }
+  extern __shared__ __align__(16) char smem_raw[];
+  char* sm = (char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const unsigned i2 = blockIdx.x;
+  for (int e = threadIdx.x; e < R1 * C; e += kThreads) {
+    const int k = e >> 7, b = (e >> 5) & 3, c = e & 31;
+    const float v = __ldg(G2 + ((size_t)k * g.m2 + i2) * C + b * 32 + c);
+    float hi, lo;
+    umma::split3(v, hi, lo);
+    const int cb = 4 * c + b;
+    const uint32_t o1 = umma::sw128_off(cb, k, 128);
+    *(float*)(sm + o1) = hi;
+    *(float*)(sm + kImg + o1) = lo;
+    *(float*)(sm + 2 * kImg + umma::sw128_off(k, cb, 64)) = hi;
+    *(float*)(sm + 2 * kImg + umma::sw128_off(32 + k, cb, 64)) = lo;
+  }
+  __syncthreads();
+  uint4* dst = reinterpret_cast<uint4*>(img + (size_t)i2 * (4 * kImg / 4));
+  const uint4* src = reinterpret_cast<const uint4*>(sm);
+  for (int e = threadIdx.x; e < 4 * kImg / 16; e += kThreads) dst[e] = src[e];
+}
+
+// ------------------------------------------------------------ async copies
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(umma::smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(umma::smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(umma::smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+
+__device__ inline void copy_img_async(char* dst, const float* __restrict__ src, int bytes) {
+  for (int e = threadIdx.x; e < bytes / 16; e += kThreads) cp_async16(dst + 16 * e, src + 4 * e);
+}
+
+__device__ __forceinline__ void sync_for_mma() {
+  umma::fence_smem_to_async();
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+}
+
+// 3xTF32 product of two smem images over K (k-steps of 8)
+__device__ inline void mma3_ss(uint32_t d, uint32_t a_hi, uint32_t a_lo, int a_rows, uint32_t b_hi, uint32_t b_lo,
+                               int b_rows, int K, uint32_t idesc) {
+  for (int k0 = 0; k0 < K; k0 += 8) {
+    const uint64_t ah = umma::sw128_desc_at(a_hi, k0, a_rows), al = umma::sw128_desc_at(a_lo, k0, a_rows);
+    const uint64_t bh = umma::sw128_desc_at(b_hi, k0, b_rows), bl = umma::sw128_desc_at(b_lo, k0, b_rows);
+    umma::mma_tf32(d, ah, bh, idesc, k0 > 0 ? 1u : 0u);
+    umma::mma_tf32(d, ah, bl, idesc, 1u);
+    umma::mma_tf32(d, al, bh, idesc, 1u);
+  }
+}
+
+// ------------------------------------------------------------ tile bookkeeping
+// Tile metadata lives in a two-slot ring: while tile t is processed, the
+// last warp fetches tile t + grid's (cp.async) and the tile table entry of
+// t + 2 grid (a register load, consumed an iteration later).
+struct TileMeta {
+  int i2, n, item0, pad;
+  unsigned key[kTileItems];
+  int start[kTileItems + 1];
+};
+
+struct MetaPrefetch {
+  int4 next;  // tile table entry of the tile after the one being fetched
+};
+
+// lanes 0..31 of the calling warp: slot <- tile `info`
+__device__ inline void fetch_meta_async(const int4& info, const int* __restrict__ item_start,
+                                        const unsigned* __restrict__ item_key, TileMeta* m) {
+  const int l = threadIdx.x & 31, n = info.z, item0 = info.y;
+  if (l == 0) {
+    m->i2 = info.x;
+    m->n = n;
+    m->item0 = item0;
+    cp_async4(&m->start[n], item_start + item0 + n);
+  }
+  if (l < n) {
+    cp_async4(&m->key[l], item_key + item0 + l);
+    cp_async4(&m->start[l], item_start + item0 + l);
+  }
+}
+
+__device__ __forceinline__ int item_i1(const TileMeta* m, int it, KGeom g) {
+  return (int)(m->key[it] - (unsigned)m->i2 * g.m1);
+}
+
+// G1 rows image of the tile's items (rows (item, a), K = k) from the split G1 images
+__device__ inline void stage_g1_rows_async(const TileMeta* m, KGeom g, const float* __restrict__ g1img, char* hi,
+                                           char* lo) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int e = threadIdx.x + i * kThreads, ia = e >> 3, kq = e & 7, it = ia >> 2, a = ia & 3;
+    if (it < m->n) {
+      const float* src = g1img + (size_t)item_i1(m, it, g) * kG1Img + a * 32 + 4 * kq;
+      const uint32_t o = umma::sw128_off(ia, 4 * kq, 128);
+      cp_async16(hi + o, src);
+      cp_async16(lo + o, src + 128);
+    }
+  }
+}
+
+// G1^T image of the tile's items (rows k, K = (item, a)); zero columns past n
+// (one 64-row image: rows k = hi, rows 32 + k = lo)
+__device__ inline void stage_g1_t_async(const TileMeta* m, KGeom g, const float* __restrict__ g1img, char* img) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int e = threadIdx.x + i * kThreads, it = e >> 5, k = e & 31;
+    const uint32_t oh = umma::sw128_off(k, 4 * it, 64), ol = umma::sw128_off(32 + k, 4 * it, 64);
+    if (it < m->n) {
+      const float* src = g1img + (size_t)item_i1(m, it, g) * kG1Img + 256 + 4 * k;
+      cp_async16(img + oh, src);
+      cp_async16(img + ol, src + 128);
+    } else {
+      *reinterpret_cast<float4*>(img + oh) = make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(img + ol) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+}
+
+// ------------------------------------------------------------ forward
+// Persistent: one 256-thread CTA per SM loops over tiles. G3 stays resident
+// in shared memory; each tile's operands and (bag, i3) list arrive by one
+// round of cp.async. Epilogue thread <-> accumulator row (item, a): the whole
+// X row (128 values) sits in registers; the two warps of a lane quarter take
+// alternate segments.
+constexpr int kMaxTilePos = kTileItems * kItemLen;  // 1024
+constexpr int kFwdG3Max = 128 * 1024;               // G3 bytes kept in smem
+
+__host__ __device__ constexpr int fwd_smem_bytes() { return 4 * kImg + kFwdG3Max + kMaxTilePos * 8 + 1024; }
+
+__global__ void __launch_bounds__(kThreads, 1) k_fwd(KGeom g, const float* __restrict__ g1img,
+                                                     const float* __restrict__ G3, const float* __restrict__ img,
+                                                     const int* __restrict__ hdr, const int4* __restrict__ tile_info,
+                                                     const int* __restrict__ item_start,
+                                                     const unsigned* __restrict__ item_key,
+                                                     const int2* __restrict__ sbi, float* __restrict__ out,
+                                                     int direct) {
+  pdl_enter();
+  extern __shared__ __align__(16) char smem_raw[];
+  char* sm = (char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  char* a_hi = sm;             // G1 rows image
+  char* a_lo = sm + kImg;
+  char* b_hi = sm + 2 * kImg;  // G2 cb image
+  char* b_lo = sm + 3 * kImg;
+  float4* s_g3 = reinterpret_cast<float4*>(sm + 4 * kImg);
+  int2* s_sbi = reinterpret_cast<int2*>(sm + 4 * kImg + kFwdG3Max);
+  __shared__ TileMeta s_m[2];
+  __shared__ uint64_t s_mbar;
+  __shared__ uint32_t s_tmem;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned m3 = g.m3;
+  const bool g3s = (size_t)32 * m3 * 16 <= (size_t)kFwdG3Max;
+  const int ntiles = hdr[4];
+  if (warp == 0) umma::tmem_alloc(&s_tmem, 128);
+  if (threadIdx.x == 32) umma::mbar_init(&s_mbar, 1);
+  if (g3s) {
+    const int n4 = 32 * (int)m3;
+    for (int e = threadIdx.x; e < n4; e += kThreads) cp_async16(s_g3 + e, reinterpret_cast<const float4*>(G3) + e);
+  }
+  int4 pf = make_int4(0, 0, 0, 0);
+  if (warp == 7 && (int)blockIdx.x < ntiles) {
+    fetch_meta_async(tile_info[blockIdx.x], item_start, item_key, &s_m[0]);
+    if ((int)(blockIdx.x + gridDim.x) < ntiles) pf = tile_info[blockIdx.x + gridDim.x];
+  }
+  cp_async_wait_all();
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tmem = s_tmem;
+  const float4* g3base = g3s ? s_g3 : reinterpret_cast<const float4*>(G3);
+  uint32_t phase = 0;
+  int slot = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, slot ^= 1) {
+    const TileMeta* m = &s_m[slot];
+    const int p0 = m->start[0], np = m->start[m->n] - p0;
+    for (int e = threadIdx.x; e < np; e += kThreads) cp_async8(s_sbi + e, sbi + p0 + e);
+    copy_img_async(b_hi, img + (size_t)m->i2 * (kImg), 2 * kImg);  // cb_hi, cb_lo
+    stage_g1_rows_async(m, g, g1img, a_hi, a_lo);
+    cp_async_wait_all();
+    sync_for_mma();
+    if (threadIdx.x == 0) {
+      constexpr uint32_t id = umma::idesc_tf32(128, 128, false, false);
+      mma3_ss(tmem, umma::smem_u32(a_hi), umma::smem_u32(a_lo), 128, umma::smem_u32(b_hi), umma::smem_u32(b_lo),
+              128, R1, id);
+      umma::commit(&s_mbar);
+    }
+    if (warp == 7) {  // next tile's metadata into the other slot
+      const int tn = t + (int)gridDim.x;
+      if (tn < ntiles) {
+        fetch_meta_async(pf, item_start, item_key, &s_m[slot ^ 1]);
+        cp_async_commit();
+        if (tn + (int)gridDim.x < ntiles) pf = tile_info[tn + gridDim.x];
+      }
+    }
+    umma::mbar_wait(&s_mbar, phase);
+    phase ^= 1u;
+    umma::fence_after_sync();
+    // ---- epilogue
+    const int q4 = warp & 3, half = warp >> 2;
+    const int row = 32 * q4 + lane, it = row >> 2, a = row & 3;
+    float x[128];  // x[4 c + b] = X[item][a][b][c]
+#pragma unroll
+    for (int j = 0; j < 4; ++j) umma::tmem_ld32(tmem + ((uint32_t)(32 * q4) << 16) + 32 * j, *(float(*)[32])(x + 32 * j));
+    if (it < m->n) {
+      const int s1 = m->start[it + 1] - p0;
+      int qq = m->start[it] - p0, ord = 0;
+      while (qq < s1) {
+        const int bag = s_sbi[qq].x;
+        int e = qq + 1;
+        while (e < s1 && s_sbi[e].x == bag) ++e;
+        if ((ord & 1) == half) {
+          float acc[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+          for (int l = qq; l < e; ++l) {
+            const float4* g3 = g3base + (unsigned)s_sbi[l].y;
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+              const float4 gv = g3[(size_t)c * m3];
+#pragma unroll
+              for (int b = 0; b < 4; ++b) {
+                const float xv = x[4 * c + b];
+                acc[4 * b + 0] = fmaf(xv, gv.x, acc[4 * b + 0]);
+                acc[4 * b + 1] = fmaf(xv, gv.y, acc[4 * b + 1]);
+                acc[4 * b + 2] = fmaf(xv, gv.z, acc[4 * b + 2]);
+                acc[4 * b + 3] = fmaf(xv, gv.w, acc[4 * b + 3]);
+              }
+            }
+          }
+          float* o = out + (size_t)bag * NOUT + a * 16;
+          if (direct) {
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+              reinterpret_cast<float4*>(o)[b] = make_float4(acc[4 * b], acc[4 * b + 1], acc[4 * b + 2], acc[4 * b + 3]);
+          } else {
+#pragma unroll
+            for (int b = 0; b < 4; ++b) red_v4(o + 4 * b, acc[4 * b], acc[4 * b + 1], acc[4 * b + 2], acc[4 * b + 3]);
+          }
+        }
+        ++ord;
+        qq = e;
+      }
+    }
+    cp_async_wait_all();  // next tile's metadata
+    umma::fence_before_sync();
+    __syncthreads();  // TMEM and smem free for the next tile
+    umma::fence_after_sync();
+  }
+  if (warp == 0) umma::tmem_free(tmem, 128);
+}
+
+// ------------------------------------------------------------ backward
+// Persistent, one CTA per SM, all 512 TMEM columns:
+//   TMEM   [0,128) X^T (lanes (c, b), cols (item, a))   [128,256) Z^T hi
+//          [256,384) Z^T lo   [384,448) dG2 tile (x G1 hi | x G1 lo)
+//          [448,512) E tile (x G2 hi | x G2 lo)
+//   smem   R12 64 KB: X operands (G2 cb image, G1 rows image), then the
+//                     64-row G2 k image and the 64-row G1^T image
+//          XZ  64 KB: per item a 512-float slot holding X (dumped from TMEM),
+//                     overwritten by Z; finally the Z image (rows (item, a),
+//                     K = (c, b)) the E GEMM reads: hi, then lo
+//          ST  97 KB: per chunk of <= kChunkPos positions: (bag, i3), the
+//                     bag's gradient row, the lookup's G3 slice (c, j)
+// Z / dG3 phase: one warp per item, lane <-> c: every lane holds the item's
+// X[., ., c] and accumulates Z[., ., c] in registers, so a position costs
+// 128 FMAs per lane and no cross-lane reduction. The next tile's first chunk
+// and X operands are fetched while this tile's GEMMs and epilogue run.
+// per-phase timestamps of block 0's first two tiles into hdr[16..] (TTB_DBG & 8)
+#define TSTAMP(k)                                                                                      \
+  do {                                                                                                 \
+    if ((dbg & 8) && threadIdx.x == 0 && blockIdx.x == 0 && t < 2 * (int)gridDim.x) {                  \
+      unsigned long long _t;                                                                           \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                                           \
+      reinterpret_cast<unsigned long long*>(hdr + 16)[(t / gridDim.x) * 9 + (k)] = _t;                 \
+    }                                                                                                  \
+  } while (0)
+
+constexpr int kChunkPos = 128;
+constexpr int kStSbi = kChunkPos * 8, kStG = kChunkPos * 256, kStG3 = kChunkPos * 512;
+constexpr int kBwdSmem = 4 * kImg + 4 * kImg + kStSbi + kStG + kStG3 + 1024;
+
+// X / Z slot element (item, a, b, c); the XOR keeps both the (c, b)-lane
+// dump and the c-lane reads free of bank conflicts
+__device__ __forceinline__ int xs_idx(int it, int a, int b, int c) { return it * 512 + (4 * a + b) * 32 + (c ^ (b << 3)); }
+
+// chunks of whole items with <= kChunkPos positions each (thread 0)
+__device__ inline void make_chunks(const TileMeta* m, int* ch) {
+  int nc = 0, it = 0;
+  const int n = m->n;
+  ch[0] = 0;
+  while (it < n) {
+    const int base = m->start[it];
+    while (it < n && m->start[it + 1] - base <= kChunkPos) ++it;
+    ch[++nc] = it;
+  }
+  ch[kTileItems + 1] = nc;
+}
+
+__device__ inline void stage_rows_async(int np, const int2* st_sbi, const float* __restrict__ gout,
+                                        const float* __restrict__ G3, unsigned m3, float4* st_g, float4* st_g3) {
+  for (int e = threadIdx.x; e < np * 16; e += kThreads) {
+    const int p = e >> 4, k = e & 15;
+    cp_async16(st_g + e, gout + (size_t)st_sbi[p].x * NOUT + 4 * k);
+  }
+  for (int e = threadIdx.x; e < np * 32; e += kThreads) {
+    const int p = e >> 5, cc = e & 31;
+    cp_async16(st_g3 + e, reinterpret_cast<const float4*>(G3) + (size_t)cc * m3 + st_sbi[p].y);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __restrict__ g1img,
+                                                     const float* __restrict__ G3, const float* __restrict__ img,
+                                                     const int4* __restrict__ tile_info,
+                                                     const int* __restrict__ item_start,
+                                                     const unsigned* __restrict__ item_key,
+                                                     const int2* __restrict__ sbi, const float* __restrict__ gout,
+                                                     float* __restrict__ dG1, float* __restrict__ dG2,
+                                                     float* __restrict__ dG3, int* __restrict__ hdr, int dbg) {
+  pdl_enter();
+  extern __shared__ __align__(16) char smem_raw[];
+  char* sm = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);
+  char* r1_hi = sm;  // X: G2 cb hi / lo; later the 64-row G2 k image
+  char* r1_lo = sm + kImg;
+  char* r2_hi = sm + 2 * kImg;  // X: G1 rows hi / lo; later the 64-row G1^T image
+  char* r2_lo = sm + 3 * kImg;
+  char* zi = sm + 4 * kImg;  // X / Z slots, then the Z image
+  float* xs = reinterpret_cast<float*>(zi);
+  int2* st_sbi = reinterpret_cast<int2*>(sm + 8 * kImg);
+  float4* st_g = reinterpret_cast<float4*>(sm + 8 * kImg + kStSbi);
+  float4* st_g3 = reinterpret_cast<float4*>(sm + 8 * kImg + kStSbi + kStG);
+  __shared__ TileMeta s_m[2];
+  __shared__ int s_chunk[2][kTileItems + 2];
+  __shared__ uint64_t s_mbar;
+  __shared__ uint32_t s_tmem;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = hdr[4];
+  const unsigned m3 = g.m3;
+  if (warp == 0) umma::tmem_alloc(&s_tmem, 512);
+  if (threadIdx.x == 32) umma::mbar_init(&s_mbar, 1);
+  int4 pf = make_int4(0, 0, 0, 0);
+  if (warp == 7 && (int)blockIdx.x < ntiles) {
+    fetch_meta_async(tile_info[blockIdx.x], item_start, item_key, &s_m[0]);
+    if ((int)(blockIdx.x + gridDim.x) < ntiles) pf = tile_info[blockIdx.x + gridDim.x];
+  }
+  cp_async_wait_all();
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tmem = s_tmem;
+  const int q4 = warp & 3, half = warp >> 2;
+  const int row = 32 * q4 + lane;  // TMEM lane of this thread: (c, b) = (row / 4, row % 4)
+  const int c = row >> 2, b = row & 3;
+  const uint32_t tl = tmem + ((uint32_t)(32 * q4) << 16);
+  // smem descriptors (start addresses are fixed for the kernel)
+  const uint64_t d_r1h = umma::desc_sw128(umma::smem_u32(r1_hi)), d_r1l = umma::desc_sw128(umma::smem_u32(r1_lo));
+  const uint64_t d_r2h = umma::desc_sw128(umma::smem_u32(r2_hi)), d_r2l = umma::desc_sw128(umma::smem_u32(r2_lo));
+  const uint64_t d_zi = umma::desc_sw128(umma::smem_u32(zi));
+  // prologue: the first tile's first chunk and X operands
+  if ((int)blockIdx.x < ntiles) {
+    const TileMeta* m = &s_m[0];
+    if (threadIdx.x == 0) make_chunks(m, s_chunk[0]);
+    __syncthreads();
+    const int np = m->start[s_chunk[0][1]] - m->start[0];
+    if (threadIdx.x < np) cp_async8(st_sbi + threadIdx.x, sbi + m->start[0] + threadIdx.x);
+    copy_img_async(r1_hi, img + (size_t)m->i2 * kImg, 2 * kImg);
+    stage_g1_rows_async(m, g, g1img, r2_hi, r2_lo);
+    cp_async_wait_all();
+    __syncthreads();
+    stage_rows_async(np, st_sbi, gout, G3, m3, st_g, st_g3);
+  }
+  uint32_t phase = 0;
+  int bad = 0, slot = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, slot ^= 1) {
+    const TileMeta* m = &s_m[slot];
+    const int* chunk = s_chunk[slot];
+    const int n = m->n, nchunk = chunk[kTileItems + 1];
+    const float* gimg = img + (size_t)m->i2 * kImg;  // kImg floats = 4 images of kImg bytes
+    TSTAMP(0);
+    // invariant: chunk 0's positions / rows and the X operands are issued
+    cp_async_wait_all();
+    sync_for_mma();
+    if (threadIdx.x == 0) {
+      constexpr uint32_t id = umma::idesc_tf32(128, 128, false, false);
+#pragma unroll
+      for (int k0 = 0; k0 < R1; k0 += 8) {
+        const uint32_t o = (uint32_t)((k0 & 31) * 4) >> 4;
+        umma::mma_tf32(tmem, d_r1h + o, d_r2h + o, id, k0 > 0 ? 1u : 0u);
+        umma::mma_tf32(tmem, d_r1h + o, d_r2l + o, id, 1u);
+        umma::mma_tf32(tmem, d_r1l + o, d_r2h + o, id, 1u);
+      }
+      umma::commit(&s_mbar);
+    }
+    if (warp == 7) {  // next tile's metadata into the other slot
+      const int tn = t + (int)gridDim.x;
+      if (tn < ntiles) {
+        fetch_meta_async(pf, item_start, item_key, &s_m[slot ^ 1]);
+        if (tn + (int)gridDim.x < ntiles) pf = tile_info[tn + gridDim.x];
+      }
+      cp_async_wait_all();
+    }
+    TSTAMP(1);
+    umma::mbar_wait(&s_mbar, phase);
+    phase ^= 1u;
+    umma::fence_after_sync();
+    TSTAMP(2);
+    // X^T -> item slots (this half's 64 columns)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      float v[32];
+      umma::tmem_ld32(tl + 64 * half + 32 * j, v);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int col = 64 * half + 32 * j + i;
+        xs[xs_idx(col >> 2, col & 3, b, c)] = v[i];
+      }
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    // the second GEMM pair's operands stream in during the Z phase
+    copy_img_async(r1_hi, gimg + 2 * kImg / 4, 2 * kImg);
+    stage_g1_t_async(m, g, g1img, r2_hi);
+    cp_async_commit();
+    TSTAMP(3);
+    for (int ch = 0; ch < nchunk; ++ch) {
+      const int it0 = chunk[ch], it1 = chunk[ch + 1];
+      const int p0 = m->start[it0];
+      if (ch > 0) {
+        const int np = m->start[it1] - p0;
+        if (threadIdx.x < np) cp_async8(st_sbi + threadIdx.x, sbi + p0 + threadIdx.x);
+        cp_async_wait_all();
+        __syncthreads();
+        stage_rows_async(np, st_sbi, gout, G3, m3, st_g, st_g3);
+        cp_async_wait_all();
+        __syncthreads();
+      }
+      // ---- Z / dG3 phase: warp <-> item, lane <-> c
+      for (int it = it0 + warp; it < it1; it += kThreads / 32) {
+        float x[16], z[16];
+#pragma unroll
+        for (int ab = 0; ab < 16; ++ab) {
+          x[ab] = xs[xs_idx(it, ab >> 2, ab & 3, lane)];
+          z[ab] = 0.f;
+        }
+        const int s1 = m->start[it + 1] - p0;
+        int qq = m->start[it] - p0;
+        while (qq < s1) {
+          const int bag = st_sbi[qq].x;
+          float gv[64];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const float4 v = st_g[qq * 16 + k];
+            gv[4 * k] = v.x;
+            gv[4 * k + 1] = v.y;
+            gv[4 * k + 2] = v.z;
+            gv[4 * k + 3] = v.w;
+          }
+          float dh[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int ab = 0; ab < 16; ++ab)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dh[j] = fmaf(x[ab], gv[4 * ab + j], dh[j]);
+          float gs[4] = {0.f, 0.f, 0.f, 0.f};
+          int e = qq;
+          for (; e < s1; ++e) {
+            const int2 pr = st_sbi[e];
+            if (pr.x != bag) break;
+            const float4 h3 = st_g3[e * 32 + lane];
+            gs[0] += h3.x;
+            gs[1] += h3.y;
+            gs[2] += h3.z;
+            gs[3] += h3.w;
+            if (!(dbg & 1)) red_v4(dG3 + ((size_t)lane * m3 + pr.y) * 4, dh[0], dh[1], dh[2], dh[3]);
+          }
+#pragma unroll
+          for (int ab = 0; ab < 16; ++ab)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) z[ab] = fmaf(gv[4 * ab + j], gs[j], z[ab]);
+          qq = e;
+        }
+        float zs = 0.f;
+#pragma unroll
+        for (int ab = 0; ab < 16; ++ab) {
+          xs[xs_idx(it, ab >> 2, ab & 3, lane)] = z[ab];
+          zs += fabsf(z[ab]);
+        }
+        bad |= !isfinite(zs);
+      }
+      if (ch == nchunk - 1) {  // slots past the tile's items hold zeros
+        for (int it = n + warp; it < kTileItems; it += kThreads / 32)
+#pragma unroll
+          for (int ab = 0; ab < 16; ++ab) xs[xs_idx(it, ab >> 2, ab & 3, lane)] = 0.f;
+      }
+      __syncthreads();  // staging reused by the next chunk / tile
+    }
+    TSTAMP(4);
+    // ---- next tile: chunk list and first chunk's positions
+    const int tn = t + (int)gridDim.x;
+    const TileMeta* mn = &s_m[slot ^ 1];
+    int npn = 0;
+    if (tn < ntiles) {
+      if (threadIdx.x == 0) make_chunks(mn, s_chunk[slot ^ 1]);
+      __syncthreads();
+      npn = mn->start[s_chunk[slot ^ 1][1]] - mn->start[0];
+      if (threadIdx.x < npn) cp_async8(st_sbi + threadIdx.x, sbi + mn->start[0] + threadIdx.x);
+      cp_async_commit();
+    }
+    // ---- Z^T into TMEM (hi / lo) and the Z image (hi) for the E GEMM
+    float zr[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      const int ia = 64 * half + i;
+      zr[i] = xs[xs_idx(ia >> 2, ia & 3, b, c)];
+    }
+#pragma unroll
+    for (int i = 0; i < 64; i += 4) {
+      float h[4], l[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) umma::split3(zr[i + u], h[u], l[u]);
+      umma::tmem_st4(tl + 128 + 64 * half + i, h[0], h[1], h[2], h[3]);
+      umma::tmem_st4(tl + 256 + 64 * half + i, l[0], l[1], l[2], l[3]);
+    }
+    __syncthreads();  // every slot read before the image overwrites them
+#pragma unroll
+    for (int i = 0; i < 64; ++i)
+      *(float*)(zi + umma::sw128_off(64 * half + i, row, 128)) = umma::tf32_rna(zr[i]);
+    umma::tmem_wait_st();
+    cp_async_wait_all();  // G2 k / G1^T images, next tile's positions
+    sync_for_mma();
+    TSTAMP(5);
+    constexpr uint32_t id64 = umma::idesc_tf32(128, 64, false, false);
+    if (threadIdx.x == 0) {
+      // dG2 tile [(c, b), (hi | lo) k] = sum_(item, a) (Z^T hi + Z^T lo) . G1^T (A from TMEM)
+#pragma unroll
+      for (int k0 = 0; k0 < 128; k0 += 8) {
+        const uint32_t o = (uint32_t)((k0 >> 5) * 64 * 128 + (k0 & 31) * 4) >> 4;
+        umma::mma_tf32_ta(tmem + 384, tmem + 128 + k0, d_r2h + o, id64, k0 > 0 ? 1u : 0u);
+        umma::mma_tf32_ta(tmem + 384, tmem + 256 + k0, d_r2h + o, id64, 1u);
+      }
+      // E tile [(item, a), (hi | lo) k] = sum_(c, b) Z . G2^T, pass 1: Z hi
+#pragma unroll
+      for (int k0 = 0; k0 < 128; k0 += 8) {
+        const uint32_t oa = (uint32_t)((k0 >> 5) * 128 * 128 + (k0 & 31) * 4) >> 4;
+        const uint32_t ob = (uint32_t)((k0 >> 5) * 64 * 128 + (k0 & 31) * 4) >> 4;
+        umma::mma_tf32(tmem + 448, d_zi + oa, d_r1h + ob, id64, k0 > 0 ? 1u : 0u);
+      }
+      umma::commit(&s_mbar);
+    }
+    // the next tile's first-chunk rows stream in meanwhile
+    if (tn < ntiles) stage_rows_async(npn, st_sbi, gout, G3, m3, st_g, st_g3);
+    umma::mbar_wait(&s_mbar, phase);
+    phase ^= 1u;
+    umma::fence_after_sync();
+    TSTAMP(6);
+    // pass 2: Z lo
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      float h, l;
+      umma::split3(zr[i], h, l);
+      *(float*)(zi + umma::sw128_off(64 * half + i, row, 128)) = l;
+    }
+    sync_for_mma();
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k0 = 0; k0 < 128; k0 += 8) {
+        const uint32_t oa = (uint32_t)((k0 >> 5) * 128 * 128 + (k0 & 31) * 4) >> 4;
+        const uint32_t ob = (uint32_t)((k0 >> 5) * 64 * 128 + (k0 & 31) * 4) >> 4;
+        umma::mma_tf32(tmem + 448, d_zi + oa, d_r1h + ob, id64, 1u);
+      }
+      umma::commit(&s_mbar);
+    }
+    umma::mbar_wait(&s_mbar, phase);
+    phase ^= 1u;
+    umma::fence_after_sync();
+    TSTAMP(7);
+    // the next tile's X operands (R12 is free now)
+    if (tn < ntiles) {
+      copy_img_async(r1_hi, img + (size_t)mn->i2 * kImg, 2 * kImg);
+      stage_g1_rows_async(mn, g, g1img, r2_hi, r2_lo);
+    }
+    if (!(dbg & 4)) {
+      float v[16], w2[16];
+      // dG2[k][i2][b][c] = D[:, k] + D[:, 32 + k]
+      umma::tmem_ld16(tl + 384 + 16 * half, v);
+      umma::tmem_ld16(tl + 384 + 32 + 16 * half, w2);
+      float* d2 = dG2 + ((size_t)m->i2 * 4 + b) * 32 + c;
+      const size_t ks = (size_t)g.m2 * C;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) red_f32(d2 + (size_t)(16 * half + i) * ks, v[i] + w2[i]);
+      // dG1[i1][a][k]
+      umma::tmem_ld16(tl + 448 + 16 * half, v);
+      umma::tmem_ld16(tl + 448 + 32 + 16 * half, w2);
+      const int it = row >> 2, a = row & 3;
+      if (it < n) {
+        float* d1 = dG1 + ((size_t)item_i1(m, it, g) * 4 + a) * R1 + 16 * half;
+#pragma unroll
+        for (int i = 0; i < 16; i += 4) red_v4(d1 + i, v[i] + w2[i], v[i + 1] + w2[i + 1], v[i + 2] + w2[i + 2], v[i + 3] + w2[i + 3]);
+      }
+    }
+    TSTAMP(8);
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+  }
+  if (bad) atomicOr(&hdr[0], 8);
+  if (warp == 0) umma::tmem_free(tmem, 512);
+}
+
+// ------------------------------------------------------------ SGD over the cores
+__global__ void __launch_bounds__(kBlock) k_sgd3(float* __restrict__ p0, float* __restrict__ p1,
+                                                 float* __restrict__ p2, const float* __restrict__ gr,
+                                                 double* __restrict__ v0, double* __restrict__ v1,
+                                                 double* __restrict__ v2, int64_t n0, int64_t n1, int64_t n2,
+                                                 double lr, double mu, int mask) {
+  pdl_enter();
+  const int64_t n = n0 + n1 + n2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float* p;
+    double* v;
+    int64_t j;
+    int k;
+    if (i < n0) {
+      p = p0, v = v0, j = i, k = 0;
+    } else if (i < n0 + n1) {
+      p = p1, v = v1, j = i - n0, k = 1;
+    } else {
+      p = p2, v = v2, j = i - n0 - n1, k = 2;
+    }
+    if (!((mask >> k) & 1)) continue;
+    p[j] = sgd_apply(p[j], gr[i], v ? v + j : nullptr, lr, mu);
+  }
+}
+
+}  // namespace fast
+
+using namespace fast;
+
+bool fast_supported(const ttb_handle* h) {
+  const DynDims& d = h->dims;
+  return d.n1 == 4 && d.n2 == 4 && d.n3 == 4 && d.r1 == 32 && d.r2 == 32;
+}
+
+static cudaError_t ensure_attr(const void* k, int bytes) {
+  return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+cudaError_t fast_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* offsets, cudaStream_t s) {
+  Workspace& w = h->w;
+  const int T = (int)h->T, B = (int)h->B;
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(w.fast_hdr, 0, (size_t)(w.zeroB + w.zeroB_bytes - (char*)w.fast_hdr), s))) return e;
+  h->bwd_zeroed = 1;
+  const int work = T > B ? T : B;
+  int grid = (work + kBlock - 1) / kBlock;
+  if (grid > 148 * 16) grid = 148 * 16;
+  {
+    ProfScope _ps(h, s, "f_keys");
+    if (idx64)
+      e = launch_pdl(k_keys<long long>, dim3(grid), dim3(kBlock), 0, s, (const long long*)idx, offsets, T, B, h->kg,
+                     w.f_key, w.f_i3, w.bag_of, w.fast_hdr);
+    else
+      e = launch_pdl(k_keys<int>, dim3(grid), dim3(kBlock), 0, s, (const int*)idx, offsets, T, B, h->kg, w.f_key,
+                     w.f_i3, w.bag_of, w.fast_hdr);
+    if (e) return e;
+  }
+  count_launch();
+  unsigned *sk, *sv;
+  int bits = 1;
+  while (bits < 32 && ((uint64_t)(h->kg.m1m2 - 1) >> bits) != 0) ++bits;
+  if ((e = launch_sort(h, w.f_key, nullptr, w.skA, w.svA, w.skB, w.svB, nullptr, T, bits, 0, &sk, &sv, s))) return e;
+  const int tiles = (T + kTile - 1) / kTile;
+  {
+    ProfScope _ps(h, s, "f_items");
+    if ((e = launch_pdl(k_items, dim3(tiles), dim3(kBlock), 0, s, (const unsigned*)sk, (const unsigned*)sv,
+                        (const int*)w.bag_of, (const unsigned*)w.f_i3, T, w.f_item_start, w.f_item_key, w.f_sbi,
+                        w.fast_hdr, w.scan_status + kScanFast * h->scan_tiles, w.scan_ctr + kScanFast)))
+      return e;
+  }
+  count_launch();
+  {
+    ProfScope _ps(h, s, "f_tiles");
+    if ((e = launch_pdl(k_tiles, dim3(1), dim3(1024), 0, s, (const unsigned*)w.f_item_key, h->kg, w.f_i2_item,
+                        w.f_tile_start, w.f_tile_info, w.fast_hdr)))
+      return e;
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t fast_forward(ttb_handle* h, const float* c0, const float* c1, const float* c2, float* out,
+                         cudaStream_t s) {
+  Workspace& w = h->w;
+  cudaError_t e;
+  const int img_smem = 4 * kImg + 1024;
+  static bool attr = false;
+  if (!attr) {
+    if ((e = ensure_attr((const void*)k_coreimg, img_smem))) return e;
+    if ((e = ensure_attr((const void*)k_fwd, fwd_smem_bytes()))) return e;
+    if ((e = ensure_attr((const void*)k_bwd, kBwdSmem))) return e;
+    attr = true;
+  }
+  {
+    ProfScope _ps(h, s, "f_coreimg");
+    if ((e = launch_pdl(k_coreimg, dim3(h->kg.m2 + (h->kg.m1 + 1) / 2), dim3(kThreads), img_smem, s, c0, c1, h->kg,
+                        w.f_img, w.f_g1img)))
+      return e;
+  }
+  count_launch();
+  const int direct = h->T == h->B;
+  if (!direct && (e = cudaMemsetAsync(out, 0, sizeof(float) * (size_t)h->B * NOUT, s))) return e;
+  const int maxt = (int)((h->T + kTileItems - 1) / kTileItems + h->kg.m2);
+  const int grid = maxt < h->num_sms ? maxt : h->num_sms;
+  {
+    ProfScope _ps(h, s, "f_fwd");
+    if ((e = launch_pdl(k_fwd, dim3(grid), dim3(kThreads), fwd_smem_bytes(), s, h->kg, (const float*)w.f_g1img, c2,
+                        (const float*)w.f_img, (const int*)w.fast_hdr, (const int4*)w.f_tile_info,
+                        (const int*)w.f_item_start, (const unsigned*)w.f_item_key, (const int2*)w.f_sbi, out,
+                        direct)))
+      return e;
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+// mode 0: gradients into g0..g2; mode 1: SGD(+momentum) on the cores (mask)
+cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const float* c2, const float* gout,
+                          float* g0, float* g1, float* g2, float* p0, float* p1, float* p2, double* v0, double* v1,
+                          double* v2, double lr, double mu, int mask, int mode, cudaStream_t s) {
+  Workspace& w = h->w;
+  cudaError_t e;
+  const int64_t n0 = (int64_t)h->kg.m1 * 4 * R1, n1 = (int64_t)R1 * h->kg.m2 * C, n2 = (int64_t)32 * h->kg.m3 * 4;
+  if (mode == 1) {
+    g0 = w.f_grad;
+    g1 = w.f_grad + n0;
+    g2 = w.f_grad + n0 + n1;
+    if ((e = cudaMemsetAsync(w.f_grad, 0, sizeof(float) * (size_t)(n0 + n1 + n2), s))) return e;
+  } else {
+    if ((e = cudaMemsetAsync(g0, 0, sizeof(float) * (size_t)n0, s))) return e;
+    if ((e = cudaMemsetAsync(g1, 0, sizeof(float) * (size_t)n1, s))) return e;
+    if ((e = cudaMemsetAsync(g2, 0, sizeof(float) * (size_t)n2, s))) return e;
+  }
+  const int maxt = (int)((h->T + kTileItems - 1) / kTileItems + h->kg.m2);
+  const int grid = maxt < h->num_sms ? maxt : h->num_sms;
+  {
+    ProfScope _ps(h, s, "f_bwd");
+    if ((e = launch_pdl(k_bwd, dim3(grid), dim3(kThreads), kBwdSmem, s, h->kg, (const float*)w.f_g1img, c2,
+                        (const float*)w.f_img, (const int4*)w.f_tile_info, (const int*)w.f_item_start,
+                        (const unsigned*)w.f_item_key, (const int2*)w.f_sbi, gout, g0, g1, g2, w.fast_hdr,
+                        getenv("TTB_DBG") ? atoi(getenv("TTB_DBG")) : 0)))
+      return e;
+  }
+  count_launch();
+  if (mode == 1) {
+    const int64_t n = n0 + n1 + n2;
+    int sg = (int)((n + kBlock - 1) / kBlock);
+    if (sg > h->num_sms * 8) sg = h->num_sms * 8;
+    ProfScope _ps(h, s, "f_sgd");
+    if ((e = launch_pdl(k_sgd3, dim3(sg), dim3(kBlock), 0, s, p0, p1, p2, (const float*)w.f_grad, v0, v1, v2, n0, n1,
+                        n2, lr, mu, mask)))
+      return e;
+    count_launch();
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace ttb

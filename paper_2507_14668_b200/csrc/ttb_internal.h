@@ -68,9 +68,23 @@ struct Workspace {
   unsigned* runs_ctr;
   int* grp_done;                    // m2: finished chunk CTAs per i2 group (self-resetting)
   float* scratch1;                  // 1-float sink for the unit core of d = 2 tables
+  // tensor-core pipeline (ttb_fast.cu); fast_hdr sits just before zero block A:
+  // [0] err bits, [1] multi-index bags, [2] work items, [3] prefixes P, [4] tiles
+  int* fast_hdr;
+  unsigned* f_key;        // T: i2-major prefix key
+  unsigned* f_i3;         // T
+  int2* f_sbi;            // T: (bag, i3) in prefix-sorted order
+  int* f_item_start;      // T + 1
+  unsigned* f_item_key;   // T
+  int* f_i2_item;         // m2 + 1
+  int* f_tile_start;      // m2 + 1
+  int4* f_tile_info;      // tiles (<= T / 32 + m2): (i2, first item, items)
+  float* f_g1img;         // m1 x 512: split G1 rows / transposed images
+  float* f_img;           // m2 x 4 x 16 KB: G2 slice images (cb hi/lo, k hi/lo)
+  float* f_grad;          // |G1| + |G2| + |G3|: gradients for the fused update
 };
 
-enum ScanId { kScanSlots = 0, kScanSegs = 1, kScanFirst = 2, kNumScans = 3 };
+enum ScanId { kScanSlots = 0, kScanSegs = 1, kScanFirst = 2, kScanFast = 3, kNumScans = 4 };
 
 }  // namespace ttb
 
@@ -101,6 +115,12 @@ struct ttb_handle {
   int cmaxb;             // chunks per i2 group in the backward (dG2 partials)
   int dg2_slots;         // dG2 partial slots per i2 written by the last backward
   int bwd_split;         // use the split backward (rows kernel + tensor-core GEMM kernel)
+  int fast_ok, fast;     // tensor-core pipeline supported / selected (ttb_fast.cu)
+  int num_sms;
+  const void* plan_idx;  // inputs of the current plan (the legacy plan behind
+  const int64_t* plan_off;  // ttb_export_plan is built from them on demand)
+  int plan_idx64;
+  int legacy_planned;
   int idx_bits, i3_bits;
   char* base;
   size_t bytes;
@@ -162,6 +182,13 @@ cudaError_t launch_sort(ttb_handle* h, const unsigned* keys_in, const unsigned* 
 cudaError_t launch_sort_raw(const unsigned* keys_in, const unsigned* vals_in, unsigned* kA, unsigned* vA, unsigned* kB,
                             unsigned* vB, int n, int bits, unsigned* hist, unsigned* status, int tiles_cap,
                             unsigned* ctr, unsigned** keys_out, unsigned** vals_out, cudaStream_t s);
+bool fast_supported(const ttb_handle* h);
+cudaError_t fast_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* offsets, cudaStream_t s);
+cudaError_t fast_forward(ttb_handle* h, const float* c0, const float* c1, const float* c2, float* out,
+                         cudaStream_t s);
+cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const float* c2, const float* gout,
+                          float* g0, float* g1, float* g2, float* p0, float* p1, float* p2, double* v0, double* v1,
+                          double* v2, double lr, double mu, int mask, int mode, cudaStream_t s);
 cudaError_t launch_sgd(float* p, const float* g, double* v, int64_t n, double lr, double mu, cudaStream_t s);
 cudaError_t launch_export_plan(ttb_handle* h, int64_t* work, int64_t* slot_occ, int64_t* seg_ids,
                                int64_t* seg_inv, int64_t* digits, cudaStream_t s);

@@ -54,6 +54,8 @@ class _TTBagFunction(torch.autograd.Function):
                 eng.check_errors()
             return (None, None, None, *([None] * len(cores)))
         grads = eng.backward(cores, grad_out)
+        if module.check_errors:
+            eng.check_errors()
         return (None, None, None, *grads)
 
 
@@ -63,7 +65,8 @@ class TTEmbeddingBag(nn.Module):
 
     def __init__(self, num_embeddings: int, embedding_dim: int, tt_ranks, tt_m=None, tt_n=None, seed: int = 0,
                  target_row_std: float = 0.1, include_last_offset: bool = False, max_indices: int = 1 << 16,
-                 max_bags: int | None = None, device=None, check_errors: bool = True, init: bool = True):
+                 max_bags: int | None = None, device=None, check_errors: bool = True, init: bool = True,
+                 deterministic: bool = False):
         super().__init__()
         tt_ranks = tuple(int(r) for r in tt_ranks)
         d = len(tt_ranks) - 1
@@ -87,7 +90,9 @@ class TTEmbeddingBag(nn.Module):
         else:
             cores = [torch.zeros(self.shape.core_extent(k), dtype=torch.float32, device=dev) for k in range(self.shape.d)]
         self.cores = nn.ParameterList([nn.Parameter(c) for c in cores])
-        self.engine = TtEngine(self.shape, max_indices, max_bags, dev)
+        # deterministic=True: fixed summation order (bitwise reproducible
+        # gradients); otherwise the tensor-core pipeline where supported
+        self.engine = TtEngine(self.shape, max_indices, max_bags, dev, deterministic=deterministic)
         self.fused_sgd = None
         self.velocity = None
 

@@ -40,8 +40,14 @@ def require_cuda(device=None) -> torch.device:
 
 
 class TtEngine:
-    def __init__(self, shape: TtShape, max_indices: int = 1 << 16, max_bags: int | None = None, device=None):
+    def __init__(self, shape: TtShape, max_indices: int = 1 << 16, max_bags: int | None = None, device=None,
+                 deterministic: bool = False):
+        """deterministic=True selects the fixed-summation-order pipeline
+        (bitwise reproducible gradients, reference-ordered plan kept on the
+        device). Otherwise the tensor-core pipeline runs where the geometry
+        supports it (n = (4, 4, 4), ranks 32: TTB_OPT_FAST)."""
         self.shape = shape
+        self.deterministic = bool(deterministic)
         self.device = require_cuda(device)
         self.lib = nat.load()
         self.is_d2 = shape.d == 2
@@ -80,6 +86,8 @@ class TtEngine:
             self.lib.ttb_destroy(self._handle)
         self._handle, self._ws = C.c_void_p(h), ws
         self.max_T, self.max_B = T, B
+        if self.deterministic:
+            self.set_option(nat.OPT_FAST, 0)
 
     def ensure_capacity(self, T: int, B: int) -> None:
         if T > self.max_T or B > self.max_B:
@@ -127,6 +135,9 @@ class TtEngine:
                                     T, B, _stream()), "plan")
         self.T, self.B = T, B
         self.plan_id += 1
+        # the library may rebuild the reference-ordered plan from these later
+        # (ttb_export_plan under TTB_OPT_FAST): keep them alive until the next plan
+        self._plan_inputs = (indices, offsets)
 
     def forward(self, cores, out: torch.Tensor | None = None) -> torch.Tensor:
         c = self.native_cores(cores)
@@ -198,7 +209,7 @@ class TtEngine:
         st = (C.c_int64 * 8)()
         nat.check(self.lib.ttb_read_status(self._handle, st, _stream()), "status")
         return dict(err=int(st[0]), T=int(st[1]), B=int(st[2]), P=int(st[3]), S=int(st[4]), U=int(st[5]),
-                    gen=int(st[6]))
+                    gen=int(st[6]), items=int(st[7]))
 
     def check_errors(self) -> dict:
         st = self.status()
@@ -207,8 +218,18 @@ class TtEngine:
             raise exc
         return st
 
+    @property
+    def fast(self) -> bool:
+        """The tensor-core pipeline runs (geometry n = (4, 4, 4), ranks 32)."""
+        return (not self.deterministic and not self.is_d2 and tuple(self.shape.n) == (4, 4, 4)
+                and tuple(self.shape.ranks) == (1, 32, 32, 1))
+
     def export_plan(self) -> dict:
         st = self.status()
+        if st["S"] < 0:
+            # tensor-core pipeline: the reference-ordered plan is built on demand
+            nat.check(self.lib.ttb_export_plan(self._handle, None, None, None, None, None, _stream()), "export_plan")
+            st = self.status()
         T, P, S = st["T"], st["P"], st["S"]
         dev = self.device
         work = torch.empty((max(P, 1), 4), dtype=torch.int64, device=dev)

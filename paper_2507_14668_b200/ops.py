@@ -70,7 +70,9 @@ class GpuTtTable:
 
     def engine(self, T: int, B: int) -> TtEngine:
         if self._engine is None:
-            self._engine = TtEngine(self.shape, max(T, 1024), max(B, 1024), self.device)
+            # the operator API exposes the reuse buffer and the unique-row
+            # aggregation, which only the deterministic pipeline keeps
+            self._engine = TtEngine(self.shape, max(T, 1024), max(B, 1024), self.device, deterministic=True)
         self._engine.ensure_capacity(T, B)
         return self._engine
 

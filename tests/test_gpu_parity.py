@@ -27,18 +27,18 @@ def golden_geom(s, p):
                       tuple(int(v) for v in s[f"{p}.r"]))
 
 
-def make_engine(g, T, B):
+def make_engine(g, T, B, deterministic=False):
     from paper_2507_14668_b200.engine import TtEngine
     from paper_2507_14668_b200.geometry import TtShape
-    return TtEngine(TtShape(g.m, g.n, g.r), max(T, 16), max(B, 16), "cuda")
+    return TtEngine(TtShape(g.m, g.n, g.r), max(T, 16), max(B, 16), "cuda", deterministic=deterministic)
 
 
 def to_dev(cores32):
     return [torch.from_numpy(np.ascontiguousarray(c, dtype=np.float32)).cuda() for c in cores32]
 
 
-def run_case(g, cores32, idx, off, gout=None):
-    eng = make_engine(g, idx.size, off.size - 1)
+def run_case(g, cores32, idx, off, gout=None, deterministic=False):
+    eng = make_engine(g, idx.size, off.size - 1, deterministic)
     dc = to_dev(cores32)
     eng.plan(torch.from_numpy(idx).cuda(), torch.from_numpy(off).cuda())
     out = eng.forward(dc).cpu().numpy()
@@ -130,6 +130,7 @@ def random_batch(rng, rows, B, max_bag, skew=False):
     return idx.astype(np.int64), off
 
 
+@pytest.mark.parametrize("deterministic", [True, False])
 @pytest.mark.parametrize("m,n,r,B,max_bag,skew", [
     ((10, 10, 10), (2, 2, 4), (1, 16, 16, 1), 300, 3, False),      # config-1 dims, small rows
     ((20, 20, 25), (4, 4, 4), (1, 32, 32, 1), 500, 20, True),      # config-2/3 dims, Zipf, pooling 20
@@ -138,13 +139,15 @@ def random_batch(rng, rows, B, max_bag, skew=False):
     ((4, 6, 9), (1, 1, 7), (1, 3, 2, 1), 100, 40, True),           # n padded with 1s, long bags (> 32)
     ((1, 30, 40), (1, 4, 4), (1, 1, 8, 1), 300, 6, True),          # d=2-shaped geometry
 ])
-def test_random_parity(m, n, r, B, max_bag, skew):
+def test_random_parity(m, n, r, B, max_bag, skew, deterministic):
     rng = np.random.default_rng(hash((m, B)) % 2**32)
     g = O.Geometry(m, n, r)
     cores32 = [c.astype(np.float32) for c in O.init_cores(g, 3)]
     idx, off = random_batch(rng, g.rows, B, max_bag, skew)
     gout = rng.standard_normal((B, g.cols)).astype(np.float32)
-    res = run_case(g, cores32, idx, off, gout)
+    res = run_case(g, cores32, idx, off, gout, deterministic)
+    if not deterministic and not res["eng"].fast:
+        pytest.skip("geometry runs the deterministic pipeline only")
     c64 = [c.astype(np.float64) for c in cores32]
     out, plan = O.forward(c64, g, idx, off, want_plan=True)
     assert rel_err(res["out"], out) < FWD_TOL
@@ -157,7 +160,10 @@ def test_random_parity(m, n, r, B, max_bag, skew):
     want = O.core_grads(c64, g, ur, ug)
     for k in range(3):
         assert rel_err(res["grads"][k], want[k]) < GRAD_TOL, k
-    assert res["eng"].status()["U"] == ur.size
+    st = res["eng"].status()
+    assert st["P"] == np.unique(idx // g.m[2]).size
+    if deterministic:
+        assert st["U"] == ur.size
 
 
 def test_d2_table_via_module():
@@ -242,7 +248,7 @@ def test_config2_full_size_properties():
     counts vs numpy, forward on a sample of bags vs the oracle's row
     reconstruction, gradient determinism (two runs bitwise equal)."""
     from paper_2507_14668_b200.embedding_bag import TTEmbeddingBag
-    emb = TTEmbeddingBag(10_000_000, 64, (1, 32, 32, 1), seed=0, max_indices=65536)
+    emb = TTEmbeddingBag(10_000_000, 64, (1, 32, 32, 1), seed=0, max_indices=65536, deterministic=True)
     idx = np.random.default_rng(1).integers(0, 10_000_000, 65536)
     off = np.arange(65537, dtype=np.int64)
     gout = np.random.default_rng(2).standard_normal((65536, 64)).astype(np.float32)
@@ -288,7 +294,7 @@ def test_dp_step_matches_fused_update():
     idx, off = random_batch(rng, shape.rows, 256, 3, skew=True)
     ti, to = torch.from_numpy(idx).cuda(), torch.from_numpy(off).cuda()
     gout = torch.from_numpy(rng.standard_normal((256, 64)).astype(np.float32)).cuda()
-    e1, e2 = TtEngine(shape, 4096, 4096), TtEngine(shape, 4096, 4096)
+    e1, e2 = TtEngine(shape, 4096, 4096, deterministic=True), TtEngine(shape, 4096, 4096, deterministic=True)
     flat = dp.FlatCores([torch.from_numpy(c).cuda() for c in host])
     fused = dp.FlatCores([torch.from_numpy(c).cuda() for c in host])
     for _ in range(3):
@@ -309,7 +315,7 @@ def test_split_backward_paths_match_oracle():
     rng = np.random.default_rng(12)
     idx, off = random_batch(rng, g.rows, 3000, 3, skew=True)
     gout = rng.standard_normal((3000, g.cols)).astype(np.float32)
-    eng = make_engine(g, idx.size, 3000)
+    eng = make_engine(g, idx.size, 3000, deterministic=True)
     eng.set_option(1, 1)
     dc = to_dev(cores32)
     eng.plan(torch.from_numpy(idx).cuda(), torch.from_numpy(off).cuda())
@@ -319,3 +325,92 @@ def test_split_backward_paths_match_oracle():
     want = O.core_grads([c.astype(np.float64) for c in cores32], g, ur, ug)
     for k in range(3):
         assert rel_err(grads[k].cpu().numpy(), want[k]) < GRAD_TOL, k
+
+
+# ------------------------------------------------------------------ tensor-core pipeline
+def test_fast_config2_full_size():
+    """BASELINE config 2 on the tensor-core pipeline (the default for this
+    geometry): prefix count, forward on a sample vs the oracle, gradients on a
+    sub-batch vs the oracle, fused SGD(+momentum) vs the oracle's update."""
+    from paper_2507_14668_b200.embedding_bag import TTEmbeddingBag
+    emb = TTEmbeddingBag(10_000_000, 64, (1, 32, 32, 1), seed=0, max_indices=65536)
+    eng = emb.engine
+    assert eng.fast
+    idx = np.random.default_rng(1).integers(0, 10_000_000, 65536)
+    off = np.arange(65537, dtype=np.int64)
+    gout = np.random.default_rng(2).standard_normal((65536, 64)).astype(np.float32)
+    ti, to = torch.from_numpy(idx).cuda(), torch.from_numpy(off).cuda()
+    cores = [c.detach() for c in emb.cores]
+    eng.plan(ti, to)
+    out = eng.forward(cores)
+    st = eng.check_errors()
+    assert st["P"] == np.unique(idx // 250).size
+    g = O.Geometry(emb.shape.m, emb.shape.n, emb.shape.ranks)
+    c64 = [c.cpu().numpy().astype(np.float64) for c in cores]
+    sample = np.random.default_rng(3).choice(65536, 2000, replace=False)
+    assert rel_err(out.cpu().numpy()[sample], O.reconstruct_rows(c64, g, idx[sample])) < FWD_TOL
+    full = [x.clone() for x in eng.backward(cores, torch.from_numpy(gout).cuda())]
+    sub = 4096
+    eng.plan(ti[:sub], to[: sub + 1])
+    eng.forward(cores)
+    gs = eng.backward(cores, torch.from_numpy(gout[:sub]).cuda())
+    ur, ug = O.unique_aggregate(idx[:sub], gout[:sub].astype(np.float64))
+    want = O.core_grads(c64, g, ur, ug)
+    for k in range(3):
+        assert rel_err(gs[k].cpu().numpy(), want[k]) < GRAD_TOL
+    # full batch against the deterministic pipeline
+    det = make_engine(g, 65536, 65536, deterministic=True)
+    det.plan(ti, to)
+    det.forward(cores)
+    gd = det.backward(cores, torch.from_numpy(gout).cuda())
+    for k in range(3):
+        assert rel_err(full[k].cpu().numpy(), gd[k].cpu().numpy().astype(np.float64)) < GRAD_TOL
+    # fused SGD(+momentum): two steps vs the oracle update on the same grads
+    work = [c.clone() for c in cores]
+    vel = [torch.zeros(c.shape, dtype=torch.float64, device="cuda") for c in cores]
+    ref = [c.cpu().numpy().astype(np.float32) for c in cores]
+    rvel = [np.zeros(c.shape) for c in ref]
+    for _ in range(2):
+        eng.plan(ti[:sub], to[: sub + 1])
+        eng.forward(work)
+        gk = [x.clone() for x in eng.backward(work, torch.from_numpy(gout[:sub]).cuda())]
+        eng.plan(ti[:sub], to[: sub + 1])
+        eng.forward(work)
+        eng.backward_sgd(work, torch.from_numpy(gout[:sub]).cuda(), 0.05, 0.9, vel)
+        for k in range(3):
+            rvel[k] = O.sgd_step(ref[k], gk[k].cpu().numpy(), 0.05, 0.9, rvel[k])
+    for k in range(3):
+        assert rel_err(work[k].cpu().numpy(), ref[k]) < 1e-5
+
+
+@pytest.mark.parametrize("B,max_bag,skew", [(2000, 1, False), (1500, 20, True), (300, 200, True)])
+def test_fast_pooled_and_hot_rows(B, max_bag, skew):
+    """Pooled bags, hot Zipf rows and items split across kItemLen: outputs and
+    gradients vs the oracle (tensor-core pipeline)."""
+    g = O.Geometry((20, 20, 25), (4, 4, 4), (1, 32, 32, 1))
+    cores32 = [c.astype(np.float32) for c in O.init_cores(g, 9)]
+    rng = np.random.default_rng(B)
+    idx, off = random_batch(rng, g.rows, B, max_bag, skew)
+    gout = rng.standard_normal((B, g.cols)).astype(np.float32)
+    res = run_case(g, cores32, idx, off, gout)
+    assert res["eng"].fast
+    c64 = [c.astype(np.float64) for c in cores32]
+    assert rel_err(res["out"], O.forward(c64, g, idx, off)) < FWD_TOL
+    ur, ug = O.unique_aggregate(idx, np.repeat(gout.astype(np.float64), np.diff(off), axis=0))
+    want = O.core_grads(c64, g, ur, ug)
+    for k in range(3):
+        assert rel_err(res["grads"][k], want[k]) < GRAD_TOL, k
+
+
+def test_fast_errors_raise():
+    from paper_2507_14668_b200.embedding_bag import TTEmbeddingBag
+    emb = TTEmbeddingBag(10000, 64, (1, 32, 32, 1), tt_m=(20, 20, 25), tt_n=(4, 4, 4))
+    assert emb.engine.fast
+    with pytest.raises(ValueError):
+        emb(torch.tensor([0, 10000], device="cuda"), torch.tensor([0, 1], device="cuda"))
+    with pytest.raises(ValueError):
+        emb(torch.tensor([0, 1], device="cuda"), torch.tensor([0, 2, 2], device="cuda"))
+    out = emb(torch.tensor([3, 4, 5], device="cuda"), torch.tensor([0, 1], device="cuda"))
+    with pytest.raises(ValueError):
+        out.backward(torch.full_like(out, float("nan")))
+        emb.engine.check_errors()
