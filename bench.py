@@ -58,7 +58,10 @@ def synthetic_batch(rank: int, cfg=CFG2):
     rng = np.random.default_rng(1 + 1000 * rank)
     idx = rng.integers(0, cfg["rows"], cfg["batch"] * cfg["pooling"]).astype(np.int64)
     off = np.arange(0, cfg["batch"] * cfg["pooling"] + 1, cfg["pooling"], dtype=np.int64)
-    gout = np.random.default_rng(2 + 1000 * rank).standard_normal((cfg["batch"], cfg["dim"])).astype(np.float32)
+    # upstream gradient of a batch-mean loss: N(0, 1) / batch (keeps many
+    # repeated SGD steps on one batch finite)
+    gout = (np.random.default_rng(2 + 1000 * rank).standard_normal((cfg["batch"], cfg["dim"]))
+            / cfg["batch"]).astype(np.float32)
     return idx, off, gout
 
 
@@ -238,7 +241,7 @@ def run_ours(args):
         "metric": "TT-EmbeddingBag lookups/sec fwd+bwd", "value": value, "unit": "lookups/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded uniform indices, N(0,1) upstream grads, reference init_random cores)",
+        "data": "synthetic (seeded uniform indices, N(0,1)/batch upstream grads, reference init_random cores)",
         "config": {
             "workload": "BASELINE configs[1]: TT-EmbeddingBag microbench, 10M rows x 64, ranks (1,32,32,1), "
                         "m=(200,200,250) n=(4,4,4), batch 65536 bags, pooling 1, uniform indices; "

@@ -120,7 +120,7 @@ def cfg3(dev, steps=3, B=65536, pooling=20, permuted=False, tables=26):
             ids = perm[ids]
         idxs.append(torch.from_numpy(ids).to(dev))
     off = torch.arange(0, T + 1, pooling, dtype=torch.int64, device=dev)
-    gout = torch.randn((B, 64), device=dev)
+    gout = torch.randn((B, 64), device=dev) / B  # batch-mean loss scale
     out = torch.empty((B, 64), device=dev)
 
     def step():
