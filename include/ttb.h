@@ -124,6 +124,16 @@ int ttb_backward_sgd(ttb_handle *h, float *core0, float *core1, float *core2,
                      double *vel2, double lr, double momentum,
                      int update_mask, ttb_stream stream);
 
+/* The tensor-core pipeline keeps split-tf32 images of cores 0 and 1 in the
+ * workspace. They are rebuilt by ttb_forward whenever the core pointers
+ * differ from the last forward / fused update, and written directly by
+ * ttb_backward_sgd's update; ttb_backward (gradients returned) drops them.
+ * A caller that changes core VALUES by any other means (an optimizer step,
+ * loading a checkpoint) while keeping the same pointers must call this
+ * before the next ttb_forward. The Python layer does so automatically
+ * (tensor version counters). */
+int ttb_cores_modified(ttb_handle *h);
+
 /* K5 alone on a flat parameter: used after the data-parallel all-reduce
  * and for dense parameters. velocity may be NULL when momentum == 0. */
 int ttb_sgd_update(float *param, const float *grad, double *velocity,

@@ -129,8 +129,10 @@ void layout(ttb_handle& h, char* base) {
   w.f_sbi = c.take<int2>(fz ? T : 0);
   w.f_item_start = c.take<int>(fz ? T + 1 : 0);
   w.f_item_key = c.take<unsigned>(fz ? T : 0);
-  w.f_i2_item = c.take<int>(fz ? g.m[1] + 1 : 0);
-  w.f_tile_start = c.take<int>(fz ? g.m[1] + 1 : 0);
+  w.f_rk = c.take<int>(fz ? T : 0);
+  w.f_cnt = c.take<int>(fz ? (size_t)g.m[0] * g.m[1] : 0);
+  w.f_start = c.take<int>(fz ? (size_t)g.m[0] * g.m[1] : 0);
+  w.f_gtot = c.take<int4>(fz ? g.m[1] : 0);
   w.f_tile_info = c.take<int4>(fz ? T / 32 + g.m[1] + 2 : 0);
   w.f_g1img = c.take<float>(fz ? (size_t)g.m[0] * 512 : 0);
   w.f_img = c.take<float>(fz ? (size_t)g.m[1] * 16384 : 0);
@@ -213,7 +215,8 @@ ttb_handle* ttb_create(const ttb_geom* g, int64_t max_T, int64_t max_B, void* wo
   cudaStream_t s = (cudaStream_t)stream;
   if (cudaMemsetAsync(h->w.zeroA, 0, h->w.zeroA_bytes + h->w.zeroB_bytes, s) != cudaSuccess ||
       cudaMemsetAsync(h->w.grp_done, 0, sizeof(int) * h->kg.m2, s) != cudaSuccess ||
-      cudaMemsetAsync(h->w.pmap, 0xFF, sizeof(unsigned) * h->kg.m1m2, s) != cudaSuccess) {
+      cudaMemsetAsync(h->w.pmap, 0xFF, sizeof(unsigned) * h->kg.m1m2, s) != cudaSuccess ||
+      (h->fast_ok && cudaMemsetAsync(h->w.f_cnt, 0, sizeof(int) * h->kg.m1m2, s) != cudaSuccess)) {
     free(h);
     return nullptr;
   }
@@ -294,6 +297,12 @@ int ttb_backward_sgd(ttb_handle* h, float* c0, float* c1, float* c2, const float
   if (e != cudaSuccess) return TTB_ECUDA;
   h->backwarded = 1;
   h->pmap_clean = 1;
+  return TTB_OK;
+}
+
+int ttb_cores_modified(ttb_handle* h) {
+  if (!h) return TTB_EINVAL;
+  h->img_valid = 0;
   return TTB_OK;
 }
 

@@ -43,17 +43,60 @@ __device__ __forceinline__ void red_f32(float* p, float a) {
   asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(a) : "memory");
 }
 
-// ------------------------------------------------------------ plan: keys
+// ------------------------------------------------------------ plan
+// One persistent kernel (grid <= SM count, all CTAs co-resident) in three
+// phases separated by grid barriers — a counting sort over the m1 m2 prefix
+// keys instead of a radix sort of the positions:
+//   0  per index: digits, i2-major prefix key, rank within its key from a
+//      warp-aggregated atomicAdd on the key's counter; per bag: bag ids
+//   A  per i2 group (warp): totals, then the group's exclusive offsets
+//      (positions, work items, tiles) and its key starts / item / tile tables
+//   B  per index: (bag, i3) scattered to start[key] + rank; counters reset
+// Order inside a prefix is arbitrary (summation order of fp32 reductions
+// only); items are runs of <= kItemLen positions of one prefix, tiles runs of
+// <= kTileItems items of one i2.
+constexpr int kPlanThreads = 512;
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ inline void grid_barrier(unsigned* bar, unsigned& target) {
+  __syncthreads();
+  target += gridDim.x;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    while (ld_acquire_u32(bar) < target) __nanosleep(32);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int warp_sum(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 template <typename IdxT>
-__global__ void __launch_bounds__(kBlock) k_keys(const IdxT* __restrict__ idx, const int64_t* __restrict__ offsets,
-                                                 int T, int B, KGeom g, unsigned* __restrict__ key,
-                                                 unsigned* __restrict__ i3o, int* __restrict__ bag_of,
-                                                 int* __restrict__ hdr) {
+__global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__ idx,
+                                                        const int64_t* __restrict__ offsets, int T, int B, KGeom g,
+                                                        unsigned* __restrict__ key, unsigned* __restrict__ i3o,
+                                                        int* __restrict__ rk, int* __restrict__ bag_of,
+                                                        int* __restrict__ cnt, int* __restrict__ start,
+                                                        int4* __restrict__ gtot, int* __restrict__ item_start,
+                                                        unsigned* __restrict__ item_key, int4* __restrict__ tile_info,
+                                                        int2* __restrict__ sbi, int* __restrict__ hdr) {
   pdl_enter();
-  const int stride = gridDim.x * blockDim.x;
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned* bar = reinterpret_cast<unsigned*>(hdr + 12);
+  unsigned target = 0;
+  const int nthr = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  // ---- phase 0
   int bits = 0, multi = 0;
-  for (int b = tid; b < B; b += stride) {
+  for (int b = tid; b < B; b += nthr) {
     const int64_t ob = offsets[b], on = offsets[b + 1];
     if (b == 0 && ob != 0) bits |= 4;
     if (b == B - 1 && on != (int64_t)T) bits |= 4;
@@ -64,132 +107,99 @@ __global__ void __launch_bounds__(kBlock) k_keys(const IdxT* __restrict__ idx, c
     if (hi - lo > 1) multi = 1;
   }
   const unsigned m2m3 = g.m2 * g.m3;
-  for (int t = tid; t < T; t += stride) {
-    long long v = (long long)idx[t];
-    if (v < 0 || v >= (long long)g.rows) {
-      bits |= 1;
-      v = 0;
+  for (int t0 = blockIdx.x * blockDim.x; t0 < T; t0 += nthr) {  // warp-uniform trip count
+    const int t = t0 + threadIdx.x;
+    const bool ok = t < T;
+    unsigned k = 0xFFFFFFFFu;
+    if (ok) {
+      long long v = (long long)idx[t];
+      if (v < 0 || v >= (long long)g.rows) {
+        bits |= 1;
+        v = 0;
+      }
+      const unsigned i = (unsigned)v, i1 = i / m2m3, r = i - i1 * m2m3, i2 = r / g.m3;
+      k = i2 * g.m1 + i1;
+      key[t] = k;
+      i3o[t] = r - i2 * g.m3;
     }
-    const unsigned i = (unsigned)v, i1 = i / m2m3, r = i - i1 * m2m3, i2 = r / g.m3;
-    key[t] = i2 * g.m1 + i1;  // i2-major prefix key
-    i3o[t] = r - i2 * g.m3;
+    const unsigned peers = __match_any_sync(0xffffffffu, k);
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (ok && lane == leader) base = atomicAdd(&cnt[k], __popc(peers));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (ok) rk[t] = base + __popc(peers & lanemask_lt());
   }
   if (bits) atomicOr(&hdr[0], bits);
   if (multi) hdr[1] = 1;
-}
-
-// ------------------------------------------------------------ plan: items
-// Over the prefix-sorted positions: item heads (prefix change, or every
-// kItemLen positions), the sorted (bag, i3) pairs, and the prefix count.
-__global__ void __launch_bounds__(kBlock) k_items(const unsigned* __restrict__ sk, const unsigned* __restrict__ sv,
-                                                  const int* __restrict__ bag_of, const unsigned* __restrict__ i3o,
-                                                  int T, int* __restrict__ item_start, unsigned* __restrict__ item_key,
-                                                  int2* __restrict__ sbi, int* __restrict__ hdr,
-                                                  unsigned long long* status, unsigned* ctr) {
-  pdl_enter();
-  __shared__ int s_tile;
-  __shared__ int s_tmp[kItems * (kBlock / 32) + 2];
-  const int tile = claim_tile(ctr, &s_tile);
-  const int base = tile * kTile;
-  bool f[kItems];
-  unsigned key[kItems];
-  int nph = 0;
-#pragma unroll
-  for (int k = 0; k < kItems; ++k) {
-    const int q = base + k * kBlock + threadIdx.x;
-    f[k] = false;
-    key[k] = 0;
-    if (q < T) {
-      key[k] = sk[q];
-      const bool ph = q == 0 || sk[q - 1] != key[k];
-      f[k] = ph || (q % kItemLen) == 0;
-      nph += ph;
-      const unsigned l = sv[q];
-      sbi[q] = make_int2(bag_of[l], (int)i3o[l]);
+  grid_barrier(bar, target);
+  // ---- phase A1: per-i2 totals (positions, items, present prefixes)
+  const int gw = tid >> 5, nw = nthr >> 5;
+  for (unsigned i2 = gw; i2 < g.m2; i2 += nw) {
+    int c = 0, it = 0, p = 0;
+    for (unsigned i1 = lane; i1 < g.m1; i1 += 32) {
+      const int v = cnt[i2 * g.m1 + i1];
+      c += v;
+      it += (v + kItemLen - 1) / kItemLen;
+      p += v > 0;
     }
+    c = warp_sum(c);
+    it = warp_sum(it);
+    p = warp_sum(p);
+    if (lane == 0) gtot[i2] = make_int4(c, it, p, 0);
   }
-  int rank[kItems];
-  long long incl;
-  tile_flag_scan(f, rank, status, tile, s_tmp, &incl);
-#pragma unroll
-  for (int k = 0; k < kItems; ++k) {
-    if (f[k]) {
-      item_start[rank[k]] = base + k * kBlock + threadIdx.x;
-      item_key[rank[k]] = key[k];
+  grid_barrier(bar, target);
+  // ---- phase A2: group offsets, key starts, item and tile tables
+  for (unsigned i2 = gw; i2 < g.m2; i2 += nw) {
+    int pc = 0, pi = 0, pt = 0;
+    for (unsigned j = lane; j < i2; j += 32) {
+      const int4 q = gtot[j];
+      pc += q.x;
+      pi += q.y;
+      pt += (q.y + kTileItems - 1) / kTileItems;
     }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) nph += __shfl_xor_sync(0xffffffffu, nph, o);
-  if ((threadIdx.x & 31) == 0 && nph) atomicAdd(&hdr[3], nph);
-  if (tile == (T + kTile - 1) / kTile - 1 && threadIdx.x == 0) {
-    hdr[2] = (int)incl;
-    item_start[incl] = T;
-  }
-}
-
-// ------------------------------------------------------------ plan: tiles
-// One CTA: first item of every i2 (binary search over the sorted item keys)
-// and the exclusive scan of ceil(items / 32) per i2.
-__global__ void __launch_bounds__(1024) k_tiles(const unsigned* __restrict__ item_key, KGeom g,
-                                                int* __restrict__ i2_item, int* __restrict__ tile_start,
-                                                int4* __restrict__ tile_info, int* __restrict__ hdr) {
-  pdl_enter();
-  __shared__ int s_w[32];
-  __shared__ int s_carry;
-  const int n = hdr[2];
-  for (unsigned i2 = threadIdx.x; i2 <= g.m2; i2 += blockDim.x) {
-    const unsigned target = i2 * g.m1;
-    int lo = 0, hi = n;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (item_key[mid] < target) lo = mid + 1;
-      else hi = mid;
+    pc = warp_sum(pc);
+    pi = warp_sum(pi);
+    pt = warp_sum(pt);
+    const int4 mine = gtot[i2];
+    const int ntile = (mine.y + kTileItems - 1) / kTileItems;
+    for (int j = lane; j < ntile; j += 32) {
+      const int left = mine.y - kTileItems * j;
+      tile_info[pt + j] = make_int4((int)i2, pi + kTileItems * j, left < kTileItems ? left : kTileItems, 0);
     }
-    i2_item[i2] = lo;
-  }
-  if (threadIdx.x == 0) s_carry = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (unsigned b0 = 0; b0 < g.m2; b0 += blockDim.x) {
-    const unsigned i2 = b0 + threadIdx.x;
-    const int v = i2 < g.m2 ? (i2_item[i2 + 1] - i2_item[i2] + kTileItems - 1) / kTileItems : 0;
-    int x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) s_w[w] = x;
-    __syncthreads();
-    if (w == 0) {
-      int y = lane < (int)(blockDim.x >> 5) ? s_w[lane] : 0;
+    int pos = pc, itm = pi;
+    for (unsigned i1b = 0; i1b < g.m1; i1b += 32) {
+      const unsigned i1 = i1b + lane, k = i2 * g.m1 + i1;
+      const int v = i1 < g.m1 ? cnt[k] : 0, ni = (v + kItemLen - 1) / kItemLen;
+      int sv = v, si = ni;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const int z = __shfl_up_sync(0xffffffffu, y, o);
-        if (lane >= o) y += z;
+        const int a = __shfl_up_sync(0xffffffffu, sv, o), b2 = __shfl_up_sync(0xffffffffu, si, o);
+        if (lane >= o) sv += a, si += b2;
       }
-      s_w[lane] = y;  // inclusive warp totals
+      const int ev = pos + sv - v, ei = itm + si - ni;
+      if (i1 < g.m1) {
+        start[k] = ev;
+        for (int j = 0; j < ni; ++j) {
+          item_start[ei + j] = ev + kItemLen * j;
+          item_key[ei + j] = k;
+        }
+      }
+      pos += __shfl_sync(0xffffffffu, sv, 31);
+      itm += __shfl_sync(0xffffffffu, si, 31);
     }
-    __syncthreads();
-    const int carry = s_carry;
-    const int excl = carry + (w ? s_w[w - 1] : 0) + x - v;
-    if (i2 < g.m2) {
-      tile_start[i2] = excl;
-      // tile table: (i2, first item, items) of each of this group's tiles
-      const int first = i2_item[i2], cnt = i2_item[i2 + 1] - first;
-      for (int j = 0; j < v; ++j) {
-        const int nn = cnt - j * kTileItems;
-        tile_info[excl + j] = make_int4((int)i2, first + j * kTileItems, nn < kTileItems ? nn : kTileItems, 0);
+    if (lane == 0) {
+      atomicAdd(&hdr[3], mine.z);
+      if (i2 == g.m2 - 1) {
+        hdr[2] = pi + mine.y;
+        hdr[4] = pt + ntile;
+        item_start[pi + mine.y] = T;
       }
     }
-    __syncthreads();
-    if (threadIdx.x == 0) s_carry = carry + s_w[31];
-    __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    tile_start[g.m2] = s_carry;
-    hdr[4] = s_carry;
-  }
+  grid_barrier(bar, target);
+  // ---- phase B: scatter (bag, i3) into prefix order; reset the counters
+  for (int t = tid; t < T; t += nthr) sbi[start[key[t]] + rk[t]] = make_int2(bag_of[t], (int)i3o[t]);
+  for (unsigned k = tid; k < g.m1m2; k += nthr) cnt[k] = 0;
 }
 
 // ------------------------------------------------------------ core images
@@ -201,16 +211,51 @@ __global__ void __launch_bounds__(1024) k_tiles(const unsigned* __restrict__ ite
 //     [2..3] k      : rows k (hi 0..31, lo 32..63), K = (c, b) (128)
 //   per i1 (512 floats): rows_hi[a][k], rows_lo[a][k], t_hi[k][a], t_lo[k][a]
 constexpr int kG1Img = 512;
+constexpr int kImgThreads = 512;
 
-__global__ void __launch_bounds__(kThreads) k_coreimg(const float* __restrict__ G1, const float* __restrict__ G2,
-                                                      KGeom g, float* __restrict__ img, float* __restrict__ g1img) {
+// Optional SGD(+momentum) step applied to each element before it is imaged:
+// the fused update of the previous backward writes the next step's images.
+struct SgdArgs {
+  const float* grad;  // flat |G1| + |G2| + |G3| gradients
+  double *v0, *v1, *v2;
+  float* p2;
+  double lr, mu;
+  int mask, on;
+};
+
+__device__ __forceinline__ float maybe_sgd(float p, const SgdArgs& u, int core, size_t flat, size_t j, double* v) {
+  if (!u.on || !((u.mask >> core) & 1)) return p;
+  return sgd_apply(p, u.grad[flat], v ? v + j : nullptr, u.lr, u.mu);
+}
+
+__global__ void __launch_bounds__(kImgThreads) k_coreimg(float* __restrict__ G1, float* __restrict__ G2, KGeom g,
+                                                         float* __restrict__ img, float* __restrict__ g1img,
+                                                         SgdArgs u) {
   pdl_enter();
-  if (blockIdx.x >= g.m2) {  // G1 images: 2 i1 per block (128 elements each)
-    const unsigned i1 = (blockIdx.x - g.m2) * 2 + (threadIdx.x >> 7);
+  const size_t n0 = (size_t)g.m1 * 4 * R1, n1 = (size_t)R1 * g.m2 * C;
+  const unsigned nb12 = g.m2 + (g.m1 + 3) / 4;
+  if (blockIdx.x >= nb12) {  // G3: update only
+    const size_t n2 = (size_t)32 * g.m3 * 4;
+    for (size_t j = (size_t)(blockIdx.x - nb12) * kImgThreads + threadIdx.x; j < n2;
+         j += (size_t)(gridDim.x - nb12) * kImgThreads) {
+      const float v = u.p2[j];
+      const float w = maybe_sgd(v, u, 2, n0 + n1 + j, j, u.v2);
+      if (u.mask & 4) u.p2[j] = w;
+    }
+    return;
+  }
+  if (blockIdx.x >= g.m2) {  // G1 images: 4 i1 per block (128 elements each)
+    const unsigned i1 = (blockIdx.x - g.m2) * 4 + (threadIdx.x >> 7);
     const int e = threadIdx.x & 127, a = e >> 5, k = e & 31;
     if (i1 < g.m1) {
+      const size_t j = (size_t)i1 * 128 + e;
+      float v = G1[j];
+      if (u.on && (u.mask & 1)) {
+        v = maybe_sgd(v, u, 0, j, j, u.v0);
+        G1[j] = v;
+      }
       float hi, lo;
-      umma::split3(__ldg(G1 + (size_t)i1 * 128 + e), hi, lo);
+      umma::split3(v, hi, lo);
       float* d = g1img + (size_t)i1 * kG1Img;
       d[e] = hi;
       d[128 + e] = lo;
@@ -222,11 +267,27 @@ __global__ void __launch_bounds__(kThreads) k_coreimg(const float* __restrict__ 
   extern __shared__ __align__(16) char smem_raw[];
   char* sm = (char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const unsigned i2 = blockIdx.x;
-  for (int e = threadIdx.x; e < R1 * C; e += kThreads) {
-    const int k = e >> 7, b = (e >> 5) & 3, c = e & 31;
-    const float v = __ldg(G2 + ((size_t)k * g.m2 + i2) * C + b * 32 + c);
+  constexpr int kPer = R1 * C / kImgThreads;  // 8
+  float vals[kPer];
+#pragma unroll
+  for (int r = 0; r < kPer; ++r) {
+    const int e = threadIdx.x + r * kImgThreads, k = e >> 7;
+    vals[r] = G2[((size_t)k * g.m2 + i2) * C + (e & 127)];
+  }
+  if (u.on && (u.mask & 2)) {
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+      const int e = threadIdx.x + r * kImgThreads, k = e >> 7;
+      const size_t j = ((size_t)k * g.m2 + i2) * C + (e & 127);
+      vals[r] = maybe_sgd(vals[r], u, 1, n0 + j, j, u.v1);
+      G2[j] = vals[r];
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kPer; ++r) {
+    const int e = threadIdx.x + r * kImgThreads, k = e >> 7, b = (e >> 5) & 3, c = e & 31;
     float hi, lo;
-    umma::split3(v, hi, lo);
+    umma::split3(vals[r], hi, lo);
     const int cb = 4 * c + b;
     const uint32_t o1 = umma::sw128_off(cb, k, 128);
     *(float*)(sm + o1) = hi;
@@ -237,7 +298,8 @@ __global__ void __launch_bounds__(kThreads) k_coreimg(const float* __restrict__ 
   __syncthreads();
   uint4* dst = reinterpret_cast<uint4*>(img + (size_t)i2 * (4 * kImg / 4));
   const uint4* src = reinterpret_cast<const uint4*>(sm);
-  for (int e = threadIdx.x; e < 4 * kImg / 16; e += kThreads) dst[e] = src[e];
+#pragma unroll
+  for (int e = threadIdx.x; e < 4 * kImg / 16; e += kImgThreads) dst[e] = src[e];
 }
 
 // ------------------------------------------------------------ async copies
@@ -834,31 +896,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
   if (warp == 0) umma::tmem_free(tmem, 512);
 }
 
-// ------------------------------------------------------------ SGD over the cores
-__global__ void __launch_bounds__(kBlock) k_sgd3(float* __restrict__ p0, float* __restrict__ p1,
-                                                 float* __restrict__ p2, const float* __restrict__ gr,
-                                                 double* __restrict__ v0, double* __restrict__ v1,
-                                                 double* __restrict__ v2, int64_t n0, int64_t n1, int64_t n2,
-                                                 double lr, double mu, int mask) {
-  pdl_enter();
-  const int64_t n = n0 + n1 + n2;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    float* p;
-    double* v;
-    int64_t j;
-    int k;
-    if (i < n0) {
-      p = p0, v = v0, j = i, k = 0;
-    } else if (i < n0 + n1) {
-      p = p1, v = v1, j = i - n0, k = 1;
-    } else {
-      p = p2, v = v2, j = i - n0 - n1, k = 2;
-    }
-    if (!((mask >> k) & 1)) continue;
-    p[j] = sgd_apply(p[j], gr[i], v ? v + j : nullptr, lr, mu);
-  }
-}
-
 }  // namespace fast
 
 using namespace fast;
@@ -878,39 +915,20 @@ cudaError_t fast_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* 
   cudaError_t e;
   if ((e = cudaMemsetAsync(w.fast_hdr, 0, (size_t)(w.zeroB + w.zeroB_bytes - (char*)w.fast_hdr), s))) return e;
   h->bwd_zeroed = 1;
-  const int work = T > B ? T : B;
-  int grid = (work + kBlock - 1) / kBlock;
-  if (grid > 148 * 16) grid = 148 * 16;
-  {
-    ProfScope _ps(h, s, "f_keys");
-    if (idx64)
-      e = launch_pdl(k_keys<long long>, dim3(grid), dim3(kBlock), 0, s, (const long long*)idx, offsets, T, B, h->kg,
-                     w.f_key, w.f_i3, w.bag_of, w.fast_hdr);
-    else
-      e = launch_pdl(k_keys<int>, dim3(grid), dim3(kBlock), 0, s, (const int*)idx, offsets, T, B, h->kg, w.f_key,
-                     w.f_i3, w.bag_of, w.fast_hdr);
-    if (e) return e;
-  }
-  count_launch();
-  unsigned *sk, *sv;
-  int bits = 1;
-  while (bits < 32 && ((uint64_t)(h->kg.m1m2 - 1) >> bits) != 0) ++bits;
-  if ((e = launch_sort(h, w.f_key, nullptr, w.skA, w.svA, w.skB, w.svB, nullptr, T, bits, 0, &sk, &sv, s))) return e;
-  const int tiles = (T + kTile - 1) / kTile;
-  {
-    ProfScope _ps(h, s, "f_items");
-    if ((e = launch_pdl(k_items, dim3(tiles), dim3(kBlock), 0, s, (const unsigned*)sk, (const unsigned*)sv,
-                        (const int*)w.bag_of, (const unsigned*)w.f_i3, T, w.f_item_start, w.f_item_key, w.f_sbi,
-                        w.fast_hdr, w.scan_status + kScanFast * h->scan_tiles, w.scan_ctr + kScanFast)))
-      return e;
-  }
-  count_launch();
-  {
-    ProfScope _ps(h, s, "f_tiles");
-    if ((e = launch_pdl(k_tiles, dim3(1), dim3(1024), 0, s, (const unsigned*)w.f_item_key, h->kg, w.f_i2_item,
-                        w.f_tile_start, w.f_tile_info, w.fast_hdr)))
-      return e;
-  }
+  int work = T > B ? T : B;
+  if ((int)h->kg.m1m2 > work) work = (int)h->kg.m1m2;
+  int grid = (work + kPlanThreads - 1) / kPlanThreads;
+  if (grid > h->num_sms) grid = h->num_sms;  // co-resident: grid barriers
+  ProfScope _ps(h, s, "f_plan");
+  if (idx64)
+    e = launch_pdl(k_fplan<long long>, dim3(grid), dim3(kPlanThreads), 0, s, (const long long*)idx, offsets, T, B,
+                   h->kg, w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_gtot, w.f_item_start,
+                   w.f_item_key, w.f_tile_info, w.f_sbi, w.fast_hdr);
+  else
+    e = launch_pdl(k_fplan<int>, dim3(grid), dim3(kPlanThreads), 0, s, (const int*)idx, offsets, T, B, h->kg,
+                   w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_gtot, w.f_item_start, w.f_item_key,
+                   w.f_tile_info, w.f_sbi, w.fast_hdr);
+  if (e) return e;
   count_launch();
   return cudaGetLastError();
 }
@@ -927,13 +945,19 @@ cudaError_t fast_forward(ttb_handle* h, const float* c0, const float* c1, const 
     if ((e = ensure_attr((const void*)k_bwd, kBwdSmem))) return e;
     attr = true;
   }
-  {
+  if (!(h->img_valid && h->img_c0 == c0 && h->img_c1 == c1)) {
+    // split tf32 images of the cores (skipped while the images written by the
+    // last fused update, or the last forward, still describe these cores)
     ProfScope _ps(h, s, "f_coreimg");
-    if ((e = launch_pdl(k_coreimg, dim3(h->kg.m2 + (h->kg.m1 + 1) / 2), dim3(kThreads), img_smem, s, c0, c1, h->kg,
-                        w.f_img, w.f_g1img)))
+    SgdArgs u = {};
+    if ((e = launch_pdl(k_coreimg, dim3(h->kg.m2 + (h->kg.m1 + 3) / 4), dim3(kImgThreads), img_smem, s,
+                        const_cast<float*>(c0), const_cast<float*>(c1), h->kg, w.f_img, w.f_g1img, u)))
       return e;
+    count_launch();
+    h->img_valid = 1;
+    h->img_c0 = c0;
+    h->img_c1 = c1;
   }
-  count_launch();
   const int direct = h->T == h->B;
   if (!direct && (e = cudaMemsetAsync(out, 0, sizeof(float) * (size_t)h->B * NOUT, s))) return e;
   const int maxt = (int)((h->T + kTileItems - 1) / kTileItems + h->kg.m2);
@@ -979,14 +1003,21 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
   }
   count_launch();
   if (mode == 1) {
-    const int64_t n = n0 + n1 + n2;
-    int sg = (int)((n + kBlock - 1) / kBlock);
-    if (sg > h->num_sms * 8) sg = h->num_sms * 8;
+    // SGD(+momentum) on all three cores, writing the next step's G1 / G2
+    // images from the updated values
+    const int img_smem = 4 * kImg + 1024;
+    const int ng3 = (int)((n2 + kImgThreads - 1) / kImgThreads);
+    SgdArgs u = {w.f_grad, v0, v1, v2, p2, lr, mu, mask, 1};
     ProfScope _ps(h, s, "f_sgd");
-    if ((e = launch_pdl(k_sgd3, dim3(sg), dim3(kBlock), 0, s, p0, p1, p2, (const float*)w.f_grad, v0, v1, v2, n0, n1,
-                        n2, lr, mu, mask)))
+    if ((e = launch_pdl(k_coreimg, dim3(h->kg.m2 + (h->kg.m1 + 3) / 4 + (ng3 < 64 ? ng3 : 64)), dim3(kImgThreads),
+                        img_smem, s, p0, p1, h->kg, w.f_img, w.f_g1img, u)))
       return e;
     count_launch();
+    h->img_valid = 1;
+    h->img_c0 = p0;
+    h->img_c1 = p1;
+  } else {
+    h->img_valid = 0;  // the caller applies its own update to the cores
   }
   return cudaGetLastError();
 }

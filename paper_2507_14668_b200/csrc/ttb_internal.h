@@ -76,8 +76,10 @@ struct Workspace {
   int2* f_sbi;            // T: (bag, i3) in prefix-sorted order
   int* f_item_start;      // T + 1
   unsigned* f_item_key;   // T
-  int* f_i2_item;         // m2 + 1
-  int* f_tile_start;      // m2 + 1
+  int* f_rk;              // T: rank of each position inside its prefix key
+  int* f_cnt;             // m1 m2: positions per prefix key (self-resetting)
+  int* f_start;           // m1 m2: first prefix-sorted position of each key
+  int4* f_gtot;           // m2: (positions, items, prefixes) per i2 group
   int4* f_tile_info;      // tiles (<= T / 32 + m2): (i2, first item, items)
   float* f_g1img;         // m1 x 512: split G1 rows / transposed images
   float* f_img;           // m2 x 4 x 16 KB: G2 slice images (cb hi/lo, k hi/lo)
@@ -131,6 +133,12 @@ struct ttb_handle {
   int pmap_clean;   // prefix table already reset (by the last backward)
   int bwd_zeroed;   // zero block B is clear for the next backward
   int64_t gen;
+  // the f_img / f_g1img core images describe the cores at img_c0 / img_c1
+  // (written by the last forward or fused update; cleared by
+  // ttb_cores_modified and by a backward that hands gradients to the caller)
+  int img_valid;
+  const float* img_c0;
+  const float* img_c1;
   ttb::Profiler prof;
 };
 

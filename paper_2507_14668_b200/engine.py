@@ -67,6 +67,7 @@ class TtEngine:
         self._unit_grad = torch.zeros((1, 1, 1), dtype=torch.float32, device=self.device) if self.is_d2 else None
         self._handle = None
         self._ws = None
+        self._sig = None
         self.max_T = 0
         self.max_B = 0
         self.plan_id = 0
@@ -139,12 +140,25 @@ class TtEngine:
         # (ttb_export_plan under TTB_OPT_FAST): keep them alive until the next plan
         self._plan_inputs = (indices, offsets)
 
+    def _core_sig(self, cores):
+        return tuple((c.data_ptr(), c._version) for c in cores)
+
+    def _check_cores(self, cores) -> None:
+        """The library caches derived images of the cores (ttb_cores_modified):
+        drop them if any core changed through torch since the library last
+        wrote or read them (torch bumps a tensor's version on every in-place
+        op; the library's own fused update does not)."""
+        if self._sig != self._core_sig(cores):
+            nat.check(self.lib.ttb_cores_modified(self._handle), "cores_modified")
+
     def forward(self, cores, out: torch.Tensor | None = None) -> torch.Tensor:
+        self._check_cores(cores)
         c = self.native_cores(cores)
         if out is None:
             out = torch.empty((self.B, self.N), dtype=torch.float32, device=self.device)
         nat.check(self.lib.ttb_forward(self._handle, _ptr(c[0]), _ptr(c[1]), _ptr(c[2]), _ptr(out), _stream()),
                   "forward")
+        self._sig = self._core_sig(cores)
         return out
 
     def _gout(self, grad_out: torch.Tensor) -> torch.Tensor:
@@ -178,6 +192,7 @@ class TtEngine:
         nat.check(self.lib.ttb_backward_sgd(self._handle, _ptr(c[0]), _ptr(c[1]), _ptr(c[2]), _ptr(gout),
                                             _ptr(v[0]), _ptr(v[1]), _ptr(v[2]), float(lr), float(momentum), mask,
                                             _stream()), "backward_sgd")
+        self._sig = self._core_sig(cores)
 
     def aggregate(self, grad_out: torch.Tensor) -> None:
         nat.check(self.lib.ttb_aggregate(self._handle, _ptr(self._gout(grad_out)), _stream()), "aggregate")

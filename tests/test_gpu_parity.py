@@ -414,3 +414,84 @@ def test_fast_errors_raise():
     with pytest.raises(ValueError):
         out.backward(torch.full_like(out, float("nan")))
         emb.engine.check_errors()
+
+
+def test_fast_fused_sgd_steps_match_oracle():
+    """Several fused-SGD steps on the tensor-core pipeline: each step's update
+    also writes the next forward's core images (no rebuild in between)."""
+    from paper_2507_14668_b200.embedding_bag import TTEmbeddingBag
+    emb = TTEmbeddingBag(10000, 64, (1, 32, 32, 1), tt_m=(20, 20, 25), tt_n=(4, 4, 4), seed=4)
+    emb.enable_fused_sgd(0.05, 0.9)
+    assert emb.engine.fast
+    g = O.Geometry(emb.shape.m, emb.shape.n, emb.shape.ranks)
+    ref = [c.detach().cpu().numpy().astype(np.float32).copy() for c in emb.cores]
+    vel = [None] * 3
+    rng = np.random.default_rng(21)
+    for step in range(4):
+        idx, off = random_batch(rng, 10000, 700, 4, skew=True)
+        out = emb(torch.from_numpy(idx).cuda(), torch.from_numpy(off[:-1]).cuda())
+        c64 = [c.astype(np.float64) for c in ref]
+        assert rel_err(out.detach().cpu().numpy(), O.forward(c64, g, idx, off)) < FWD_TOL, step
+        gout = torch.from_numpy(rng.standard_normal(out.shape).astype(np.float32)).cuda()
+        out.backward(gout)
+        ur, ug = O.unique_aggregate(idx, np.repeat(gout.cpu().numpy().astype(np.float64), np.diff(off), axis=0))
+        want = O.core_grads(c64, g, ur, ug)
+        for k in range(3):
+            vel[k] = O.sgd_step(ref[k], want[k], 0.05, 0.9, vel[k])
+    for k in range(3):
+        assert rel_err(emb.cores[k].detach().cpu().numpy(), ref[k]) < 1e-5, k
+
+
+def test_fast_core_images_follow_core_changes():
+    """Core values changed outside the fused update (torch in-place ops, or
+    ttb_sgd_update after a gradient-returning backward) reach the next
+    forward: the cached core images are dropped."""
+    from paper_2507_14668_b200 import _native as nat
+    from paper_2507_14668_b200.engine import _ptr, _stream
+    g = O.Geometry((20, 20, 25), (4, 4, 4), (1, 32, 32, 1))
+    cores32 = [c.astype(np.float32) for c in O.init_cores(g, 5)]
+    rng = np.random.default_rng(3)
+    idx, off = random_batch(rng, g.rows, 500, 3, skew=False)
+    eng = make_engine(g, idx.size, off.size - 1)
+    assert eng.fast
+    dc = to_dev(cores32)
+    ti, to = torch.from_numpy(idx).cuda(), torch.from_numpy(off).cuda()
+
+    def check():
+        eng.plan(ti, to)
+        out = eng.forward(dc).cpu().numpy()
+        want = O.forward([c.cpu().numpy().astype(np.float64) for c in dc], g, idx, off)
+        assert rel_err(out, want) < FWD_TOL
+
+    check()
+    with torch.no_grad():
+        dc[1].mul_(0.5)  # torch in-place: version bump
+    check()
+    grads = eng.backward(dc, torch.randn(off.size - 1, g.cols, device="cuda"))
+    for c, gr in zip(dc, grads):  # raw-pointer update the version counter does not see
+        nat.check(eng.lib.ttb_sgd_update(_ptr(c), _ptr(gr), None, c.numel(), 0.5, 0.0, _stream()))
+    check()
+
+
+def test_staged_loop_matches_direct():
+    """StagedLoop (side-stream uploads / downloads, double-buffered) returns
+    the same per-step results as running the steps with plain copies."""
+    from paper_2507_14668_b200.embedding_bag import TTEmbeddingBag
+    from paper_2507_14668_b200.staging import StagedLoop, stage_batches
+    rng = np.random.default_rng(8)
+    batches = []
+    for _ in range(3):
+        idx, off = random_batch(rng, 10000, 400, 3, skew=True)
+        batches.append([torch.from_numpy(idx), torch.from_numpy(off[:-1].copy())])
+    emb = TTEmbeddingBag(10000, 64, (1, 32, 32, 1), tt_m=(20, 20, 25), tt_n=(4, 4, 4), seed=1)
+    want = [emb(b[0].cuda(), b[1].cuda()).detach().cpu() for b in batches]
+    # same shapes per step are required by the staging slots: use one batch
+    loop = StagedLoop(stage_batches(batches[:1]), torch.empty(400, 64), "cuda")
+
+    def compute(i, o):
+        out = emb(i, o)
+        return out, None
+
+    loop.run(compute, 4)
+    for k in (2, 3):  # pooled bags sum with fp32 reductions: order not fixed
+        assert rel_err(loop.result(k).numpy(), want[0].numpy()) < FWD_TOL
