@@ -132,6 +132,8 @@ void layout(ttb_handle& h, char* base) {
   w.f_rk = c.take<int>(fz ? T : 0);
   w.f_cnt = c.take<int>(fz ? (size_t)g.m[0] * g.m[1] : 0);
   w.f_start = c.take<int>(fz ? (size_t)g.m[0] * g.m[1] : 0);
+  w.f_rstart = c.take<int>(fz ? (size_t)g.m[0] * g.m[1] : 0);
+  w.f_split = c.take<int>(fz ? (size_t)g.m[0] * g.m[1] : 0);
   w.f_gtot = c.take<int4>(fz ? g.m[1] : 0);
   w.f_tile_info = c.take<int4>(fz ? T / 32 + g.m[1] + 2 : 0);
   w.f_g1img = c.take<float>(fz ? (size_t)g.m[0] * 512 : 0);

@@ -50,11 +50,13 @@ __device__ __forceinline__ void red_f32(float* p, float a) {
 //   0  per index: digits, i2-major prefix key, rank within its key from a
 //      warp-aggregated atomicAdd on the key's counter; per bag: bag ids
 //   A  per i2 group (warp): totals, then the group's exclusive offsets
-//      (positions, work items, tiles) and its key starts / item / tile tables
-//   B  per index: (bag, i3) scattered to start[key] + rank; counters reset
+//      (positions, work items, tiles); the group's items are laid out by
+//      descending length (counting sort by length), with their item / tile
+//      tables and each key's item positions; counters reset
+//   B  per index: (bag, i3) scattered to its item's position + rank
 // Order inside a prefix is arbitrary (summation order of fp32 reductions
 // only); items are runs of <= kItemLen positions of one prefix, tiles runs of
-// <= kTileItems items of one i2.
+// <= kTileItems items of one i2 of similar lengths.
 constexpr int kPlanThreads = 512;
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
@@ -86,10 +88,13 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
                                                         unsigned* __restrict__ key, unsigned* __restrict__ i3o,
                                                         int* __restrict__ rk, int* __restrict__ bag_of,
                                                         int* __restrict__ cnt, int* __restrict__ start,
+                                                        int* __restrict__ rstart, int* __restrict__ split,
                                                         int4* __restrict__ gtot, int* __restrict__ item_start,
                                                         unsigned* __restrict__ item_key, int4* __restrict__ tile_info,
                                                         int2* __restrict__ sbi, int* __restrict__ hdr) {
   pdl_enter();
+  __shared__ int s_hist[kPlanThreads / 32][2 * (kItemLen + 1)];
+  __shared__ int s_poff[kPlanThreads / 32][kItemLen + 1];
   unsigned* bar = reinterpret_cast<unsigned*>(hdr + 12);
   unsigned target = 0;
   const int nthr = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -166,27 +171,64 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
       const int left = mine.y - kTileItems * j;
       tile_info[pt + j] = make_int4((int)i2, pi + kTileItems * j, left < kTileItems ? left : kTileItems, 0);
     }
-    int pos = pc, itm = pi;
+    // items in descending length inside the group: full items (kItemLen
+    // lookups) first, then each key's remainder item by length, so the items
+    // of a tile have similar lengths (balanced epilogue / Z-phase work).
+    // Item i's lookups are [item_start[i], item_start[i + 1]) as before.
+    int* hist = s_hist[threadIdx.x >> 5];  // [L] items of length L, then cursors
+    int* ioff = hist + kItemLen + 1;       // [L] first item (group-relative) of length L
+    for (int L = lane; L <= kItemLen; L += 32) hist[L] = 0;
+    __syncwarp();
     for (unsigned i1b = 0; i1b < g.m1; i1b += 32) {
-      const unsigned i1 = i1b + lane, k = i2 * g.m1 + i1;
-      const int v = i1 < g.m1 ? cnt[k] : 0, ni = (v + kItemLen - 1) / kItemLen;
-      int sv = v, si = ni;
+      const unsigned i1 = i1b + lane;
+      const int v = i1 < g.m1 ? cnt[i2 * g.m1 + i1] : 0;
+      if (v >= kItemLen) atomicAdd(&hist[kItemLen], v / kItemLen);
+      if (v % kItemLen) atomicAdd(&hist[v % kItemLen], 1);
+    }
+    __syncwarp();
+    {  // lane l <-> length L = kItemLen - l (descending); exclusive scans of items and lookups
+      const int L = kItemLen - lane, h = hist[L];
+      int si = h, sp = h * L;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const int a = __shfl_up_sync(0xffffffffu, sv, o), b2 = __shfl_up_sync(0xffffffffu, si, o);
-        if (lane >= o) sv += a, si += b2;
+        const int a2 = __shfl_up_sync(0xffffffffu, si, o), b2 = __shfl_up_sync(0xffffffffu, sp, o);
+        if (lane >= o) si += a2, sp += b2;
       }
-      const int ev = pos + sv - v, ei = itm + si - ni;
-      if (i1 < g.m1) {
-        start[k] = ev;
-        for (int j = 0; j < ni; ++j) {
-          item_start[ei + j] = ev + kItemLen * j;
-          item_key[ei + j] = k;
-        }
-      }
-      pos += __shfl_sync(0xffffffffu, sv, 31);
-      itm += __shfl_sync(0xffffffffu, si, 31);
+      ioff[L] = si - h;
+      hist[L] = si - h;  // cursor
+      hist[0] = 0;
+      // lookup offset of length L's first item, kept in the key loop below via ioff
+      s_poff[threadIdx.x >> 5][L] = sp - h * L;
     }
+    __syncwarp();
+    const int* poff = s_poff[threadIdx.x >> 5];
+    for (unsigned i1b = 0; i1b < g.m1; i1b += 32) {
+      const unsigned i1 = i1b + lane, k = i2 * g.m1 + i1;
+      const int v = i1 < g.m1 ? cnt[k] : 0;
+      if (v > 0) {
+        const int nf = v / kItemLen, r = v % kItemLen;
+        int fp = 0, rp = 0;
+        if (nf) {
+          const int f = atomicAdd(&hist[kItemLen], nf);
+          fp = pc + poff[kItemLen] + (f - ioff[kItemLen]) * kItemLen;
+          for (int j = 0; j < nf; ++j) {
+            item_start[pi + f + j] = fp + kItemLen * j;
+            item_key[pi + f + j] = k;
+          }
+        }
+        if (r) {
+          const int q = atomicAdd(&hist[r], 1);
+          rp = pc + poff[r] + (q - ioff[r]) * r;
+          item_start[pi + q] = rp;
+          item_key[pi + q] = k;
+        }
+        start[k] = fp;                   // lookups with rank < nf * kItemLen: start + rank
+        rstart[k] = rp - nf * kItemLen;  // the rest: rstart + rank
+        split[k] = nf * kItemLen;
+        cnt[k] = 0;                      // counters reset for the next plan
+      }
+    }
+    __syncwarp();
     if (lane == 0) {
       atomicAdd(&hdr[3], mine.z);
       if (i2 == g.m2 - 1) {
@@ -197,9 +239,12 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
     }
   }
   grid_barrier(bar, target);
-  // ---- phase B: scatter (bag, i3) into prefix order; reset the counters
-  for (int t = tid; t < T; t += nthr) sbi[start[key[t]] + rk[t]] = make_int2(bag_of[t], (int)i3o[t]);
-  for (unsigned k = tid; k < g.m1m2; k += nthr) cnt[k] = 0;
+  // ---- phase B: scatter (bag, i3) into item order
+  for (int t = tid; t < T; t += nthr) {
+    const unsigned k = key[t];
+    const int r = rk[t];
+    sbi[(r < split[k] ? start[k] : rstart[k]) + r] = make_int2(bag_of[t], (int)i3o[t]);
+  }
 }
 
 // ------------------------------------------------------------ core images
@@ -265,7 +310,7 @@ __global__ void __launch_bounds__(kImgThreads) k_coreimg(float* __restrict__ G1,
     return;
   }
   extern __shared__ __align__(16) char smem_raw[];
-  char* sm = (char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  char* sm = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);
   const unsigned i2 = blockIdx.x;
   constexpr int kPer = R1 * C / kImgThreads;  // 8
   float vals[kPer];
@@ -409,26 +454,37 @@ __device__ inline void stage_g1_t_async(const TileMeta* m, KGeom g, const float*
 }
 
 // ------------------------------------------------------------ forward
-// Persistent: one 256-thread CTA per SM loops over tiles. G3 stays resident
-// in shared memory; each tile's operands and (bag, i3) list arrive by one
-// round of cp.async. Epilogue thread <-> accumulator row (item, a): the whole
-// X row (128 values) sits in registers; the two warps of a lane quarter take
-// alternate segments.
+// Persistent: one 512-thread CTA per SM loops over a contiguous range of
+// tiles (consecutive tiles mostly share i2: the G2 image is reloaded only when
+// it changes). G3 stays resident in shared memory; each tile's operands and
+// (bag, i3) list arrive by one round of cp.async and one thread issues the
+// 3xTF32 X MMA. Epilogue thread <-> accumulator row (item, a): the four warps
+// of a lane quadrant take every fourth segment of the item, reading the X row
+// from TMEM in two halves of c (64 registers).
 constexpr int kMaxTilePos = kTileItems * kItemLen;  // 1024
 constexpr int kFwdG3Max = 128 * 1024;               // G3 bytes kept in smem
+constexpr int kFwdThreads = 512;
 
 __host__ __device__ constexpr int fwd_smem_bytes() { return 4 * kImg + kFwdG3Max + kMaxTilePos * 8 + 1024; }
 
-__global__ void __launch_bounds__(kThreads, 1) k_fwd(KGeom g, const float* __restrict__ g1img,
-                                                     const float* __restrict__ G3, const float* __restrict__ img,
-                                                     const int* __restrict__ hdr, const int4* __restrict__ tile_info,
-                                                     const int* __restrict__ item_start,
-                                                     const unsigned* __restrict__ item_key,
-                                                     const int2* __restrict__ sbi, float* __restrict__ out,
-                                                     int direct) {
+__global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __restrict__ g1img,
+                                                        const float* __restrict__ G3, const float* __restrict__ img,
+                                                        const int* __restrict__ hdr, const int4* __restrict__ tile_info,
+                                                        const int* __restrict__ item_start,
+                                                        const unsigned* __restrict__ item_key,
+                                                        const int2* __restrict__ sbi, float* __restrict__ out,
+                                                        int direct, int dbg) {
   pdl_enter();
   extern __shared__ __align__(16) char smem_raw[];
-  char* sm = (char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  char* sm = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);
+#define FSTAMP(k)                                                                                     \
+  do {                                                                                                \
+    if ((dbg & 16) && threadIdx.x == 0 && blockIdx.x == 0 && t - tb < 4) {                           \
+      unsigned long long _t;                                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                                          \
+      reinterpret_cast<unsigned long long*>(const_cast<int*>(hdr) + 16)[(k) * 4 + (t - tb)] = _t;     \
+    }                                                                                                 \
+  } while (0)
   char* a_hi = sm;             // G1 rows image
   char* a_lo = sm + kImg;
   char* b_hi = sm + 2 * kImg;  // G2 cb image
@@ -440,74 +496,103 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd(KGeom g, const float* __res
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned m3 = g.m3;
-  const bool g3s = (size_t)32 * m3 * 16 <= (size_t)kFwdG3Max;
   const int ntiles = hdr[4];
+  const int tb = (int)(((long long)ntiles * blockIdx.x) / gridDim.x);
+  const int te = (int)(((long long)ntiles * (blockIdx.x + 1)) / gridDim.x);
   if (warp == 0) umma::tmem_alloc(&s_tmem, 128);
   if (threadIdx.x == 32) umma::mbar_init(&s_mbar, 1);
-  if (g3s) {
-    const int n4 = 32 * (int)m3;
-    for (int e = threadIdx.x; e < n4; e += kThreads) cp_async16(s_g3 + e, reinterpret_cast<const float4*>(G3) + e);
-  }
+  for (int e = threadIdx.x; e < 32 * (int)m3; e += kFwdThreads)  // m3 <= 256 (fast_supported)
+    cp_async16(s_g3 + e, reinterpret_cast<const float4*>(G3) + e);
   int4 pf = make_int4(0, 0, 0, 0);
-  if (warp == 7 && (int)blockIdx.x < ntiles) {
-    fetch_meta_async(tile_info[blockIdx.x], item_start, item_key, &s_m[0]);
-    if ((int)(blockIdx.x + gridDim.x) < ntiles) pf = tile_info[blockIdx.x + gridDim.x];
+  if (warp == 15 && tb < te) {
+    fetch_meta_async(tile_info[tb], item_start, item_key, &s_m[0]);
+    if (tb + 1 < te) pf = tile_info[tb + 1];
   }
   cp_async_wait_all();
   umma::fence_before_sync();
   __syncthreads();
   umma::fence_after_sync();
   const uint32_t tmem = s_tmem;
-  const float4* g3base = g3s ? s_g3 : reinterpret_cast<const float4*>(G3);
+  const int q4 = warp & 3, quarter = warp >> 2;
+  const int row = 32 * q4 + lane, it = row >> 2, a = row & 3;
+  const uint32_t trow = tmem + ((uint32_t)(32 * q4) << 16);
   uint32_t phase = 0;
-  int slot = 0;
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, slot ^= 1) {
+  int slot = 0, last_i2 = -1;
+  for (int t = tb; t < te; ++t, slot ^= 1) {
     const TileMeta* m = &s_m[slot];
+    FSTAMP(0);
+    if (warp == 15 && t + 1 < te) {  // next tile's metadata into the other slot (lands with this tile's operands)
+      fetch_meta_async(pf, item_start, item_key, &s_m[slot ^ 1]);
+      if (t + 2 < te) pf = tile_info[t + 2];
+    }
     const int p0 = m->start[0], np = m->start[m->n] - p0;
-    for (int e = threadIdx.x; e < np; e += kThreads) cp_async8(s_sbi + e, sbi + p0 + e);
-    copy_img_async(b_hi, img + (size_t)m->i2 * (kImg), 2 * kImg);  // cb_hi, cb_lo
-    stage_g1_rows_async(m, g, g1img, a_hi, a_lo);
+    for (int e = threadIdx.x; e < np; e += kFwdThreads) cp_async8(s_sbi + e, sbi + p0 + e);
+    if (m->i2 != last_i2) {  // cb_hi, cb_lo
+      const float* src = img + (size_t)m->i2 * kImg;
+      for (int e = threadIdx.x; e < 2 * kImg / 16; e += kFwdThreads) cp_async16(b_hi + 16 * e, src + 4 * e);
+      last_i2 = m->i2;
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {  // the items' G1 rows (hi, lo)
+      const int e = threadIdx.x + i * kFwdThreads, ia = e >> 3, kq = e & 7, iu = ia >> 2, au = ia & 3;
+      if (iu < m->n) {
+        const float* src = g1img + (size_t)item_i1(m, iu, g) * kG1Img + au * 32 + 4 * kq;
+        const uint32_t o = umma::sw128_off(ia, 4 * kq, 128);
+        cp_async16(a_hi + o, src);
+        cp_async16(a_lo + o, src + 128);
+      }
+    }
     cp_async_wait_all();
     sync_for_mma();
+    FSTAMP(1);
     if (threadIdx.x == 0) {
       constexpr uint32_t id = umma::idesc_tf32(128, 128, false, false);
       mma3_ss(tmem, umma::smem_u32(a_hi), umma::smem_u32(a_lo), 128, umma::smem_u32(b_hi), umma::smem_u32(b_lo),
               128, R1, id);
       umma::commit(&s_mbar);
     }
-    if (warp == 7) {  // next tile's metadata into the other slot
-      const int tn = t + (int)gridDim.x;
-      if (tn < ntiles) {
-        fetch_meta_async(pf, item_start, item_key, &s_m[slot ^ 1]);
-        cp_async_commit();
-        if (tn + (int)gridDim.x < ntiles) pf = tile_info[tn + gridDim.x];
-      }
-    }
     umma::mbar_wait(&s_mbar, phase);
     phase ^= 1u;
     umma::fence_after_sync();
-    // ---- epilogue
-    const int q4 = warp & 3, half = warp >> 2;
-    const int row = 32 * q4 + lane, it = row >> 2, a = row & 3;
-    float x[128];  // x[4 c + b] = X[item][a][b][c]
-#pragma unroll
-    for (int j = 0; j < 4; ++j) umma::tmem_ld32(tmem + ((uint32_t)(32 * q4) << 16) + 32 * j, *(float(*)[32])(x + 32 * j));
-    if (it < m->n) {
-      const int s1 = m->start[it + 1] - p0;
-      int qq = m->start[it] - p0, ord = 0;
+    FSTAMP(2);
+    // ---- epilogue: warp-uniform loop over this thread's segments (tcgen05.ld is collective)
+    const bool live = it < m->n && !(dbg & 512);
+    const int s1 = live ? m->start[it + 1] - p0 : 0;
+    int qq = live ? m->start[it] - p0 : 0, ord = 0;
+    for (;;) {
+      bool have = false;
+      int bag = 0, e = qq;
       while (qq < s1) {
-        const int bag = s_sbi[qq].x;
-        int e = qq + 1;
+        bag = s_sbi[qq].x;
+        e = qq + 1;
         while (e < s1 && s_sbi[e].x == bag) ++e;
-        if ((ord & 1) == half) {
-          float acc[16];
+        if ((ord & 3) == quarter) {
+          have = true;
+          break;
+        }
+        ++ord;
+        qq = e;
+      }
+      if (!__any_sync(0xffffffffu, have)) break;
+      float acc[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+      for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch) {
+        float x[64];  // x[4 c' + b] = X[item][a][b][16 ch + c']
+        if (!(dbg & 64)) {
+          umma::tmem_ld32(trow + 64 * ch, *(float(*)[32])(x));
+          umma::tmem_ld32(trow + 64 * ch + 32, *(float(*)[32])(x + 32));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) x[i] = __uint_as_float((unsigned)(lane + i));
+        }
+        if (have && !(dbg & 32)) {
           for (int l = qq; l < e; ++l) {
-            const float4* g3 = g3base + (unsigned)s_sbi[l].y;
+            const float4* g3 = s_g3 + (unsigned)s_sbi[l].y + 16 * ch * m3;
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              const float4 gv = g3[(size_t)c * m3];
+            for (int c = 0; c < 16; ++c) {
+              const float4 gv = g3[c * m3];
 #pragma unroll
               for (int b = 0; b < 4; ++b) {
                 const float xv = x[4 * c + b];
@@ -518,26 +603,34 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd(KGeom g, const float* __res
               }
             }
           }
-          float* o = out + (size_t)bag * NOUT + a * 16;
-          if (direct) {
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-              reinterpret_cast<float4*>(o)[b] = make_float4(acc[4 * b], acc[4 * b + 1], acc[4 * b + 2], acc[4 * b + 3]);
-          } else {
-#pragma unroll
-            for (int b = 0; b < 4; ++b) red_v4(o + 4 * b, acc[4 * b], acc[4 * b + 1], acc[4 * b + 2], acc[4 * b + 3]);
-          }
         }
+      }
+      if (have && !(dbg & 128)) {
+        float* o = out + (size_t)bag * NOUT + a * 16;
+        if (direct) {
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            reinterpret_cast<float4*>(o)[b] = make_float4(acc[4 * b], acc[4 * b + 1], acc[4 * b + 2], acc[4 * b + 3]);
+        } else {
+#pragma unroll
+          for (int b = 0; b < 4; ++b) red_v4(o + 4 * b, acc[4 * b], acc[4 * b + 1], acc[4 * b + 2], acc[4 * b + 3]);
+        }
+      }
+      if (have) {
         ++ord;
         qq = e;
       }
+      if (dbg & 256) break;
     }
+    FSTAMP(4);
     cp_async_wait_all();  // next tile's metadata
     umma::fence_before_sync();
     __syncthreads();  // TMEM and smem free for the next tile
     umma::fence_after_sync();
+    FSTAMP(3);
   }
   if (warp == 0) umma::tmem_free(tmem, 128);
+#undef FSTAMP
 }
 
 // ------------------------------------------------------------ backward
@@ -559,10 +652,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd(KGeom g, const float* __res
 // per-phase timestamps of block 0's first two tiles into hdr[16..] (TTB_DBG & 8)
 #define TSTAMP(k)                                                                                      \
   do {                                                                                                 \
-    if ((dbg & 8) && threadIdx.x == 0 && blockIdx.x == 0 && t < 2 * (int)gridDim.x) {                  \
+    if ((dbg & 8) && threadIdx.x == 0 && blockIdx.x == 0 && t < 2) {                                   \
       unsigned long long _t;                                                                           \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                                           \
-      reinterpret_cast<unsigned long long*>(hdr + 16)[(t / gridDim.x) * 9 + (k)] = _t;                 \
+      reinterpret_cast<unsigned long long*>(hdr + 16)[t * 9 + (k)] = _t;                               \
     }                                                                                                  \
   } while (0)
 
@@ -625,13 +718,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = hdr[4];
+  // contiguous tile range: consecutive tiles mostly share i2, and the dG2
+  // slice accumulates in TMEM until i2 changes
+  const int tb = (int)(((long long)ntiles * blockIdx.x) / gridDim.x);
+  const int te = (int)(((long long)ntiles * (blockIdx.x + 1)) / gridDim.x);
   const unsigned m3 = g.m3;
   if (warp == 0) umma::tmem_alloc(&s_tmem, 512);
   if (threadIdx.x == 32) umma::mbar_init(&s_mbar, 1);
   int4 pf = make_int4(0, 0, 0, 0);
-  if (warp == 7 && (int)blockIdx.x < ntiles) {
-    fetch_meta_async(tile_info[blockIdx.x], item_start, item_key, &s_m[0]);
-    if ((int)(blockIdx.x + gridDim.x) < ntiles) pf = tile_info[blockIdx.x + gridDim.x];
+  if (warp == 7 && tb < te) {
+    fetch_meta_async(tile_info[tb], item_start, item_key, &s_m[0]);
+    if (tb + 1 < te) pf = tile_info[tb + 1];
   }
   cp_async_wait_all();
   umma::fence_before_sync();
@@ -647,7 +744,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
   const uint64_t d_r2h = umma::desc_sw128(umma::smem_u32(r2_hi)), d_r2l = umma::desc_sw128(umma::smem_u32(r2_lo));
   const uint64_t d_zi = umma::desc_sw128(umma::smem_u32(zi));
   // prologue: the first tile's first chunk and X operands
-  if ((int)blockIdx.x < ntiles) {
+  if (tb < te) {
     const TileMeta* m = &s_m[0];
     if (threadIdx.x == 0) make_chunks(m, s_chunk[0]);
     __syncthreads();
@@ -661,7 +758,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
   }
   uint32_t phase = 0;
   int bad = 0, slot = 0;
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, slot ^= 1) {
+  int prev_i2 = -1;
+  for (int t = tb; t < te; ++t, slot ^= 1) {
     const TileMeta* m = &s_m[slot];
     const int* chunk = s_chunk[slot];
     const int n = m->n, nchunk = chunk[kTileItems + 1];
@@ -682,10 +780,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
       umma::commit(&s_mbar);
     }
     if (warp == 7) {  // next tile's metadata into the other slot
-      const int tn = t + (int)gridDim.x;
-      if (tn < ntiles) {
+      const int tn = t + 1;
+      if (tn < te) {
         fetch_meta_async(pf, item_start, item_key, &s_m[slot ^ 1]);
-        if (tn + (int)gridDim.x < ntiles) pf = tile_info[tn + gridDim.x];
+        if (tn + 1 < te) pf = tile_info[tn + 1];
       }
       cp_async_wait_all();
     }
@@ -785,10 +883,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
     }
     TSTAMP(4);
     // ---- next tile: chunk list and first chunk's positions
-    const int tn = t + (int)gridDim.x;
+    const int tn = t + 1;
     const TileMeta* mn = &s_m[slot ^ 1];
     int npn = 0;
-    if (tn < ntiles) {
+    if (tn < te) {
       if (threadIdx.x == 0) make_chunks(mn, s_chunk[slot ^ 1]);
       __syncthreads();
       npn = mn->start[s_chunk[slot ^ 1][1]] - mn->start[0];
@@ -819,12 +917,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
     sync_for_mma();
     TSTAMP(5);
     constexpr uint32_t id64 = umma::idesc_tf32(128, 64, false, false);
+    const bool acc2 = m->i2 == prev_i2;  // same i2 as the previous tile: keep accumulating dG2 in TMEM
     if (threadIdx.x == 0) {
       // dG2 tile [(c, b), (hi | lo) k] = sum_(item, a) (Z^T hi + Z^T lo) . G1^T (A from TMEM)
 #pragma unroll
       for (int k0 = 0; k0 < 128; k0 += 8) {
         const uint32_t o = (uint32_t)((k0 >> 5) * 64 * 128 + (k0 & 31) * 4) >> 4;
-        umma::mma_tf32_ta(tmem + 384, tmem + 128 + k0, d_r2h + o, id64, k0 > 0 ? 1u : 0u);
+        umma::mma_tf32_ta(tmem + 384, tmem + 128 + k0, d_r2h + o, id64, (acc2 || k0 > 0) ? 1u : 0u);
         umma::mma_tf32_ta(tmem + 384, tmem + 256 + k0, d_r2h + o, id64, 1u);
       }
       // E tile [(item, a), (hi | lo) k] = sum_(c, b) Z . G2^T, pass 1: Z hi
@@ -837,7 +936,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
       umma::commit(&s_mbar);
     }
     // the next tile's first-chunk rows stream in meanwhile
-    if (tn < ntiles) stage_rows_async(npn, st_sbi, gout, G3, m3, st_g, st_g3);
+    if (tn < te) stage_rows_async(npn, st_sbi, gout, G3, m3, st_g, st_g3);
     umma::mbar_wait(&s_mbar, phase);
     phase ^= 1u;
     umma::fence_after_sync();
@@ -864,19 +963,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
     umma::fence_after_sync();
     TSTAMP(7);
     // the next tile's X operands (R12 is free now)
-    if (tn < ntiles) {
+    if (tn < te) {
       copy_img_async(r1_hi, img + (size_t)mn->i2 * kImg, 2 * kImg);
       stage_g1_rows_async(mn, g, g1img, r2_hi, r2_lo);
     }
     if (!(dbg & 4)) {
       float v[16], w2[16];
-      // dG2[k][i2][b][c] = D[:, k] + D[:, 32 + k]
-      umma::tmem_ld16(tl + 384 + 16 * half, v);
-      umma::tmem_ld16(tl + 384 + 32 + 16 * half, w2);
-      float* d2 = dG2 + ((size_t)m->i2 * 4 + b) * 32 + c;
-      const size_t ks = (size_t)g.m2 * C;
+      // dG2[k][i2][b][c] = D[:, k] + D[:, 32 + k], once per run of tiles of one i2
+      if (tn >= te || mn->i2 != m->i2) {
+        umma::tmem_ld16(tl + 384 + 16 * half, v);
+        umma::tmem_ld16(tl + 384 + 32 + 16 * half, w2);
+        float* d2 = dG2 + ((size_t)m->i2 * 4 + b) * 32 + c;
+        const size_t ks = (size_t)g.m2 * C;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) red_f32(d2 + (size_t)(16 * half + i) * ks, v[i] + w2[i]);
+        for (int i = 0; i < 16; ++i) red_f32(d2 + (size_t)(16 * half + i) * ks, v[i] + w2[i]);
+      }
       // dG1[i1][a][k]
       umma::tmem_ld16(tl + 448 + 16 * half, v);
       umma::tmem_ld16(tl + 448 + 32 + 16 * half, w2);
@@ -888,6 +989,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
       }
     }
     TSTAMP(8);
+    prev_i2 = m->i2;
     umma::fence_before_sync();
     __syncthreads();
     umma::fence_after_sync();
@@ -902,7 +1004,8 @@ using namespace fast;
 
 bool fast_supported(const ttb_handle* h) {
   const DynDims& d = h->dims;
-  return d.n1 == 4 && d.n2 == 4 && d.n3 == 4 && d.r1 == 32 && d.r2 == 32;
+  // G3 (32 x m3 x 4 fp32) stays resident in the forward kernel's shared memory
+  return d.n1 == 4 && d.n2 == 4 && d.n3 == 4 && d.r1 == 32 && d.r2 == 32 && h->kg.m3 <= 256;
 }
 
 static cudaError_t ensure_attr(const void* k, int bytes) {
@@ -922,11 +1025,12 @@ cudaError_t fast_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* 
   ProfScope _ps(h, s, "f_plan");
   if (idx64)
     e = launch_pdl(k_fplan<long long>, dim3(grid), dim3(kPlanThreads), 0, s, (const long long*)idx, offsets, T, B,
-                   h->kg, w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_gtot, w.f_item_start,
+                   h->kg, w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_rstart, w.f_split, w.f_gtot, w.f_item_start,
                    w.f_item_key, w.f_tile_info, w.f_sbi, w.fast_hdr);
   else
     e = launch_pdl(k_fplan<int>, dim3(grid), dim3(kPlanThreads), 0, s, (const int*)idx, offsets, T, B, h->kg,
-                   w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_gtot, w.f_item_start, w.f_item_key,
+                   w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_rstart, w.f_split, w.f_gtot, w.f_item_start,
+                   w.f_item_key,
                    w.f_tile_info, w.f_sbi, w.fast_hdr);
   if (e) return e;
   count_launch();
@@ -964,10 +1068,10 @@ cudaError_t fast_forward(ttb_handle* h, const float* c0, const float* c1, const 
   const int grid = maxt < h->num_sms ? maxt : h->num_sms;
   {
     ProfScope _ps(h, s, "f_fwd");
-    if ((e = launch_pdl(k_fwd, dim3(grid), dim3(kThreads), fwd_smem_bytes(), s, h->kg, (const float*)w.f_g1img, c2,
+    if ((e = launch_pdl(k_fwd, dim3(grid), dim3(kFwdThreads), fwd_smem_bytes(), s, h->kg, (const float*)w.f_g1img, c2,
                         (const float*)w.f_img, (const int*)w.fast_hdr, (const int4*)w.f_tile_info,
                         (const int*)w.f_item_start, (const unsigned*)w.f_item_key, (const int2*)w.f_sbi, out,
-                        direct)))
+                        direct, getenv("TTB_DBG") ? atoi(getenv("TTB_DBG")) : 0)))
       return e;
   }
   count_launch();

@@ -56,6 +56,11 @@ class StagedLoop:
         d2h = self.d2h_stream if overlap else cur
         ev_in = [torch.cuda.Event() for _ in range(D)]
         ev_free: list = [None] * D
+        ev_out = [torch.cuda.Event() for _ in range(D)]
+        # each result stays referenced until the compute stream has waited for
+        # its download (instead of record_stream, whose deferred frees make the
+        # caching allocator fall back to fresh cudaMallocs under this pattern)
+        hold: list = [None] * D
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize(self.device)
         start.record(cur)
@@ -79,6 +84,9 @@ class StagedLoop:
             if not overlap:
                 upload(k)
             cur.wait_event(ev_in[s])
+            if hold[s] is not None:
+                cur.wait_event(ev_out[s])
+                hold[s] = None
             result, finish = compute(*self.dev_in[s])
             ev = torch.cuda.Event()
             ev.record(cur)
@@ -86,8 +94,8 @@ class StagedLoop:
             with torch.cuda.stream(d2h):
                 self.host_out[s].copy_(result.detach(), non_blocking=True)
             self.out_ready[s].record(d2h)
-            if overlap:
-                result.record_stream(d2h)
+            ev_out[s].record(d2h)
+            hold[s] = result
             if finish is not None:
                 finish()
             fr = torch.cuda.Event()
