@@ -21,7 +21,7 @@ def launches(path):
             per[r[ii]] = (r[ki].split("(")[0].replace("void ", "").strip(), float(r[vi].replace(",", "")))
     items = list(per.values())
     # one step = the launches between consecutive plan_mark kernels; use the last full step
-    starts = [k for k, (n, _) in enumerate(items) if "k_plan_mark" in n]
+    starts = [k for k, (n, _) in enumerate(items) if "k_plan_mark" in n or "k_fplan" in n]
     step = items[starts[-2]:starts[-1]] if len(starts) >= 2 else items
     tot = sum(t for _, t in step)
     agg = defaultdict(lambda: [0.0, 0])
@@ -85,7 +85,9 @@ def traffic(path):
     res = {}
     for r in data:
         name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "").split("<")[0].strip()
-        key = name.replace("k_", "", 1)
+        base = name.split("::")[-1]
+        fast = {"k_fplan": "f_plan", "k_fwd": "f_fwd", "k_bwd": "f_bwd", "k_coreimg": "f_sgd"}
+        key = fast[base] if "fast::" in name and base in fast else base.replace("k_", "", 1)
         tot = 0.0
         for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             j = hdr.index(m)
