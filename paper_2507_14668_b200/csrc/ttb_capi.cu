@@ -134,6 +134,7 @@ void layout(ttb_handle& h, char* base) {
   w.f_start = c.take<int>(fz ? (size_t)g.m[0] * g.m[1] : 0);
   w.f_rstart = c.take<int>(fz ? (size_t)g.m[0] * g.m[1] : 0);
   w.f_split = c.take<int>(fz ? (size_t)g.m[0] * g.m[1] : 0);
+  w.f_cta = c.take<int>(fz ? 1025 : 0);
   w.f_gtot = c.take<int4>(fz ? g.m[1] : 0);
   w.f_tile_info = c.take<int4>(fz ? T / 32 + g.m[1] + 2 : 0);
   w.f_g1img = c.take<float>(fz ? (size_t)g.m[0] * 512 : 0);
@@ -210,7 +211,7 @@ ttb_handle* ttb_create(const ttb_geom* g, int64_t max_T, int64_t max_B, void* wo
   {
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
-      h->num_sms = sms;
+      h->num_sms = sms > 1024 ? 1024 : sms;
     else
       h->num_sms = 148;
   }

@@ -58,6 +58,7 @@ __device__ __forceinline__ void red_f32(float* p, float a) {
 // only); items are runs of <= kItemLen positions of one prefix, tiles runs of
 // <= kTileItems items of one i2 of similar lengths.
 constexpr int kPlanThreads = 512;
+constexpr int kTileCost = 32;  // per-tile fixed cost in lookup units (CTA range balancing)
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -90,6 +91,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
                                                         int* __restrict__ cnt, int* __restrict__ start,
                                                         int* __restrict__ rstart, int* __restrict__ split,
                                                         int4* __restrict__ gtot, int* __restrict__ item_start,
+                                                        int* __restrict__ cta_tiles, int ctas,
                                                         unsigned* __restrict__ item_key, int4* __restrict__ tile_info,
                                                         int2* __restrict__ sbi, int* __restrict__ hdr) {
   pdl_enter();
@@ -167,10 +169,6 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
     pt = warp_sum(pt);
     const int4 mine = gtot[i2];
     const int ntile = (mine.y + kTileItems - 1) / kTileItems;
-    for (int j = lane; j < ntile; j += 32) {
-      const int left = mine.y - kTileItems * j;
-      tile_info[pt + j] = make_int4((int)i2, pi + kTileItems * j, left < kTileItems ? left : kTileItems, 0);
-    }
     // items in descending length inside the group: full items (kItemLen
     // lookups) first, then each key's remainder item by length, so the items
     // of a tile have similar lengths (balanced epilogue / Z-phase work).
@@ -205,23 +203,33 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
     for (unsigned i1b = 0; i1b < g.m1; i1b += 32) {
       const unsigned i1 = i1b + lane, k = i2 * g.m1 + i1;
       const int v = i1 < g.m1 ? cnt[k] : 0;
+      const int nf = v / kItemLen, r = v % kItemLen;
+      int f = 0, fp = 0, rp = 0;
+      if (nf) {
+        f = atomicAdd(&hist[kItemLen], nf);
+        fp = pc + poff[kItemLen] + (f - ioff[kItemLen]) * kItemLen;
+      }
+      // full items: the whole warp writes each key's run (hot keys own
+      // thousands of items — one lane alone would serialise on them)
+      unsigned many = __ballot_sync(0xffffffffu, nf > 0);
+      while (many) {
+        const int src = __ffs(many) - 1;
+        many &= many - 1;
+        const int sf = __shfl_sync(0xffffffffu, f, src), sfp = __shfl_sync(0xffffffffu, fp, src);
+        const int snf = __shfl_sync(0xffffffffu, nf, src);
+        const unsigned sk = __shfl_sync(0xffffffffu, k, src);
+        for (int j = lane; j < snf; j += 32) {
+          item_start[pi + sf + j] = sfp + kItemLen * j;
+          item_key[pi + sf + j] = sk;
+        }
+      }
+      if (r) {
+        const int q = atomicAdd(&hist[r], 1);
+        rp = pc + poff[r] + (q - ioff[r]) * r;
+        item_start[pi + q] = rp;
+        item_key[pi + q] = k;
+      }
       if (v > 0) {
-        const int nf = v / kItemLen, r = v % kItemLen;
-        int fp = 0, rp = 0;
-        if (nf) {
-          const int f = atomicAdd(&hist[kItemLen], nf);
-          fp = pc + poff[kItemLen] + (f - ioff[kItemLen]) * kItemLen;
-          for (int j = 0; j < nf; ++j) {
-            item_start[pi + f + j] = fp + kItemLen * j;
-            item_key[pi + f + j] = k;
-          }
-        }
-        if (r) {
-          const int q = atomicAdd(&hist[r], 1);
-          rp = pc + poff[r] + (q - ioff[r]) * r;
-          item_start[pi + q] = rp;
-          item_key[pi + q] = k;
-        }
         start[k] = fp;                   // lookups with rank < nf * kItemLen: start + rank
         rstart[k] = rp - nf * kItemLen;  // the rest: rstart + rank
         split[k] = nf * kItemLen;
@@ -229,6 +237,12 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
       }
     }
     __syncwarp();
+    // tiles: (i2, first item, items, first lookup position)
+    for (int j = lane; j < ntile; j += 32) {
+      const int left = mine.y - kTileItems * j;
+      tile_info[pt + j] = make_int4((int)i2, pi + kTileItems * j, left < kTileItems ? left : kTileItems,
+                                    item_start[pi + kTileItems * j]);
+    }
     if (lane == 0) {
       atomicAdd(&hdr[3], mine.z);
       if (i2 == g.m2 - 1) {
@@ -239,6 +253,22 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
     }
   }
   grid_barrier(bar, target);
+  // ---- phase B: per-CTA tile ranges for the step kernels (grid = ctas):
+  // contiguous tile runs of equal weight (lookups + kTileCost per tile)
+  {
+    const int nt = hdr[4];
+    const long long wtot = (long long)T + (long long)kTileCost * nt;
+    for (int b = tid; b <= ctas; b += nthr) {
+      const long long target = wtot * b / ctas;
+      int lo = 0, hi = nt;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((long long)tile_info[mid].w + (long long)kTileCost * mid < target) lo = mid + 1;
+        else hi = mid;
+      }
+      cta_tiles[b] = lo;
+    }
+  }
   // ---- phase B: scatter (bag, i3) into item order
   for (int t = tid; t < T; t += nthr) {
     const unsigned k = key[t];
@@ -473,7 +503,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
                                                         const int* __restrict__ item_start,
                                                         const unsigned* __restrict__ item_key,
                                                         const int2* __restrict__ sbi, float* __restrict__ out,
-                                                        int direct, int dbg) {
+                                                        const int* __restrict__ cta_tiles, int direct, int dbg) {
   pdl_enter();
   extern __shared__ __align__(16) char smem_raw[];
   char* sm = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -497,8 +527,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned m3 = g.m3;
   const int ntiles = hdr[4];
-  const int tb = (int)(((long long)ntiles * blockIdx.x) / gridDim.x);
-  const int te = (int)(((long long)ntiles * (blockIdx.x + 1)) / gridDim.x);
+  const int tb = cta_tiles[blockIdx.x], te = cta_tiles[blockIdx.x + 1];  // weight-balanced (k_fplan)
+  (void)ntiles;
   if (warp == 0) umma::tmem_alloc(&s_tmem, 128);
   if (threadIdx.x == 32) umma::mbar_init(&s_mbar, 1);
   for (int e = threadIdx.x; e < 32 * (int)m3; e += kFwdThreads)  // m3 <= 256 (fast_supported)
@@ -699,7 +729,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
                                                      const unsigned* __restrict__ item_key,
                                                      const int2* __restrict__ sbi, const float* __restrict__ gout,
                                                      float* __restrict__ dG1, float* __restrict__ dG2,
-                                                     float* __restrict__ dG3, int* __restrict__ hdr, int dbg) {
+                                                     float* __restrict__ dG3, int* __restrict__ hdr,
+                                                     const int* __restrict__ cta_tiles, int dbg) {
   pdl_enter();
   extern __shared__ __align__(16) char smem_raw[];
   char* sm = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -720,8 +751,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
   const int ntiles = hdr[4];
   // contiguous tile range: consecutive tiles mostly share i2, and the dG2
   // slice accumulates in TMEM until i2 changes
-  const int tb = (int)(((long long)ntiles * blockIdx.x) / gridDim.x);
-  const int te = (int)(((long long)ntiles * (blockIdx.x + 1)) / gridDim.x);
+  const int tb = cta_tiles[blockIdx.x], te = cta_tiles[blockIdx.x + 1];  // weight-balanced (k_fplan)
+  (void)ntiles;
   const unsigned m3 = g.m3;
   if (warp == 0) umma::tmem_alloc(&s_tmem, 512);
   if (threadIdx.x == 32) umma::mbar_init(&s_mbar, 1);
@@ -1025,11 +1056,11 @@ cudaError_t fast_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* 
   ProfScope _ps(h, s, "f_plan");
   if (idx64)
     e = launch_pdl(k_fplan<long long>, dim3(grid), dim3(kPlanThreads), 0, s, (const long long*)idx, offsets, T, B,
-                   h->kg, w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_rstart, w.f_split, w.f_gtot, w.f_item_start,
+                   h->kg, w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_rstart, w.f_split, w.f_gtot, w.f_item_start, w.f_cta, h->num_sms,
                    w.f_item_key, w.f_tile_info, w.f_sbi, w.fast_hdr);
   else
     e = launch_pdl(k_fplan<int>, dim3(grid), dim3(kPlanThreads), 0, s, (const int*)idx, offsets, T, B, h->kg,
-                   w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_rstart, w.f_split, w.f_gtot, w.f_item_start,
+                   w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_rstart, w.f_split, w.f_gtot, w.f_item_start, w.f_cta, h->num_sms,
                    w.f_item_key,
                    w.f_tile_info, w.f_sbi, w.fast_hdr);
   if (e) return e;
@@ -1064,14 +1095,13 @@ cudaError_t fast_forward(ttb_handle* h, const float* c0, const float* c1, const 
   }
   const int direct = h->T == h->B;
   if (!direct && (e = cudaMemsetAsync(out, 0, sizeof(float) * (size_t)h->B * NOUT, s))) return e;
-  const int maxt = (int)((h->T + kTileItems - 1) / kTileItems + h->kg.m2);
-  const int grid = maxt < h->num_sms ? maxt : h->num_sms;
+  const int grid = h->num_sms;  // = the plan's CTA ranges (k_fplan cta_tiles)
   {
     ProfScope _ps(h, s, "f_fwd");
     if ((e = launch_pdl(k_fwd, dim3(grid), dim3(kFwdThreads), fwd_smem_bytes(), s, h->kg, (const float*)w.f_g1img, c2,
                         (const float*)w.f_img, (const int*)w.fast_hdr, (const int4*)w.f_tile_info,
                         (const int*)w.f_item_start, (const unsigned*)w.f_item_key, (const int2*)w.f_sbi, out,
-                        direct, getenv("TTB_DBG") ? atoi(getenv("TTB_DBG")) : 0)))
+                        (const int*)w.f_cta, direct, getenv("TTB_DBG") ? atoi(getenv("TTB_DBG")) : 0)))
       return e;
   }
   count_launch();
@@ -1095,14 +1125,13 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
     if ((e = cudaMemsetAsync(g1, 0, sizeof(float) * (size_t)n1, s))) return e;
     if ((e = cudaMemsetAsync(g2, 0, sizeof(float) * (size_t)n2, s))) return e;
   }
-  const int maxt = (int)((h->T + kTileItems - 1) / kTileItems + h->kg.m2);
-  const int grid = maxt < h->num_sms ? maxt : h->num_sms;
+  const int grid = h->num_sms;  // = the plan's CTA ranges (k_fplan cta_tiles)
   {
     ProfScope _ps(h, s, "f_bwd");
     if ((e = launch_pdl(k_bwd, dim3(grid), dim3(kThreads), kBwdSmem, s, h->kg, (const float*)w.f_g1img, c2,
                         (const float*)w.f_img, (const int4*)w.f_tile_info, (const int*)w.f_item_start,
                         (const unsigned*)w.f_item_key, (const int2*)w.f_sbi, gout, g0, g1, g2, w.fast_hdr,
-                        getenv("TTB_DBG") ? atoi(getenv("TTB_DBG")) : 0)))
+                        (const int*)w.f_cta, getenv("TTB_DBG") ? atoi(getenv("TTB_DBG")) : 0)))
       return e;
   }
   count_launch();

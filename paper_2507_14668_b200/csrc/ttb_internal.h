@@ -81,6 +81,7 @@ struct Workspace {
   int* f_start;           // m1 m2: position of each key's first full item
   int* f_rstart;          // m1 m2: position of its remainder item, minus the full items' lookups
   int* f_split;           // m1 m2: lookups of the key in full items
+  int* f_cta;             // kMaxCtas + 1: first tile of each step-kernel CTA
   int4* f_gtot;           // m2: (positions, items, prefixes) per i2 group
   int4* f_tile_info;      // tiles (<= T / 32 + m2): (i2, first item, items)
   float* f_g1img;         // m1 x 512: split G1 rows / transposed images
