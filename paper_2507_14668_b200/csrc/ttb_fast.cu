@@ -93,8 +93,17 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
                                                         int4* __restrict__ gtot, int* __restrict__ item_start,
                                                         int* __restrict__ cta_tiles, int ctas,
                                                         unsigned* __restrict__ item_key, int4* __restrict__ tile_info,
-                                                        int2* __restrict__ sbi, int* __restrict__ hdr) {
+                                                        int2* __restrict__ sbi, int* __restrict__ hdr, int dbg) {
   pdl_enter();
+#define PSTAMP(i)                                                                                          \
+  do {                                                                                                     \
+    if (dbg && threadIdx.x == 0 && blockIdx.x == 0) {                                                      \
+      unsigned long long _t;                                                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                                               \
+      reinterpret_cast<unsigned long long*>(hdr + 16)[i] = _t;                                             \
+    }                                                                                                      \
+  } while (0)
+  PSTAMP(0);
   __shared__ int s_hist[kPlanThreads / 32][2 * (kItemLen + 1)];
   __shared__ int s_poff[kPlanThreads / 32][kItemLen + 1];
   unsigned* bar = reinterpret_cast<unsigned*>(hdr + 12);
@@ -139,6 +148,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
   if (bits) atomicOr(&hdr[0], bits);
   if (multi) hdr[1] = 1;
   grid_barrier(bar, target);
+  PSTAMP(1);
   // ---- phase A1: per-i2 totals (positions, items, present prefixes)
   const int gw = tid >> 5, nw = nthr >> 5;
   for (unsigned i2 = gw; i2 < g.m2; i2 += nw) {
@@ -155,6 +165,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
     if (lane == 0) gtot[i2] = make_int4(c, it, p, 0);
   }
   grid_barrier(bar, target);
+  PSTAMP(2);
   // ---- phase A2: group offsets, key starts, item and tile tables
   for (unsigned i2 = gw; i2 < g.m2; i2 += nw) {
     int pc = 0, pi = 0, pt = 0;
@@ -253,6 +264,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
     }
   }
   grid_barrier(bar, target);
+  PSTAMP(3);
   // ---- phase B: per-CTA tile ranges for the step kernels (grid = ctas):
   // contiguous tile runs of equal weight (lookups + kTileCost per tile)
   {
@@ -275,6 +287,9 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
     const int r = rk[t];
     sbi[(r < split[k] ? start[k] : rstart[k]) + r] = make_int2(bag_of[t], (int)i3o[t]);
   }
+  __syncthreads();
+  PSTAMP(4);
+#undef PSTAMP
 }
 
 // ------------------------------------------------------------ core images
@@ -1057,12 +1072,12 @@ cudaError_t fast_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* 
   if (idx64)
     e = launch_pdl(k_fplan<long long>, dim3(grid), dim3(kPlanThreads), 0, s, (const long long*)idx, offsets, T, B,
                    h->kg, w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_rstart, w.f_split, w.f_gtot, w.f_item_start, w.f_cta, h->num_sms,
-                   w.f_item_key, w.f_tile_info, w.f_sbi, w.fast_hdr);
+                   w.f_item_key, w.f_tile_info, w.f_sbi, w.fast_hdr, getenv("TTB_DBG") ? 1 : 0);
   else
     e = launch_pdl(k_fplan<int>, dim3(grid), dim3(kPlanThreads), 0, s, (const int*)idx, offsets, T, B, h->kg,
                    w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_rstart, w.f_split, w.f_gtot, w.f_item_start, w.f_cta, h->num_sms,
                    w.f_item_key,
-                   w.f_tile_info, w.f_sbi, w.fast_hdr);
+                   w.f_tile_info, w.f_sbi, w.fast_hdr, getenv("TTB_DBG") ? 1 : 0);
   if (e) return e;
   count_launch();
   return cudaGetLastError();
