@@ -87,7 +87,7 @@ def traffic(path):
         name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "").split("<")[0].strip()
         base = name.split("::")[-1]
         fast = {"k_fplan": "f_plan", "k_fwd": "f_fwd", "k_bwd": "f_bwd", "k_coreimg": "f_sgd"}
-        key = fast[base] if "fast::" in name and base in fast else base.replace("k_", "", 1)
+        key = fast[base] if base in fast else base.replace("k_", "", 1)
         tot = 0.0
         for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             j = hdr.index(m)
