@@ -76,9 +76,14 @@ class ModelConfig:
 def feature_interaction(vectors: Sequence[torch.Tensor]) -> torch.Tensor:
     """concat(vectors[0], all pairwise dots), pairs (0,1), (0,2), .., (1,2).."""
     stack = torch.stack(list(vectors), dim=1)  # (B, v, D)
+    v = stack.shape[1]
     gram = torch.bmm(stack, stack.transpose(1, 2))
-    iu = torch.triu_indices(stack.shape[1], stack.shape[1], offset=1, device=stack.device)
-    return torch.cat([vectors[0], gram[:, iu[0], iu[1]]], dim=1)
+    iu = torch.triu_indices(v, v, offset=1, device=stack.device)
+    # one flat column gather: its backward is an index_add along dim 1
+    # (two-tensor advanced indexing would backpropagate through the much
+    # slower sort-based index_put_ kernel)
+    pairs = gram.reshape(gram.shape[0], v * v).index_select(1, iu[0] * v + iu[1])
+    return torch.cat([vectors[0], pairs], dim=1)
 
 
 class Mlp(nn.Module):
@@ -106,6 +111,33 @@ class Mlp(nn.Module):
         return x
 
 
+class _DenseBagSum(torch.autograd.Function):
+    """Sum-pooled lookup of a small dense table: forward gathers rows and
+    index_adds them into their bags, backward index_adds the bag gradients
+    into the touched rows (atomic adds: torch's embedding_bag backward sorts
+    the indices first, which dominated the DLRM step for 11 small fields)."""
+
+    @staticmethod
+    def forward(ctx, rows, indices, bag_of, n_bags):
+        gathered = rows.index_select(0, indices)
+        if bag_of is None:
+            out = gathered
+        else:
+            out = torch.zeros((n_bags, rows.shape[1]), dtype=rows.dtype, device=rows.device)
+            out.index_add_(0, bag_of, gathered)
+        ctx.save_for_backward(indices, bag_of)
+        ctx.n_rows = rows.shape[0]
+        return out
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        indices, bag_of = ctx.saved_tensors
+        g = grad_out if bag_of is None else grad_out.index_select(0, bag_of)
+        grad = torch.zeros((ctx.n_rows, grad_out.shape[1]), dtype=grad_out.dtype, device=grad_out.device)
+        grad.index_add_(0, indices, g.contiguous())
+        return grad, None, None, None
+
+
 class DenseField(nn.Module):
     """Small field below tt_threshold: plain (rows, dim) table, sum pooling."""
 
@@ -120,7 +152,14 @@ class DenseField(nn.Module):
         if self.check_errors and indices.numel() and (
                 int(indices.min()) < 0 or int(indices.max()) >= self.rows.shape[0]):
             raise ValueError(f"index outside [0, {self.rows.shape[0]})")
-        return torch.nn.functional.embedding_bag(indices, self.rows, offsets[:-1], mode="sum")
+        n_bags = offsets.numel() - 1
+        if indices.numel() == n_bags:  # one index per bag (offsets must then be 0..B)
+            bag_of = None
+        else:
+            sizes = offsets[1:] - offsets[:-1]
+            bag_of = torch.repeat_interleave(torch.arange(n_bags, device=indices.device), sizes,
+                                             output_size=indices.numel())
+        return _DenseBagSum.apply(self.rows, indices, bag_of, n_bags)
 
 
 class DlrmModel(nn.Module):
