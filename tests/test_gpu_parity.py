@@ -495,3 +495,73 @@ def test_staged_loop_matches_direct():
     loop.run(compute, 4)
     for k in (2, 3):  # pooled bags sum with fp32 reductions: order not fixed
         assert rel_err(loop.result(k).numpy(), want[0].numpy()) < FWD_TOL
+
+
+def test_fast_config3_shape_vs_deterministic():
+    """Config-3-shaped batch (10M x 64, ranks 32, Zipf(1.05), pooling 20) on
+    the tensor-core pipeline — hot prefixes with thousands of lookups (full
+    work items, warp-cooperative item writes, length-sorted tiles, weighted
+    CTA ranges) — against the deterministic pipeline (parity-pinned on the
+    oracle), native and permuted ids; a sample of bags against the oracle."""
+    from bench_extras import zipf
+    from paper_2507_14668_b200.embedding_bag import TTEmbeddingBag
+    B, pool = 16384, 20
+    emb = TTEmbeddingBag(10_000_000, 64, (1, 32, 32, 1), seed=0, max_indices=B * pool, max_bags=B)
+    assert emb.engine.fast
+    g = O.Geometry(emb.shape.m, emb.shape.n, emb.shape.ranks)
+    cores = [c.detach() for c in emb.cores]
+    c64 = [c.cpu().numpy().astype(np.float64) for c in cores]
+    det = make_engine(g, B * pool, B, deterministic=True)
+    for permuted in (False, True):
+        rng = np.random.default_rng(4 + permuted)
+        idx = zipf(10_000_000, B * pool, rng)
+        if permuted:
+            idx = np.random.default_rng(123).permutation(10_000_000)[idx]
+        off = np.arange(0, B * pool + 1, pool, dtype=np.int64)
+        gout = (rng.standard_normal((B, 64)) / B).astype(np.float32)
+        ti, to, tg = torch.from_numpy(idx).cuda(), torch.from_numpy(off).cuda(), torch.from_numpy(gout).cuda()
+        emb.engine.plan(ti, to)
+        out = emb.engine.forward(cores)
+        grads = [x.clone() for x in emb.engine.backward(cores, tg)]
+        det.plan(ti, to)
+        want = det.forward(cores)
+        gd = det.backward(cores, tg)
+        assert rel_err(out.cpu().numpy(), want.cpu().numpy()) < FWD_TOL
+        for k in range(3):
+            assert rel_err(grads[k].cpu().numpy(), gd[k].cpu().numpy()) < GRAD_TOL, (permuted, k)
+        bags = np.random.default_rng(9).choice(B, 64, replace=False)
+        ref = np.stack([O.reconstruct_rows(c64, g, idx[off[b]:off[b + 1]]).sum(0) for b in bags])
+        assert rel_err(out.cpu().numpy()[bags], ref) < FWD_TOL
+
+
+def test_fast_int32_indices_and_last_offset():
+    """int32 indices and include_last_offset=True through the module on the
+    tensor-core pipeline, against the oracle."""
+    from paper_2507_14668_b200.embedding_bag import TTEmbeddingBag
+    emb = TTEmbeddingBag(10000, 64, (1, 32, 32, 1), tt_m=(20, 20, 25), tt_n=(4, 4, 4), seed=6,
+                         include_last_offset=True)
+    assert emb.engine.fast
+    g = O.Geometry(emb.shape.m, emb.shape.n, emb.shape.ranks)
+    rng = np.random.default_rng(12)
+    idx, off = random_batch(rng, 10000, 900, 5, skew=True)
+    out = emb(torch.from_numpy(idx.astype(np.int32)).cuda(), torch.from_numpy(off).cuda())
+    c64 = [c.detach().cpu().numpy().astype(np.float64) for c in emb.cores]
+    assert rel_err(out.detach().cpu().numpy(), O.forward(c64, g, idx, off)) < FWD_TOL
+
+
+def test_large_m3_runs_deterministic_pipeline():
+    """m3 > 256 (G3 no longer fits the forward kernel's shared memory): the
+    engine selects the deterministic pipeline, which matches the oracle."""
+    g = O.Geometry((8, 8, 300), (4, 4, 4), (1, 32, 32, 1))
+    cores32 = [c.astype(np.float32) for c in O.init_cores(g, 3)]
+    rng = np.random.default_rng(2)
+    idx, off = random_batch(rng, g.rows, 400, 3, skew=False)
+    gout = rng.standard_normal((400, g.cols)).astype(np.float32)
+    res = run_case(g, cores32, idx, off, gout)
+    assert not res["eng"].fast
+    c64 = [c.astype(np.float64) for c in cores32]
+    assert rel_err(res["out"], O.forward(c64, g, idx, off)) < FWD_TOL
+    ur, ug = O.unique_aggregate(idx, np.repeat(gout.astype(np.float64), np.diff(off), axis=0))
+    want = O.core_grads(c64, g, ur, ug)
+    for k in range(3):
+        assert rel_err(res["grads"][k], want[k]) < GRAD_TOL, k
