@@ -717,6 +717,11 @@ __device__ inline void make_chunks(const TileMeta* m, int* ch) {
   int nc = 0, it = 0;
   const int n = m->n;
   ch[0] = 0;
+  if (m->start[n] - m->start[0] <= kChunkPos) {  // the common case: one chunk
+    ch[1] = n;
+    ch[kTileItems + 1] = 1;
+    return;
+  }
   while (it < n) {
     const int base = m->start[it];
     while (it < n && m->start[it + 1] - base <= kChunkPos) ++it;
@@ -928,17 +933,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
       __syncthreads();  // staging reused by the next chunk / tile
     }
     TSTAMP(4);
-    // ---- next tile: chunk list and first chunk's positions
     const int tn = t + 1;
     const TileMeta* mn = &s_m[slot ^ 1];
     int npn = 0;
-    if (tn < te) {
-      if (threadIdx.x == 0) make_chunks(mn, s_chunk[slot ^ 1]);
-      __syncthreads();
-      npn = mn->start[s_chunk[slot ^ 1][1]] - mn->start[0];
-      if (threadIdx.x < npn) cp_async8(st_sbi + threadIdx.x, sbi + mn->start[0] + threadIdx.x);
-      cp_async_commit();
-    }
     // ---- Z^T into TMEM (hi / lo) and the Z image (hi) for the E GEMM
     float zr[64];
 #pragma unroll
@@ -954,24 +951,36 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
       umma::tmem_st4(tl + 128 + 64 * half + i, h[0], h[1], h[2], h[3]);
       umma::tmem_st4(tl + 256 + 64 * half + i, l[0], l[1], l[2], l[3]);
     }
-    __syncthreads();  // every slot read before the image overwrites them
-#pragma unroll
-    for (int i = 0; i < 64; ++i)
-      *(float*)(zi + umma::sw128_off(64 * half + i, row, 128)) = umma::tf32_rna(zr[i]);
     umma::tmem_wait_st();
-    cp_async_wait_all();  // G2 k / G1^T images, next tile's positions
-    sync_for_mma();
-    TSTAMP(5);
+    cp_async_wait_all();  // G2 k / G1^T images (issued before the Z phase)
+    sync_for_mma();       // every slot read before the image overwrites them; Z^T is in TMEM
     constexpr uint32_t id64 = umma::idesc_tf32(128, 64, false, false);
     const bool acc2 = m->i2 == prev_i2;  // same i2 as the previous tile: keep accumulating dG2 in TMEM
     if (threadIdx.x == 0) {
-      // dG2 tile [(c, b), (hi | lo) k] = sum_(item, a) (Z^T hi + Z^T lo) . G1^T (A from TMEM)
+      // dG2 tile [(c, b), (hi | lo) k] = sum_(item, a) (Z^T hi + Z^T lo) . G1^T (A from TMEM);
+      // issued before the Z image is written (only the E GEMM reads it)
 #pragma unroll
       for (int k0 = 0; k0 < 128; k0 += 8) {
         const uint32_t o = (uint32_t)((k0 >> 5) * 64 * 128 + (k0 & 31) * 4) >> 4;
         umma::mma_tf32_ta(tmem + 384, tmem + 128 + k0, d_r2h + o, id64, (acc2 || k0 > 0) ? 1u : 0u);
         umma::mma_tf32_ta(tmem + 384, tmem + 256 + k0, d_r2h + o, id64, 1u);
       }
+    }
+    // ---- next tile: chunk list and first chunk's positions
+    if (tn < te) {
+      if (threadIdx.x == 0) make_chunks(mn, s_chunk[slot ^ 1]);
+      __syncthreads();
+      npn = mn->start[s_chunk[slot ^ 1][1]] - mn->start[0];
+      if (threadIdx.x < npn) cp_async8(st_sbi + threadIdx.x, sbi + mn->start[0] + threadIdx.x);
+      cp_async_commit();
+    }
+#pragma unroll
+    for (int i = 0; i < 64; ++i)
+      *(float*)(zi + umma::sw128_off(64 * half + i, row, 128)) = umma::tf32_rna(zr[i]);
+    cp_async_wait_all();  // next tile's positions
+    sync_for_mma();
+    TSTAMP(5);
+    if (threadIdx.x == 0) {
       // E tile [(item, a), (hi | lo) k] = sum_(c, b) Z . G2^T, pass 1: Z hi
 #pragma unroll
       for (int k0 = 0; k0 < 128; k0 += 8) {
