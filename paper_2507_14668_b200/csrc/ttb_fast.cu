@@ -510,7 +510,7 @@ constexpr int kMaxTilePos = kTileItems * kItemLen;  // 1024
 constexpr int kFwdG3Max = 128 * 1024;               // G3 bytes kept in smem
 constexpr int kFwdThreads = 512;
 
-__host__ __device__ constexpr int fwd_smem_bytes() { return 4 * kImg + kFwdG3Max + kMaxTilePos * 8 + 1024; }
+__host__ __device__ constexpr int fwd_smem_bytes() { return 4 * kImg + kFwdG3Max + 2 * kMaxTilePos * 8 + 1024; }
 
 __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __restrict__ g1img,
                                                         const float* __restrict__ G3, const float* __restrict__ img,
@@ -535,8 +535,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
   char* b_hi = sm + 2 * kImg;  // G2 cb image
   char* b_lo = sm + 3 * kImg;
   float4* s_g3 = reinterpret_cast<float4*>(sm + 4 * kImg);
-  int2* s_sbi = reinterpret_cast<int2*>(sm + 4 * kImg + kFwdG3Max);
-  __shared__ TileMeta s_m[2];
+  int2* s_sbi2 = reinterpret_cast<int2*>(sm + 4 * kImg + kFwdG3Max);  // two (bag, i3) stages
+  __shared__ TileMeta s_m[3];
   __shared__ uint64_t s_mbar;
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -558,48 +558,63 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
   __syncthreads();
   umma::fence_after_sync();
   const uint32_t tmem = s_tmem;
-  const int q4 = warp & 3, quarter = warp >> 2;
-  const int row = 32 * q4 + lane, it = row >> 2, a = row & 3;
-  const uint32_t trow = tmem + ((uint32_t)(32 * q4) << 16);
-  uint32_t phase = 0;
-  int slot = 0, last_i2 = -1;
-  for (int t = tb; t < te; ++t, slot ^= 1) {
-    const TileMeta* m = &s_m[slot];
-    FSTAMP(0);
-    if (warp == 15 && t + 1 < te) {  // next tile's metadata into the other slot (lands with this tile's operands)
-      fetch_meta_async(pf, item_start, item_key, &s_m[slot ^ 1]);
-      if (t + 2 < te) pf = tile_info[t + 2];
-    }
-    const int p0 = m->start[0], np = m->start[m->n] - p0;
-    for (int e = threadIdx.x; e < np; e += kFwdThreads) cp_async8(s_sbi + e, sbi + p0 + e);
-    if (m->i2 != last_i2) {  // cb_hi, cb_lo
-      const float* src = img + (size_t)m->i2 * kImg;
+  int last_i2 = -1;
+  // all threads: tile u's (bag, i3) list and X operands (cp.async), and the
+  // metadata of tile u+1 (warp 15)
+  auto stage = [&](int u) {
+    const TileMeta* mu = &s_m[(u - tb) % 3];
+    const int q0 = mu->start[0], nq = mu->start[mu->n] - q0;
+    int2* st = s_sbi2 + ((u - tb) & 1) * kMaxTilePos;
+    for (int e = threadIdx.x; e < nq; e += kFwdThreads) cp_async8(st + e, sbi + q0 + e);
+    if (mu->i2 != last_i2) {  // cb_hi, cb_lo
+      const float* src = img + (size_t)mu->i2 * kImg;
       for (int e = threadIdx.x; e < 2 * kImg / 16; e += kFwdThreads) cp_async16(b_hi + 16 * e, src + 4 * e);
-      last_i2 = m->i2;
+      last_i2 = mu->i2;
     }
 #pragma unroll
     for (int i = 0; i < 2; ++i) {  // the items' G1 rows (hi, lo)
       const int e = threadIdx.x + i * kFwdThreads, ia = e >> 3, kq = e & 7, iu = ia >> 2, au = ia & 3;
-      if (iu < m->n) {
-        const float* src = g1img + (size_t)item_i1(m, iu, g) * kG1Img + au * 32 + 4 * kq;
+      if (iu < mu->n) {
+        const float* src = g1img + (size_t)item_i1(mu, iu, g) * kG1Img + au * 32 + 4 * kq;
         const uint32_t o = umma::sw128_off(ia, 4 * kq, 128);
         cp_async16(a_hi + o, src);
         cp_async16(a_lo + o, src + 128);
       }
     }
-    cp_async_wait_all();
-    sync_for_mma();
-    FSTAMP(1);
+    if (warp == 15 && u + 1 < te) {
+      fetch_meta_async(pf, item_start, item_key, &s_m[(u + 1 - tb) % 3]);
+      if (u + 2 < te) pf = tile_info[u + 2];
+    }
+  };
+  auto issue_mma = [&]() {
     if (threadIdx.x == 0) {
       constexpr uint32_t id = umma::idesc_tf32(128, 128, false, false);
       mma3_ss(tmem, umma::smem_u32(a_hi), umma::smem_u32(a_lo), 128, umma::smem_u32(b_hi), umma::smem_u32(b_lo),
               128, R1, id);
       umma::commit(&s_mbar);
     }
-    umma::mbar_wait(&s_mbar, phase);
+  };
+  if (tb < te) {
+    stage(tb);
+    cp_async_wait_all();
+    sync_for_mma();
+    issue_mma();
+  }
+  const int q4 = warp & 3, quarter = warp >> 2;
+  const int row = 32 * q4 + lane, it = row >> 2, a = row & 3;
+  const uint32_t trow = tmem + ((uint32_t)(32 * q4) << 16);
+  uint32_t phase = 0;
+  for (int t = tb; t < te; ++t) {
+    const TileMeta* m = &s_m[(t - tb) % 3];
+    const int2* s_sbi = s_sbi2 + ((t - tb) & 1) * kMaxTilePos;
+    FSTAMP(0);
+    umma::mbar_wait(&s_mbar, phase);  // X of tile t; its operands are free again
     phase ^= 1u;
     umma::fence_after_sync();
+    FSTAMP(1);
+    if (t + 1 < te) stage(t + 1);  // lands while this tile is closed
     FSTAMP(2);
+    const int p0 = m->start[0];
     // ---- epilogue: warp-uniform loop over this thread's segments (tcgen05.ld is collective)
     const bool live = it < m->n && !(dbg & 512);
     const int s1 = live ? m->start[it + 1] - p0 : 0;
@@ -668,10 +683,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
       if (dbg & 256) break;
     }
     FSTAMP(4);
-    cp_async_wait_all();  // next tile's metadata
-    umma::fence_before_sync();
-    __syncthreads();  // TMEM and smem free for the next tile
-    umma::fence_after_sync();
+    FSTAMP(4);
+    cp_async_wait_all();  // the next tile's operands, list and metadata
+    sync_for_mma();       // TMEM read by every epilogue thread; operands visible to the tensor core
+    if (t + 1 < te) issue_mma();
     FSTAMP(3);
   }
   if (warp == 0) umma::tmem_free(tmem, 128);
