@@ -58,7 +58,8 @@ __device__ __forceinline__ void red_f32(float* p, float a) {
 // only); items are runs of <= kItemLen positions of one prefix, tiles runs of
 // <= kTileItems items of one i2 of similar lengths.
 constexpr int kPlanThreads = 512;
-constexpr int kTileCost = 32;  // per-tile fixed cost in lookup units (CTA range balancing)
+constexpr int kTileCost = 32;
+constexpr int kA2Regs = 8;     // per-lane registers caching an i2 group's prefix counters (m1 <= 256)  // per-tile fixed cost in lookup units (CTA range balancing)
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -187,12 +188,24 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
     int* hist = s_hist[threadIdx.x >> 5];  // [L] items of length L, then cursors
     int* ioff = hist + kItemLen + 1;       // [L] first item (group-relative) of length L
     for (int L = lane; L <= kItemLen; L += 32) hist[L] = 0;
+    // the group's counters: the first 32 kA2Regs in registers (one round of
+    // loads for both passes), the rest re-read
+    int cv[kA2Regs];
+#pragma unroll
+    for (int r = 0; r < kA2Regs; ++r) {
+      const unsigned i1 = 32 * r + lane;
+      cv[r] = i1 < g.m1 ? cnt[i2 * g.m1 + i1] : 0;
+    }
     __syncwarp();
-    for (unsigned i1b = 0; i1b < g.m1; i1b += 32) {
-      const unsigned i1 = i1b + lane;
-      const int v = i1 < g.m1 ? cnt[i2 * g.m1 + i1] : 0;
+    auto pass1 = [&](int v) {
       if (v >= kItemLen) atomicAdd(&hist[kItemLen], v / kItemLen);
       if (v % kItemLen) atomicAdd(&hist[v % kItemLen], 1);
+    };
+#pragma unroll
+    for (int r = 0; r < kA2Regs; ++r) pass1(cv[r]);
+    for (unsigned i1b = 32 * kA2Regs; i1b < g.m1; i1b += 32) {
+      const unsigned i1 = i1b + lane;
+      pass1(i1 < g.m1 ? cnt[i2 * g.m1 + i1] : 0);
     }
     __syncwarp();
     {  // lane l <-> length L = kItemLen - l (descending); exclusive scans of items and lookups
@@ -211,9 +224,8 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
     }
     __syncwarp();
     const int* poff = s_poff[threadIdx.x >> 5];
-    for (unsigned i1b = 0; i1b < g.m1; i1b += 32) {
-      const unsigned i1 = i1b + lane, k = i2 * g.m1 + i1;
-      const int v = i1 < g.m1 ? cnt[k] : 0;
+    auto pass2 = [&](unsigned i1, int v) {
+      const unsigned k = i2 * g.m1 + i1;
       const int nf = v / kItemLen, r = v % kItemLen;
       int f = 0, fp = 0, rp = 0;
       if (nf) {
@@ -246,6 +258,12 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
         split[k] = nf * kItemLen;
         cnt[k] = 0;                      // counters reset for the next plan
       }
+    };
+#pragma unroll
+    for (int r = 0; r < kA2Regs; ++r) pass2(32 * r + lane, cv[r]);  // (zero counts past m1 are no-ops)
+    for (unsigned i1b = 32 * kA2Regs; i1b < g.m1; i1b += 32) {
+      const unsigned i1 = i1b + lane;
+      pass2(i1, i1 < g.m1 ? cnt[i2 * g.m1 + i1] : 0);
     }
     __syncwarp();
     // tiles: (i2, first item, items, first lookup position)
