@@ -876,15 +876,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
     phase ^= 1u;
     umma::fence_after_sync();
     TSTAMP(2);
-    // X^T -> item slots (this half's 64 columns)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      float v[32];
-      umma::tmem_ld32(tl + 64 * half + 32 * j, v);
+    // X^T -> item slots (this half's 64 columns, both loads in flight together)
+    {
+      uint32_t v0[32], v1[32];
+      umma::tmem_ld32_nw(tl + 64 * half, v0);
+      umma::tmem_ld32_nw(tl + 64 * half + 32, v1);
+      umma::tmem_wait_ld();
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        const int col = 64 * half + 32 * j + i;
-        xs[xs_idx(col >> 2, col & 3, b, c)] = v[i];
+        const int col = 64 * half + i;
+        xs[xs_idx(col >> 2, col & 3, b, c)] = __uint_as_float(v0[i]);
+        xs[xs_idx((col + 32) >> 2, (col + 32) & 3, b, c)] = __uint_as_float(v1[i]);
       }
     }
     umma::fence_before_sync();
@@ -977,12 +979,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
       zr[i] = xs[xs_idx(ia >> 2, ia & 3, b, c)];
     }
 #pragma unroll
-    for (int i = 0; i < 64; i += 4) {
-      float h[4], l[4];
+    for (int hh = 0; hh < 2; ++hh) {
+      float h[32], l[32];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) umma::split3(zr[i + u], h[u], l[u]);
-      umma::tmem_st4(tl + 128 + 64 * half + i, h[0], h[1], h[2], h[3]);
-      umma::tmem_st4(tl + 256 + 64 * half + i, l[0], l[1], l[2], l[3]);
+      for (int u = 0; u < 32; ++u) umma::split3(zr[32 * hh + u], h[u], l[u]);
+      umma::tmem_st32(tl + 128 + 64 * half + 32 * hh, h);
+      umma::tmem_st32(tl + 256 + 64 * half + 32 * hh, l);
     }
     umma::tmem_wait_st();
     cp_async_wait_all();  // G2 k / G1^T images (issued before the Z phase)
