@@ -391,15 +391,31 @@ __global__ void __launch_bounds__(kImgThreads) k_coreimg(float* __restrict__ G1,
       G2[j] = vals[r];
     }
   }
+  // the slice in shared memory first (row k padded to 129 floats), then each
+  // image row written by one warp — 32 consecutive K of one 128-byte row, no
+  // bank conflicts (a direct scatter from the load layout is 16-way)
+  float* raw = reinterpret_cast<float*>(sm + 4 * kImg);
 #pragma unroll
   for (int r = 0; r < kPer; ++r) {
-    const int e = threadIdx.x + r * kImgThreads, k = e >> 7, b = (e >> 5) & 3, c = e & 31;
+    const int e = threadIdx.x + r * kImgThreads;
+    raw[(e >> 7) * 129 + (e & 127)] = vals[r];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int r = 0; r < 128 / (kImgThreads / 32); ++r) {  // cb images: row cb = 4 c + b, K = k = lane
+    const int cb = warp + r * (kImgThreads / 32), b = cb & 3, c = cb >> 2;
     float hi, lo;
-    umma::split3(vals[r], hi, lo);
-    const int cb = 4 * c + b;
-    const uint32_t o1 = umma::sw128_off(cb, k, 128);
+    umma::split3(raw[lane * 129 + b * 32 + c], hi, lo);
+    const uint32_t o1 = umma::sw128_off(cb, lane, 128);
     *(float*)(sm + o1) = hi;
     *(float*)(sm + kImg + o1) = lo;
+  }
+#pragma unroll
+  for (int r = 0; r < 128 / (kImgThreads / 32); ++r) {  // k images: row k, K = cb (block of 32)
+    const int unit = warp + r * (kImgThreads / 32), k = unit >> 2, cb = 32 * (unit & 3) + lane;
+    float hi, lo;
+    umma::split3(raw[k * 129 + (cb & 3) * 32 + (cb >> 2)], hi, lo);
     *(float*)(sm + 2 * kImg + umma::sw128_off(k, cb, 64)) = hi;
     *(float*)(sm + 2 * kImg + umma::sw128_off(32 + k, cb, 64)) = lo;
   }
@@ -1131,7 +1147,7 @@ cudaError_t fast_forward(ttb_handle* h, const float* c0, const float* c1, const 
                          cudaStream_t s) {
   Workspace& w = h->w;
   cudaError_t e;
-  const int img_smem = 4 * kImg + 1024;
+  const int img_smem = 4 * kImg + 32 * 129 * 4 + 1024;
   static bool attr = false;
   if (!attr) {
     if ((e = ensure_attr((const void*)k_coreimg, img_smem))) return e;
@@ -1197,7 +1213,7 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
   if (mode == 1) {
     // SGD(+momentum) on all three cores, writing the next step's G1 / G2
     // images from the updated values
-    const int img_smem = 4 * kImg + 1024;
+    const int img_smem = 4 * kImg + 32 * 129 * 4 + 1024;
     const int ng3 = (int)((n2 + kImgThreads - 1) / kImgThreads);
     SgdArgs u = {w.f_grad, v0, v1, v2, p2, lr, mu, mask, 1};
     ProfScope _ps(h, s, "f_sgd");
