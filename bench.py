@@ -151,11 +151,12 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("TTB_DIST_BACKEND", "nccl")  # gloo: several ranks on one GPU (tests)
+        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
     lib = nat.load()
     cfg = CFG2
     emb = TTEmbeddingBag(cfg["rows"], cfg["dim"], cfg["ranks"], seed=0, max_indices=cfg["batch"] * cfg["pooling"],
@@ -174,16 +175,22 @@ def run_ours(args):
     out = torch.empty((cfg["batch"], cfg["dim"]), dtype=torch.float32, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
-    def step():
+    def local_step():
         eng.plan(idx, off)
         eng.forward(cores, out=out)
         if world == 1:
             eng.backward_sgd(cores, gout, LR, MU, vel)
         else:
             eng.backward(cores, gout, grads=grads)
-            dp.allreduce_grads(flat_g)  # NCCL SUM over ranks: the DP exchange step
-            nat.check(lib.ttb_sgd_update(_ptr(flat_p), _ptr(flat_g), _ptr(flat_v), flat_p.numel(), LR, MU,
-                                         _stream()))
+
+    def dp_tail():  # the DP exchange step: NCCL SUM of the core gradients, then the same update on every rank
+        dp.allreduce_grads(flat_g)
+        nat.check(lib.ttb_sgd_update(_ptr(flat_p), _ptr(flat_g), _ptr(flat_v), flat_p.numel(), LR, MU, _stream()))
+
+    def step():
+        local_step()
+        if world > 1:
+            dp_tail()
 
     for _ in range(max(args.warmup, 3) if not args.quick else args.warmup):
         step()
@@ -193,22 +200,28 @@ def run_ours(args):
     step()
     torch.cuda.synchronize()
     launches_per_step = nat.launch_count() - l0
-    eager_step = step
-    use_graph = not args.no_graph and world == 1
+    eager_local = local_step
+    use_graph = not args.no_graph
     if use_graph:
-        # the whole step (plan + forward + backward + update: ~25 kernels and a
-        # few memsets) as one CUDA graph: no host round trips between kernels
+        # the rank-local step (plan + forward + backward [+ fused update]) as
+        # one CUDA graph: no host round trips between kernels; with N > 1 the
+        # collective and the update follow it eagerly
         graph = torch.cuda.CUDAGraph()
         s_cap = torch.cuda.Stream()
         s_cap.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s_cap):
-            step()
+            local_step()
             torch.cuda.synchronize()
             with torch.cuda.graph(graph, stream=s_cap):
-                step()
+                local_step()
         torch.cuda.current_stream().wait_stream(s_cap)
         torch.cuda.synchronize()
-        step = graph.replay
+        if world > 1:
+            def step():
+                graph.replay()
+                dp_tail()
+        else:
+            step = graph.replay
         for _ in range(3):
             step()
         torch.cuda.synchronize()
@@ -249,17 +262,21 @@ def run_ours(args):
             "batch_per_gpu": cfg["batch"], "pooling": cfg["pooling"],
             "parallelism": f"dp{world}" + (" (NCCL all-reduce of core grads)" if world > 1 else ""),
             "l2": "flushed between timed steps (512 MiB write, outside the timed events)",
-            "launch": "one CUDA graph per step" if use_graph else "eager launches",
+            "launch": ("one CUDA graph per step" + (" + NCCL all-reduce and update" if world > 1 else ""))
+                      if use_graph else "eager launches",
         },
         "counts": host_counts(idx_h, off_h, shape, st),
         "pipeline": "tensor-core (TTB_OPT_FAST)" if eng.fast else "deterministic",
         "gpu_launches": int(launches_per_step * args.steps),
         "clocks": clk,
     }
+    if rank == 0 and not args.quick:  # rank-local work only (no collectives)
+        result.update(profile_and_roofline(args, torch, eng, lib, emb, eager_local, flush, st, dev))
+    if not args.quick and not args.no_e2e:  # every rank (the DP update all-reduces)
+        e2e = e2e_run(args, torch, cfg, rank, dev, world)
+        if rank == 0:
+            result["e2e"] = e2e
     if rank == 0 and not args.quick:
-        result.update(profile_and_roofline(args, torch, eng, lib, emb, eager_step, flush, st, dev))
-        if not args.no_e2e:
-            result["e2e"] = e2e_run(args, torch, cfg, rank, dev, world)
         if world == 1 and not args.no_cpu_baseline:
             result["cpu_baseline"] = cpu_baseline(args, cfg)
         if world == 1 and not args.no_extras:
@@ -363,11 +380,22 @@ def e2e_run(args, torch, cfg, rank, dev, world):
     streams, double-buffered (paper_2507_14668_b200.staging): step k+1's
     inputs upload and step k's output drains while step k / k+1 compute, the
     way a production input pipeline prefetches. `serial_ms_per_step` is the
-    same loop with every copy on the compute stream, for comparison."""
+    same loop with every copy on the compute stream, for comparison. With
+    N > 1 every rank runs the loop on its own batch and the backward's core
+    gradients are all-reduced before the update (data parallel); the time is
+    the max over ranks."""
+    import torch.distributed as dist
+    from paper_2507_14668_b200 import _native as nat
     from paper_2507_14668_b200.embedding_bag import TTEmbeddingBag
+    from paper_2507_14668_b200.engine import _ptr, _stream
     from paper_2507_14668_b200.staging import StagedLoop
     emb = TTEmbeddingBag(cfg["rows"], cfg["dim"], cfg["ranks"], seed=0, max_indices=cfg["batch"] * cfg["pooling"],
-                         max_bags=cfg["batch"], device=dev, check_errors=False).enable_fused_sgd(LR, MU)
+                         max_bags=cfg["batch"], device=dev, check_errors=False)
+    if world == 1:
+        emb.enable_fused_sgd(LR, MU)
+    else:
+        lib = nat.load()
+        vel = [torch.zeros(c.shape, dtype=torch.float64, device=dev) for c in emb.cores]
     idx_h, off_h, gout_h = synthetic_batch(rank, cfg)
     host_in = [torch.from_numpy(idx_h).pin_memory(),
                torch.from_numpy(off_h[:-1].copy()).pin_memory(),  # nn.EmbeddingBag-style B offsets
@@ -376,19 +404,39 @@ def e2e_run(args, torch, cfg, rank, dev, world):
 
     def compute(idx_d, off_d, gout_d):
         out = emb(idx_d, off_d)
-        return out, (lambda: out.backward(gout_d))
+        if world == 1:
+            return out, (lambda: out.backward(gout_d))
+
+        def finish():
+            out.backward(gout_d)
+            flat = torch.cat([c.grad.reshape(-1) for c in emb.cores])
+            dist.all_reduce(flat)
+            with torch.no_grad():
+                for c, g, v in zip(emb.cores, torch.split(flat, [c.numel() for c in emb.cores]), vel):
+                    nat.check(lib.ttb_sgd_update(_ptr(c), _ptr(g), _ptr(v), c.numel(), LR, MU, _stream()))
+                    c.grad = None
+        return out, finish
 
     loop = StagedLoop(host_in, host_out, dev)
     steps = max(10, args.steps)
     loop.run(compute, 3)
+    if world > 1:
+        dist.barrier()
     ms = loop.run(compute, steps)
+    if world > 1:
+        dist.barrier()
     ms_serial = loop.run(compute, steps, overlap=False)
+    if world > 1:
+        t = torch.tensor([ms, ms_serial], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, ms_serial = float(t[0]), float(t[1])
     emb.engine.check_errors()
     return {"value": world * cfg["batch"] * cfg["pooling"] / (ms / 1e3), "unit": "lookups/s", "ms_per_step": ms,
             "h2d_bytes_per_step": loop.h2d_bytes, "d2h_bytes_per_step": loop.d2h_bytes,
             "serial_ms_per_step": ms_serial,
-            "path": "TTEmbeddingBag.forward + autograd backward (fused SGD); pinned host inputs in and pooled "
-                    "output out every step on side copy streams (double-buffered, overlapping compute)"}
+            "path": "TTEmbeddingBag.forward + autograd backward (" + ("fused SGD" if world == 1 else
+                    "core grads all-reduced, then SGD") + "); pinned host inputs in and pooled output out every "
+                    "step on side copy streams (double-buffered, overlapping compute)"}
 
 
 # ------------------------------------------------------------------ CPU legs (oracle port)
