@@ -541,10 +541,13 @@ __device__ inline void stage_g1_t_async(const TileMeta* m, KGeom g, const float*
 // of a lane quadrant take every fourth segment of the item, reading the X row
 // from TMEM in two halves of c (64 registers).
 constexpr int kMaxTilePos = kTileItems * kItemLen;  // 1024
-constexpr int kFwdG3Max = 128 * 1024;               // G3 bytes kept in smem
+constexpr int kFwdMaxM3 = 288;                       // G3 (32 x m3 x 4 fp32) kept in smem
+constexpr int kFwdG3Max = 32 * kFwdMaxM3 * 16;
 constexpr int kFwdThreads = 512;
 
-__host__ __device__ constexpr int fwd_smem_bytes() { return 4 * kImg + kFwdG3Max + 2 * kMaxTilePos * 8 + 1024; }
+// G3 region sized by the table's m3 (the (bag, i3) stages follow it)
+__host__ __device__ constexpr int fwd_g3_bytes(unsigned m3) { return (int)(32 * m3 * 16 + 1023) & ~1023; }
+__host__ __device__ constexpr int fwd_smem_bytes(unsigned m3) { return 4 * kImg + fwd_g3_bytes(m3) + 2 * kMaxTilePos * 8 + 1024; }
 
 __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __restrict__ g1img,
                                                         const float* __restrict__ G3, const float* __restrict__ img,
@@ -569,7 +572,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
   char* b_hi = sm + 2 * kImg;  // G2 cb image
   char* b_lo = sm + 3 * kImg;
   float4* s_g3 = reinterpret_cast<float4*>(sm + 4 * kImg);
-  int2* s_sbi2 = reinterpret_cast<int2*>(sm + 4 * kImg + kFwdG3Max);  // two (bag, i3) stages
+  int2* s_sbi2 = reinterpret_cast<int2*>(sm + 4 * kImg + fwd_g3_bytes(g.m3));  // two (bag, i3) stages
   __shared__ TileMeta s_m[3];
   __shared__ uint64_t s_mbar;
   __shared__ uint32_t s_tmem;
@@ -580,7 +583,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
   (void)ntiles;
   if (warp == 0) umma::tmem_alloc(&s_tmem, 128);
   if (threadIdx.x == 32) umma::mbar_init(&s_mbar, 1);
-  for (int e = threadIdx.x; e < 32 * (int)m3; e += kFwdThreads)  // m3 <= 256 (fast_supported)
+  for (int e = threadIdx.x; e < 32 * (int)m3; e += kFwdThreads)  // m3 <= kFwdMaxM3 (fast_supported)
     cp_async16(s_g3 + e, reinterpret_cast<const float4*>(G3) + e);
   int4 pf = make_int4(0, 0, 0, 0);
   if (warp == 15 && tb < te) {
@@ -1111,7 +1114,7 @@ using namespace fast;
 bool fast_supported(const ttb_handle* h) {
   const DynDims& d = h->dims;
   // G3 (32 x m3 x 4 fp32) stays resident in the forward kernel's shared memory
-  return d.n1 == 4 && d.n2 == 4 && d.n3 == 4 && d.r1 == 32 && d.r2 == 32 && h->kg.m3 <= 256;
+  return d.n1 == 4 && d.n2 == 4 && d.n3 == 4 && d.r1 == 32 && d.r2 == 32 && h->kg.m3 <= (unsigned)kFwdMaxM3;
 }
 
 static cudaError_t ensure_attr(const void* k, int bytes) {
@@ -1151,7 +1154,7 @@ cudaError_t fast_forward(ttb_handle* h, const float* c0, const float* c1, const 
   static bool attr = false;
   if (!attr) {
     if ((e = ensure_attr((const void*)k_coreimg, img_smem))) return e;
-    if ((e = ensure_attr((const void*)k_fwd, fwd_smem_bytes()))) return e;
+    if ((e = ensure_attr((const void*)k_fwd, fwd_smem_bytes(kFwdMaxM3)))) return e;
     if ((e = ensure_attr((const void*)k_bwd, kBwdSmem))) return e;
     attr = true;
   }
@@ -1173,7 +1176,7 @@ cudaError_t fast_forward(ttb_handle* h, const float* c0, const float* c1, const 
   const int grid = h->num_sms;  // = the plan's CTA ranges (k_fplan cta_tiles)
   {
     ProfScope _ps(h, s, "f_fwd");
-    if ((e = launch_pdl(k_fwd, dim3(grid), dim3(kFwdThreads), fwd_smem_bytes(), s, h->kg, (const float*)w.f_g1img, c2,
+    if ((e = launch_pdl(k_fwd, dim3(grid), dim3(kFwdThreads), fwd_smem_bytes(h->kg.m3), s, h->kg, (const float*)w.f_g1img, c2,
                         (const float*)w.f_img, (const int*)w.fast_hdr, (const int4*)w.f_tile_info,
                         (const int*)w.f_item_start, (const unsigned*)w.f_item_key, (const int2*)w.f_sbi, out,
                         (const int*)w.f_cta, direct, getenv("TTB_DBG") ? atoi(getenv("TTB_DBG")) : 0)))

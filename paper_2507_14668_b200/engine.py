@@ -237,7 +237,7 @@ class TtEngine:
     def fast(self) -> bool:
         """The tensor-core pipeline runs (geometry n = (4, 4, 4), ranks 32)."""
         return (not self.deterministic and not self.is_d2 and tuple(self.shape.n) == (4, 4, 4)
-                and tuple(self.shape.ranks) == (1, 32, 32, 1) and self.shape.m[2] <= 256)
+                and tuple(self.shape.ranks) == (1, 32, 32, 1) and self.shape.m[2] <= 288)
 
     def export_plan(self) -> dict:
         st = self.status()

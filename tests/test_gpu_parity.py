@@ -534,6 +534,36 @@ def test_fast_config3_shape_vs_deterministic():
         assert rel_err(out.cpu().numpy()[bags], ref) < FWD_TOL
 
 
+def test_fast_m3_261_kaggle_field():
+    """The Criteo-Kaggle 10,131,227-row field factorises to m = (171, 227, 261):
+    G3 (133.6 KB) still fits the forward's shared memory -> tensor-core
+    pipeline; outputs and gradients vs the deterministic pipeline and a
+    sample vs the oracle."""
+    from paper_2507_14668_b200.embedding_bag import TTEmbeddingBag
+    emb = TTEmbeddingBag(10_131_227, 64, (1, 32, 32, 1), seed=1, max_indices=8192)
+    assert tuple(emb.shape.m) == (171, 227, 261) and emb.engine.fast
+    g = O.Geometry(emb.shape.m, emb.shape.n, emb.shape.ranks)
+    rng = np.random.default_rng(14)
+    idx = rng.integers(0, 10_131_227, 8192)
+    off = np.arange(8193, dtype=np.int64)
+    gout = rng.standard_normal((8192, 64)).astype(np.float32)
+    cores = [c.detach() for c in emb.cores]
+    ti, to, tg = torch.from_numpy(idx).cuda(), torch.from_numpy(off).cuda(), torch.from_numpy(gout).cuda()
+    emb.engine.plan(ti, to)
+    out = emb.engine.forward(cores)
+    grads = [x.clone() for x in emb.engine.backward(cores, tg)]
+    det = make_engine(g, 8192, 8192, deterministic=True)
+    det.plan(ti, to)
+    want = det.forward(cores)
+    gd = det.backward(cores, tg)
+    assert rel_err(out.cpu().numpy(), want.cpu().numpy()) < FWD_TOL
+    for k in range(3):
+        assert rel_err(grads[k].cpu().numpy(), gd[k].cpu().numpy()) < GRAD_TOL, k
+    c64 = [c.cpu().numpy().astype(np.float64) for c in cores]
+    sample = rng.choice(8192, 256, replace=False)
+    assert rel_err(out.cpu().numpy()[sample], O.reconstruct_rows(c64, g, idx[sample])) < FWD_TOL
+
+
 def test_fast_int32_indices_and_last_offset():
     """int32 indices and include_last_offset=True through the module on the
     tensor-core pipeline, against the oracle."""
@@ -550,7 +580,7 @@ def test_fast_int32_indices_and_last_offset():
 
 
 def test_large_m3_runs_deterministic_pipeline():
-    """m3 > 256 (G3 no longer fits the forward kernel's shared memory): the
+    """m3 > 288 (G3 no longer fits the forward kernel's shared memory): the
     engine selects the deterministic pipeline, which matches the oracle."""
     g = O.Geometry((8, 8, 300), (4, 4, 4), (1, 32, 32, 1))
     cores32 = [c.astype(np.float32) for c in O.init_cores(g, 3)]
