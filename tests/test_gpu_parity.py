@@ -595,3 +595,22 @@ def test_large_m3_runs_deterministic_pipeline():
     want = O.core_grads(c64, g, ur, ug)
     for k in range(3):
         assert rel_err(res["grads"][k], want[k]) < GRAD_TOL, k
+
+
+@pytest.mark.parametrize("m,B,max_bag", [((300, 7, 25), 700, 3), ((20, 20, 25), 1, 1), ((20, 20, 25), 3, 2)])
+def test_fast_edge_geometries(m, B, max_bag):
+    """Tensor-core pipeline edge cases: m1 > 256 (the plan's per-group counters
+    no longer fit its register cache), a single lookup, a three-bag batch."""
+    g = O.Geometry(m, (4, 4, 4), (1, 32, 32, 1))
+    cores32 = [c.astype(np.float32) for c in O.init_cores(g, 8)]
+    rng = np.random.default_rng(B)
+    idx, off = random_batch(rng, g.rows, B, max_bag, skew=False)
+    gout = rng.standard_normal((B, g.cols)).astype(np.float32)
+    res = run_case(g, cores32, idx, off, gout)
+    assert res["eng"].fast
+    c64 = [c.astype(np.float64) for c in cores32]
+    assert rel_err(res["out"], O.forward(c64, g, idx, off)) < FWD_TOL
+    ur, ug = O.unique_aggregate(idx, np.repeat(gout.astype(np.float64), np.diff(off), axis=0))
+    want = O.core_grads(c64, g, ur, ug)
+    for k in range(3):
+        assert rel_err(res["grads"][k], want[k]) < GRAD_TOL, k
