@@ -541,9 +541,12 @@ __device__ inline void stage_g1_t_async(const TileMeta* m, KGeom g, const float*
 // of a lane quadrant take every fourth segment of the item, reading the X row
 // from TMEM in two halves of c (64 registers).
 constexpr int kMaxTilePos = kTileItems * kItemLen;  // 1024
+
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 constexpr int kFwdMaxM3 = 288;                       // G3 (32 x m3 x 4 fp32) kept in smem
 constexpr int kFwdG3Max = 32 * kFwdMaxM3 * 16;
 constexpr int kFwdThreads = 512;
+constexpr int kFwdSplitRounds = 4;  // rows with <= this many segments: c split across the quarters
 
 // G3 region sized by the table's m3 (the (bag, i3) stages follow it)
 __host__ __device__ constexpr int fwd_g3_bytes(unsigned m3) { return (int)(32 * m3 * 16 + 1023) & ~1023; }
@@ -581,7 +584,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
   const int ntiles = hdr[4];
   const int tb = cta_tiles[blockIdx.x], te = cta_tiles[blockIdx.x + 1];  // weight-balanced (k_fplan)
   (void)ntiles;
-  if (warp == 0) umma::tmem_alloc(&s_tmem, 128);
+  if (warp == 0) umma::tmem_alloc(&s_tmem, 256);  // X, then the quarters' partial sums
   if (threadIdx.x == 32) umma::mbar_init(&s_mbar, 1);
   for (int e = threadIdx.x; e < 32 * (int)m3; e += kFwdThreads)  // m3 <= kFwdMaxM3 (fast_supported)
     cp_async16(s_g3 + e, reinterpret_cast<const float4*>(G3) + e);
@@ -652,45 +655,45 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
     if (t + 1 < te) stage(t + 1);  // lands while this tile is closed
     FSTAMP(2);
     const int p0 = m->start[0];
-    // ---- epilogue: warp-uniform loop over this thread's segments (tcgen05.ld is collective)
-    const bool live = it < m->n && !(dbg & 512);
+    // ---- epilogue. The four warps of a lane quadrant share its 32 rows
+    // (item, a) and split each segment's contraction over c: quarter q
+    // closes c in [8q, 8q + 8) (its 32 X columns stay in registers for the
+    // whole tile), parks its 16 partial sums in TMEM, and quarter 0 adds the
+    // four and stores the bag row. Every segment of a row costs each warp a
+    // quarter of the work, whatever the item lengths of the tile.
+    const bool live = it < m->n;
     const int s1 = live ? m->start[it + 1] - p0 : 0;
-    int qq = live ? m->start[it] - p0 : 0, ord = 0;
-    for (;;) {
-      bool have = false;
-      int bag = 0, e = qq;
-      while (qq < s1) {
-        bag = s_sbi[qq].x;
-        e = qq + 1;
-        while (e < s1 && s_sbi[e].x == bag) ++e;
-        if ((ord & 3) == quarter) {
-          have = true;
-          break;
+    int qq = live ? m->start[it] - p0 : 0;
+    int nseg = 0;  // segments (runs of one bag) of this row
+    for (int e = qq; e < s1;) {
+      const int bag = s_sbi[e].x;
+      ++e;
+      while (e < s1 && s_sbi[e].x == bag) ++e;
+      ++nseg;
+    }
+    const int rounds = __reduce_max_sync(0xffffffffu, nseg);  // same rows -> same count in all 4 warps
+    if (rounds <= kFwdSplitRounds) {
+      float x[32];  // x[4 c' + b] = X[item][a][b][8 quarter + c']
+      umma::tmem_ld32(trow + 32 * quarter, x);
+      const uint32_t tpart = trow + 128;  // partial sums: 16 columns per quarter
+      for (int r = 0; r < rounds; ++r) {
+        const bool have = r < nseg;
+        int bag = 0, e = qq;
+        if (have) {
+          bag = s_sbi[qq].x;
+          e = qq + 1;
+          while (e < s1 && s_sbi[e].x == bag) ++e;
         }
-        ++ord;
-        qq = e;
-      }
-      if (!__any_sync(0xffffffffu, have)) break;
-      float acc[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) acc[i] = 0.f;
-#pragma unroll
-      for (int ch = 0; ch < 2; ++ch) {
-        float x[64];  // x[4 c' + b] = X[item][a][b][16 ch + c']
-        if (!(dbg & 64)) {
-          umma::tmem_ld32(trow + 64 * ch, *(float(*)[32])(x));
-          umma::tmem_ld32(trow + 64 * ch + 32, *(float(*)[32])(x + 32));
-        } else {
-#pragma unroll
-          for (int i = 0; i < 64; ++i) x[i] = __uint_as_float((unsigned)(lane + i));
-        }
-        if (have && !(dbg & 32)) {
+        float acc[16];
+  #pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+        if (have) {
           for (int l = qq; l < e; ++l) {
-            const float4* g3 = s_g3 + (unsigned)s_sbi[l].y + 16 * ch * m3;
-#pragma unroll
-            for (int c = 0; c < 16; ++c) {
+            const float4* g3 = s_g3 + (unsigned)s_sbi[l].y + 8 * quarter * m3;
+  #pragma unroll
+            for (int c = 0; c < 8; ++c) {
               const float4 gv = g3[c * m3];
-#pragma unroll
+  #pragma unroll
               for (int b = 0; b < 4; ++b) {
                 const float xv = x[4 * c + b];
                 acc[4 * b + 0] = fmaf(xv, gv.x, acc[4 * b + 0]);
@@ -701,23 +704,97 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
             }
           }
         }
-      }
-      if (have && !(dbg & 128)) {
-        float* o = out + (size_t)bag * NOUT + a * 16;
-        if (direct) {
-#pragma unroll
-          for (int b = 0; b < 4; ++b)
-            reinterpret_cast<float4*>(o)[b] = make_float4(acc[4 * b], acc[4 * b + 1], acc[4 * b + 2], acc[4 * b + 3]);
-        } else {
-#pragma unroll
-          for (int b = 0; b < 4; ++b) red_v4(o + 4 * b, acc[4 * b], acc[4 * b + 1], acc[4 * b + 2], acc[4 * b + 3]);
+        if (quarter != 0) {
+          umma::tmem_st16(tpart + 16 * quarter, acc);
+          umma::tmem_wait_st();
         }
-      }
-      if (have) {
-        ++ord;
+        named_sync(1 + q4, 128);  // the quadrant's partials are in TMEM
+        if (quarter == 0) {
+          float p[16];
+  #pragma unroll
+          for (int qd = 1; qd < 4; ++qd) {
+            umma::tmem_ld16(tpart + 16 * qd, p);
+  #pragma unroll
+            for (int i = 0; i < 16; ++i) acc[i] += p[i];
+          }
+          if (have) {
+            float* o = out + (size_t)bag * NOUT + a * 16;
+            if (direct) {
+  #pragma unroll
+              for (int bb = 0; bb < 4; ++bb)
+                reinterpret_cast<float4*>(o)[bb] =
+                    make_float4(acc[4 * bb], acc[4 * bb + 1], acc[4 * bb + 2], acc[4 * bb + 3]);
+            } else {
+  #pragma unroll
+              for (int bb = 0; bb < 4; ++bb)
+                red_v4(o + 4 * bb, acc[4 * bb], acc[4 * bb + 1], acc[4 * bb + 2], acc[4 * bb + 3]);
+            }
+          }
+        }
+        umma::fence_before_sync();
+        named_sync(1 + q4, 128);  // partial columns free for the next round
+        umma::fence_after_sync();
         qq = e;
       }
-      if (dbg & 256) break;
+    } else {
+      // long items (hot prefixes): the quarters take alternate segments, each
+      // closing all 32 values of c (two 64-column halves of the X row)
+      int ord = 0;
+      for (;;) {
+        bool have = false;
+        int bag = 0, e = qq;
+        while (qq < s1) {
+          bag = s_sbi[qq].x;
+          e = qq + 1;
+          while (e < s1 && s_sbi[e].x == bag) ++e;
+          if ((ord & 3) == quarter) {
+            have = true;
+            break;
+          }
+          ++ord;
+          qq = e;
+        }
+        if (!__any_sync(0xffffffffu, have)) break;
+        float acc[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          float xh[64];  // xh[4 c' + b] = X[item][a][b][16 ch + c']
+          umma::tmem_ld32(trow + 64 * ch, *(float(*)[32])(xh));
+          umma::tmem_ld32(trow + 64 * ch + 32, *(float(*)[32])(xh + 32));
+          if (have) {
+            for (int l = qq; l < e; ++l) {
+              const float4* g3 = s_g3 + (unsigned)s_sbi[l].y + 16 * ch * m3;
+#pragma unroll
+              for (int c = 0; c < 16; ++c) {
+                const float4 gv = g3[c * m3];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                  const float xv = xh[4 * c + b];
+                  acc[4 * b + 0] = fmaf(xv, gv.x, acc[4 * b + 0]);
+                  acc[4 * b + 1] = fmaf(xv, gv.y, acc[4 * b + 1]);
+                  acc[4 * b + 2] = fmaf(xv, gv.z, acc[4 * b + 2]);
+                  acc[4 * b + 3] = fmaf(xv, gv.w, acc[4 * b + 3]);
+                }
+              }
+            }
+          }
+        }
+        if (have) {
+          float* o = out + (size_t)bag * NOUT + a * 16;
+          if (direct) {
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+              reinterpret_cast<float4*>(o)[b] = make_float4(acc[4 * b], acc[4 * b + 1], acc[4 * b + 2], acc[4 * b + 3]);
+          } else {
+#pragma unroll
+            for (int b = 0; b < 4; ++b) red_v4(o + 4 * b, acc[4 * b], acc[4 * b + 1], acc[4 * b + 2], acc[4 * b + 3]);
+          }
+          ++ord;
+          qq = e;
+        }
+      }
     }
     FSTAMP(4);
     FSTAMP(4);
@@ -726,7 +803,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
     if (t + 1 < te) issue_mma();
     FSTAMP(3);
   }
-  if (warp == 0) umma::tmem_free(tmem, 128);
+  if (warp == 0) umma::tmem_free(tmem, 256);
 #undef FSTAMP
 }
 
