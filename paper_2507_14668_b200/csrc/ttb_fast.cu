@@ -59,7 +59,8 @@ __device__ __forceinline__ void red_f32(float* p, float a) {
 // <= kTileItems items of one i2 of similar lengths.
 constexpr int kPlanThreads = 512;
 constexpr int kTileCost = 32;
-constexpr int kA2Regs = 8;     // per-lane registers caching an i2 group's prefix counters (m1 <= 256)  // per-tile fixed cost in lookup units (CTA range balancing)
+constexpr int kA2Regs = 8;
+constexpr int kPlanRegs = 4;   // lookups per thread whose plan fields stay in registers (phase 0 -> B)     // per-lane registers caching an i2 group's prefix counters (m1 <= 256)  // per-tile fixed cost in lookup units (CTA range balancing)
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -124,10 +125,15 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
     if (hi - lo > 1) multi = 1;
   }
   const unsigned m2m3 = g.m2 * g.m3;
-  for (int t0 = blockIdx.x * blockDim.x; t0 < T; t0 += nthr) {  // warp-uniform trip count
+  // the first kPlanRegs lookups of this thread keep (key, rank, i3) in
+  // registers for phase B (same thread <-> lookup mapping there)
+  unsigned rkey[kPlanRegs], ri3[kPlanRegs];
+  int rrk[kPlanRegs];
+  int iter = 0;
+  for (int t0 = blockIdx.x * blockDim.x; t0 < T; t0 += nthr, ++iter) {  // warp-uniform trip count
     const int t = t0 + threadIdx.x;
     const bool ok = t < T;
-    unsigned k = 0xFFFFFFFFu;
+    unsigned k = 0xFFFFFFFFu, i3 = 0;
     if (ok) {
       long long v = (long long)idx[t];
       if (v < 0 || v >= (long long)g.rows) {
@@ -136,15 +142,26 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
       }
       const unsigned i = (unsigned)v, i1 = i / m2m3, r = i - i1 * m2m3, i2 = r / g.m3;
       k = i2 * g.m1 + i1;
-      key[t] = k;
-      i3o[t] = r - i2 * g.m3;
+      i3 = r - i2 * g.m3;
+      if (iter >= kPlanRegs) {
+        key[t] = k;
+        i3o[t] = i3;
+      }
     }
     const unsigned peers = __match_any_sync(0xffffffffu, k);
     const int leader = __ffs(peers) - 1;
     int base = 0;
     if (ok && lane == leader) base = atomicAdd(&cnt[k], __popc(peers));
     base = __shfl_sync(0xffffffffu, base, leader);
-    if (ok) rk[t] = base + __popc(peers & lanemask_lt());
+    const int rank = base + __popc(peers & lanemask_lt());
+#pragma unroll
+    for (int q = 0; q < kPlanRegs; ++q)
+      if (q == iter) {
+        rkey[q] = k;
+        ri3[q] = i3;
+        rrk[q] = rank;
+      }
+    if (ok && iter >= kPlanRegs) rk[t] = rank;
   }
   if (bits) atomicOr(&hdr[0], bits);
   if (multi) hdr[1] = 1;
@@ -266,11 +283,15 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
       pass2(i1, i1 < g.m1 ? cnt[i2 * g.m1 + i1] : 0);
     }
     __syncwarp();
-    // tiles: (i2, first item, items, first lookup position)
+    // tiles: (i2, first item, items, first lookup position); the position of
+    // the tile's first item from the length buckets (items [ioff[L], hist[L])
+    // have length L), not re-read from global memory
     for (int j = lane; j < ntile; j += 32) {
-      const int left = mine.y - kTileItems * j;
-      tile_info[pt + j] = make_int4((int)i2, pi + kTileItems * j, left < kTileItems ? left : kTileItems,
-                                    item_start[pi + kTileItems * j]);
+      const int left = mine.y - kTileItems * j, f = kTileItems * j;
+      int L = kItemLen;
+      while (L > 1 && hist[L] <= f) --L;
+      tile_info[pt + j] = make_int4((int)i2, pi + f, left < kTileItems ? left : kTileItems,
+                                    pc + poff[L] + (f - ioff[L]) * L);
     }
     if (lane == 0) {
       atomicAdd(&hdr[3], mine.z);
@@ -300,10 +321,27 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
     }
   }
   // ---- phase B: scatter (bag, i3) into item order
-  for (int t = tid; t < T; t += nthr) {
-    const unsigned k = key[t];
-    const int r = rk[t];
-    sbi[(r < split[k] ? start[k] : rstart[k]) + r] = make_int2(bag_of[t], (int)i3o[t]);
+  {
+    const bool one = hdr[1] == 0 && T == B;  // one lookup per bag: bag id = lookup index
+    int it2 = 0;
+    for (int t = tid; t < T; t += nthr, ++it2) {
+      unsigned k, i3;
+      int r;
+      if (it2 < kPlanRegs) {
+#pragma unroll
+        for (int q = 0; q < kPlanRegs; ++q)
+          if (q == it2) {
+            k = rkey[q];
+            i3 = ri3[q];
+            r = rrk[q];
+          }
+      } else {
+        k = key[t];
+        i3 = i3o[t];
+        r = rk[t];
+      }
+      sbi[(r < split[k] ? start[k] : rstart[k]) + r] = make_int2(one ? t : bag_of[t], (int)i3);
+    }
   }
   __syncthreads();
   PSTAMP(4);
