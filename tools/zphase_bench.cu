@@ -51,7 +51,8 @@ __global__ void __launch_bounds__(NT, 1) zb(int reps, int npos_per_item, float* 
           }
         }
         float dh[4] = {0.f, 0.f, 0.f, 0.f};
-        if (MODE == 4) {  // 16 independent chains of 4, then a 4-way add per j
+        if (MODE == 7) {
+        } else if (MODE == 4) {  // 16 independent chains of 4, then a 4-way add per j
           float p4[4][4];
 #pragma unroll
           for (int q = 0; q < 4; ++q)
@@ -71,6 +72,12 @@ __global__ void __launch_bounds__(NT, 1) zb(int reps, int npos_per_item, float* 
         }
         float gs[4] = {0.f, 0.f, 0.f, 0.f};
         int e = qq;
+        if (MODE == 8) {
+          const float4 h3 = st_g3[e * 32 + lane];
+          gs[0] = h3.x; gs[1] = h3.y; gs[2] = h3.z; gs[3] = h3.w;
+          red_v4(dG3 + ((size_t)lane * m3 + st_sbi[e].y) * 4, dh[0], dh[1], dh[2], dh[3]);
+          ++e;
+        } else
         for (; e < s1; ++e) {
           const int2 pr = st_sbi[e];
           if (pr.x != bag) break;
@@ -79,7 +86,9 @@ __global__ void __launch_bounds__(NT, 1) zb(int reps, int npos_per_item, float* 
           if (MODE != 1) red_v4(dG3 + ((size_t)lane * m3 + pr.y) * 4, dh[0], dh[1], dh[2], dh[3]);
           else bad += dh[0] + dh[1] + dh[2] + dh[3];
         }
-        if (MODE == 5) {
+        if (MODE == 6) {
+          bad += gs[0] + gs[1] + gs[2] + gs[3] + gv[0];
+        } else if (MODE == 5) {
 #pragma unroll
           for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -229,22 +238,28 @@ int main() {
   }
   float* big;
   cudaMalloc(&big, 148 * 1024 * 4);
+  cudaFuncSetAttribute(zb<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(zb<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(zb<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   for (int npi : {2})
-    for (int mode = 0; mode < 6; ++mode) {
+    for (int mode = 0; mode < 9; ++mode) {
       const int reps = 200;
       if (mode == 0) zb<0><<<148, 256, smem>>>(reps, npi, dG3, 250, sink, cyc);
       else if (mode == 1) zb<1><<<148, 256, smem>>>(reps, npi, dG3, 250, sink, cyc);
       else if (mode == 2) zb<2><<<148, 256, smem>>>(reps, npi, dG3, 250, sink, cyc);
       else if (mode == 3) zb<3><<<148, 256, smem>>>(reps, npi, dG3, 250, sink, cyc);
       else if (mode == 4) zb<4><<<148, 256, smem>>>(reps, npi, dG3, 250, sink, cyc);
-      else zb<5><<<148, 256, smem>>>(reps, npi, dG3, 250, sink, cyc);
+      else if (mode == 5) zb<5><<<148, 256, smem>>>(reps, npi, dG3, 250, sink, cyc);
+      else if (mode == 6) zb<6><<<148, 256, smem>>>(reps, npi, dG3, 250, sink, cyc);
+      else if (mode == 7) zb<7><<<148, 256, smem>>>(reps, npi, dG3, 250, sink, cyc);
+      else zb<8><<<148, 256, smem>>>(reps, npi, dG3, 250, sink, cyc);
       cudaError_t e = cudaDeviceSynchronize();
       if (e) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
       unsigned long long h;
       cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
       const double per_tile = (double)h / reps;
       printf("positions/item %d %s: %.0f cycles per tile of 32 items (%.0f per position per warp-slot)\n", npi,
-             mode == 0 ? "LDS.128 bcast" : mode == 1 ? "no red       " : mode == 2 ? "LDS.32 bcast " : mode == 3 ? "gv in regs   " : mode == 4 ? "dh 16 chains " : "z j-outer    ", per_tile, per_tile / (4.0 * npi));
+             mode == 0 ? "LDS.128 bcast" : mode == 1 ? "no red       " : mode == 2 ? "LDS.32 bcast " : mode == 3 ? "gv in regs   " : mode == 4 ? "dh 16 chains " : mode == 5 ? "z j-outer    " : mode == 6 ? "no z         " : mode == 7 ? "no dh        " : "no bag loop  ", per_tile, per_tile / (4.0 * npi));
     }
   return 0;
 }
