@@ -582,7 +582,6 @@ constexpr int kMaxTilePos = kTileItems * kItemLen;  // 1024
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 constexpr int kFwdMaxM3 = 288;                       // G3 (32 x m3 x 4 fp32) kept in smem
-constexpr int kFwdG3Max = 32 * kFwdMaxM3 * 16;
 constexpr int kFwdThreads = 512;
 constexpr int kFwdSplitRounds = 4;  // rows with <= this many segments: c split across the quarters
 

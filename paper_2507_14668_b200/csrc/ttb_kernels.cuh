@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(kBlock) k_prefix_products_tc(D d, KGeom g, con
   pdl_enter();
   if constexpr (kTcPrefix<D>) {
     constexpr int R1 = FixT<D>::r1, C = FixT<D>::n2 * FixT<D>::r2, M = 128, N1 = 4;
-    extern __shared__ __align__(128) float smem[];
+    extern __shared__ __align__(16) float smem[];
     __shared__ int s_free[kMaxChunk], s_slot[kMaxChunk], s_w[kBlock / 32 + 2];
     __shared__ uint64_t s_mbar;
     __shared__ uint32_t s_tmem;
@@ -1322,7 +1322,7 @@ __global__ void __launch_bounds__(kBlock) k_bwd_gemm_tc(D d, KGeom g, const floa
   pdl_enter();
   if constexpr (kTcBwd<D>) {
     constexpr int C = 128, R1 = 32, N1 = 4, ROWS = kTcBwdChunk * N1;  // 64
-    extern __shared__ __align__(128) float smem[];
+    extern __shared__ __align__(16) float smem[];
     __shared__ int s_free[kMaxChunk], s_slot[kMaxChunk], s_w[kBlock / 32 + 2];
     __shared__ uint64_t s_mbar;
     __shared__ uint32_t s_tmem;
@@ -1501,7 +1501,7 @@ __global__ void __launch_bounds__(kBlock) k_bwd_gemm_tc2(D d, KGeom g, const flo
   pdl_enter();
   if constexpr (kTcBwd<D>) {
     constexpr int C = 128, R1 = 32, N1 = 4, CH = kTcBwdChunk, ROWS = CH * N1;  // 64
-    extern __shared__ __align__(128) float smem[];
+    extern __shared__ __align__(16) float smem[];
     __shared__ int s_free[kMaxGroup], s_slot[kMaxGroup], s_w[kBlock / 32 + 2];
     __shared__ uint64_t s_mbar;
     __shared__ uint32_t s_tmem;
