@@ -276,12 +276,15 @@ def run_ours(args):
         e2e = e2e_run(args, torch, cfg, rank, dev, world)
         if rank == 0:
             result["e2e"] = e2e
+    if not args.quick and not args.no_extras:  # every rank (data-parallel DLRM, BASELINE config 5)
+        import bench_extras
+        cfg5 = bench_extras.cfg5(dev, world, rank)
     if rank == 0 and not args.quick:
         if world == 1 and not args.no_cpu_baseline:
             result["cpu_baseline"] = cpu_baseline(args, cfg)
-        if world == 1 and not args.no_extras:
-            import bench_extras
-            result["extras"] = bench_extras.run_all(dev)
+        if not args.no_extras:
+            result["extras"] = bench_extras.run_all(dev) if world == 1 else {}
+            result["extras"]["cfg5_dlrm_dp"] = cfg5
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

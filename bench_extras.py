@@ -101,6 +101,42 @@ def cfg4(dev, steps=5, B=65536):
     return r
 
 
+def cfg5(dev, world=1, rank=0, steps=5, global_batch=524288):
+    """BASELINE config 5: the config-4 TT-DLRM trained data parallel — global
+    batch 524,288 split over the ranks, one NCCL all-reduce of every gradient
+    per step (DlrmModel.train_step_dp); time = max over ranks."""
+    import torch.distributed as dist
+    from paper_2507_14668_b200.model import DlrmModel, ModelConfig
+    torch.backends.cuda.matmul.allow_tf32 = False
+    cfg = ModelConfig(n_dense=13, rows_per_field=KAGGLE_ROWS, emb_dim=64, ranks=(1, 32, 32, 1), tt_threshold=1000,
+                      bottom_sizes=(512, 256), top_sizes=(512, 256), loss="bce", seed=0)
+    B = global_batch // world
+    rng = np.random.default_rng(11 + rank)
+    model = DlrmModel(cfg, device=dev, max_indices=B, check_errors=False)
+    dense, sparse, labels = _dlrm_batch(cfg, B, rng, dev, 1, 1)
+    step = lambda: model.train_step_dp(dense, sparse, labels, 0.05, 0.9, global_batch=global_batch)  # noqa: E731
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        step()
+    b.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(b) / steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"value": global_batch / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms, "global_batch": global_batch,
+            "batch_per_gpu": B, "n_gpus": world,
+            "workload": f"cfg5: config-4 TT-DLRM, data parallel over {world} GPU(s), global batch {global_batch}, "
+                        "one all-reduce of TT-core + dense-field + MLP gradients per step, SGD momentum 0.9, "
+                        "fp32 MLPs, eager (not graph-captured)"}
+
+
 def cfg3(dev, steps=3, B=65536, pooling=20, permuted=False, tables=26):
     from paper_2507_14668_b200.engine import TtEngine
     from paper_2507_14668_b200.geometry import TtShape, factorize_dims, init_random_cores

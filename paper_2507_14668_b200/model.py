@@ -259,6 +259,52 @@ class DlrmModel(nn.Module):
         return float(loss) if sync_loss else loss
 
 
+    # ------------------------------------------------------------ data parallel
+    def train_step_dp(self, dense, sparse, labels, lr: float, momentum: float = 0.0, global_batch: int | None = None,
+                      group=None, sync_loss: bool = False):
+        """One data-parallel SGD(+momentum) step on this rank's shard of the
+        batch (Rec-AD DP; BASELINE config 5): every
+        parameter's gradient — TT cores, dense fields, MLPs — lands in one
+        flat fp32 buffer, scaled by local_B / global_B so the SUM over ranks
+        is the gradient of the global batch mean (model.py:85-86), is
+        all-reduced once, and every rank applies the same update (fp64
+        velocity, one rounding), keeping the replicas identical."""
+        import torch.distributed as dist
+        if lr < 0 or not 0.0 <= momentum < 1.0:
+            raise ValueError("need lr >= 0 and 0 <= momentum < 1")
+        world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+        local_b = int(labels.numel())
+        global_b = int(global_batch) if global_batch is not None else local_b * world
+        for fld in self.fields:
+            if isinstance(fld, TTEmbeddingBag):
+                fld.disable_fused_sgd()
+        for p in self.parameters():
+            p.grad = None
+        z = self.forward(dense, sparse)
+        loss, gz = self.loss_and_logit_grad(z, labels)
+        z.backward(gz * (local_b / global_b))
+        named = self.named_ref_params()
+        flat = torch.cat([(p.grad if p.grad is not None else torch.zeros_like(p)).reshape(-1) for _, p in named])
+        if world > 1:
+            dist.all_reduce(flat, group=group)
+        lib = nat.load()
+        off = 0
+        with torch.no_grad():
+            for name, p in named:
+                g = flat[off:off + p.numel()]
+                off += p.numel()
+                v = None
+                if momentum > 0.0:
+                    v = self._velocity.get(name)
+                    if v is None:
+                        v = torch.zeros(p.shape, dtype=torch.float64, device=p.device)
+                        self._velocity[name] = v
+                nat.check(lib.ttb_sgd_update(_ptr(p), _ptr(g), _ptr(v), p.numel(), float(lr), float(momentum),
+                                             _stream()), "sgd_update")
+                p.grad = None
+        return float(loss) if sync_loss else loss
+
+
 def bags_field_tensors(bags_per_field, device):
     """Reference Dataset.bags (field -> sample -> bag) -> [(indices, offsets)]."""
     from .engine import bags_to_tensors
