@@ -11,7 +11,8 @@ import os
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libttb.so"
+# TTB_LIB_PATH: an alternative build of the same ABI (A/B timing in tools/)
+LIB_PATH = Path(os.environ.get("TTB_LIB_PATH", str(_HERE / "libttb.so")))
 
 TTB_OK = 0
 TTB_EINVAL = -1

@@ -860,13 +860,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
 // X[., ., c] and accumulates Z[., ., c] in registers, so a position costs
 // 128 FMAs per lane and no cross-lane reduction. The next tile's first chunk
 // and X operands are fetched while this tile's GEMMs and epilogue run.
-// per-phase timestamps of block 0's first two tiles into hdr[16..] (TTB_DBG & 8)
+// per-phase SM cycles (thread 0, summed over block 0's tiles) into hdr[16..]
+// as 9 u64 + the tile count (TTB_DBG & 8); phase k = TSTAMP(k-1) .. TSTAMP(k)
 #define TSTAMP(k)                                                                                      \
   do {                                                                                                 \
-    if ((dbg & 8) && threadIdx.x == 0 && blockIdx.x == 0 && t < 2) {                                   \
-      unsigned long long _t;                                                                           \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                                           \
-      reinterpret_cast<unsigned long long*>(hdr + 16)[t * 9 + (k)] = _t;                               \
+    if ((dbg & 8) && threadIdx.x == 0 && blockIdx.x == 0) {                                            \
+      const long long _t = clock64();                                                                  \
+      if ((k) > 0) s_tacc[(k)] += _t - s_tacc[0];                                                       \
+      s_tacc[0] = _t;                                                                                  \
     }                                                                                                  \
   } while (0)
 
@@ -908,6 +909,7 @@ __device__ inline void stage_rows_async(int np, const int2* st_sbi, const float*
   }
 }
 
+template <bool kRows>
 __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __restrict__ g1img,
                                                      const float* __restrict__ G3, const float* __restrict__ img,
                                                      const int4* __restrict__ tile_info,
@@ -932,6 +934,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
   __shared__ TileMeta s_m[2];
   __shared__ int s_chunk[2][kTileItems + 2];
   __shared__ uint64_t s_mbar;
+  __shared__ long long s_tacc[10];
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = hdr[4];
@@ -940,6 +943,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
   const int tb = cta_tiles[blockIdx.x], te = cta_tiles[blockIdx.x + 1];  // weight-balanced (k_fplan)
   (void)ntiles;
   const unsigned m3 = g.m3;
+  if (threadIdx.x < 10) s_tacc[threadIdx.x] = 0;
   if (warp == 0) umma::tmem_alloc(&s_tmem, 512);
   if (threadIdx.x == 32) umma::mbar_init(&s_mbar, 1);
   int4 pf = make_int4(0, 0, 0, 0);
@@ -1049,41 +1053,98 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
           x[ab] = xs[xs_idx(it, ab >> 2, ab & 3, lane)];
           z[ab] = 0.f;
         }
-        const int s1 = m->start[it + 1] - p0;
-        int qq = m->start[it] - p0;
-        while (qq < s1) {
-          const int bag = st_sbi[qq].x;
-          float gv[64];
+        if (kRows) {
+          // the item's (<= kItemLen) positions, one per lane, grouped by row
+          // (equal i3): a row's gradient rows are summed first, so dG3 gets one
+          // reduction and Z one rank-4 update per distinct row of the item
+          const int s0 = m->start[it] - p0, nq = m->start[it + 1] - p0 - s0;
+          const int my_i3 = lane < nq ? st_sbi[s0 + lane].y : -1;
+          const unsigned grp = __match_any_sync(0xffffffffu, lane < nq ? my_i3 : (int)(0x80000000u | lane));
+          unsigned lead = __ballot_sync(0xffffffffu, lane < nq && (__ffs(grp) - 1) == lane);
+          while (lead) {
+            const int ld = __ffs(lead) - 1;
+            lead &= lead - 1;
+            unsigned mem = __shfl_sync(0xffffffffu, grp, ld);
+            const int i3 = __shfl_sync(0xffffffffu, my_i3, ld);
+            float gv[64];
+            {
+              const int q = s0 + ld;
 #pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const float4 v = st_g[qq * 16 + k];
-            gv[4 * k] = v.x;
-            gv[4 * k + 1] = v.y;
-            gv[4 * k + 2] = v.z;
-            gv[4 * k + 3] = v.w;
+              for (int k = 0; k < 16; ++k) {
+                const float4 v = st_g[q * 16 + k];
+                gv[4 * k] = v.x;
+                gv[4 * k + 1] = v.y;
+                gv[4 * k + 2] = v.z;
+                gv[4 * k + 3] = v.w;
+              }
+            }
+            mem &= mem - 1;
+            while (mem) {
+              const int q = s0 + __ffs(mem) - 1;
+              mem &= mem - 1;
+#pragma unroll
+              for (int k = 0; k < 16; ++k) {
+                const float4 v = st_g[q * 16 + k];
+                gv[4 * k] += v.x;
+                gv[4 * k + 1] += v.y;
+                gv[4 * k + 2] += v.z;
+                gv[4 * k + 3] += v.w;
+              }
+            }
+            float dh[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int ab = 0; ab < 16; ++ab)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) dh[j] = fmaf(x[ab], gv[4 * ab + j], dh[j]);
+            if (!(dbg & 1)) red_v4(dG3 + ((size_t)lane * m3 + i3) * 4, dh[0], dh[1], dh[2], dh[3]);
+            const float4 h3 = st_g3[(s0 + ld) * 32 + lane];
+#pragma unroll
+            for (int ab = 0; ab < 16; ++ab) {
+              z[ab] = fmaf(gv[4 * ab], h3.x, z[ab]);
+              z[ab] = fmaf(gv[4 * ab + 1], h3.y, z[ab]);
+              z[ab] = fmaf(gv[4 * ab + 2], h3.z, z[ab]);
+              z[ab] = fmaf(gv[4 * ab + 3], h3.w, z[ab]);
+            }
           }
-          float dh[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-          for (int ab = 0; ab < 16; ++ab)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) dh[j] = fmaf(x[ab], gv[4 * ab + j], dh[j]);
-          float gs[4] = {0.f, 0.f, 0.f, 0.f};
-          int e = qq;
-          for (; e < s1; ++e) {
-            const int2 pr = st_sbi[e];
-            if (pr.x != bag) break;
-            const float4 h3 = st_g3[e * 32 + lane];
-            gs[0] += h3.x;
-            gs[1] += h3.y;
-            gs[2] += h3.z;
-            gs[3] += h3.w;
-            if (!(dbg & 1)) red_v4(dG3 + ((size_t)lane * m3 + pr.y) * 4, dh[0], dh[1], dh[2], dh[3]);
+        } else {
+          // positions in plan order; runs of one bag share the gradient row,
+          // X^T g and the Z update
+          const int s1 = m->start[it + 1] - p0;
+          int qq = m->start[it] - p0;
+          while (qq < s1) {
+            const int bag = st_sbi[qq].x;
+            float gv[64];
+  #pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              const float4 v = st_g[qq * 16 + k];
+              gv[4 * k] = v.x;
+              gv[4 * k + 1] = v.y;
+              gv[4 * k + 2] = v.z;
+              gv[4 * k + 3] = v.w;
+            }
+            float dh[4] = {0.f, 0.f, 0.f, 0.f};
+  #pragma unroll
+            for (int ab = 0; ab < 16; ++ab)
+  #pragma unroll
+              for (int j = 0; j < 4; ++j) dh[j] = fmaf(x[ab], gv[4 * ab + j], dh[j]);
+            float gs[4] = {0.f, 0.f, 0.f, 0.f};
+            int e = qq;
+            for (; e < s1; ++e) {
+              const int2 pr = st_sbi[e];
+              if (pr.x != bag) break;
+              const float4 h3 = st_g3[e * 32 + lane];
+              gs[0] += h3.x;
+              gs[1] += h3.y;
+              gs[2] += h3.z;
+              gs[3] += h3.w;
+              if (!(dbg & 1)) red_v4(dG3 + ((size_t)lane * m3 + pr.y) * 4, dh[0], dh[1], dh[2], dh[3]);
+            }
+  #pragma unroll
+            for (int ab = 0; ab < 16; ++ab)
+  #pragma unroll
+              for (int j = 0; j < 4; ++j) z[ab] = fmaf(gv[4 * ab + j], gs[j], z[ab]);
+            qq = e;
           }
-#pragma unroll
-          for (int ab = 0; ab < 16; ++ab)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) z[ab] = fmaf(gv[4 * ab + j], gs[j], z[ab]);
-          qq = e;
         }
         float zs = 0.f;
 #pragma unroll
@@ -1123,16 +1184,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
     cp_async_wait_all();  // G2 k / G1^T images (issued before the Z phase)
     sync_for_mma();       // every slot read before the image overwrites them; Z^T is in TMEM
     constexpr uint32_t id64 = umma::idesc_tf32(128, 64, false, false);
+    constexpr uint32_t id32 = umma::idesc_tf32(128, 32, false, false);  // B rows 0-31: the hi half
     const bool acc2 = m->i2 == prev_i2;  // same i2 as the previous tile: keep accumulating dG2 in TMEM
     if (threadIdx.x == 0) {
+      const long long _c0 = clock64();
       // dG2 tile [(c, b), (hi | lo) k] = sum_(item, a) (Z^T hi + Z^T lo) . G1^T (A from TMEM);
       // issued before the Z image is written (only the E GEMM reads it)
 #pragma unroll
       for (int k0 = 0; k0 < 128; k0 += 8) {
         const uint32_t o = (uint32_t)((k0 >> 5) * 64 * 128 + (k0 & 31) * 4) >> 4;
         umma::mma_tf32_ta(tmem + 384, tmem + 128 + k0, d_r2h + o, id64, (acc2 || k0 > 0) ? 1u : 0u);
-        umma::mma_tf32_ta(tmem + 384, tmem + 256 + k0, d_r2h + o, id64, 1u);
+        umma::mma_tf32_ta(tmem + 384, tmem + 256 + k0, d_r2h + o, id32, 1u);  // Z lo . G1 hi only
       }
+      if ((dbg & 8) && blockIdx.x == 0) s_tacc[9] += clock64() - _c0;
     }
     // ---- next tile: chunk list and first chunk's positions
     if (tn < te) {
@@ -1177,7 +1241,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
       for (int k0 = 0; k0 < 128; k0 += 8) {
         const uint32_t oa = (uint32_t)((k0 >> 5) * 128 * 128 + (k0 & 31) * 4) >> 4;
         const uint32_t ob = (uint32_t)((k0 >> 5) * 64 * 128 + (k0 & 31) * 4) >> 4;
-        umma::mma_tf32(tmem + 448, d_zi + oa, d_r1h + ob, id64, 1u);
+        umma::mma_tf32(tmem + 448, d_zi + oa, d_r1h + ob, id32, 1u);  // Z lo . G2 hi only
       }
       umma::commit(&s_mbar);
     }
@@ -1218,6 +1282,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
     umma::fence_after_sync();
   }
   if (bad) atomicOr(&hdr[0], 8);
+  if ((dbg & 8) && threadIdx.x == 0 && blockIdx.x == 0) {
+    s_tacc[0] = te - tb;
+    for (int q = 0; q < 10; ++q) reinterpret_cast<long long*>(hdr + 16)[q] = s_tacc[q];
+  }
   if (warp == 0) umma::tmem_free(tmem, 512);
 }
 
@@ -1269,7 +1337,8 @@ cudaError_t fast_forward(ttb_handle* h, const float* c0, const float* c1, const 
   if (!attr) {
     if ((e = ensure_attr((const void*)k_coreimg, img_smem))) return e;
     if ((e = ensure_attr((const void*)k_fwd, fwd_smem_bytes(kFwdMaxM3)))) return e;
-    if ((e = ensure_attr((const void*)k_bwd, kBwdSmem))) return e;
+    if ((e = ensure_attr((const void*)k_bwd<false>, kBwdSmem))) return e;
+    if ((e = ensure_attr((const void*)k_bwd<true>, kBwdSmem))) return e;
     attr = true;
   }
   if (!(h->img_valid && h->img_c0 == c0 && h->img_c1 == c1)) {
@@ -1320,7 +1389,8 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
   const int grid = h->num_sms;  // = the plan's CTA ranges (k_fplan cta_tiles)
   {
     ProfScope _ps(h, s, "f_bwd");
-    if ((e = launch_pdl(k_bwd, dim3(grid), dim3(kThreads), kBwdSmem, s, h->kg, (const float*)w.f_g1img, c2,
+    // pooled bags (more lookups than bags) repeat rows inside a prefix: group by row
+    if ((e = launch_pdl(h->T > h->B ? k_bwd<true> : k_bwd<false>, dim3(grid), dim3(kThreads), kBwdSmem, s, h->kg, (const float*)w.f_g1img, c2,
                         (const float*)w.f_img, (const int4*)w.f_tile_info, (const int*)w.f_item_start,
                         (const unsigned*)w.f_item_key, (const int2*)w.f_sbi, gout, g0, g1, g2, w.fast_hdr,
                         (const int*)w.f_cta, getenv("TTB_DBG") ? atoi(getenv("TTB_DBG")) : 0)))

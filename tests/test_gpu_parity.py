@@ -402,6 +402,28 @@ def test_fast_pooled_and_hot_rows(B, max_bag, skew):
         assert rel_err(res["grads"][k], want[k]) < GRAD_TOL, k
 
 
+@pytest.mark.parametrize("pool", [1, 7])
+def test_fast_repeated_rows(pool):
+    """Few distinct rows repeated within and across bags (the backward groups
+    an item's positions by row when bags are pooled, by bag run otherwise)."""
+    g = O.Geometry((20, 20, 25), (4, 4, 4), (1, 32, 32, 1))
+    cores32 = [c.astype(np.float32) for c in O.init_cores(g, 3)]
+    rng = np.random.default_rng(pool)
+    B = 1200
+    rows = rng.integers(0, g.rows, 40)
+    idx = rows[rng.integers(0, 40, B * pool)]
+    off = np.arange(0, B * pool + 1, pool, dtype=np.int64)
+    gout = rng.standard_normal((B, g.cols)).astype(np.float32)
+    res = run_case(g, cores32, idx, off, gout)
+    assert res["eng"].fast
+    c64 = [c.astype(np.float64) for c in cores32]
+    assert rel_err(res["out"], O.forward(c64, g, idx, off)) < FWD_TOL
+    ur, ug = O.unique_aggregate(idx, np.repeat(gout.astype(np.float64), np.diff(off), axis=0))
+    want = O.core_grads(c64, g, ur, ug)
+    for k in range(3):
+        assert rel_err(res["grads"][k], want[k]) < GRAD_TOL, k
+
+
 def test_fast_errors_raise():
     from paper_2507_14668_b200.embedding_bag import TTEmbeddingBag
     emb = TTEmbeddingBag(10000, 64, (1, 32, 32, 1), tt_m=(20, 20, 25), tt_n=(4, 4, 4))
