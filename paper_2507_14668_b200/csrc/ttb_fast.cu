@@ -874,35 +874,40 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
 constexpr int kChunkPos = 128;
 constexpr int kStSbi = kChunkPos * 8, kStG = kChunkPos * 256, kStG3 = kChunkPos * 512;
 constexpr int kBwdSmem = 4 * kImg + 4 * kImg + kStSbi + kStG + kStG3 + 1024;
+// row-grouped backward (pooled batches): G3 slices are read per distinct row
+// from L2 instead of staged per position, so a chunk holds 3x the positions
+constexpr int kChunkRows = (kStSbi + kStG + kStG3) / (8 + 256);
 
 // X / Z slot element (item, a, b, c); the XOR keeps both the (c, b)-lane
 // dump and the c-lane reads free of bank conflicts
 __device__ __forceinline__ int xs_idx(int it, int a, int b, int c) { return it * 512 + (4 * a + b) * 32 + (c ^ (b << 3)); }
 
-// chunks of whole items with <= kChunkPos positions each (thread 0)
-__device__ inline void make_chunks(const TileMeta* m, int* ch) {
+// chunks of whole items with <= cap positions each (thread 0)
+__device__ inline void make_chunks(const TileMeta* m, int* ch, int cap) {
   int nc = 0, it = 0;
   const int n = m->n;
   ch[0] = 0;
-  if (m->start[n] - m->start[0] <= kChunkPos) {  // the common case: one chunk
+  if (m->start[n] - m->start[0] <= cap) {  // the common case: one chunk
     ch[1] = n;
     ch[kTileItems + 1] = 1;
     return;
   }
   while (it < n) {
     const int base = m->start[it];
-    while (it < n && m->start[it + 1] - base <= kChunkPos) ++it;
+    while (it < n && m->start[it + 1] - base <= cap) ++it;
     ch[++nc] = it;
   }
   ch[kTileItems + 1] = nc;
 }
 
+template <bool kG3>
 __device__ inline void stage_rows_async(int np, const int2* st_sbi, const float* __restrict__ gout,
                                         const float* __restrict__ G3, unsigned m3, float4* st_g, float4* st_g3) {
   for (int e = threadIdx.x; e < np * 16; e += kThreads) {
     const int p = e >> 4, k = e & 15;
     cp_async16(st_g + e, gout + (size_t)st_sbi[p].x * NOUT + 4 * k);
   }
+  if (kG3)
   for (int e = threadIdx.x; e < np * 32; e += kThreads) {
     const int p = e >> 5, cc = e & 31;
     cp_async16(st_g3 + e, reinterpret_cast<const float4*>(G3) + (size_t)cc * m3 + st_sbi[p].y);
@@ -928,13 +933,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
   char* r2_lo = sm + 3 * kImg;
   char* zi = sm + 4 * kImg;  // X / Z slots, then the Z image
   float* xs = reinterpret_cast<float*>(zi);
+  constexpr int kCap = kRows ? kChunkRows : kChunkPos;  // positions per staged chunk
   int2* st_sbi = reinterpret_cast<int2*>(sm + 8 * kImg);
-  float4* st_g = reinterpret_cast<float4*>(sm + 8 * kImg + kStSbi);
-  float4* st_g3 = reinterpret_cast<float4*>(sm + 8 * kImg + kStSbi + kStG);
+  float4* st_g = reinterpret_cast<float4*>(sm + 8 * kImg + kCap * 8);
+  float4* st_g3 = st_g + kCap * 16;  // per-position G3 slices (bag-run path only)
   __shared__ TileMeta s_m[2];
   __shared__ int s_chunk[2][kTileItems + 2];
   __shared__ uint64_t s_mbar;
-  __shared__ long long s_tacc[10];
+  __shared__ long long s_tacc[12];
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = hdr[4];
@@ -943,7 +949,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
   const int tb = cta_tiles[blockIdx.x], te = cta_tiles[blockIdx.x + 1];  // weight-balanced (k_fplan)
   (void)ntiles;
   const unsigned m3 = g.m3;
-  if (threadIdx.x < 10) s_tacc[threadIdx.x] = 0;
+  if (threadIdx.x < 12) s_tacc[threadIdx.x] = 0;
   if (warp == 0) umma::tmem_alloc(&s_tmem, 512);
   if (threadIdx.x == 32) umma::mbar_init(&s_mbar, 1);
   int4 pf = make_int4(0, 0, 0, 0);
@@ -967,15 +973,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
   // prologue: the first tile's first chunk and X operands
   if (tb < te) {
     const TileMeta* m = &s_m[0];
-    if (threadIdx.x == 0) make_chunks(m, s_chunk[0]);
+    if (threadIdx.x == 0) make_chunks(m, s_chunk[0], kCap);
     __syncthreads();
     const int np = m->start[s_chunk[0][1]] - m->start[0];
-    if (threadIdx.x < np) cp_async8(st_sbi + threadIdx.x, sbi + m->start[0] + threadIdx.x);
+    for (int e = threadIdx.x; e < np; e += kThreads) cp_async8(st_sbi + e, sbi + m->start[0] + e);
     copy_img_async(r1_hi, img + (size_t)m->i2 * kImg, 2 * kImg);
     stage_g1_rows_async(m, g, g1img, r2_hi, r2_lo);
     cp_async_wait_all();
     __syncthreads();
-    stage_rows_async(np, st_sbi, gout, G3, m3, st_g, st_g3);
+    stage_rows_async<!kRows>(np, st_sbi, gout, G3, m3, st_g, st_g3);
   }
   uint32_t phase = 0;
   int bad = 0, slot = 0;
@@ -1037,13 +1043,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
       const int it0 = chunk[ch], it1 = chunk[ch + 1];
       const int p0 = m->start[it0];
       if (ch > 0) {
+        const long long _c0 = clock64();
         const int np = m->start[it1] - p0;
-        if (threadIdx.x < np) cp_async8(st_sbi + threadIdx.x, sbi + p0 + threadIdx.x);
+        for (int e = threadIdx.x; e < np; e += kThreads) cp_async8(st_sbi + e, sbi + p0 + e);
         cp_async_wait_all();
         __syncthreads();
-        stage_rows_async(np, st_sbi, gout, G3, m3, st_g, st_g3);
+        stage_rows_async<!kRows>(np, st_sbi, gout, G3, m3, st_g, st_g3);
         cp_async_wait_all();
         __syncthreads();
+        if ((dbg & 8) && threadIdx.x == 0 && blockIdx.x == 0) s_tacc[10] += clock64() - _c0;
       }
       // ---- Z / dG3 phase: warp <-> item, lane <-> c
       for (int it = it0 + warp; it < it1; it += kThreads / 32) {
@@ -1066,6 +1074,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
             lead &= lead - 1;
             unsigned mem = __shfl_sync(0xffffffffu, grp, ld);
             const int i3 = __shfl_sync(0xffffffffu, my_i3, ld);
+            const float4 h3 = __ldg(reinterpret_cast<const float4*>(G3) + (size_t)lane * m3 + i3);
             float gv[64];
             {
               const int q = s0 + ld;
@@ -1097,7 +1106,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
 #pragma unroll
               for (int j = 0; j < 4; ++j) dh[j] = fmaf(x[ab], gv[4 * ab + j], dh[j]);
             if (!(dbg & 1)) red_v4(dG3 + ((size_t)lane * m3 + i3) * 4, dh[0], dh[1], dh[2], dh[3]);
-            const float4 h3 = st_g3[(s0 + ld) * 32 + lane];
 #pragma unroll
             for (int ab = 0; ab < 16; ++ab) {
               z[ab] = fmaf(gv[4 * ab], h3.x, z[ab]);
@@ -1159,7 +1167,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
 #pragma unroll
           for (int ab = 0; ab < 16; ++ab) xs[xs_idx(it, ab >> 2, ab & 3, lane)] = 0.f;
       }
-      __syncthreads();  // staging reused by the next chunk / tile
+      {
+        const long long _c0 = clock64();
+        __syncthreads();  // staging reused by the next chunk / tile
+        if ((dbg & 8) && threadIdx.x == 0 && blockIdx.x == 0) s_tacc[11] += clock64() - _c0;
+      }
     }
     TSTAMP(4);
     const int tn = t + 1;
@@ -1200,10 +1212,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
     }
     // ---- next tile: chunk list and first chunk's positions
     if (tn < te) {
-      if (threadIdx.x == 0) make_chunks(mn, s_chunk[slot ^ 1]);
+      if (threadIdx.x == 0) make_chunks(mn, s_chunk[slot ^ 1], kCap);
       __syncthreads();
       npn = mn->start[s_chunk[slot ^ 1][1]] - mn->start[0];
-      if (threadIdx.x < npn) cp_async8(st_sbi + threadIdx.x, sbi + mn->start[0] + threadIdx.x);
+      for (int e = threadIdx.x; e < npn; e += kThreads) cp_async8(st_sbi + e, sbi + mn->start[0] + e);
       cp_async_commit();
     }
 #pragma unroll
@@ -1223,7 +1235,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
       umma::commit(&s_mbar);
     }
     // the next tile's first-chunk rows stream in meanwhile
-    if (tn < te) stage_rows_async(npn, st_sbi, gout, G3, m3, st_g, st_g3);
+    if (tn < te) stage_rows_async<!kRows>(npn, st_sbi, gout, G3, m3, st_g, st_g3);
     umma::mbar_wait(&s_mbar, phase);
     phase ^= 1u;
     umma::fence_after_sync();
@@ -1284,7 +1296,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
   if (bad) atomicOr(&hdr[0], 8);
   if ((dbg & 8) && threadIdx.x == 0 && blockIdx.x == 0) {
     s_tacc[0] = te - tb;
-    for (int q = 0; q < 10; ++q) reinterpret_cast<long long*>(hdr + 16)[q] = s_tacc[q];
+    for (int q = 0; q < 12; ++q) reinterpret_cast<long long*>(hdr + 16)[q] = s_tacc[q];
   }
   if (warp == 0) umma::tmem_free(tmem, 512);
 }

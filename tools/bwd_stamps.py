@@ -30,10 +30,11 @@ for rep in range(3):
     torch.cuda.synchronize()
 base = (eng._ws.data_ptr() + 255) & ~255
 o = base - eng._ws.data_ptr()
-h = eng._ws[o: o + 256].cpu().numpy().view(np.int64)[8:18]
+h = eng._ws[o: o + 256].cpu().numpy().view(np.int64)[8:20]
 nt = max(int(h[0]), 1)
 tot = h[1:9].sum()
 print(f"{wl}: {nt} tiles in block 0, {tot / nt:.0f} cycles per tile")
 for nm, v in zip(names, h[1:9]):
     print(f"  {nm:14s} {v / nt:8.0f} cyc  {100 * v / max(tot, 1):5.1f}%")
-print(f"  (dG2 MMA issue, 32 MMAs: {h[9] / nt:.0f} cyc)")
+print(f"  (dG2 MMA issue, 32 MMAs: {h[9] / nt:.0f} cyc; Z phase: chunk staging {h[10] / nt:.0f}, "
+      f"end-of-chunk barrier wait {h[11] / nt:.0f})")
