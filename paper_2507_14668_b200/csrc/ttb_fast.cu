@@ -876,7 +876,7 @@ constexpr int kStSbi = kChunkPos * 8, kStG = kChunkPos * 256, kStG3 = kChunkPos 
 constexpr int kBwdSmem = 4 * kImg + 4 * kImg + kStSbi + kStG + kStG3 + 1024;
 // row-grouped backward (pooled batches): G3 slices are read per distinct row
 // from L2 instead of staged per position, so a chunk holds 3x the positions
-constexpr int kChunkRows = (kStSbi + kStG + kStG3) / (8 + 256);
+constexpr int kChunkRows = (kStSbi + kStG + kStG3 - 8 * 256) / (8 + 256) & ~7;  // + 8 warps' 256 B row scratch
 
 // X / Z slot element (item, a, b, c); the XOR keeps both the (c, b)-lane
 // dump and the c-lane reads free of bank conflicts
@@ -937,6 +937,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
   int2* st_sbi = reinterpret_cast<int2*>(sm + 8 * kImg);
   float4* st_g = reinterpret_cast<float4*>(sm + 8 * kImg + kCap * 8);
   float4* st_g3 = st_g + kCap * 16;  // per-position G3 slices (bag-run path only)
+  float4* st_acc = st_g + kCap * 16;  // row path: per-warp summed gradient row
   __shared__ TileMeta s_m[2];
   __shared__ int s_chunk[2][kTileItems + 2];
   __shared__ uint64_t s_mbar;
@@ -1075,31 +1076,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
             unsigned mem = __shfl_sync(0xffffffffu, grp, ld);
             const int i3 = __shfl_sync(0xffffffffu, my_i3, ld);
             const float4 h3 = __ldg(reinterpret_cast<const float4*>(G3) + (size_t)lane * m3 + i3);
+            // the row's summed gradient row: lane-parallel (two floats per
+            // lane per member) into the warp's scratch, then broadcast reads
+            const float4* src = st_g + (s0 + ld) * 16;
+            if (mem & (mem - 1)) {
+              float2 acc = make_float2(0.f, 0.f);
+              for (; mem; mem &= mem - 1) {
+                const float2 v = reinterpret_cast<const float2*>(st_g + (s0 + __ffs(mem) - 1) * 16)[lane];
+                acc.x += v.x;
+                acc.y += v.y;
+              }
+              reinterpret_cast<float2*>(st_acc + warp * 16)[lane] = acc;
+              __syncwarp();
+              src = st_acc + warp * 16;
+            }
             float gv[64];
-            {
-              const int q = s0 + ld;
 #pragma unroll
-              for (int k = 0; k < 16; ++k) {
-                const float4 v = st_g[q * 16 + k];
-                gv[4 * k] = v.x;
-                gv[4 * k + 1] = v.y;
-                gv[4 * k + 2] = v.z;
-                gv[4 * k + 3] = v.w;
-              }
+            for (int k = 0; k < 16; ++k) {
+              const float4 v = src[k];
+              gv[4 * k] = v.x;
+              gv[4 * k + 1] = v.y;
+              gv[4 * k + 2] = v.z;
+              gv[4 * k + 3] = v.w;
             }
-            mem &= mem - 1;
-            while (mem) {
-              const int q = s0 + __ffs(mem) - 1;
-              mem &= mem - 1;
-#pragma unroll
-              for (int k = 0; k < 16; ++k) {
-                const float4 v = st_g[q * 16 + k];
-                gv[4 * k] += v.x;
-                gv[4 * k + 1] += v.y;
-                gv[4 * k + 2] += v.z;
-                gv[4 * k + 3] += v.w;
-              }
-            }
+            __syncwarp();  // the scratch is rewritten by the next row
             float dh[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int ab = 0; ab < 16; ++ab)
