@@ -1218,53 +1218,48 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
       for (int e = threadIdx.x; e < npn; e += kThreads) cp_async8(st_sbi + e, sbi + mn->start[0] + e);
       cp_async_commit();
     }
+    // Z image hi (the slots' region) and lo (the dead staging rows, past the
+    // next tile's positions): both E passes back to back
+    char* zlo = sm + 8 * kImg + 4096;
 #pragma unroll
-    for (int i = 0; i < 64; ++i)
-      *(float*)(zi + umma::sw128_off(64 * half + i, row, 128)) = umma::tf32_rna(zr[i]);
+    for (int i = 0; i < 64; ++i) {
+      float hh, ll;
+      umma::split3(zr[i], hh, ll);
+      const uint32_t o = umma::sw128_off(64 * half + i, row, 128);
+      *(float*)(zi + o) = hh;
+      *(float*)(zlo + o) = ll;
+    }
     cp_async_wait_all();  // next tile's positions
     sync_for_mma();
     TSTAMP(5);
     if (threadIdx.x == 0) {
-      // E tile [(item, a), (hi | lo) k] = sum_(c, b) Z . G2^T, pass 1: Z hi
+      // E tile [(item, a), (hi | lo) k] = sum_(c, b) (Z hi . G2^T + Z lo . G2 hi^T)
+      const uint64_t d_zl = umma::desc_sw128(umma::smem_u32(zlo));
 #pragma unroll
       for (int k0 = 0; k0 < 128; k0 += 8) {
         const uint32_t oa = (uint32_t)((k0 >> 5) * 128 * 128 + (k0 & 31) * 4) >> 4;
         const uint32_t ob = (uint32_t)((k0 >> 5) * 64 * 128 + (k0 & 31) * 4) >> 4;
         umma::mma_tf32(tmem + 448, d_zi + oa, d_r1h + ob, id64, k0 > 0 ? 1u : 0u);
       }
-      umma::commit(&s_mbar);
-    }
-    // the next tile's first-chunk rows stream in meanwhile
-    if (tn < te) stage_rows_async<!kRows>(npn, st_sbi, gout, G3, m3, st_g, st_g3);
-    umma::mbar_wait(&s_mbar, phase);
-    phase ^= 1u;
-    umma::fence_after_sync();
-    TSTAMP(6);
-    // pass 2: Z lo
-#pragma unroll
-    for (int i = 0; i < 64; ++i) {
-      float h, l;
-      umma::split3(zr[i], h, l);
-      *(float*)(zi + umma::sw128_off(64 * half + i, row, 128)) = l;
-    }
-    sync_for_mma();
-    if (threadIdx.x == 0) {
 #pragma unroll
       for (int k0 = 0; k0 < 128; k0 += 8) {
         const uint32_t oa = (uint32_t)((k0 >> 5) * 128 * 128 + (k0 & 31) * 4) >> 4;
         const uint32_t ob = (uint32_t)((k0 >> 5) * 64 * 128 + (k0 & 31) * 4) >> 4;
-        umma::mma_tf32(tmem + 448, d_zi + oa, d_r1h + ob, id32, 1u);  // Z lo . G2 hi only
+        umma::mma_tf32(tmem + 448, d_zl + oa, d_r1h + ob, id32, 1u);  // Z lo . G2 hi only
       }
       umma::commit(&s_mbar);
     }
     umma::mbar_wait(&s_mbar, phase);
     phase ^= 1u;
     umma::fence_after_sync();
+    TSTAMP(6);
     TSTAMP(7);
-    // the next tile's X operands (R12 is free now)
+    // the next tile's X operands (R12 is free now), then its first-chunk rows
+    // (the staging region is free once the E GEMM has read the Z lo image)
     if (tn < te) {
       copy_img_async(r1_hi, img + (size_t)mn->i2 * kImg, 2 * kImg);
       stage_g1_rows_async(mn, g, g1img, r2_hi, r2_lo);
+      stage_rows_async<!kRows>(npn, st_sbi, gout, G3, m3, st_g, st_g3);
     }
     if (!(dbg & 4)) {
       float v[16], w2[16];
