@@ -589,6 +589,7 @@ constexpr int kFwdSplitRounds = 4;  // rows with <= this many segments: c split 
 __host__ __device__ constexpr int fwd_g3_bytes(unsigned m3) { return (int)(32 * m3 * 16 + 1023) & ~1023; }
 __host__ __device__ constexpr int fwd_smem_bytes(unsigned m3) { return 4 * kImg + fwd_g3_bytes(m3) + 2 * kMaxTilePos * 8 + 1024; }
 
+template <bool kPooled>
 __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __restrict__ g1img,
                                                         const float* __restrict__ G3, const float* __restrict__ img,
                                                         const int* __restrict__ hdr, const int4* __restrict__ tile_info,
@@ -795,24 +796,64 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
         float acc[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+        if (kPooled) {
+          // per quarter of c: the segment's G3 slices summed first, then one
+          // rank-8 update of the 16 outputs (a segment of k lookups costs 512
+          // FMA + 128 (k - 1) adds instead of 512 k FMA)
 #pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
-          float xh[64];  // xh[4 c' + b] = X[item][a][b][16 ch + c']
-          umma::tmem_ld32(trow + 64 * ch, *(float(*)[32])(xh));
-          umma::tmem_ld32(trow + 64 * ch + 32, *(float(*)[32])(xh + 32));
-          if (have) {
-            for (int l = qq; l < e; ++l) {
-              const float4* g3 = s_g3 + (unsigned)s_sbi[l].y + 16 * ch * m3;
+          for (int cq = 0; cq < 4; ++cq) {
+            float xq[32];  // xq[4 c' + b] = X[item][a][b][8 cq + c']
+            umma::tmem_ld32(trow + 32 * cq, xq);
+            if (have) {
+              float4 gs[8];
+              {
+                const float4* g3 = s_g3 + (unsigned)s_sbi[qq].y + 8 * cq * m3;
 #pragma unroll
-              for (int c = 0; c < 16; ++c) {
-                const float4 gv = g3[c * m3];
+                for (int c = 0; c < 8; ++c) gs[c] = g3[c * m3];
+              }
+              for (int l = qq + 1; l < e; ++l) {
+                const float4* g3 = s_g3 + (unsigned)s_sbi[l].y + 8 * cq * m3;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                  const float4 gv = g3[c * m3];
+                  gs[c].x += gv.x;
+                  gs[c].y += gv.y;
+                  gs[c].z += gv.z;
+                  gs[c].w += gv.w;
+                }
+              }
+#pragma unroll
+              for (int c = 0; c < 8; ++c)
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
-                  const float xv = xh[4 * c + b];
-                  acc[4 * b + 0] = fmaf(xv, gv.x, acc[4 * b + 0]);
-                  acc[4 * b + 1] = fmaf(xv, gv.y, acc[4 * b + 1]);
-                  acc[4 * b + 2] = fmaf(xv, gv.z, acc[4 * b + 2]);
-                  acc[4 * b + 3] = fmaf(xv, gv.w, acc[4 * b + 3]);
+                  const float xv = xq[4 * c + b];
+                  acc[4 * b + 0] = fmaf(xv, gs[c].x, acc[4 * b + 0]);
+                  acc[4 * b + 1] = fmaf(xv, gs[c].y, acc[4 * b + 1]);
+                  acc[4 * b + 2] = fmaf(xv, gs[c].z, acc[4 * b + 2]);
+                  acc[4 * b + 3] = fmaf(xv, gs[c].w, acc[4 * b + 3]);
+                }
+            }
+          }
+        } else {
+  #pragma unroll
+          for (int ch = 0; ch < 2; ++ch) {
+            float xh[64];  // xh[4 c' + b] = X[item][a][b][16 ch + c']
+            umma::tmem_ld32(trow + 64 * ch, *(float(*)[32])(xh));
+            umma::tmem_ld32(trow + 64 * ch + 32, *(float(*)[32])(xh + 32));
+            if (have) {
+              for (int l = qq; l < e; ++l) {
+                const float4* g3 = s_g3 + (unsigned)s_sbi[l].y + 16 * ch * m3;
+  #pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                  const float4 gv = g3[c * m3];
+  #pragma unroll
+                  for (int b = 0; b < 4; ++b) {
+                    const float xv = xh[4 * c + b];
+                    acc[4 * b + 0] = fmaf(xv, gv.x, acc[4 * b + 0]);
+                    acc[4 * b + 1] = fmaf(xv, gv.y, acc[4 * b + 1]);
+                    acc[4 * b + 2] = fmaf(xv, gv.z, acc[4 * b + 2]);
+                    acc[4 * b + 3] = fmaf(xv, gv.w, acc[4 * b + 3]);
+                  }
                 }
               }
             }
@@ -1343,7 +1384,8 @@ cudaError_t fast_forward(ttb_handle* h, const float* c0, const float* c1, const 
   static bool attr = false;
   if (!attr) {
     if ((e = ensure_attr((const void*)k_coreimg, img_smem))) return e;
-    if ((e = ensure_attr((const void*)k_fwd, fwd_smem_bytes(kFwdMaxM3)))) return e;
+    if ((e = ensure_attr((const void*)k_fwd<false>, fwd_smem_bytes(kFwdMaxM3)))) return e;
+    if ((e = ensure_attr((const void*)k_fwd<true>, fwd_smem_bytes(kFwdMaxM3)))) return e;
     if ((e = ensure_attr((const void*)k_bwd<false>, kBwdSmem))) return e;
     if ((e = ensure_attr((const void*)k_bwd<true>, kBwdSmem))) return e;
     attr = true;
@@ -1366,7 +1408,8 @@ cudaError_t fast_forward(ttb_handle* h, const float* c0, const float* c1, const 
   const int grid = h->num_sms;  // = the plan's CTA ranges (k_fplan cta_tiles)
   {
     ProfScope _ps(h, s, "f_fwd");
-    if ((e = launch_pdl(k_fwd, dim3(grid), dim3(kFwdThreads), fwd_smem_bytes(h->kg.m3), s, h->kg, (const float*)w.f_g1img, c2,
+    // pooled bags: segments of several lookups (G3 slices summed before the product)
+    if ((e = launch_pdl(h->T > h->B ? k_fwd<true> : k_fwd<false>, dim3(grid), dim3(kFwdThreads), fwd_smem_bytes(h->kg.m3), s, h->kg, (const float*)w.f_g1img, c2,
                         (const float*)w.f_img, (const int*)w.fast_hdr, (const int4*)w.f_tile_info,
                         (const int*)w.f_item_start, (const unsigned*)w.f_item_key, (const int2*)w.f_sbi, out,
                         (const int*)w.f_cta, direct, getenv("TTB_DBG") ? atoi(getenv("TTB_DBG")) : 0)))
