@@ -1,3 +1,5 @@
+"""Step-by-step smoke of the tensor-core pipeline (plan, forward, backward),
+synchronising after each: python tools/debug_fast.py [B] [big]"""
 import sys
 import numpy as np
 import torch
@@ -20,10 +22,3 @@ out = eng.forward(cores)
 torch.cuda.synchronize(); print("fwd ok", flush=True)
 g = eng.backward(cores, torch.randn(B, 64, device=dev))
 torch.cuda.synchronize(); print("bwd ok", flush=True)
-base = (eng._ws.data_ptr() + 255) & ~255
-off = base - eng._ws.data_ptr()
-h = eng._ws[off: off + 256].cpu().numpy().view(np.uint64)
-ts = h[8:8 + 18].astype(np.int64)
-for it in range(2):
-    row = ts[it * 9: it * 9 + 9]
-    print("tile", it, "phase deltas (ns):", list(np.diff(row)))
