@@ -432,13 +432,16 @@ __global__ void __launch_bounds__(kImgThreads) k_coreimg(float* __restrict__ G1,
   // the slice in shared memory first (row k padded to 129 floats), then each
   // image row written by one warp — 32 consecutive K of one 128-byte row, no
   // bank conflicts (a direct scatter from the load layout is 16-way)
-  float* raw = reinterpret_cast<float*>(sm + 4 * kImg);
+  float* raw = reinterpret_cast<float*>(sm);
 #pragma unroll
   for (int r = 0; r < kPer; ++r) {
     const int e = threadIdx.x + r * kImgThreads;
     raw[(e >> 7) * 129 + (e & 127)] = vals[r];
   }
   __syncthreads();
+  // image rows go straight to global memory: each warp store is one whole
+  // (swizzled) 128-byte row, and the CTA needs only the 16.5 KB slice buffer
+  char* gi = reinterpret_cast<char*>(img + (size_t)i2 * (4 * kImg / 4));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
   for (int r = 0; r < 128 / (kImgThreads / 32); ++r) {  // cb images: row cb = 4 c + b, K = k = lane
@@ -446,22 +449,17 @@ __global__ void __launch_bounds__(kImgThreads) k_coreimg(float* __restrict__ G1,
     float hi, lo;
     umma::split3(raw[lane * 129 + b * 32 + c], hi, lo);
     const uint32_t o1 = umma::sw128_off(cb, lane, 128);
-    *(float*)(sm + o1) = hi;
-    *(float*)(sm + kImg + o1) = lo;
+    *(float*)(gi + o1) = hi;
+    *(float*)(gi + kImg + o1) = lo;
   }
 #pragma unroll
   for (int r = 0; r < 128 / (kImgThreads / 32); ++r) {  // k images: row k, K = cb (block of 32)
     const int unit = warp + r * (kImgThreads / 32), k = unit >> 2, cb = 32 * (unit & 3) + lane;
     float hi, lo;
     umma::split3(raw[k * 129 + (cb & 3) * 32 + (cb >> 2)], hi, lo);
-    *(float*)(sm + 2 * kImg + umma::sw128_off(k, cb, 64)) = hi;
-    *(float*)(sm + 2 * kImg + umma::sw128_off(32 + k, cb, 64)) = lo;
+    *(float*)(gi + 2 * kImg + umma::sw128_off(k, cb, 64)) = hi;
+    *(float*)(gi + 2 * kImg + umma::sw128_off(32 + k, cb, 64)) = lo;
   }
-  __syncthreads();
-  uint4* dst = reinterpret_cast<uint4*>(img + (size_t)i2 * (4 * kImg / 4));
-  const uint4* src = reinterpret_cast<const uint4*>(sm);
-#pragma unroll
-  for (int e = threadIdx.x; e < 4 * kImg / 16; e += kImgThreads) dst[e] = src[e];
 }
 
 // ------------------------------------------------------------ async copies
@@ -1380,7 +1378,7 @@ cudaError_t fast_forward(ttb_handle* h, const float* c0, const float* c1, const 
                          cudaStream_t s) {
   Workspace& w = h->w;
   cudaError_t e;
-  const int img_smem = 4 * kImg + 32 * 129 * 4 + 1024;
+  const int img_smem = 32 * 129 * 4 + 1024;
   static bool attr = false;
   if (!attr) {
     if ((e = ensure_attr((const void*)k_coreimg, img_smem))) return e;
@@ -1450,7 +1448,7 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
   if (mode == 1) {
     // SGD(+momentum) on all three cores, writing the next step's G1 / G2
     // images from the updated values
-    const int img_smem = 4 * kImg + 32 * 129 * 4 + 1024;
+    const int img_smem = 32 * 129 * 4 + 1024;
     const int ng3 = (int)((n2 + kImgThreads - 1) / kImgThreads);
     SgdArgs u = {w.f_grad, v0, v1, v2, p2, lr, mu, mask, 1};
     ProfScope _ps(h, s, "f_sgd");
