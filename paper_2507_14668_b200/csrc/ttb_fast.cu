@@ -1154,12 +1154,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
             }
           }
         } else {
-          // positions in plan order; runs of one bag share the gradient row,
-          // X^T g and the Z update
+          // one lookup per bag (T = B): every position is its own bag, so a
+          // position is one gradient row, one dG3 reduction and one Z update
           const int s1 = m->start[it + 1] - p0;
-          int qq = m->start[it] - p0;
-          while (qq < s1) {
-            const int bag = st_sbi[qq].x;
+          for (int qq = m->start[it] - p0; qq < s1; ++qq) {
+            const int i3 = st_sbi[qq].y;
+            const float4 h3 = st_g3[qq * 32 + lane];
             float gv[64];
   #pragma unroll
             for (int k = 0; k < 16; ++k) {
@@ -1174,23 +1174,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
             for (int ab = 0; ab < 16; ++ab)
   #pragma unroll
               for (int j = 0; j < 4; ++j) dh[j] = fmaf(x[ab], gv[4 * ab + j], dh[j]);
-            float gs[4] = {0.f, 0.f, 0.f, 0.f};
-            int e = qq;
-            for (; e < s1; ++e) {
-              const int2 pr = st_sbi[e];
-              if (pr.x != bag) break;
-              const float4 h3 = st_g3[e * 32 + lane];
-              gs[0] += h3.x;
-              gs[1] += h3.y;
-              gs[2] += h3.z;
-              gs[3] += h3.w;
-              if (!(dbg & 1)) red_v4(dG3 + ((size_t)lane * m3 + pr.y) * 4, dh[0], dh[1], dh[2], dh[3]);
+            if (!(dbg & 1)) red_v4(dG3 + ((size_t)lane * m3 + i3) * 4, dh[0], dh[1], dh[2], dh[3]);
+  #pragma unroll
+            for (int ab = 0; ab < 16; ++ab) {
+              z[ab] = fmaf(gv[4 * ab], h3.x, z[ab]);
+              z[ab] = fmaf(gv[4 * ab + 1], h3.y, z[ab]);
+              z[ab] = fmaf(gv[4 * ab + 2], h3.z, z[ab]);
+              z[ab] = fmaf(gv[4 * ab + 3], h3.w, z[ab]);
             }
-  #pragma unroll
-            for (int ab = 0; ab < 16; ++ab)
-  #pragma unroll
-              for (int j = 0; j < 4; ++j) z[ab] = fmaf(gv[4 * ab + j], gs[j], z[ab]);
-            qq = e;
           }
         }
         float zs = 0.f;
@@ -1437,7 +1428,8 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
   const int grid = h->num_sms;  // = the plan's CTA ranges (k_fplan cta_tiles)
   {
     ProfScope _ps(h, s, "f_bwd");
-    // pooled bags (more lookups than bags) repeat rows inside a prefix: group by row
+    // pooled bags (more lookups than bags) repeat rows inside a prefix: group
+    // by row; otherwise (T = B, bags are single lookups) position by position
     if ((e = launch_pdl(h->T > h->B ? k_bwd<true> : k_bwd<false>, dim3(grid), dim3(kThreads), kBwdSmem, s, h->kg, (const float*)w.f_g1img, c2,
                         (const float*)w.f_img, (const int4*)w.f_tile_info, (const int*)w.f_item_start,
                         (const unsigned*)w.f_item_key, (const int2*)w.f_sbi, gout, g0, g1, g2, w.fast_hdr,
