@@ -891,14 +891,18 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
 //   smem   R12 64 KB: X operands (G2 cb image, G1 rows image), then the
 //                     64-row G2 k image and the 64-row G1^T image
 //          XZ  64 KB: per item a 512-float slot holding X (dumped from TMEM),
-//                     overwritten by Z; finally the Z image (rows (item, a),
-//                     K = (c, b)) the E GEMM reads: hi, then lo
-//          ST  97 KB: per chunk of <= kChunkPos positions: (bag, i3), the
-//                     bag's gradient row, the lookup's G3 slice (c, j)
+//                     overwritten by Z; finally the Z hi image (rows (item, a),
+//                     K = (c, b)) the E GEMM reads
+//          ST  97 KB: per chunk of positions: (bag, i3), the bag's gradient
+//                     row and (bag-run path) the lookup's G3 slice (c, j); the
+//                     row path adds a per-warp 256 B row scratch. Once the Z
+//                     phase is done it holds the Z lo image (at 4 KB, past the
+//                     next tile's (bag, i3) list)
 // Z / dG3 phase: one warp per item, lane <-> c: every lane holds the item's
 // X[., ., c] and accumulates Z[., ., c] in registers, so a position costs
-// 128 FMAs per lane and no cross-lane reduction. The next tile's first chunk
-// and X operands are fetched while this tile's GEMMs and epilogue run.
+// 128 FMAs per lane and no cross-lane reduction (k_bwd<true>: per distinct
+// row of the item instead). The next tile's X operands and first-chunk rows
+// are fetched after the E GEMM, during the dG1 / dG2 reductions.
 // per-phase SM cycles (thread 0, summed over block 0's tiles) into hdr[16..]
 // as 9 u64 + the tile count (TTB_DBG & 8); phase k = TSTAMP(k-1) .. TSTAMP(k)
 #define TSTAMP(k)                                                                                      \
