@@ -745,14 +745,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
           umma::tmem_wait_st();
         }
         named_sync(1 + q4, 128);  // the quadrant's partials are in TMEM
-        if (quarter == 0) {
-          float p[16];
+        if (quarter == 0) {  // the three partials in flight together, one wait
+          uint32_t p12[32], p3[16];
+          umma::tmem_ld32_nw(tpart + 16, p12);
+          umma::tmem_ld16_nw(tpart + 48, p3);
+          umma::tmem_wait_ld();
   #pragma unroll
-          for (int qd = 1; qd < 4; ++qd) {
-            umma::tmem_ld16(tpart + 16 * qd, p);
-  #pragma unroll
-            for (int i = 0; i < 16; ++i) acc[i] += p[i];
-          }
+          for (int i = 0; i < 16; ++i)
+            acc[i] += (__uint_as_float(p12[i]) + __uint_as_float(p12[16 + i])) + __uint_as_float(p3[i]);
           if (have) {
             float* o = out + (size_t)bag * NOUT + a * 16;
             if (direct) {
