@@ -1254,7 +1254,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
     }
     // Z image hi (the slots' region) and lo (the dead staging rows, past the
     // next tile's positions): both E passes back to back
-    char* zlo = sm + 8 * kImg + 4096;
+    // (bag-run path: exactly the G3-slice staging, so the next tile's gradient
+    // rows can stream in while the E GEMM runs)
+    char* zlo = sm + 8 * kImg + (kRows ? 4096 : kChunkPos * 8 + kChunkPos * 256);
 #pragma unroll
     for (int i = 0; i < 64; ++i) {
       float hh, ll;
@@ -1283,6 +1285,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
       }
       umma::commit(&s_mbar);
     }
+    if (!kRows && tn < te)  // the next tile's first-chunk gradient rows
+      for (int e = threadIdx.x; e < npn * 16; e += kThreads)
+        cp_async16(st_g + e, gout + (size_t)st_sbi[e >> 4].x * NOUT + 4 * (e & 15));
     umma::mbar_wait(&s_mbar, phase);
     phase ^= 1u;
     umma::fence_after_sync();
@@ -1293,7 +1298,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
     if (tn < te) {
       copy_img_async(r1_hi, img + (size_t)mn->i2 * kImg, 2 * kImg);
       stage_g1_rows_async(mn, g, g1img, r2_hi, r2_lo);
-      stage_rows_async<!kRows>(npn, st_sbi, gout, G3, m3, st_g, st_g3);
+      if (kRows) {
+        stage_rows_async<false>(npn, st_sbi, gout, G3, m3, st_g, st_g3);
+      } else {  // the G3 slices (their region held the Z lo image)
+        for (int e = threadIdx.x; e < npn * 32; e += kThreads)
+          cp_async16(st_g3 + e, reinterpret_cast<const float4*>(G3) + (size_t)(e & 31) * m3 + st_sbi[e >> 5].y);
+      }
     }
     if (!(dbg & 4)) {
       float v[16], w2[16];
