@@ -936,8 +936,11 @@ __device__ inline void make_chunks(const TileMeta* m, int* ch, int cap) {
     return;
   }
   while (it < n) {
-    const int base = m->start[it];
+    const int first = it, base = m->start[it];
     while (it < n && m->start[it + 1] - base <= cap) ++it;
+    // whole rounds of one item per warp where possible (items have similar
+    // lengths inside a tile, so the warps finish a chunk together)
+    if (it < n && it - first > kThreads / 32) it = first + (it - first) / (kThreads / 32) * (kThreads / 32);
     ch[++nc] = it;
   }
   ch[kTileItems + 1] = nc;
