@@ -139,10 +139,30 @@ int ttb_cores_modified(ttb_handle *h);
 int ttb_sgd_update(float *param, const float *grad, double *velocity,
                    int64_t n, double lr, double momentum, ttb_stream stream);
 
+/* fused_update with the reference's validation (backward.py:186-204): the
+ * gradient is checked for non-finite values first (TTB_ERRBIT_NONFINITE is
+ * OR-ed into the caller's DEVICE int *err), and the update runs only if *err
+ * is still 0 — otherwise param and velocity are left untouched. Calling
+ * ttb_check_finite on several gradients before their updates gives the
+ * reference's all-or-nothing semantics across arrays. Stream-ordered. */
+int ttb_check_finite(const float *grad, int64_t n, int *err, ttb_stream stream);
+int ttb_sgd_update_checked(float *param, const float *grad, double *velocity,
+                           int64_t n, double lr, double momentum, int *err,
+                           ttb_stream stream);
+
 /* SYNCS `stream`. status[0] = device error bits (TTB_ERRBIT_*), [1] = T,
  * [2] = B, [3] = P (distinct prefixes), [4] = S (bag-prefix segments),
  * [5] = U (distinct rows; valid after backward), [6] = plan generation. */
 int ttb_read_status(ttb_handle *h, int64_t status[8], ttb_stream stream);
+
+/* The reference's work counters for the current plan (SYNCS `stream`):
+ * su[0] = S, the (bag, prefix) segments (lookup.py:280-284, 294-295);
+ * su[1] = U, the distinct rows (backward.py:81-87, 218-222). The tensor-core
+ * pipeline counts them on demand from the plan's inputs (which must still be
+ * valid) — its step kernels never form them; afterwards ttb_read_status
+ * reports them too. The deterministic pipeline reports U = -1 until a
+ * backward ran. */
+int ttb_plan_counts(ttb_handle *h, int64_t su[2], ttb_stream stream);
 
 /* Plan read-back (after ttb_plan). Any pointer may be NULL. Sizes use the
  * counts of ttb_read_status.
@@ -154,6 +174,20 @@ int ttb_read_status(ttb_handle *h, int64_t status[8], ttb_stream stream);
 int ttb_export_plan(ttb_handle *h, int64_t *work, int64_t *slot_occ,
                     int64_t *seg_ids, int64_t *seg_inv, int64_t *digits,
                     ttb_stream stream);
+
+/* Tensor-core pipeline plan read-back (after ttb_plan with TTB_OPT_FAST;
+ * SYNCS `stream`). counts (host) = {work items, tiles, step-kernel CTAs, T};
+ * every pointer is a nullable DEVICE buffer:
+ *   item_start  items + 1 int32: first position of each item (last = T)
+ *   item_key    items u32: the item's prefix key i2 * m1 + i1
+ *   tile_info   tiles x 4 int32: (i2, first item, items, first position)
+ *   sbi         T x 2 int32: (bag, i3) of every position, item order
+ *   cta_tiles   CTAs + 1 int32: first tile of each step-kernel CTA
+ * A work item is a run of <= 32 lookups of one prefix (the reuse unit of
+ * lookup.py:127-149); a tile is <= 32 items of one i2. */
+int ttb_export_fast_plan(ttb_handle *h, int64_t counts[4], int32_t *item_start,
+                         uint32_t *item_key, int32_t *tile_info, int32_t *sbi,
+                         int32_t *cta_tiles, ttb_stream stream);
 
 /* unique_aggregate read-back (after ttb_backward / ttb_backward_sgd):
  * rows U int64 in first-occurrence order, grads U x N fp32 (nullable) —

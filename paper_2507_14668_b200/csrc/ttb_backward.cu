@@ -314,17 +314,19 @@ __global__ void __launch_bounds__(kBlock) k_dg13_reduce(KGeom g, int G1S, int N3
 }
 
 __global__ void k_sgd(float* __restrict__ p, const float* __restrict__ gr, double* __restrict__ v, int64_t n,
-                      double lr, double mu) {
+                      double lr, double mu, const int* __restrict__ err) {
   pdl_enter();
+  if (err && *(volatile const int*)err != 0) return;  // a latched error cancels the update
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = sgd_apply(p[i], gr[i], v ? v + i : nullptr, lr, mu);
 }
 
-cudaError_t launch_sgd(float* p, const float* g, double* v, int64_t n, double lr, double mu, cudaStream_t s) {
+cudaError_t launch_sgd(float* p, const float* g, double* v, int64_t n, double lr, double mu, cudaStream_t s,
+                       const int* err) {
   if (n <= 0) return cudaSuccess;
   int64_t grid = (n + kBlock - 1) / kBlock;
   if (grid > 148 * 8) grid = 148 * 8;
-  launch_pdl(k_sgd, dim3((int)grid), dim3(kBlock), 0, s, p, g, v, n, lr, mu);
+  launch_pdl(k_sgd, dim3((int)grid), dim3(kBlock), 0, s, p, g, v, n, lr, mu, err);
   count_launch();
   return cudaGetLastError();
 }
@@ -352,11 +354,8 @@ static size_t bwd_smem(const D& d, int ch) {
 // would otherwise sit on every launch path.
 template <class K>
 static cudaError_t ensure_smem(K kernel, size_t bytes) {
-  static size_t done = 0;
-  if (bytes <= done || bytes <= 48 * 1024) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e == cudaSuccess) done = bytes;
-  return e;
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  return ensure_kernel_smem((const void*)kernel, bytes);
 }
 
 template <class D>

@@ -2,6 +2,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
+
 #include "ttb_internal.h"
 
 namespace ttb {
@@ -10,6 +12,43 @@ bool choose_chunks(const DynDims& d, int* chf, int* chb);
 }  // namespace ttb
 
 using namespace ttb;
+
+namespace ttb {
+// (kernel, device) -> dynamic shared memory bytes already allowed
+namespace {
+struct SmemAttr {
+  const void* kernel;
+  int device;
+  size_t bytes;
+};
+std::mutex g_attr_mu;
+SmemAttr g_attr[256];
+int g_nattr = 0;
+}  // namespace
+
+cudaError_t ensure_kernel_smem(const void* kernel, size_t bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(g_attr_mu);
+  int slot = -1;
+  for (int i = 0; i < g_nattr; ++i)
+    if (g_attr[i].kernel == kernel && g_attr[i].device == dev) {
+      if (g_attr[i].bytes >= bytes) return cudaSuccess;
+      slot = i;
+      break;
+    }
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  if (slot < 0 && g_nattr < 256) {
+    slot = g_nattr++;
+    g_attr[slot].kernel = kernel;
+    g_attr[slot].device = dev;
+  }
+  if (slot >= 0) g_attr[slot].bytes = bytes;
+  return cudaSuccess;
+}
+}  // namespace ttb
 
 namespace {
 
@@ -140,6 +179,7 @@ void layout(ttb_handle& h, char* base) {
   w.f_g1img = c.take<float>(fz ? (size_t)g.m[0] * 512 : 0);
   w.f_img = c.take<float>(fz ? (size_t)g.m[1] * 16384 : 0);
   w.f_grad = c.take<float>(fz ? (size_t)(G1S * g.m[0] + G2S * g.m[1] + G3S * g.m[2]) : 0);
+  w.f_rowbits = c.take<unsigned>(fz ? (size_t)(g.m[0] * g.m[1] * g.m[2] / 32 + 1) : 0);
   h.bytes = c.off + 256;
 }
 
@@ -208,6 +248,7 @@ ttb_handle* ttb_create(const ttb_geom* g, int64_t max_T, int64_t max_B, void* wo
   layout(*h, base);
   h->base = base;
   h->pmap_clean = 1;
+  h->su_gen = -1;
   {
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
@@ -318,6 +359,24 @@ int ttb_sgd_update(float* param, const float* grad, double* velocity, int64_t n,
   return cuda_status(launch_sgd(param, grad, velocity, n, lr, momentum, (cudaStream_t)stream));
 }
 
+int ttb_check_finite(const float* grad, int64_t n, int* err, ttb_stream stream) {
+  if (!grad || !err || n < 0) return TTB_EINVAL;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return cuda_status(launch_gradcheck(grad, n, err, sms, (cudaStream_t)stream));
+}
+
+int ttb_sgd_update_checked(float* param, const float* grad, double* velocity, int64_t n, double lr, double momentum,
+                           int* err, ttb_stream stream) {
+  if (!param || !grad || !err || n < 0) return TTB_EINVAL;
+  if (!(lr >= 0.0) || !(momentum >= 0.0 && momentum < 1.0)) return TTB_EINVAL;
+  if (momentum > 0.0 && !velocity) return TTB_EINVAL;
+  if (momentum == 0.0) velocity = nullptr;
+  int rc = ttb_check_finite(grad, n, err, stream);
+  if (rc) return rc;
+  return cuda_status(launch_sgd(param, grad, velocity, n, lr, momentum, (cudaStream_t)stream, err));
+}
+
 int ttb_read_status(ttb_handle* h, int64_t status[8], ttb_stream stream) {
   if (!h || !status) return TTB_EINVAL;
   int hdr[16];
@@ -333,8 +392,9 @@ int ttb_read_status(ttb_handle* h, int64_t status[8], ttb_stream stream) {
     if (cudaStreamSynchronize(s) != cudaSuccess) return TTB_ECUDA;
     status[0] = fh[0] | (h->legacy_planned ? hdr[0] : 0);
     status[3] = fh[3];
-    status[4] = h->legacy_planned ? hdr[2] : -1;  // segments: known once the legacy plan was built
-    status[5] = -1;                               // unique rows: not formed by this pipeline
+    const bool counted = h->su_gen == h->gen;  // ttb_plan_counts ran on this plan
+    status[4] = counted ? h->su[0] : (h->legacy_planned ? hdr[2] : -1);
+    status[5] = counted ? h->su[1] : -1;  // unique rows: not formed by this pipeline's step kernels
     status[7] = fh[2];                            // work items
     return TTB_OK;
   }
@@ -343,6 +403,27 @@ int ttb_read_status(ttb_handle* h, int64_t status[8], ttb_stream stream) {
   status[4] = hdr[2];
   status[5] = h->backwarded ? hdr[3] : 0;
   status[7] = 0;
+  return TTB_OK;
+}
+
+int ttb_plan_counts(ttb_handle* h, int64_t su[2], ttb_stream stream) {
+  if (!h || !su) return TTB_EINVAL;
+  if (!h->planned) return TTB_ESTATE;
+  if (!h->fast) {  // the deterministic pipeline forms both (U after a backward)
+    int64_t st[8];
+    int rc = ttb_read_status(h, st, stream);
+    if (rc) return rc;
+    su[0] = st[4];
+    su[1] = h->backwarded ? st[5] : -1;
+    return TTB_OK;
+  }
+  if (h->su_gen != h->gen) {
+    if (fast_count_su(h, h->plan_idx, h->plan_idx64, h->plan_off, h->su, (cudaStream_t)stream) != cudaSuccess)
+      return TTB_ECUDA;
+    h->su_gen = h->gen;
+  }
+  su[0] = h->su[0];
+  su[1] = h->su[1];
   return TTB_OK;
 }
 
@@ -357,6 +438,28 @@ int ttb_export_plan(ttb_handle* h, int64_t* work, int64_t* slot_occ, int64_t* se
     h->legacy_planned = 1;
   }
   return cuda_status(launch_export_plan(h, work, slot_occ, seg_ids, seg_inv, digits, (cudaStream_t)stream));
+}
+
+int ttb_export_fast_plan(ttb_handle* h, int64_t counts[4], int32_t* item_start, uint32_t* item_key,
+                         int32_t* tile_info, int32_t* sbi, int32_t* cta_tiles, ttb_stream stream) {
+  if (!h || !counts) return TTB_EINVAL;
+  if (!h->planned || !h->fast) return TTB_ESTATE;
+  cudaStream_t s = (cudaStream_t)stream;
+  int fh[8];
+  if (cudaMemcpyAsync(fh, h->w.fast_hdr, sizeof(fh), cudaMemcpyDeviceToHost, s) != cudaSuccess) return TTB_ECUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return TTB_ECUDA;
+  const int64_t items = fh[2], tiles = fh[4];
+  counts[0] = items;
+  counts[1] = tiles;
+  counts[2] = h->num_sms;
+  counts[3] = h->T;
+  const cudaMemcpyKind dd = cudaMemcpyDeviceToDevice;
+  if (item_start && cudaMemcpyAsync(item_start, h->w.f_item_start, sizeof(int) * (items + 1), dd, s)) return TTB_ECUDA;
+  if (item_key && cudaMemcpyAsync(item_key, h->w.f_item_key, sizeof(unsigned) * items, dd, s)) return TTB_ECUDA;
+  if (tile_info && cudaMemcpyAsync(tile_info, h->w.f_tile_info, sizeof(int4) * tiles, dd, s)) return TTB_ECUDA;
+  if (sbi && cudaMemcpyAsync(sbi, h->w.f_sbi, sizeof(int2) * h->T, dd, s)) return TTB_ECUDA;
+  if (cta_tiles && cudaMemcpyAsync(cta_tiles, h->w.f_cta, sizeof(int) * (h->num_sms + 1), dd, s)) return TTB_ECUDA;
+  return cudaStreamSynchronize(s) == cudaSuccess ? TTB_OK : TTB_ECUDA;
 }
 
 int ttb_export_unique(ttb_handle* h, int64_t* rows, float* grads, ttb_stream stream) {

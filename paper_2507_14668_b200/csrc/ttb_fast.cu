@@ -367,7 +367,25 @@ struct SgdArgs {
   float* p2;
   double lr, mu;
   int mask, on;
+  const int* err;     // device error word: any bit set -> no update (cores untouched)
 };
+
+// Finiteness pre-pass over the final gradients (fused_update rejects a
+// non-finite gradient before touching any core, backward.py:190-194): sets
+// TTB_ERRBIT_NONFINITE in *err; the update kernel that follows reads it.
+__global__ void __launch_bounds__(256) k_gradcheck(const float* __restrict__ g, int64_t n, int* __restrict__ err) {
+  pdl_enter();
+  bool bad = false;
+  const int64_t n4 = (reinterpret_cast<uintptr_t>(g) & 15) ? 0 : n >> 2;
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = g4[i];
+    bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+  }
+  for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(g[i]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, TTB_ERRBIT_NONFINITE);
+}
 
 __device__ __forceinline__ float maybe_sgd(float p, const SgdArgs& u, int core, size_t flat, size_t j, double* v) {
   if (!u.on || !((u.mask >> core) & 1)) return p;
@@ -378,6 +396,10 @@ __global__ void __launch_bounds__(kImgThreads) k_coreimg(float* __restrict__ G1,
                                                          float* __restrict__ img, float* __restrict__ g1img,
                                                          SgdArgs u) {
   pdl_enter();
+  // an error latched by the plan or the backward (range, empty bag,
+  // non-finite gradient) cancels the update: the images are rebuilt from the
+  // unchanged cores and velocities
+  if (u.on && u.err && *(volatile const int*)u.err != 0) u.on = 0;
   const size_t n0 = (size_t)g.m1 * 4 * R1, n1 = (size_t)R1 * g.m2 * C;
   const unsigned nb12 = g.m2 + (g.m1 + 3) / 4;
   if (blockIdx.x >= nb12) {  // G3: update only
@@ -1152,6 +1174,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
 #pragma unroll
               for (int j = 0; j < 4; ++j) dh[j] = fmaf(x[ab], gv[4 * ab + j], dh[j]);
             if (!(dbg & 1)) red_v4(dG3 + ((size_t)lane * m3 + i3) * 4, dh[0], dh[1], dh[2], dh[3]);
+            bad |= !isfinite((dh[0] + dh[1]) + (dh[2] + dh[3]));
 #pragma unroll
             for (int ab = 0; ab < 16; ++ab) {
               z[ab] = fmaf(gv[4 * ab], h3.x, z[ab]);
@@ -1182,6 +1205,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
   #pragma unroll
               for (int j = 0; j < 4; ++j) dh[j] = fmaf(x[ab], gv[4 * ab + j], dh[j]);
             if (!(dbg & 1)) red_v4(dG3 + ((size_t)lane * m3 + i3) * 4, dh[0], dh[1], dh[2], dh[3]);
+            bad |= !isfinite((dh[0] + dh[1]) + (dh[2] + dh[3]));
   #pragma unroll
             for (int ab = 0; ab < 16; ++ab) {
               z[ab] = fmaf(gv[4 * ab], h3.x, z[ab]);
@@ -1347,14 +1371,84 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
 
 using namespace fast;
 
+// ------------------------------------------------------------ counters S, U
+// The reference's counters (lookup.py:294-295 segments S = bag-prefix pairs;
+// backward.py:218-222 distinct rows U) for the current plan, on demand (the
+// step kernels never need them). U: test-and-set of one bit per row. S: per
+// bag (one warp), the number of distinct prefix keys among its lookups.
+template <typename IdxT>
+__global__ void __launch_bounds__(256) k_count_su(const IdxT* __restrict__ idx, const int64_t* __restrict__ offsets,
+                                                  int T, int B, KGeom g, unsigned* __restrict__ rowbits,
+                                                  int* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  int u = 0;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+    long long v = (long long)idx[t];
+    if (v < 0 || v >= (long long)g.rows) continue;
+    const unsigned bit = 1u << (v & 31);
+    u += (atomicOr(&rowbits[v >> 5], bit) & bit) == 0;
+  }
+  int sseg = 0;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int b = warp; b < B; b += nwarps) {
+    const int lo = (int)offsets[b], hi = (int)offsets[b + 1];
+    for (int p0 = lo; p0 < hi; p0 += 32) {
+      const int p = p0 + lane;
+      const bool ok = p < hi;
+      const unsigned key = ok ? (unsigned)((unsigned long long)idx[p] / g.m3) : 0xFFFFFFFFu;
+      // first occurrence inside this chunk of 32 ...
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      bool first = ok && (__ffs(peers) - 1) == lane;
+      // ... and not seen in an earlier chunk of the bag
+      for (int q = lo; first && q < p0; ++q) first = (unsigned)((unsigned long long)idx[q] / g.m3) != key;
+      sseg += first;
+    }
+  }
+  u = warp_sum(u);
+  sseg = warp_sum(sseg);
+  if (lane == 0) {
+    if (u) atomicAdd(&counts[1], u);
+    if (sseg) atomicAdd(&counts[0], sseg);
+  }
+}
+
+cudaError_t fast_count_su(ttb_handle* h, const void* idx, int idx64, const int64_t* offsets, int64_t su[2],
+                          cudaStream_t s) {
+  Workspace& w = h->w;
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(w.f_rowbits, 0, sizeof(unsigned) * ((size_t)h->kg.rows / 32 + 1), s))) return e;
+  if ((e = cudaMemsetAsync(w.fast_hdr + 8, 0, 2 * sizeof(int), s))) return e;
+  const int grid = 4 * h->num_sms;
+  if (idx64)
+    k_count_su<long long><<<grid, 256, 0, s>>>((const long long*)idx, offsets, (int)h->T, (int)h->B, h->kg,
+                                               w.f_rowbits, w.fast_hdr + 8);
+  else
+    k_count_su<int><<<grid, 256, 0, s>>>((const int*)idx, offsets, (int)h->T, (int)h->B, h->kg, w.f_rowbits,
+                                         w.fast_hdr + 8);
+  count_launch();
+  if ((e = cudaGetLastError())) return e;
+  int c[2];
+  if ((e = cudaMemcpyAsync(c, w.fast_hdr + 8, sizeof(c), cudaMemcpyDeviceToHost, s))) return e;
+  if ((e = cudaStreamSynchronize(s))) return e;
+  su[0] = c[0];
+  su[1] = c[1];
+  return cudaSuccess;
+}
+
+cudaError_t launch_gradcheck(const float* g, int64_t n, int* err, int num_sms, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int64_t gb = (n / 4 + 255) / 256;
+  if (gb < 1) gb = 1;
+  if (gb > 2 * num_sms) gb = 2 * num_sms;
+  cudaError_t e = launch_pdl(k_gradcheck, dim3((int)gb), dim3(256), 0, s, g, n, err);
+  if (e == cudaSuccess) count_launch();
+  return e;
+}
+
 bool fast_supported(const ttb_handle* h) {
   const DynDims& d = h->dims;
   // G3 (32 x m3 x 4 fp32) stays resident in the forward kernel's shared memory
   return d.n1 == 4 && d.n2 == 4 && d.n3 == 4 && d.r1 == 32 && d.r2 == 32 && h->kg.m3 <= (unsigned)kFwdMaxM3;
-}
-
-static cudaError_t ensure_attr(const void* k, int bytes) {
-  return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 cudaError_t fast_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* offsets, cudaStream_t s) {
@@ -1367,13 +1461,23 @@ cudaError_t fast_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* 
   if ((int)h->kg.m1m2 > work) work = (int)h->kg.m1m2;
   int grid = (work + kPlanThreads - 1) / kPlanThreads;
   if (grid > h->num_sms) grid = h->num_sms;  // co-resident: grid barriers
+  {
+    // the grid barriers need every CTA resident at once: bound the grid by
+    // the occupancy of this device and launch cooperatively (an SM partition
+    // too small for the grid then fails the launch instead of hanging)
+    int occ = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+             &occ, idx64 ? (const void*)k_fplan<long long> : (const void*)k_fplan<int>, kPlanThreads, 0)))
+      return e;
+    if (occ < 1) return cudaErrorCooperativeLaunchTooLarge;
+  }
   ProfScope _ps(h, s, "f_plan");
   if (idx64)
-    e = launch_pdl(k_fplan<long long>, dim3(grid), dim3(kPlanThreads), 0, s, (const long long*)idx, offsets, T, B,
+    e = launch_pdl_coop(k_fplan<long long>, dim3(grid), dim3(kPlanThreads), 0, s, (const long long*)idx, offsets, T, B,
                    h->kg, w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_rstart, w.f_split, w.f_gtot, w.f_item_start, w.f_cta, h->num_sms,
                    w.f_item_key, w.f_tile_info, w.f_sbi, w.fast_hdr, getenv("TTB_DBG") ? 1 : 0);
   else
-    e = launch_pdl(k_fplan<int>, dim3(grid), dim3(kPlanThreads), 0, s, (const int*)idx, offsets, T, B, h->kg,
+    e = launch_pdl_coop(k_fplan<int>, dim3(grid), dim3(kPlanThreads), 0, s, (const int*)idx, offsets, T, B, h->kg,
                    w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_rstart, w.f_split, w.f_gtot, w.f_item_start, w.f_cta, h->num_sms,
                    w.f_item_key,
                    w.f_tile_info, w.f_sbi, w.fast_hdr, getenv("TTB_DBG") ? 1 : 0);
@@ -1387,15 +1491,11 @@ cudaError_t fast_forward(ttb_handle* h, const float* c0, const float* c1, const 
   Workspace& w = h->w;
   cudaError_t e;
   const int img_smem = 32 * 129 * 4 + 1024;
-  static bool attr = false;
-  if (!attr) {
-    if ((e = ensure_attr((const void*)k_coreimg, img_smem))) return e;
-    if ((e = ensure_attr((const void*)k_fwd<false>, fwd_smem_bytes(kFwdMaxM3)))) return e;
-    if ((e = ensure_attr((const void*)k_fwd<true>, fwd_smem_bytes(kFwdMaxM3)))) return e;
-    if ((e = ensure_attr((const void*)k_bwd<false>, kBwdSmem))) return e;
-    if ((e = ensure_attr((const void*)k_bwd<true>, kBwdSmem))) return e;
-    attr = true;
-  }
+  if ((e = ensure_kernel_smem((const void*)k_coreimg, img_smem))) return e;
+  if ((e = ensure_kernel_smem((const void*)k_fwd<false>, fwd_smem_bytes(kFwdMaxM3)))) return e;
+  if ((e = ensure_kernel_smem((const void*)k_fwd<true>, fwd_smem_bytes(kFwdMaxM3)))) return e;
+  if ((e = ensure_kernel_smem((const void*)k_bwd<false>, kBwdSmem))) return e;
+  if ((e = ensure_kernel_smem((const void*)k_bwd<true>, kBwdSmem))) return e;
   if (!(h->img_valid && h->img_c0 == c0 && h->img_c1 == c1)) {
     // split tf32 images of the cores (skipped while the images written by the
     // last fused update, or the last forward, still describe these cores)
@@ -1459,7 +1559,11 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
     // images from the updated values
     const int img_smem = 32 * 129 * 4 + 1024;
     const int ng3 = (int)((n2 + kImgThreads - 1) / kImgThreads);
-    SgdArgs u = {w.f_grad, v0, v1, v2, p2, lr, mu, mask, 1};
+    {
+      ProfScope _pc(h, s, "f_gradcheck");
+      if ((e = launch_gradcheck(w.f_grad, n0 + n1 + n2, w.fast_hdr, h->num_sms, s))) return e;
+    }
+    SgdArgs u = {w.f_grad, v0, v1, v2, p2, lr, mu, mask, 1, w.fast_hdr};
     ProfScope _ps(h, s, "f_sgd");
     if ((e = launch_pdl(k_coreimg, dim3(h->kg.m2 + (h->kg.m1 + 3) / 4 + (ng3 < 64 ? ng3 : 64)), dim3(kImgThreads),
                         img_smem, s, p0, p1, h->kg, w.f_img, w.f_g1img, u)))

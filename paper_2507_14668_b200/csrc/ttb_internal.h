@@ -87,6 +87,7 @@ struct Workspace {
   float* f_g1img;         // m1 x 512: split G1 rows / transposed images
   float* f_img;           // m2 x 4 x 16 KB: G2 slice images (cb hi/lo, k hi/lo)
   float* f_grad;          // |G1| + |G2| + |G3|: gradients for the fused update
+  unsigned* f_rowbits;    // rows / 32 + 1: row bitmap of the on-demand U count
 };
 
 enum ScanId { kScanSlots = 0, kScanSegs = 1, kScanFirst = 2, kScanFast = 3, kNumScans = 4 };
@@ -139,6 +140,8 @@ struct ttb_handle {
   // the f_img / f_g1img core images describe the cores at img_c0 / img_c1
   // (written by the last forward or fused update; cleared by
   // ttb_cores_modified and by a backward that hands gradients to the caller)
+  int64_t su_gen;       // plan generation whose S / U were counted (fast pipeline), -1 none
+  int64_t su[2];
   int img_valid;
   const float* img_c0;
   const float* img_c1;
@@ -162,6 +165,27 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+// Same, launched cooperatively: the launch fails (instead of a later
+// deadlock) unless every CTA of the grid is co-resident — required by
+// kernels that synchronise their CTAs with software grid barriers.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl_coop(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                   Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
@@ -194,13 +218,21 @@ cudaError_t launch_sort_raw(const unsigned* keys_in, const unsigned* vals_in, un
                             unsigned* vB, int n, int bits, unsigned* hist, unsigned* status, int tiles_cap,
                             unsigned* ctr, unsigned** keys_out, unsigned** vals_out, cudaStream_t s);
 bool fast_supported(const ttb_handle* h);
+// Raises a kernel's max dynamic shared memory to >= bytes on the CURRENT
+// device (cudaFuncSetAttribute is per device context). Thread safe; the
+// attribute is set once per (kernel, device, size increase).
+cudaError_t ensure_kernel_smem(const void* kernel, size_t bytes);
 cudaError_t fast_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* offsets, cudaStream_t s);
+cudaError_t fast_count_su(ttb_handle* h, const void* idx, int idx64, const int64_t* offsets, int64_t su[2],
+                          cudaStream_t s);
 cudaError_t fast_forward(ttb_handle* h, const float* c0, const float* c1, const float* c2, float* out,
                          cudaStream_t s);
 cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const float* c2, const float* gout,
                           float* g0, float* g1, float* g2, float* p0, float* p1, float* p2, double* v0, double* v1,
                           double* v2, double lr, double mu, int mask, int mode, cudaStream_t s);
-cudaError_t launch_sgd(float* p, const float* g, double* v, int64_t n, double lr, double mu, cudaStream_t s);
+cudaError_t launch_sgd(float* p, const float* g, double* v, int64_t n, double lr, double mu, cudaStream_t s,
+                       const int* err = nullptr);
+cudaError_t launch_gradcheck(const float* g, int64_t n, int* err, int num_sms, cudaStream_t s);
 cudaError_t launch_export_plan(ttb_handle* h, int64_t* work, int64_t* slot_occ, int64_t* seg_ids,
                                int64_t* seg_inv, int64_t* digits, cudaStream_t s);
 cudaError_t launch_export_unique(ttb_handle* h, int64_t* rows, float* grads, cudaStream_t s);

@@ -84,7 +84,28 @@ def dp_step(engine, flat: FlatCores, indices, offsets, grad_out, lr: float, mome
     out = engine.forward(flat.cores)
     engine.backward(flat.cores, grad_out, grads=flat.grads)
     allreduce_grads(flat.grad, group)
-    lib = nat.load()
-    nat.check(lib.ttb_sgd_update(_ptr(flat.param), _ptr(flat.grad), _ptr(flat.velocity) if momentum > 0 else None,
-                                 flat.param.numel(), float(lr), float(momentum), _stream()), "sgd_update")
+    checked_update(flat.param, flat.grad, flat.velocity if momentum > 0 else None, lr, momentum)
     return out
+
+
+def checked_update(param: torch.Tensor, grad: torch.Tensor, velocity, lr: float, momentum: float,
+                   err: torch.Tensor | None = None, raise_now: bool = True) -> torch.Tensor:
+    """fused_update semantics (backward.py:186-204) on a flat buffer: the
+    gradient is checked for non-finite values on the device first and the
+    update is skipped (param and velocity untouched) if any is found.
+    `err` (one int32 on the device) accumulates the error bits; with
+    raise_now the call syncs and raises ValueError like the reference."""
+    from . import _native as nat
+    from .engine import _ptr, _stream
+
+    if err is None:
+        err = torch.zeros(1, dtype=torch.int32, device=param.device)
+    lib = nat.load()
+    nat.check(lib.ttb_sgd_update_checked(_ptr(param), _ptr(grad), _ptr(velocity) if momentum > 0 else None,
+                                         param.numel(), float(lr), float(momentum), _ptr(err), _stream()),
+              "sgd_update_checked")
+    if raise_now:
+        exc = nat.errbits_to_exception(int(err.item()))
+        if exc is not None:
+            raise exc
+    return err

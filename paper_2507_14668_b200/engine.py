@@ -128,6 +128,11 @@ class TtEngine:
             raise ValueError("empty batch")
         if indices.dtype not in (torch.int64, torch.int32):
             raise ValueError("indices must be int64 or int32")
+        if indices.device != self.device or offsets.device != self.device:
+            # the kernels dereference these pointers on self.device: a host or
+            # foreign-device tensor would be an illegal access, not an error
+            raise ValueError(f"indices and offsets must be on {self.device}, got {indices.device} / "
+                             f"{offsets.device}")
         if offsets.dtype != torch.int64:
             offsets = offsets.to(torch.int64)
         indices, offsets = indices.contiguous(), offsets.contiguous()
@@ -226,6 +231,13 @@ class TtEngine:
         return dict(err=int(st[0]), T=int(st[1]), B=int(st[2]), P=int(st[3]), S=int(st[4]), U=int(st[5]),
                     gen=int(st[6]), items=int(st[7]))
 
+    def plan_counts(self) -> dict:
+        """S (bag-prefix segments) and U (distinct rows) of the current plan,
+        counted on the device (syncs)."""
+        su = (C.c_int64 * 2)()
+        nat.check(self.lib.ttb_plan_counts(self._handle, su, _stream()), "plan_counts")
+        return dict(S=int(su[0]), U=int(su[1]))
+
     def check_errors(self) -> dict:
         st = self.status()
         exc = nat.errbits_to_exception(st["err"])
@@ -259,6 +271,28 @@ class TtEngine:
                    seg_inv=seg_inv.cpu().numpy(), digits=digits.cpu().numpy(), **st)
         if self.is_d2:
             out["digits"] = out["digits"][:, 1:]
+        return out
+
+    def export_fast_plan(self) -> dict:
+        """The tensor-core pipeline's own plan (k_fplan output) as numpy:
+        item_start (items+1), item_key (items), tile_info (tiles, 4),
+        sbi (T, 2) = (bag, i3) per position, cta_tiles (CTAs+1)."""
+        cnt = (C.c_int64 * 4)()
+        nat.check(self.lib.ttb_export_fast_plan(self._handle, cnt, None, None, None, None, None, _stream()),
+                  "export_fast_plan")
+        items, tiles, ctas, T = (int(v) for v in cnt)
+        dev = self.device
+        bufs = dict(item_start=torch.empty(items + 1, dtype=torch.int32, device=dev),
+                    item_key=torch.empty(max(items, 1), dtype=torch.int32, device=dev),
+                    tile_info=torch.empty((max(tiles, 1), 4), dtype=torch.int32, device=dev),
+                    sbi=torch.empty((T, 2), dtype=torch.int32, device=dev),
+                    cta_tiles=torch.empty(ctas + 1, dtype=torch.int32, device=dev))
+        nat.check(self.lib.ttb_export_fast_plan(self._handle, cnt, *(_ptr(bufs[k]) for k in (
+            "item_start", "item_key", "tile_info", "sbi", "cta_tiles")), _stream()), "export_fast_plan")
+        out = {k: v.cpu().numpy() for k, v in bufs.items()}
+        out["item_key"] = out["item_key"][:items].view(np.uint32)
+        out["tile_info"] = out["tile_info"][:tiles]
+        out.update(items=items, tiles=tiles, ctas=ctas, T=T)
         return out
 
     def export_unique(self):

@@ -153,12 +153,13 @@ class DenseField(nn.Module):
                 int(indices.min()) < 0 or int(indices.max()) >= self.rows.shape[0]):
             raise ValueError(f"index outside [0, {self.rows.shape[0]})")
         n_bags = offsets.numel() - 1
-        if indices.numel() == n_bags:  # one index per bag (offsets must then be 0..B)
-            bag_of = None
-        else:
-            sizes = offsets[1:] - offsets[:-1]
-            bag_of = torch.repeat_interleave(torch.arange(n_bags, device=indices.device), sizes,
-                                             output_size=indices.numel())
+        # bag ids from the offsets, always (the reference pools by bag id,
+        # model.py:222-226: a batch with as many indices as bags may still
+        # hold an empty bag next to a multi-index one); output_size avoids a
+        # device->host sync
+        sizes = offsets[1:] - offsets[:-1]
+        bag_of = torch.repeat_interleave(torch.arange(n_bags, device=indices.device), sizes,
+                                         output_size=indices.numel())
         return _DenseBagSum.apply(self.rows, indices, bag_of, n_bags)
 
 

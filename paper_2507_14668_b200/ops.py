@@ -279,16 +279,26 @@ def fused_update(table: GpuTtTable, grads: CoreGrads, opt: OptimizerState) -> No
         g = torch.as_tensor(np.asarray(g) if not torch.is_tensor(g) else g).to(table.device, torch.float32)
         if tuple(g.shape) != tuple(table.cores[k].shape):
             raise ValueError(f"core {k} gradient extent {tuple(g.shape)}")
-        if not torch.isfinite(g).all():
-            raise ValueError("non-finite gradient")
         gs.append(g.contiguous())
     lib = nat.load()
-    if opt.momentum > 0.0 and opt.velocity is None:
-        opt.velocity = [torch.zeros(c.shape, dtype=torch.float64, device=table.device) for c in table.cores]
+    # every gradient is validated on the device before any core changes
+    # (backward.py:190-194): one error word, checked for all cores first,
+    # gates each core's update kernel
+    err = torch.zeros(1, dtype=torch.int32, device=table.device)
+    for g in gs:
+        nat.check(lib.ttb_check_finite(_ptr(g), g.numel(), _ptr(err), _stream()), "check_finite")
+    velocity = opt.velocity
+    if opt.momentum > 0.0 and velocity is None:
+        velocity = [torch.zeros(c.shape, dtype=torch.float64, device=table.device) for c in table.cores]
     for k, (core, g) in enumerate(zip(table.cores, gs)):
-        v = opt.velocity[k] if opt.momentum > 0.0 else None
-        nat.check(lib.ttb_sgd_update(_ptr(core), _ptr(g), _ptr(v), core.numel(), float(opt.lr), float(opt.momentum),
-                                     _stream()), "sgd_update")
+        v = velocity[k] if opt.momentum > 0.0 else None
+        nat.check(lib.ttb_sgd_update_checked(_ptr(core), _ptr(g), _ptr(v), core.numel(), float(opt.lr),
+                                             float(opt.momentum), _ptr(err), _stream()), "sgd_update")
+    exc = nat.errbits_to_exception(int(err.item()))
+    if exc is not None:
+        raise exc
+    if opt.momentum > 0.0:
+        opt.velocity = velocity
 
 
 def backward_batch(table: GpuTtTable, batch: EmbGradBatch, opt: OptimizerState, buffer: Optional[ReuseBuffer] = None,

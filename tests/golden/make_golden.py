@@ -210,6 +210,36 @@ def gen_dlrm():
     np.savez_compressed(OUT / "dlrm.npz", **s)
 
 
+def gen_dlrm_tc():
+    """The production TT geometry inside a DLRM (emb 64, ranks (1, 32, 32, 1),
+    n = (4, 4, 4)): the configuration the GPU's tensor-core pipeline runs
+    (BASELINE configs 4/5), one 12,000-row TT field + one dense field, bags of
+    1-3 indices, 3 SGD+momentum steps, fp32."""
+    s = {}
+    rows = (12000, 700)
+    cfg = md.ModelConfig(n_dense=5, rows_per_field=rows, emb_dim=64, ranks=(1, 32, 32, 1),
+                         tt_threshold=1000, bottom_sizes=(32,), top_sizes=(32,), loss="bce", seed=9)
+    spec = dd.DatasetSpec(n_samples=192, n_dense=5, rows_per_field=rows, min_bag=1, max_bag=3, seed=4)
+    ds = dd.gen_synthetic(spec)
+    model = md.DlrmModel(cfg, dtype=np.float32)
+    for name, arr in model.named_params():
+        s[f"init.{name}"] = arr.copy()
+    s["data.labels"] = ds.labels
+    s["data.dense"] = ds.dense
+    for f in range(len(rows)):
+        idx, off = batch_arrays(ds.bags[f])
+        s[f"data.idx{f}"], s[f"data.off{f}"] = idx, off
+    losses = []
+    bs = 64
+    for step in range(3):
+        sub = ds.select(np.arange(step * bs, (step + 1) * bs))
+        losses.append(model.train_step(sub, lr=0.05, momentum=0.9))
+        for name, arr in model.named_params():
+            s[f"step{step}.{name}"] = arr.copy()
+    s["losses"] = np.array(losses)
+    np.savez_compressed(OUT / "dlrm_tc.npz", **s)
+
+
 def gen_reorder():
     """Frequencies, hot rows, communities and the bijection of the reference's
     reorder pipeline on a skewed synthetic trace with planted clusters."""
@@ -251,6 +281,7 @@ if __name__ == "__main__":
     gen_plans_forward()
     gen_backward()
     gen_dlrm()
+    gen_dlrm_tc()
     gen_reorder()
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size)

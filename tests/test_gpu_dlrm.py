@@ -64,3 +64,39 @@ def test_checkpoint_bytes_match_reference(golden, tmp_path):
     bad.write_bytes(s["ckpt_final"].tobytes()[:-3])
     with pytest.raises(ValueError):
         M.load_checkpoint(bad)
+
+
+def test_dlrm_tensor_core_pipeline_matches_reference(golden):
+    """The same reference train_step (model.py:347-365) with the production
+    TT geometry (emb 64, ranks (1, 32, 32, 1)), so the TT field runs the
+    tensor-core pipeline (k_fplan / k_fwd / k_bwd / fused SGD) — golden run in
+    tests/golden/dlrm_tc.npz (make_golden.py gen_dlrm_tc)."""
+    from paper_2507_14668_b200.embedding_bag import TTEmbeddingBag
+    from paper_2507_14668_b200.model import DlrmModel, ModelConfig
+    torch.backends.cuda.matmul.allow_tf32 = False
+    s = golden("dlrm_tc")
+    rows = (12000, 700)
+    cfg = ModelConfig(n_dense=5, rows_per_field=rows, emb_dim=64, ranks=(1, 32, 32, 1), tt_threshold=1000,
+                      bottom_sizes=(32,), top_sizes=(32,), loss="bce", seed=9)
+    model = DlrmModel(cfg)
+    assert isinstance(model.fields[0], TTEmbeddingBag) and model.fields[0].engine.fast
+    params = dict(model.named_ref_params())
+    for name, p in params.items():
+        assert np.array_equal(p.detach().cpu().numpy(), s[f"init.{name}"]), name
+    dense = torch.from_numpy(s["data.dense"].astype(np.float32)).cuda()
+    labels = torch.from_numpy(s["data.labels"]).cuda()
+    bs = 64
+    for step in range(3):
+        lo, hi = step * bs, (step + 1) * bs
+        sparse = []
+        for f in range(len(rows)):
+            idx, off = s[f"data.idx{f}"], s[f"data.off{f}"]
+            sparse.append((torch.from_numpy(idx[off[lo]:off[hi]]).cuda(),
+                           torch.from_numpy(off[lo:hi + 1] - off[lo]).cuda()))
+        loss = model.train_step(dense[lo:hi], sparse, labels[lo:hi], lr=0.05, momentum=0.9)
+        assert abs(loss - s["losses"][step]) <= 1e-5 * max(1.0, abs(s["losses"][step])), (step, loss)
+        for name, p in params.items():
+            got = p.detach().cpu().numpy().astype(np.float64)
+            want = s[f"step{step}.{name}"].astype(np.float64)
+            err = np.abs(got - want).max() / max(1e-3, np.abs(want).max())
+            assert err < 1e-4, (step, name, err)
