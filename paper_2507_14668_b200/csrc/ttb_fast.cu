@@ -24,24 +24,12 @@
 #include <stdio.h>
 #include <stdlib.h>
 
-#include "ttb_internal.h"
-#include "ttb_umma.cuh"
+#include "ttb_fast.cuh"
 
 namespace ttb {
 namespace fast {
 
-constexpr int kItemLen = 32;    // max lookups per work item
-constexpr int kTileItems = 32;  // items per tile: M = 32 * n1 = 128
-constexpr int R1 = 32, C = 128, NOUT = 64;
-constexpr int kImg = 16384;     // bytes of one 128 x 32 / 32 x 128 fp32 image
 constexpr int kThreads = 256;
-
-__device__ __forceinline__ void red_v4(float* p, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
-}
-__device__ __forceinline__ void red_f32(float* p, float a) {
-  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(a) : "memory");
-}
 
 // ------------------------------------------------------------ plan
 // One persistent kernel (grid <= SM count, all CTAs co-resident) in three
@@ -79,11 +67,6 @@ __device__ inline void grid_barrier(unsigned* bar, unsigned& target) {
   __syncthreads();
 }
 
-__device__ __forceinline__ int warp_sum(int v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
 
 template <typename IdxT>
 __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__ idx,
@@ -356,7 +339,6 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
 //     [0] cb_hi  [1] cb_lo : rows (c, b) = 4 c + b (128), K = k (32)
 //     [2..3] k      : rows k (hi 0..31, lo 32..63), K = (c, b) (128)
 //   per i1 (512 floats): rows_hi[a][k], rows_lo[a][k], t_hi[k][a], t_lo[k][a]
-constexpr int kG1Img = 512;
 constexpr int kImgThreads = 512;
 
 // Optional SGD(+momentum) step applied to each element before it is imaged:
@@ -484,32 +466,11 @@ __global__ void __launch_bounds__(kImgThreads) k_coreimg(float* __restrict__ G1,
   }
 }
 
-// ------------------------------------------------------------ async copies
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(umma::smem_u32(smem)), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(umma::smem_u32(smem)), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(umma::smem_u32(smem)), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 
 __device__ inline void copy_img_async(char* dst, const float* __restrict__ src, int bytes) {
   for (int e = threadIdx.x; e < bytes / 16; e += kThreads) cp_async16(dst + 16 * e, src + 4 * e);
 }
 
-__device__ __forceinline__ void sync_for_mma() {
-  umma::fence_smem_to_async();
-  umma::fence_before_sync();
-  __syncthreads();
-  umma::fence_after_sync();
-}
 
 // 3xTF32 product of two smem images over K (k-steps of 8)
 __device__ inline void mma3_ss(uint32_t d, uint32_t a_hi, uint32_t a_lo, int a_rows, uint32_t b_hi, uint32_t b_lo,
@@ -527,35 +488,6 @@ __device__ inline void mma3_ss(uint32_t d, uint32_t a_hi, uint32_t a_lo, int a_r
 // Tile metadata lives in a two-slot ring: while tile t is processed, the
 // last warp fetches tile t + grid's (cp.async) and the tile table entry of
 // t + 2 grid (a register load, consumed an iteration later).
-struct TileMeta {
-  int i2, n, item0, pad;
-  unsigned key[kTileItems];
-  int start[kTileItems + 1];
-};
-
-struct MetaPrefetch {
-  int4 next;  // tile table entry of the tile after the one being fetched
-};
-
-// lanes 0..31 of the calling warp: slot <- tile `info`
-__device__ inline void fetch_meta_async(const int4& info, const int* __restrict__ item_start,
-                                        const unsigned* __restrict__ item_key, TileMeta* m) {
-  const int l = threadIdx.x & 31, n = info.z, item0 = info.y;
-  if (l == 0) {
-    m->i2 = info.x;
-    m->n = n;
-    m->item0 = item0;
-    cp_async4(&m->start[n], item_start + item0 + n);
-  }
-  if (l < n) {
-    cp_async4(&m->key[l], item_key + item0 + l);
-    cp_async4(&m->start[l], item_start + item0 + l);
-  }
-}
-
-__device__ __forceinline__ int item_i1(const TileMeta* m, int it, KGeom g) {
-  return (int)(m->key[it] - (unsigned)m->i2 * g.m1);
-}
 
 // G1 rows image of the tile's items (rows (item, a), K = k) from the split G1 images
 __device__ inline void stage_g1_rows_async(const TileMeta* m, KGeom g, const float* __restrict__ g1img, char* hi,
@@ -600,7 +532,6 @@ __device__ inline void stage_g1_t_async(const TileMeta* m, KGeom g, const float*
 // from TMEM in two halves of c (64 registers).
 constexpr int kMaxTilePos = kTileItems * kItemLen;  // 1024
 
-__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 constexpr int kFwdMaxM3 = 288;                       // G3 (32 x m3 x 4 fp32) kept in smem
 constexpr int kFwdThreads = 512;
 constexpr int kFwdSplitRounds = 4;  // rows with <= this many segments: c split across the quarters
@@ -1547,7 +1478,10 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
     ProfScope _ps(h, s, "f_bwd");
     // pooled bags (more lookups than bags) repeat rows inside a prefix: group
     // by row; otherwise (T = B, bags are single lookups) position by position
-    if ((e = launch_pdl(h->T > h->B ? k_bwd<true> : k_bwd<false>, dim3(grid), dim3(kThreads), kBwdSmem, s, h->kg, (const float*)w.f_g1img, c2,
+    // v2 (ttb_bwd2.cu, opt-in): one-lookup bags only; pooled batches keep the row-grouped v1
+    if (h->bwd_v2 && h->T == h->B) {
+      if ((e = launch_bwd2(h, c1, c2, gout, g0, g1, g2, s))) return e;
+    } else if ((e = launch_pdl(h->T > h->B ? k_bwd<true> : k_bwd<false>, dim3(grid), dim3(kThreads), kBwdSmem, s, h->kg, (const float*)w.f_g1img, c2,
                         (const float*)w.f_img, (const int4*)w.f_tile_info, (const int*)w.f_item_start,
                         (const unsigned*)w.f_item_key, (const int2*)w.f_sbi, gout, g0, g1, g2, w.fast_hdr,
                         (const int*)w.f_cta, getenv("TTB_DBG") ? atoi(getenv("TTB_DBG")) : 0)))

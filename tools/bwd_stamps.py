@@ -22,7 +22,8 @@ cores = [torch.from_numpy(c).to(dev) for c in init_random_cores(shape, 0)]
 ti = torch.from_numpy(idx).to(dev)
 to = torch.arange(0, T + 1, pool, dtype=torch.int64, device=dev)
 gout = torch.randn(B, 64, device=dev) / B
-names = ["mma X issue", "X wait", "X^T dump", "Z phase", "Z^T/TMEM+img", "E pass 1", "E pass 2", "reductions"]
+names = ["X wait", "G1^T stage", "SIMT (grp 0)", "SIMT end sync", "E/dG2 issue + staging", "E wait",
+         "epilogue + next X", "-"]
 for rep in range(3):
     eng.plan(ti, to)
     eng.forward(cores)
@@ -36,5 +37,6 @@ tot = h[1:9].sum()
 print(f"{wl}: {nt} tiles in block 0, {tot / nt:.0f} cycles per tile")
 for nm, v in zip(names, h[1:9]):
     print(f"  {nm:14s} {v / nt:8.0f} cyc  {100 * v / max(tot, 1):5.1f}%")
-print(f"  (dG2 MMA issue, 32 MMAs: {h[9] / nt:.0f} cyc; Z phase: chunk staging {h[10] / nt:.0f}, "
-      f"end-of-chunk barrier wait {h[11] / nt:.0f})")
+if h[9:12].sum():
+    print(f"  SIMT split (grp 0): quad setup {h[9] / nt:.0f}, lookups {h[10] / nt:.0f}, quad epilogue {h[11] / nt:.0f}")
+
