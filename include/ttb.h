@@ -239,12 +239,6 @@ int ttb_profile_read(ttb_handle *h, char *names, double *ms, int64_t *calls,
  *   number of work items. Changing the option drops the current plan. */
 #define TTB_OPT_BWD_SPLIT 1
 #define TTB_OPT_FAST 2
-/* TTB_OPT_BWD_V2 (3): 1 = the alternative tensor-core backward for
- * one-lookup bags (ttb_bwd2.cu: X^T read straight from TMEM through 4-lane
- * block transposes, G2 staged from the fp32 core, 16 warps) instead of the
- * default one (X^T staged through shared memory). Same results within the
- * tolerances; for A/B measurements. */
-#define TTB_OPT_BWD_V2 3
 int ttb_set_option(ttb_handle *h, int option, int value);
 /* FP32 FMA throughput probe: blocks x 256 threads x iters x 16 flops; the
  * caller times it with CUDA events to get the measured FP32 peak. */

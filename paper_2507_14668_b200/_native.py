@@ -30,7 +30,6 @@ ERRBIT_NONFINITE = 8
 
 OPT_BWD_SPLIT = 1
 OPT_FAST = 2
-OPT_BWD_V2 = 3
 
 # every symbol include/ttb.h declares (tests check the .so exports them all)
 EXPORTS = [

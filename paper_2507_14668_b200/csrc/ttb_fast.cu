@@ -1478,10 +1478,7 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
     ProfScope _ps(h, s, "f_bwd");
     // pooled bags (more lookups than bags) repeat rows inside a prefix: group
     // by row; otherwise (T = B, bags are single lookups) position by position
-    // v2 (ttb_bwd2.cu, opt-in): one-lookup bags only; pooled batches keep the row-grouped v1
-    if (h->bwd_v2 && h->T == h->B) {
-      if ((e = launch_bwd2(h, c1, c2, gout, g0, g1, g2, s))) return e;
-    } else if ((e = launch_pdl(h->T > h->B ? k_bwd<true> : k_bwd<false>, dim3(grid), dim3(kThreads), kBwdSmem, s, h->kg, (const float*)w.f_g1img, c2,
+    if ((e = launch_pdl(h->T > h->B ? k_bwd<true> : k_bwd<false>, dim3(grid), dim3(kThreads), kBwdSmem, s, h->kg, (const float*)w.f_g1img, c2,
                         (const float*)w.f_img, (const int4*)w.f_tile_info, (const int*)w.f_item_start,
                         (const unsigned*)w.f_item_key, (const int2*)w.f_sbi, gout, g0, g1, g2, w.fast_hdr,
                         (const int*)w.f_cta, getenv("TTB_DBG") ? atoi(getenv("TTB_DBG")) : 0)))

@@ -1,5 +1,5 @@
-// Device helpers shared by the tensor-core pipeline's kernels (ttb_fast.cu,
-// ttb_bwd2.cu): tile constants, fp32 reductions, cp.async, the per-tile
+// Device helpers of the tensor-core pipeline (ttb_fast.cu):
+// tile constants, fp32 reductions, cp.async, the per-tile
 // metadata ring.
 #pragma once
 #include "ttb_internal.h"

@@ -122,7 +122,6 @@ struct ttb_handle {
   int dg2_slots;         // dG2 partial slots per i2 written by the last backward
   int bwd_split;         // use the split backward (rows kernel + tensor-core GEMM kernel)
   int fast_ok, fast;     // tensor-core pipeline supported / selected (ttb_fast.cu)
-  int bwd_v2;            // tensor-core pipeline: the quad-transpose backward (ttb_bwd2.cu, A/B)
   int num_sms;
   const void* plan_idx;  // inputs of the current plan (the legacy plan behind
   const int64_t* plan_off;  // ttb_export_plan is built from them on demand)
@@ -233,8 +232,6 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
                           double* v2, double lr, double mu, int mask, int mode, cudaStream_t s);
 cudaError_t launch_sgd(float* p, const float* g, double* v, int64_t n, double lr, double mu, cudaStream_t s,
                        const int* err = nullptr);
-cudaError_t launch_bwd2(ttb_handle* h, const float* c1, const float* c2, const float* gout, float* g0, float* g1,
-                        float* g2, cudaStream_t s);
 cudaError_t launch_gradcheck(const float* g, int64_t n, int* err, int num_sms, cudaStream_t s);
 cudaError_t launch_export_plan(ttb_handle* h, int64_t* work, int64_t* slot_occ, int64_t* seg_ids,
                                int64_t* seg_inv, int64_t* digits, cudaStream_t s);

@@ -103,7 +103,6 @@ int ttb_set_option(ttb_handle* h, int option, int value) {
       h->fast = value ? 1 : 0;
       h->planned = h->forwarded = h->backwarded = 0;  // a plan belongs to one pipeline
       return TTB_OK;
-    case 3: h->bwd_v2 = value ? 1 : 0; return TTB_OK;  // TTB_OPT_BWD_V2
     default: return TTB_EINVAL;
   }
 }

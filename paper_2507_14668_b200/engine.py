@@ -12,7 +12,6 @@ front: geometry (m1, m2) becomes (1, m1, m2), ranks (1, R, 1) become
 from __future__ import annotations
 
 import ctypes as C
-import os
 
 import numpy as np
 import torch
@@ -90,8 +89,6 @@ class TtEngine:
         self.max_T, self.max_B = T, B
         if self.deterministic:
             self.set_option(nat.OPT_FAST, 0)
-        elif os.environ.get("TTB_BWD_V2"):  # A/B: the alternative backward kernel (ttb_bwd2.cu)
-            self.set_option(nat.OPT_BWD_V2, 1)
 
     def ensure_capacity(self, T: int, B: int) -> None:
         if T > self.max_T or B > self.max_B:

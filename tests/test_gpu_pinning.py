@@ -310,23 +310,3 @@ def test_dense_field_empty_and_multi_index_bags():
     out = f(idx, off)
     rows = f.rows.detach()
     assert torch.allclose(out[0], rows[3] + rows[7]) and torch.equal(out[1], torch.zeros_like(out[1]))
-
-
-@pytest.mark.parametrize("B", [8192, 700])
-def test_alternative_backward_v2_vs_oracle(B):
-    """The opt-in backward (TTB_OPT_BWD_V2, ttb_bwd2.cu: X^T read from TMEM via
-    4-lane block transposes, staged gradient rows) against the fp64 oracle."""
-    from paper_2507_14668_b200 import _native as nat
-    emb = module(10_000_000, 3, B, B)
-    emb.engine.set_option(nat.OPT_BWD_V2, 1)
-    g = O.Geometry(emb.shape.m, emb.shape.n, emb.shape.ranks)
-    rng = np.random.default_rng(40 + B)
-    idx = rng.integers(0, 10_000_000, B)
-    idx[: B // 8] = idx[B // 8: B // 4]  # repeated rows
-    off = np.arange(B + 1, dtype=np.int64)
-    gout = rng.standard_normal((B, 64)).astype(np.float32)
-    out, grads, c64 = run_fast(emb, idx, off, gout)
-    assert rel_err(out, O.forward(c64, g, idx, off)) < FWD_TOL
-    want = oracle_grads_chunked(c64, g, idx, off, gout)
-    for k in range(3):
-        assert rel_err(grads[k], want[k]) < GRAD_TOL, k
