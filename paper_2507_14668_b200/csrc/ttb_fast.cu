@@ -355,8 +355,12 @@ struct SgdArgs {
 // Finiteness pre-pass over the final gradients (fused_update rejects a
 // non-finite gradient before touching any core, backward.py:190-194): sets
 // TTB_ERRBIT_NONFINITE in *err; the update kernel that follows reads it.
-__global__ void __launch_bounds__(256) k_gradcheck(const float* __restrict__ g, int64_t n, int* __restrict__ err) {
+__global__ void __launch_bounds__(256) k_gradcheck(const float* __restrict__ g, int64_t n, int* __restrict__ err,
+                                                   const int* __restrict__ suspect) {
   pdl_enter();
+  // the backward flags any contribution that is non-finite or >= 2^95 in
+  // magnitude; without one, every final sum (< 2^31 terms) is finite
+  if (suspect && *(volatile const int*)suspect == 0) return;
   bool bad = false;
   const int64_t n4 = (reinterpret_cast<uintptr_t>(g) & 15) ? 0 : n >> 2;
   const float4* g4 = reinterpret_cast<const float4*>(g);
@@ -879,7 +883,7 @@ constexpr int kChunkRows = (kStSbi + kStG + kStG3 - 8 * 256) / (8 + 256) & ~7;  
 __device__ __forceinline__ int xs_idx(int it, int a, int b, int c) { return it * 512 + (4 * a + b) * 32 + (c ^ (b << 3)); }
 
 // chunks of whole items with <= cap positions each (thread 0)
-__device__ inline void make_chunks(const TileMeta* m, int* ch, int cap) {
+__device__ inline void make_chunks(const TileMeta* m, int* ch, int cap, int round = kThreads / 32) {
   int nc = 0, it = 0;
   const int n = m->n;
   ch[0] = 0;
@@ -893,7 +897,7 @@ __device__ inline void make_chunks(const TileMeta* m, int* ch, int cap) {
     while (it < n && m->start[it + 1] - base <= cap) ++it;
     // whole rounds of one item per warp where possible (items have similar
     // lengths inside a tile, so the warps finish a chunk together)
-    if (it < n && it - first > kThreads / 32) it = first + (it - first) / (kThreads / 32) * (kThreads / 32);
+    if (it < n && it - first > round) it = first + (it - first) / round * round;
     ch[++nc] = it;
   }
   ch[kTileItems + 1] = nc;
@@ -984,7 +988,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
     stage_rows_async<!kRows>(np, st_sbi, gout, G3, m3, st_g, st_g3);
   }
   uint32_t phase = 0;
-  int bad = 0, slot = 0;
+  bool bad = false;
+  int slot = 0;
   int prev_i2 = -1;
   for (int t = tb; t < te; ++t, slot ^= 1) {
     const TileMeta* m = &s_m[slot];
@@ -1105,7 +1110,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
 #pragma unroll
               for (int j = 0; j < 4; ++j) dh[j] = fmaf(x[ab], gv[4 * ab + j], dh[j]);
             if (!(dbg & 1)) red_v4(dG3 + ((size_t)lane * m3 + i3) * 4, dh[0], dh[1], dh[2], dh[3]);
-            bad |= !isfinite((dh[0] + dh[1]) + (dh[2] + dh[3]));
+            bad |= suspicious(dh[0]) | suspicious(dh[1]) | suspicious(dh[2]) | suspicious(dh[3]);
 #pragma unroll
             for (int ab = 0; ab < 16; ++ab) {
               z[ab] = fmaf(gv[4 * ab], h3.x, z[ab]);
@@ -1136,7 +1141,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
   #pragma unroll
               for (int j = 0; j < 4; ++j) dh[j] = fmaf(x[ab], gv[4 * ab + j], dh[j]);
             if (!(dbg & 1)) red_v4(dG3 + ((size_t)lane * m3 + i3) * 4, dh[0], dh[1], dh[2], dh[3]);
-            bad |= !isfinite((dh[0] + dh[1]) + (dh[2] + dh[3]));
+            bad |= suspicious(dh[0]) | suspicious(dh[1]) | suspicious(dh[2]) | suspicious(dh[3]);
   #pragma unroll
             for (int ab = 0; ab < 16; ++ab) {
               z[ab] = fmaf(gv[4 * ab], h3.x, z[ab]);
@@ -1146,13 +1151,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
             }
           }
         }
-        float zs = 0.f;
 #pragma unroll
-        for (int ab = 0; ab < 16; ++ab) {
-          xs[xs_idx(it, ab >> 2, ab & 3, lane)] = z[ab];
-          zs += fabsf(z[ab]);
-        }
-        bad |= !isfinite(zs);
+        for (int ab = 0; ab < 16; ++ab) xs[xs_idx(it, ab >> 2, ab & 3, lane)] = z[ab];
       }
       if (ch == nchunk - 1) {  // slots past the tile's items hold zeros
         for (int it = n + warp; it < kTileItems; it += kThreads / 32)
@@ -1272,7 +1272,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
         float* d2 = dG2 + ((size_t)m->i2 * 4 + b) * 32 + c;
         const size_t ks = (size_t)g.m2 * C;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) red_f32(d2 + (size_t)(16 * half + i) * ks, v[i] + w2[i]);
+        for (int i = 0; i < 16; ++i) {
+          bad |= suspicious(v[i] + w2[i]);
+          red_f32(d2 + (size_t)(16 * half + i) * ks, v[i] + w2[i]);
+        }
       }
       // dG1[i1][a][k]
       umma::tmem_ld16(tl + 448 + 16 * half, v);
@@ -1281,7 +1284,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
       if (it < n) {
         float* d1 = dG1 + ((size_t)item_i1(m, it, g) * 4 + a) * R1 + 16 * half;
 #pragma unroll
-        for (int i = 0; i < 16; i += 4) red_v4(d1 + i, v[i] + w2[i], v[i + 1] + w2[i + 1], v[i + 2] + w2[i + 2], v[i + 3] + w2[i + 3]);
+        for (int i = 0; i < 16; i += 4) {
+          bad |= suspicious(v[i] + w2[i]) | suspicious(v[i + 1] + w2[i + 1]) | suspicious(v[i + 2] + w2[i + 2]) |
+                 suspicious(v[i + 3] + w2[i + 3]);
+          red_v4(d1 + i, v[i] + w2[i], v[i + 1] + w2[i + 1], v[i + 2] + w2[i + 2], v[i + 3] + w2[i + 3]);
+        }
       }
     }
     TSTAMP(8);
@@ -1290,13 +1297,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
     __syncthreads();
     umma::fence_after_sync();
   }
-  if (bad) atomicOr(&hdr[0], 8);
+  if (bad) hdr[kHdrSuspect] = 1;
   if ((dbg & 8) && threadIdx.x == 0 && blockIdx.x == 0) {
     s_tacc[0] = te - tb;
     for (int q = 0; q < 12; ++q) reinterpret_cast<long long*>(hdr + 16)[q] = s_tacc[q];
   }
   if (warp == 0) umma::tmem_free(tmem, 512);
 }
+
+
 
 }  // namespace fast
 
@@ -1366,12 +1375,12 @@ cudaError_t fast_count_su(ttb_handle* h, const void* idx, int idx64, const int64
   return cudaSuccess;
 }
 
-cudaError_t launch_gradcheck(const float* g, int64_t n, int* err, int num_sms, cudaStream_t s) {
+cudaError_t launch_gradcheck(const float* g, int64_t n, int* err, int num_sms, cudaStream_t s, const int* suspect) {
   if (n <= 0) return cudaSuccess;
   int64_t gb = (n / 4 + 255) / 256;
   if (gb < 1) gb = 1;
   if (gb > 2 * num_sms) gb = 2 * num_sms;
-  cudaError_t e = launch_pdl(k_gradcheck, dim3((int)gb), dim3(256), 0, s, g, n, err);
+  cudaError_t e = launch_pdl(k_gradcheck, dim3((int)gb), dim3(256), 0, s, g, n, err, suspect);
   if (e == cudaSuccess) count_launch();
   return e;
 }
@@ -1492,7 +1501,8 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
     const int ng3 = (int)((n2 + kImgThreads - 1) / kImgThreads);
     {
       ProfScope _pc(h, s, "f_gradcheck");
-      if ((e = launch_gradcheck(w.f_grad, n0 + n1 + n2, w.fast_hdr, h->num_sms, s))) return e;
+      if ((e = launch_gradcheck(w.f_grad, n0 + n1 + n2, w.fast_hdr, h->num_sms, s, w.fast_hdr + kHdrSuspect)))
+        return e;
     }
     SgdArgs u = {w.f_grad, v0, v1, v2, p2, lr, mu, mask, 1, w.fast_hdr};
     ProfScope _ps(h, s, "f_sgd");
@@ -1504,6 +1514,13 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
     h->img_c0 = p0;
     h->img_c1 = p1;
   } else {
+    // the caller's gradients: a suspect contribution (see kHdrSuspect) gets
+    // the exact scan, which latches TTB_ERRBIT_NONFINITE (tt_core_grads
+    // rejects non-finite gradients, backward.py:119-128)
+    ProfScope _pc(h, s, "f_gradcheck");
+    if ((e = launch_gradcheck(g0, n0, w.fast_hdr, h->num_sms, s, w.fast_hdr + kHdrSuspect))) return e;
+    if ((e = launch_gradcheck(g1, n1, w.fast_hdr, h->num_sms, s, w.fast_hdr + kHdrSuspect))) return e;
+    if ((e = launch_gradcheck(g2, n2, w.fast_hdr, h->num_sms, s, w.fast_hdr + kHdrSuspect))) return e;
     h->img_valid = 0;  // the caller applies its own update to the cores
   }
   return cudaGetLastError();

@@ -20,6 +20,14 @@ __device__ __forceinline__ void red_f32(float* p, float a) {
   asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(a) : "memory");
 }
 
+// fast_hdr word set by the backward when some gradient contribution is
+// non-finite or >= 2^95 in magnitude. Without one, every final gradient is
+// finite: each element sums < 2^31 contributions from 0, and a rounded sum
+// moves by at most twice the addend (|fl(s + x) - s| <= 2|x|), so it stays
+// below 2^127. The finiteness scan before the fused update runs only if set.
+constexpr int kHdrSuspect = 6;
+__device__ __forceinline__ bool suspicious(float v) { return !(fabsf(v) < 0x1p95f); }
+
 __device__ __forceinline__ int warp_sum(int v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -232,7 +232,8 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
                           double* v2, double lr, double mu, int mask, int mode, cudaStream_t s);
 cudaError_t launch_sgd(float* p, const float* g, double* v, int64_t n, double lr, double mu, cudaStream_t s,
                        const int* err = nullptr);
-cudaError_t launch_gradcheck(const float* g, int64_t n, int* err, int num_sms, cudaStream_t s);
+cudaError_t launch_gradcheck(const float* g, int64_t n, int* err, int num_sms, cudaStream_t s,
+                             const int* suspect = nullptr);
 cudaError_t launch_export_plan(ttb_handle* h, int64_t* work, int64_t* slot_occ, int64_t* seg_ids,
                                int64_t* seg_inv, int64_t* digits, cudaStream_t s);
 cudaError_t launch_export_unique(ttb_handle* h, int64_t* rows, float* grads, cudaStream_t s);

@@ -161,3 +161,34 @@ def test_counter_laws():
     b = O.counters_backward(T=10, U=6, d=3, with_buffer=True)
     assert b["slice_mults"] == 42 and b["row_adds"] == 4
     assert O.counters_backward(T=10, U=6, d=3, with_buffer=False)["slice_mults"] == 48
+
+
+@pytest.mark.parametrize("name,rows,ranks,bs", [("dlrm", (4000, 500, 118), (1, 4, 4, 1), 32),
+                                                 ("dlrm_tc", (12000, 700), (1, 32, 32, 1), 64)])
+def test_dlrm_oracle_matches_reference_run(golden, name, rows, ranks, bs):
+    """oracle/dlrm_oracle.py (the CPU DLRM step bench.py times for configs 1
+    and 4) reproduces the reference's train_step bit for bit: three SGD +
+    momentum steps from the reference's initial parameters."""
+    from oracle import dlrm_oracle as D
+    z = golden(name)
+    params = {k[5:]: np.array(v) for k, v in z.items() if k.startswith("init.")}
+    emb = params["top.0.w"].shape[0] - len(rows) * (len(rows) + 1) // 2
+    fields = []
+    for f, r in enumerate(rows):
+        if f"field_{f}.core0" in params:
+            m, n = O.factorize(r, emb, 3)
+            fields.append(O.Geometry(tuple(m), tuple(n), ranks))
+        else:
+            fields.append(None)
+    vel = {}
+    for step in range(3):
+        sp = []
+        for f in range(len(rows)):
+            i, o = z[f"data.idx{f}"], z[f"data.off{f}"]
+            a, b = o[step * bs], o[(step + 1) * bs]
+            sp.append((i[a:b], o[step * bs:(step + 1) * bs + 1] - a))
+        sl = slice(step * bs, (step + 1) * bs)
+        loss = D.train_step(params, fields, z["data.dense"][sl], sp, z["data.labels"][sl], 0.05, 0.9, vel)
+        assert loss == z["losses"][step]
+        for k, p in params.items():
+            assert np.array_equal(p, z[f"step{step}.{k}"]), (step, k)

@@ -22,8 +22,9 @@ cores = [torch.from_numpy(c).to(dev) for c in init_random_cores(shape, 0)]
 ti = torch.from_numpy(idx).to(dev)
 to = torch.arange(0, T + 1, pool, dtype=torch.int64, device=dev)
 gout = torch.randn(B, 64, device=dev) / B
-names = ["X wait", "G1^T stage", "SIMT (grp 0)", "SIMT end sync", "E/dG2 issue + staging", "E wait",
-         "epilogue + next X", "-"]
+names = (["X issue + meta", "X wait", "imgs issue + X tmem ld", "Z phase", "Z lo image + sync", "MMA issue + next rows + E wait",
+          "next X operands", "reductions"] if wl == "cfg2" else
+         ["X issue", "X wait", "X^T dump", "Z phase", "Z^T/image + dG2 issue", "E wait", "-", "reductions + next"])
 for rep in range(3):
     eng.plan(ti, to)
     eng.forward(cores)
