@@ -29,7 +29,7 @@
 namespace ttb {
 namespace fast {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;  // backward: 16 warps, four per TMEM lane quadrant
 
 // ------------------------------------------------------------ plan
 // One persistent kernel (grid <= SM count, all CTAs co-resident) in three
@@ -497,7 +497,7 @@ __device__ inline void mma3_ss(uint32_t d, uint32_t a_hi, uint32_t a_lo, int a_r
 __device__ inline void stage_g1_rows_async(const TileMeta* m, KGeom g, const float* __restrict__ g1img, char* hi,
                                            char* lo) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 1024 / kThreads; ++i) {
     const int e = threadIdx.x + i * kThreads, ia = e >> 3, kq = e & 7, it = ia >> 2, a = ia & 3;
     if (it < m->n) {
       const float* src = g1img + (size_t)item_i1(m, it, g) * kG1Img + a * 32 + 4 * kq;
@@ -512,7 +512,7 @@ __device__ inline void stage_g1_rows_async(const TileMeta* m, KGeom g, const flo
 // (one 64-row image: rows k = hi, rows 32 + k = lo)
 __device__ inline void stage_g1_t_async(const TileMeta* m, KGeom g, const float* __restrict__ g1img, char* img) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 1024 / kThreads; ++i) {
     const int e = threadIdx.x + i * kThreads, it = e >> 5, k = e & 31;
     const uint32_t oh = umma::sw128_off(k, 4 * it, 64), ol = umma::sw128_off(32 + k, 4 * it, 64);
     if (it < m->n) {
@@ -876,7 +876,10 @@ constexpr int kStSbi = kChunkPos * 8, kStG = kChunkPos * 256, kStG3 = kChunkPos 
 constexpr int kBwdSmem = 4 * kImg + 4 * kImg + kStSbi + kStG + kStG3 + 1024;
 // row-grouped backward (pooled batches): G3 slices are read per distinct row
 // from L2 instead of staged per position, so a chunk holds 3x the positions
-constexpr int kChunkRows = (kStSbi + kStG + kStG3 - 8 * 256) / (8 + 256) & ~7;  // + 8 warps' 256 B row scratch
+constexpr int kChunkRows = (kStSbi + kStG + kStG3 - (kThreads / 32) * 256) / (8 + 256) & ~7;  // + per-warp 256 B row scratch
+// warps per TMEM lane quadrant, and the columns each takes of a 128- / 32-column operand
+constexpr int kQuadWarps = kThreads / 128, kSpan = 128 / kQuadWarps, kRedCols = 32 / kQuadWarps;
+static_assert(kSpan == 32 && kRedCols == 8, "column split below assumes 16 warps");
 
 // X / Z slot element (item, a, b, c); the XOR keeps both the (c, b)-lane
 // dump and the c-lane reads free of bank conflicts
@@ -914,6 +917,24 @@ __device__ inline void stage_rows_async(int np, const int2* st_sbi, const float*
   for (int e = threadIdx.x; e < np * 32; e += kThreads) {
     const int p = e >> 5, cc = e & 31;
     cp_async16(st_g3 + e, reinterpret_cast<const float4*>(G3) + (size_t)cc * m3 + st_sbi[p].y);
+  }
+}
+
+// one gradient row g (16 float4, (a, b) major) against the item's X^T column
+// x[(a, b)] (lane c): dH[c, :] = sum_ab x[ab] g[ab, :] and Z[ab, c] += g[ab, :] . h3
+__device__ __forceinline__ void lookup_update(const float4* src, const float (&x)[16], float (&z)[16], float4 h3,
+                                              float (&dh)[4]) {
+#pragma unroll
+  for (int ab = 0; ab < 16; ++ab) {
+    const float4 v = src[ab];
+    dh[0] = fmaf(x[ab], v.x, dh[0]);
+    dh[1] = fmaf(x[ab], v.y, dh[1]);
+    dh[2] = fmaf(x[ab], v.z, dh[2]);
+    dh[3] = fmaf(x[ab], v.w, dh[3]);
+    z[ab] = fmaf(v.x, h3.x, z[ab]);
+    z[ab] = fmaf(v.y, h3.y, z[ab]);
+    z[ab] = fmaf(v.z, h3.z, z[ab]);
+    z[ab] = fmaf(v.w, h3.w, z[ab]);
   }
 }
 
@@ -957,7 +978,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
   if (warp == 0) umma::tmem_alloc(&s_tmem, 512);
   if (threadIdx.x == 32) umma::mbar_init(&s_mbar, 1);
   int4 pf = make_int4(0, 0, 0, 0);
-  if (warp == 7 && tb < te) {
+  if (warp == kThreads / 32 - 1 && tb < te) {
     fetch_meta_async(tile_info[tb], item_start, item_key, &s_m[0]);
     if (tb + 1 < te) pf = tile_info[tb + 1];
   }
@@ -966,7 +987,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
   __syncthreads();
   umma::fence_after_sync();
   const uint32_t tmem = s_tmem;
-  const int q4 = warp & 3, half = warp >> 2;
+  const int q4 = warp & 3, qw = warp >> 2;  // lane quadrant, and this warp's share of its columns
   const int row = 32 * q4 + lane;  // TMEM lane of this thread: (c, b) = (row / 4, row % 4)
   const int c = row >> 2, b = row & 3;
   const uint32_t tl = tmem + ((uint32_t)(32 * q4) << 16);
@@ -1011,7 +1032,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
       }
       umma::commit(&s_mbar);
     }
-    if (warp == 7) {  // next tile's metadata into the other slot
+    if (warp == kThreads / 32 - 1) {  // next tile's metadata into the other slot
       const int tn = t + 1;
       if (tn < te) {
         fetch_meta_async(pf, item_start, item_key, &s_m[slot ^ 1]);
@@ -1024,17 +1045,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
     phase ^= 1u;
     umma::fence_after_sync();
     TSTAMP(2);
-    // X^T -> item slots (this half's 64 columns, both loads in flight together)
+    // X^T -> item slots (this warp's 32 columns)
     {
-      uint32_t v0[32], v1[32];
-      umma::tmem_ld32_nw(tl + 64 * half, v0);
-      umma::tmem_ld32_nw(tl + 64 * half + 32, v1);
+      uint32_t v0[kSpan];
+      umma::tmem_ld32_nw(tl + kSpan * qw, v0);
       umma::tmem_wait_ld();
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int col = 64 * half + i;
+      for (int i = 0; i < kSpan; ++i) {
+        const int col = kSpan * qw + i;
         xs[xs_idx(col >> 2, col & 3, b, c)] = __uint_as_float(v0[i]);
-        xs[xs_idx((col + 32) >> 2, (col + 32) & 3, b, c)] = __uint_as_float(v1[i]);
       }
     }
     umma::fence_before_sync();
@@ -1094,61 +1113,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
               __syncwarp();
               src = st_acc + warp * 16;
             }
-            float gv[64];
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              const float4 v = src[k];
-              gv[4 * k] = v.x;
-              gv[4 * k + 1] = v.y;
-              gv[4 * k + 2] = v.z;
-              gv[4 * k + 3] = v.w;
-            }
-            __syncwarp();  // the scratch is rewritten by the next row
             float dh[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (int ab = 0; ab < 16; ++ab)
-#pragma unroll
-              for (int j = 0; j < 4; ++j) dh[j] = fmaf(x[ab], gv[4 * ab + j], dh[j]);
+            lookup_update(src, x, z, h3, dh);
+            __syncwarp();  // the scratch is rewritten by the next row
             if (!(dbg & 1)) red_v4(dG3 + ((size_t)lane * m3 + i3) * 4, dh[0], dh[1], dh[2], dh[3]);
             bad |= suspicious(dh[0]) | suspicious(dh[1]) | suspicious(dh[2]) | suspicious(dh[3]);
-#pragma unroll
-            for (int ab = 0; ab < 16; ++ab) {
-              z[ab] = fmaf(gv[4 * ab], h3.x, z[ab]);
-              z[ab] = fmaf(gv[4 * ab + 1], h3.y, z[ab]);
-              z[ab] = fmaf(gv[4 * ab + 2], h3.z, z[ab]);
-              z[ab] = fmaf(gv[4 * ab + 3], h3.w, z[ab]);
-            }
           }
         } else {
           // one lookup per bag (T = B): every position is its own bag, so a
           // position is one gradient row, one dG3 reduction and one Z update
-          const int s1 = m->start[it + 1] - p0;
+          const int s1 = (dbg & 64) ? 0 : m->start[it + 1] - p0;  // (ablations: TTB_DBG 64 / 32)
           for (int qq = m->start[it] - p0; qq < s1; ++qq) {
             const int i3 = st_sbi[qq].y;
             const float4 h3 = st_g3[qq * 32 + lane];
-            float gv[64];
-  #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              const float4 v = st_g[qq * 16 + k];
-              gv[4 * k] = v.x;
-              gv[4 * k + 1] = v.y;
-              gv[4 * k + 2] = v.z;
-              gv[4 * k + 3] = v.w;
-            }
             float dh[4] = {0.f, 0.f, 0.f, 0.f};
-  #pragma unroll
-            for (int ab = 0; ab < 16; ++ab)
-  #pragma unroll
-              for (int j = 0; j < 4; ++j) dh[j] = fmaf(x[ab], gv[4 * ab + j], dh[j]);
+            if (!(dbg & 32)) lookup_update(st_g + qq * 16, x, z, h3, dh);
             if (!(dbg & 1)) red_v4(dG3 + ((size_t)lane * m3 + i3) * 4, dh[0], dh[1], dh[2], dh[3]);
             bad |= suspicious(dh[0]) | suspicious(dh[1]) | suspicious(dh[2]) | suspicious(dh[3]);
-  #pragma unroll
-            for (int ab = 0; ab < 16; ++ab) {
-              z[ab] = fmaf(gv[4 * ab], h3.x, z[ab]);
-              z[ab] = fmaf(gv[4 * ab + 1], h3.y, z[ab]);
-              z[ab] = fmaf(gv[4 * ab + 2], h3.z, z[ab]);
-              z[ab] = fmaf(gv[4 * ab + 3], h3.w, z[ab]);
-            }
           }
         }
 #pragma unroll
@@ -1170,20 +1151,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
     const TileMeta* mn = &s_m[slot ^ 1];
     int npn = 0;
     // ---- Z^T into TMEM (hi / lo) and the Z image (hi) for the E GEMM
-    float zr[64];
+    // (one split serves both: Z^T hi / lo to TMEM now, the Z images after the barrier)
+    float zh[kSpan], zl[kSpan];
 #pragma unroll
-    for (int i = 0; i < 64; ++i) {
-      const int ia = 64 * half + i;
-      zr[i] = xs[xs_idx(ia >> 2, ia & 3, b, c)];
+    for (int i = 0; i < kSpan; ++i) {
+      const int ia = kSpan * qw + i;
+      umma::split2(xs[xs_idx(ia >> 2, ia & 3, b, c)], zh[i], zl[i]);
     }
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      float h[32], l[32];
-#pragma unroll
-      for (int u = 0; u < 32; ++u) umma::split3(zr[32 * hh + u], h[u], l[u]);
-      umma::tmem_st32(tl + 128 + 64 * half + 32 * hh, h);
-      umma::tmem_st32(tl + 256 + 64 * half + 32 * hh, l);
-    }
+    umma::tmem_st32(tl + 128 + kSpan * qw, zh);
+    umma::tmem_st32(tl + 256 + kSpan * qw, zl);
     umma::tmem_wait_st();
     cp_async_wait_all();  // G2 k / G1^T images (issued before the Z phase)
     sync_for_mma();       // every slot read before the image overwrites them; Z^T is in TMEM
@@ -1216,12 +1192,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
     // rows can stream in while the E GEMM runs)
     char* zlo = sm + 8 * kImg + (kRows ? 4096 : kChunkPos * 8 + kChunkPos * 256);
 #pragma unroll
-    for (int i = 0; i < 64; ++i) {
-      float hh, ll;
-      umma::split3(zr[i], hh, ll);
-      const uint32_t o = umma::sw128_off(64 * half + i, row, 128);
-      *(float*)(zi + o) = hh;
-      *(float*)(zlo + o) = ll;
+    for (int i = 0; i < kSpan; ++i) {
+      const uint32_t o = umma::sw128_off(kSpan * qw + i, row, 128);
+      *(float*)(zi + o) = zh[i];
+      *(float*)(zlo + o) = zl[i];
     }
     cp_async_wait_all();  // next tile's positions
     sync_for_mma();
@@ -1264,27 +1238,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
       }
     }
     if (!(dbg & 4)) {
-      float v[16], w2[16];
+      float v[kRedCols], w2[kRedCols];
       // dG2[k][i2][b][c] = D[:, k] + D[:, 32 + k], once per run of tiles of one i2
       if (tn >= te || mn->i2 != m->i2) {
-        umma::tmem_ld16(tl + 384 + 16 * half, v);
-        umma::tmem_ld16(tl + 384 + 32 + 16 * half, w2);
+        umma::tmem_ld8(tl + 384 + kRedCols * qw, v);
+        umma::tmem_ld8(tl + 384 + 32 + kRedCols * qw, w2);
         float* d2 = dG2 + ((size_t)m->i2 * 4 + b) * 32 + c;
         const size_t ks = (size_t)g.m2 * C;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
+        for (int i = 0; i < kRedCols; ++i) {
           bad |= suspicious(v[i] + w2[i]);
-          red_f32(d2 + (size_t)(16 * half + i) * ks, v[i] + w2[i]);
+          red_f32(d2 + (size_t)(kRedCols * qw + i) * ks, v[i] + w2[i]);
         }
       }
       // dG1[i1][a][k]
-      umma::tmem_ld16(tl + 448 + 16 * half, v);
-      umma::tmem_ld16(tl + 448 + 32 + 16 * half, w2);
+      umma::tmem_ld8(tl + 448 + kRedCols * qw, v);
+      umma::tmem_ld8(tl + 448 + 32 + kRedCols * qw, w2);
       const int it = row >> 2, a = row & 3;
       if (it < n) {
-        float* d1 = dG1 + ((size_t)item_i1(m, it, g) * 4 + a) * R1 + 16 * half;
+        float* d1 = dG1 + ((size_t)item_i1(m, it, g) * 4 + a) * R1 + kRedCols * qw;
 #pragma unroll
-        for (int i = 0; i < 16; i += 4) {
+        for (int i = 0; i < kRedCols; i += 4) {
           bad |= suspicious(v[i] + w2[i]) | suspicious(v[i + 1] + w2[i + 1]) | suspicious(v[i + 2] + w2[i + 2]) |
                  suspicious(v[i + 3] + w2[i + 3]);
           red_v4(d1 + i, v[i] + w2[i], v[i + 1] + w2[i + 1], v[i + 2] + w2[i + 2], v[i + 3] + w2[i + 3]);

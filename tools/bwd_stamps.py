@@ -22,9 +22,8 @@ cores = [torch.from_numpy(c).to(dev) for c in init_random_cores(shape, 0)]
 ti = torch.from_numpy(idx).to(dev)
 to = torch.arange(0, T + 1, pool, dtype=torch.int64, device=dev)
 gout = torch.randn(B, 64, device=dev) / B
-names = (["X issue + meta", "X wait", "imgs issue + X tmem ld", "Z phase", "Z lo image + sync", "MMA issue + next rows + E wait",
-          "next X operands", "reductions"] if wl == "cfg2" else
-         ["X issue", "X wait", "X^T dump", "Z phase", "Z^T/image + dG2 issue", "E wait", "-", "reductions + next"])
+names = ["X issue + meta", "X wait", "X^T dump", "Z phase", "Z^T/image + dG2 issue", "E wait", "-",
+         "reductions + next staging"]
 for rep in range(3):
     eng.plan(ti, to)
     eng.forward(cores)
