@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-sample", type=int, default=8192, help="lookups in the CPU-baseline sample")
+    ap.add_argument("--ref-sample", type=int, default=CFG2["batch"],
+                    help="lookups per reference-arm step (default: the whole config-2 batch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip configs 1/3/4 (reported under extras)")
@@ -260,7 +262,7 @@ def run_ours(args):
                         "m=(200,200,250) n=(4,4,4), batch 65536 bags, pooling 1, uniform indices; "
                         "step = plan + forward + backward + SGD(lr 0.05, momentum 0.9)",
             "batch_per_gpu": cfg["batch"], "pooling": cfg["pooling"],
-            "parallelism": f"dp{world}" + (" (NCCL all-reduce of core grads)" if world > 1 else ""),
+            "parallelism": f"dp{world}" + (f" ({dist.get_backend()} all-reduce of core grads)" if world > 1 else ""),
             "l2": "flushed between timed steps (512 MiB write, outside the timed events)",
             "launch": ("one CUDA graph per step" + (" + NCCL all-reduce and update" if world > 1 else ""))
                       if use_graph else "eager launches",
@@ -283,7 +285,9 @@ def run_ours(args):
         if world == 1 and not args.no_cpu_baseline:
             result["cpu_baseline"] = cpu_baseline(args, cfg)
         if not args.no_extras:
-            result["extras"] = bench_extras.run_all(dev) if world == 1 else {}
+            pk = result.get("step_roofline", {})
+            peaks = (pk["fp32_peak_tflops"], pk["hbm_gbs"]) if pk else None
+            result["extras"] = bench_extras.run_all(dev, peaks, cpu=not args.no_cpu_baseline) if world == 1 else {}
             result["extras"]["cfg5_dlrm_dp"] = cfg5
     if world > 1:
         dist.barrier()
@@ -511,8 +515,9 @@ def run_reference(args):
     import multiprocessing as mp
     from oracle import ttb_oracle as O
     cfg = CFG2
-    sample = max(args.cpu_sample, 16384)
+    sample = min(args.ref_sample, cfg["batch"] * cfg["pooling"])
     g, cores, idx, off, gout = cpu_step_sample(cfg, sample)
+    full = sample == cfg["batch"] * cfg["pooling"]
     ncores = os.cpu_count() or 1
     nw = max(1, min(ncores, sample // 256))
     bounds = np.linspace(0, gout.shape[0], nw + 1).astype(int)
@@ -540,8 +545,13 @@ def run_reference(args):
         "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32 cores, f64 gradient accumulation (reference semantics)", "data": "synthetic",
-        "config": {"workload": "BASELINE configs[1] (10M x 64, ranks 32, pooling 1, uniform), bounded sample of "
-                               f"{idx.size} lookups per step", "parallelism": f"{nw} CPU processes"},
+        "config": {"workload": "BASELINE configs[1]: TT-EmbeddingBag microbench, 10M rows x 64, ranks (1,32,32,1), "
+                               "m=(200,200,250) n=(4,4,4), batch 65536 bags, pooling 1, uniform indices; "
+                               "step = plan + forward + backward + SGD(lr 0.05, momentum 0.9)"
+                               + ("" if full else f" (sample of {idx.size} lookups per step)"),
+                   "batch_per_gpu": idx.size // cfg["pooling"], "pooling": cfg["pooling"],
+                   "parallelism": f"{nw} CPU processes (bags sharded, core gradients summed)",
+                   "same_config": full},
         "cpu_baseline": {"value": value, "unit": "lookups/s", "cores": nw, "kind": "port",
                          "sample": f"{idx.size} lookups/step sharded over {nw} processes (oracle/ttb_oracle.py)",
                          "cpu": _cpu_model()},
@@ -549,8 +559,35 @@ def run_reference(args):
     }), flush=True)
 
 
+def self_launch(args) -> int:
+    """`--gpus N` without a torchrun environment: re-run this command as N
+    local ranks (torch.distributed.run, rendezvous on 127.0.0.1) and relay
+    rank 0's JSON line, checking that it reports N GPUs."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py"), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the rank count is visible in the NCCL init lines (stderr)
+    r = subprocess.run(cmd, stdout=subprocess.PIPE, text=True, env=env)
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    if r.returncode != 0 or len(lines) != 1:
+        sys.stderr.write(r.stdout)
+        return r.returncode or 1
+    d = json.loads(lines[0])
+    if d.get("n_gpus") != args.gpus:
+        sys.stderr.write(f"rank 0 reported n_gpus={d.get('n_gpus')}, expected {args.gpus}\n")
+        return 1
+    print(lines[0], flush=True)
+    return 0
+
+
 if __name__ == "__main__":
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(a))
     if a.impl == "reference":
         run_reference(a)
     else:

@@ -43,3 +43,18 @@ def test_own_arm_line():
     assert 0 < rf["frac"] <= 1 and abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-6
     assert d["gpu_launches"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= d["clocks"].keys()
+
+
+def test_gpus_flag_self_launches_ranks():
+    """`--gpus N` without a torchrun environment launches N local ranks
+    itself (torch.distributed.run on 127.0.0.1) and relays rank 0's line,
+    which must report N GPUs. CPU: the reference arm (rank 0 works, the
+    other ranks exit)."""
+    d = _run(["--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0", "--ref-sample", "2048"], 600)
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["config"]["same_config"] is False
+
+
+def test_reference_arm_full_batch_is_same_config():
+    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "0"], 900)
+    assert d["config"]["same_config"] is True and d["config"]["batch_per_gpu"] == 65536
