@@ -124,6 +124,25 @@ int ttb_backward_sgd(ttb_handle *h, float *core0, float *core1, float *core2,
                      double *vel2, double lr, double momentum,
                      int update_mask, ttb_stream stream);
 
+/* K4 + Adagrad (torch.optim.Adagrad semantics, no lr / weight decay) fused
+ * like ttb_backward_sgd: s <- s + g^2 (fp64 squared-gradient sums, one per
+ * core element, zero-initialised by the caller); core <- f32(f64(core) -
+ * lr g / (sqrt(s) + eps)). North-star item (3) names Adagrad next to SGD;
+ * the reference implements only SGD(+momentum), so this rule
+ * follows PyTorch's published algorithm. Tensor-core pipeline only
+ * (TTB_ESTATE otherwise: use ttb_backward + ttb_adagrad_update). */
+int ttb_backward_adagrad(ttb_handle *h, float *core0, float *core1, float *core2,
+                         const float *grad_out, double *sum0, double *sum1,
+                         double *sum2, double lr, double eps, int update_mask,
+                         ttb_stream stream);
+
+/* The same Adagrad step on a flat parameter. err (DEVICE int, may be NULL):
+ * when given, the gradient is checked first and a non-finite value latches
+ * TTB_ERRBIT_NONFINITE and cancels the update (as ttb_sgd_update_checked). */
+int ttb_adagrad_update(float *param, const float *grad, double *state_sum,
+                       int64_t n, double lr, double eps, int *err,
+                       ttb_stream stream);
+
 /* The tensor-core pipeline keeps split-tf32 images of cores 0 and 1 in the
  * workspace. They are rebuilt by ttb_forward whenever the core pointers
  * differ from the last forward / fused update, and written directly by
@@ -239,6 +258,11 @@ int ttb_profile_read(ttb_handle *h, char *names, double *ms, int64_t *calls,
  *   number of work items. Changing the option drops the current plan. */
 #define TTB_OPT_BWD_SPLIT 1
 #define TTB_OPT_FAST 2
+/* TTB_OPT_ALLOW_EMPTY (3): 1 = empty bags are allowed and pool to zero rows,
+ * as torch.nn.EmbeddingBag does (the drop-in promise); 0 (the
+ * default) = the reference's ValueError for an empty bag (lookup.py:90-91).
+ * The batch itself must still hold at least one index (ttb_plan: EEMPTY). */
+#define TTB_OPT_ALLOW_EMPTY 3
 int ttb_set_option(ttb_handle *h, int option, int value);
 /* FP32 FMA throughput probe: blocks x 256 threads x iters x 16 flops; the
  * caller times it with CUDA events to get the measured FP32 peak. */

@@ -24,7 +24,7 @@ import numpy as np
 
 __all__ = [
     "Geometry", "factorize", "digits_of", "init_cores", "reuse_plan", "segments",
-    "forward", "forward_direct", "unique_aggregate", "core_grads", "sgd_step",
+    "forward", "forward_direct", "unique_aggregate", "core_grads", "sgd_step", "adagrad_step",
     "counters_forward", "counters_backward", "reconstruct_rows",
     "count_frequencies", "build_bijection", "apply_bijection",
 ]
@@ -305,6 +305,26 @@ def sgd_step(core, grad, lr, momentum=0.0, velocity=None):
         return velocity
     np.subtract(core, lr * g, out=core, casting="same_kind")
     return velocity
+
+
+def adagrad_step(core, grad, lr, eps=1e-10, state_sum=None):
+    """In-place Adagrad, fp64 squared-gradient sums, one rounding into the
+    core. NOT in the reference (it has SGD(+momentum) only, SPEC.md:282);
+    BASELINE north_star item (3) names Adagrad, so this restates
+    torch.optim.Adagrad (lr_decay = weight_decay = 0): s = fma(g, g, s);
+    p += (-lr * g) / (sqrt(s) + eps). Pinned against torch.optim.Adagrad in
+    float64 (tests/test_oracle_golden.py); parity to the reference: unpinned.
+    Returns the state."""
+    g = np.asarray(grad, dtype=np.float64)
+    if not np.isfinite(g).all():
+        raise ValueError("non-finite gradient")
+    if state_sum is None:
+        state_sum = np.zeros(g.shape, dtype=np.float64)
+    # torch's addcmul_ is one fused multiply-add (s + g*g rounded once); the
+    # 64-bit-mantissa long double reproduces it (the device uses __fma_rn)
+    state_sum[...] = (state_sum.astype(np.longdouble) + g.astype(np.longdouble) ** 2).astype(np.float64)
+    np.add(core, (-lr * g) / (np.sqrt(state_sum) + eps), out=core, casting="same_kind")
+    return state_sum
 
 
 # ----------------------------------------------------------------- counters

@@ -30,11 +30,12 @@ ERRBIT_NONFINITE = 8
 
 OPT_BWD_SPLIT = 1
 OPT_FAST = 2
+OPT_ALLOW_EMPTY = 3
 
 # every symbol include/ttb.h declares (tests check the .so exports them all)
 EXPORTS = [
     "ttb_abi_version", "ttb_strerror", "ttb_launch_count", "ttb_workspace_bytes", "ttb_create",
-    "ttb_destroy", "ttb_plan", "ttb_forward", "ttb_backward", "ttb_aggregate", "ttb_backward_sgd", "ttb_cores_modified", "ttb_sgd_update",
+    "ttb_destroy", "ttb_plan", "ttb_forward", "ttb_backward", "ttb_aggregate", "ttb_backward_sgd", "ttb_cores_modified", "ttb_sgd_update", "ttb_backward_adagrad", "ttb_adagrad_update",
     "ttb_check_finite", "ttb_sgd_update_checked", "ttb_export_fast_plan", "ttb_plan_counts",
     "ttb_read_status", "ttb_export_plan", "ttb_export_unique", "ttb_export_slots",
     "ttb_profile_enable", "ttb_profile_read", "ttb_set_option", "ttb_fma_peak",
@@ -65,6 +66,8 @@ _PROTOS = {
     "ttb_backward_sgd": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _dbl, _int, _vp]),
     "ttb_cores_modified": (_int, [_vp]),
     "ttb_sgd_update": (_int, [_vp, _vp, _vp, _i64, _dbl, _dbl, _vp]),
+    "ttb_backward_adagrad": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _dbl, _int, _vp]),
+    "ttb_adagrad_update": (_int, [_vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _vp]),
     "ttb_check_finite": (_int, [_vp, _i64, _vp, _vp]),
     "ttb_sgd_update_checked": (_int, [_vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _vp]),
     "ttb_read_status": (_int, [_vp, C.POINTER(_i64), _vp]),

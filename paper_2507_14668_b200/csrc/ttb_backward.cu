@@ -321,6 +321,24 @@ __global__ void k_sgd(float* __restrict__ p, const float* __restrict__ gr, doubl
     p[i] = sgd_apply(p[i], gr[i], v ? v + i : nullptr, lr, mu);
 }
 
+__global__ void k_adagrad(float* __restrict__ p, const float* __restrict__ gr, double* __restrict__ st, int64_t n,
+                          double lr, double eps, const int* __restrict__ err) {
+  pdl_enter();
+  if (err && *(volatile const int*)err != 0) return;  // a latched error cancels the update
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = adagrad_apply(p[i], gr[i], st + i, lr, eps);
+}
+
+cudaError_t launch_adagrad(float* p, const float* g, double* st, int64_t n, double lr, double eps, cudaStream_t s,
+                           const int* err) {
+  if (n <= 0) return cudaSuccess;
+  int64_t grid = (n + kBlock - 1) / kBlock;
+  if (grid > 148 * 8) grid = 148 * 8;
+  launch_pdl(k_adagrad, dim3((int)grid), dim3(kBlock), 0, s, p, g, st, n, lr, eps, err);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sgd(float* p, const float* g, double* v, int64_t n, double lr, double mu, cudaStream_t s,
                        const int* err) {
   if (n <= 0) return cudaSuccess;
@@ -547,6 +565,10 @@ static cudaError_t dispatch(const DynDims& d, bool aligned, F&& f) {
 cudaError_t launch_forward(ttb_handle* h, const float* c0, const float* c1, const float* c2, float* out,
                            cudaStream_t s) {
   const bool al = (((uintptr_t)c0 | (uintptr_t)c1 | (uintptr_t)c2 | (uintptr_t)out) & 15) == 0;
+  if (h->allow_empty) {  // rows of empty bags read zero whatever the close kernels write
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(float) * (size_t)h->B * h->dims.n1 * h->dims.n2 * h->dims.n3, s);
+    if (e != cudaSuccess) return e;
+  }
   return dispatch(h->dims, al, [&](auto d) { return forward_impl<decltype(d)>(h, c0, c1, c2, out, s); });
 }
 

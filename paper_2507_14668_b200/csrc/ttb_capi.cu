@@ -344,6 +344,32 @@ int ttb_backward_sgd(ttb_handle* h, float* c0, float* c1, float* c2, const float
   return TTB_OK;
 }
 
+int ttb_backward_adagrad(ttb_handle* h, float* c0, float* c1, float* c2, const float* grad_out, double* s0,
+                         double* s1, double* s2, double lr, double eps, int update_mask, ttb_stream stream) {
+  if (!h || !c0 || !c1 || !c2 || !grad_out) return TTB_EINVAL;
+  if (!(lr >= 0.0) || !(eps >= 0.0)) return TTB_EINVAL;
+  if (((update_mask & 1) && !s0) || ((update_mask & 2) && !s1) || ((update_mask & 4) && !s2)) return TTB_EINVAL;
+  if (!h->forwarded) return TTB_ESTATE;
+  if (!h->fast) return TTB_ESTATE;  // deterministic pipeline: ttb_backward, then ttb_adagrad_update
+  cudaError_t e = fast_backward(h, c0, c1, c2, grad_out, nullptr, nullptr, nullptr, c0, c1, c2, s0, s1, s2, lr, eps,
+                                update_mask, 1, (cudaStream_t)stream, 1);
+  if (e != cudaSuccess) return TTB_ECUDA;
+  h->backwarded = 1;
+  h->pmap_clean = 1;
+  return TTB_OK;
+}
+
+int ttb_adagrad_update(float* param, const float* grad, double* state_sum, int64_t n, double lr, double eps,
+                       int* err, ttb_stream stream) {
+  if (!param || !grad || !state_sum || n < 0) return TTB_EINVAL;
+  if (!(lr >= 0.0) || !(eps >= 0.0)) return TTB_EINVAL;
+  if (err) {
+    int rc = ttb_check_finite(grad, n, err, stream);
+    if (rc) return rc;
+  }
+  return cuda_status(launch_adagrad(param, grad, state_sum, n, lr, eps, (cudaStream_t)stream, err));
+}
+
 int ttb_cores_modified(ttb_handle* h) {
   if (!h) return TTB_EINVAL;
   h->img_valid = 0;

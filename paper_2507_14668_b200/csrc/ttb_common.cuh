@@ -202,4 +202,16 @@ __device__ __forceinline__ float sgd_apply(float p, float g, double* vel, double
   return (float)__dsub_rn((double)p, step);
 }
 
+// Adagrad (torch.optim.Adagrad semantics, no weight / lr decay): the
+// squared-gradient sum s in fp64, s <- fma(g, g, s), p <- f32(p + (-lr g) / (sqrt(s) + eps)),
+// one rounding into the parameter like sgd_apply. (The reference has no
+// Adagrad — SPEC.md:282; BASELINE north_star asks for it next to SGD.)
+__device__ __forceinline__ float adagrad_apply(float p, float g, double* s, double lr, double eps) {
+  const double gd = (double)g;
+  const double ss = __fma_rn(gd, gd, *s);  // torch's addcmul_: one rounding
+  *s = ss;
+  const double step = __ddiv_rn(__dmul_rn(-lr, gd), __dadd_rn(__dsqrt_rn(ss), eps));
+  return (float)__dadd_rn((double)p, step);
+}
+
 }  // namespace ttb

@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
                                                         int4* __restrict__ gtot, int* __restrict__ item_start,
                                                         int* __restrict__ cta_tiles, int ctas,
                                                         unsigned* __restrict__ item_key, int4* __restrict__ tile_info,
-                                                        int2* __restrict__ sbi, int* __restrict__ hdr, int dbg) {
+                                                        int2* __restrict__ sbi, int* __restrict__ hdr, int dbg,
+                                                        int allow_empty) {
   pdl_enter();
 #define PSTAMP(i)                                                                                          \
   do {                                                                                                     \
@@ -101,7 +102,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
     const int64_t ob = offsets[b], on = offsets[b + 1];
     if (b == 0 && ob != 0) bits |= 4;
     if (b == B - 1 && on != (int64_t)T) bits |= 4;
-    if (on == ob) bits |= 2;
+    if (on == ob) bits |= allow_empty ? 0 : 2;
     else if (on < ob) bits |= 4;
     const int lo = (int)(ob < 0 ? 0 : (ob > T ? T : ob)), hi = (int)(on < lo ? lo : (on > T ? T : on));
     for (int t = lo; t < hi; ++t) bag_of[t] = b;
@@ -347,9 +348,10 @@ struct SgdArgs {
   const float* grad;  // flat |G1| + |G2| + |G3| gradients
   double *v0, *v1, *v2;
   float* p2;
-  double lr, mu;
+  double lr, mu;       // Adagrad: mu carries eps
   int mask, on;
   const int* err;     // device error word: any bit set -> no update (cores untouched)
+  int adagrad;        // 0: SGD(+momentum), v = velocity; 1: Adagrad, v = squared-gradient sums
 };
 
 // Finiteness pre-pass over the final gradients (fused_update rejects a
@@ -375,6 +377,7 @@ __global__ void __launch_bounds__(256) k_gradcheck(const float* __restrict__ g, 
 
 __device__ __forceinline__ float maybe_sgd(float p, const SgdArgs& u, int core, size_t flat, size_t j, double* v) {
   if (!u.on || !((u.mask >> core) & 1)) return p;
+  if (u.adagrad) return adagrad_apply(p, u.grad[flat], v + j, u.lr, u.mu);
   return sgd_apply(p, u.grad[flat], v ? v + j : nullptr, u.lr, u.mu);
 }
 
@@ -1389,12 +1392,12 @@ cudaError_t fast_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* 
   if (idx64)
     e = launch_pdl_coop(k_fplan<long long>, dim3(grid), dim3(kPlanThreads), 0, s, (const long long*)idx, offsets, T, B,
                    h->kg, w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_rstart, w.f_split, w.f_gtot, w.f_item_start, w.f_cta, h->num_sms,
-                   w.f_item_key, w.f_tile_info, w.f_sbi, w.fast_hdr, getenv("TTB_DBG") ? 1 : 0);
+                   w.f_item_key, w.f_tile_info, w.f_sbi, w.fast_hdr, getenv("TTB_DBG") ? 1 : 0, h->allow_empty);
   else
     e = launch_pdl_coop(k_fplan<int>, dim3(grid), dim3(kPlanThreads), 0, s, (const int*)idx, offsets, T, B, h->kg,
                    w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_rstart, w.f_split, w.f_gtot, w.f_item_start, w.f_cta, h->num_sms,
                    w.f_item_key,
-                   w.f_tile_info, w.f_sbi, w.fast_hdr, getenv("TTB_DBG") ? 1 : 0);
+                   w.f_tile_info, w.f_sbi, w.fast_hdr, getenv("TTB_DBG") ? 1 : 0, h->allow_empty);
   if (e) return e;
   count_launch();
   return cudaGetLastError();
@@ -1423,7 +1426,9 @@ cudaError_t fast_forward(ttb_handle* h, const float* c0, const float* c1, const 
     h->img_c0 = c0;
     h->img_c1 = c1;
   }
-  const int direct = h->T == h->B;
+  // one store per lookup into its bag's row; with empty bags allowed, T = B
+  // no longer means one lookup per bag (and empty rows must read zero)
+  const int direct = h->T == h->B && !h->allow_empty;
   if (!direct && (e = cudaMemsetAsync(out, 0, sizeof(float) * (size_t)h->B * NOUT, s))) return e;
   const int grid = h->num_sms;  // = the plan's CTA ranges (k_fplan cta_tiles)
   {
@@ -1442,7 +1447,7 @@ cudaError_t fast_forward(ttb_handle* h, const float* c0, const float* c1, const 
 // mode 0: gradients into g0..g2; mode 1: SGD(+momentum) on the cores (mask)
 cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const float* c2, const float* gout,
                           float* g0, float* g1, float* g2, float* p0, float* p1, float* p2, double* v0, double* v1,
-                          double* v2, double lr, double mu, int mask, int mode, cudaStream_t s) {
+                          double* v2, double lr, double mu, int mask, int mode, cudaStream_t s, int adagrad) {
   Workspace& w = h->w;
   cudaError_t e;
   const int64_t n0 = (int64_t)h->kg.m1 * 4 * R1, n1 = (int64_t)R1 * h->kg.m2 * C, n2 = (int64_t)32 * h->kg.m3 * 4;
@@ -1478,7 +1483,7 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
       if ((e = launch_gradcheck(w.f_grad, n0 + n1 + n2, w.fast_hdr, h->num_sms, s, w.fast_hdr + kHdrSuspect)))
         return e;
     }
-    SgdArgs u = {w.f_grad, v0, v1, v2, p2, lr, mu, mask, 1, w.fast_hdr};
+    SgdArgs u = {w.f_grad, v0, v1, v2, p2, lr, mu, mask, 1, w.fast_hdr, adagrad};
     ProfScope _ps(h, s, "f_sgd");
     if ((e = launch_pdl(k_coreimg, dim3(h->kg.m2 + (h->kg.m1 + 3) / 4 + (ng3 < 64 ? ng3 : 64)), dim3(kImgThreads),
                         img_smem, s, p0, p1, h->kg, w.f_img, w.f_g1img, u)))

@@ -121,6 +121,7 @@ struct ttb_handle {
   int cmaxb;             // chunks per i2 group in the backward (dG2 partials)
   int dg2_slots;         // dG2 partial slots per i2 written by the last backward
   int bwd_split;         // use the split backward (rows kernel + tensor-core GEMM kernel)
+  int allow_empty;       // TTB_OPT_ALLOW_EMPTY: empty bags pool to zero rows (nn.EmbeddingBag) instead of an error
   int fast_ok, fast;     // tensor-core pipeline supported / selected (ttb_fast.cu)
   int num_sms;
   const void* plan_idx;  // inputs of the current plan (the legacy plan behind
@@ -229,9 +230,11 @@ cudaError_t fast_forward(ttb_handle* h, const float* c0, const float* c1, const 
                          cudaStream_t s);
 cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const float* c2, const float* gout,
                           float* g0, float* g1, float* g2, float* p0, float* p1, float* p2, double* v0, double* v1,
-                          double* v2, double lr, double mu, int mask, int mode, cudaStream_t s);
+                          double* v2, double lr, double mu, int mask, int mode, cudaStream_t s, int adagrad = 0);
 cudaError_t launch_sgd(float* p, const float* g, double* v, int64_t n, double lr, double mu, cudaStream_t s,
                        const int* err = nullptr);
+cudaError_t launch_adagrad(float* p, const float* g, double* st, int64_t n, double lr, double eps, cudaStream_t s,
+                           const int* err = nullptr);
 cudaError_t launch_gradcheck(const float* g, int64_t n, int* err, int num_sms, cudaStream_t s,
                              const int* suspect = nullptr);
 cudaError_t launch_export_plan(ttb_handle* h, int64_t* work, int64_t* slot_occ, int64_t* seg_ids,

@@ -17,7 +17,8 @@ __global__ void __launch_bounds__(kBlock) k_plan_mark(const IdxT* __restrict__ i
                                                       const int64_t* __restrict__ offsets, int T, int B,
                                                       KGeom g, unsigned* __restrict__ pmap,
                                                       unsigned* __restrict__ keys32, int* __restrict__ bag_of,
-                                                      int* __restrict__ bag_off, int* __restrict__ err) {
+                                                      int* __restrict__ bag_off, int* __restrict__ err,
+                                                      int allow_empty) {
   pdl_enter();
   const int stride = gridDim.x * blockDim.x;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -29,7 +30,7 @@ __global__ void __launch_bounds__(kBlock) k_plan_mark(const IdxT* __restrict__ i
     if (b == B && ob != (int64_t)T) bits |= 4;
     if (b < B) {
       const int64_t on = offsets[b + 1];
-      if (on == ob) bits |= 2;
+      if (on == ob) bits |= allow_empty ? 0 : 2;
       else if (on < ob) bits |= 4;
       // bag id of each index (clamped so malformed offsets cannot write out of range)
       const int lo = (int)(ob < 0 ? 0 : (ob > T ? T : ob)), hi = (int)(on < lo ? lo : (on > T ? T : on));
@@ -303,10 +304,10 @@ cudaError_t launch_plan(ttb_handle* h, const void* idx, int idx64, const int64_t
   ProfScope _ps(h, s, "plan_mark");
   if (idx64)
     launch_pdl(k_plan_mark<long long>, dim3(grid), dim3(kBlock), 0, s, (const long long*)idx, offsets, T, B, h->kg, w.pmap, w.keys32,
-                                                   w.bag_of, w.bag_off, w.err);
+                                                   w.bag_of, w.bag_off, w.err, h->allow_empty);
   else
     launch_pdl(k_plan_mark<int>, dim3(grid), dim3(kBlock), 0, s, (const int*)idx, offsets, T, B, h->kg, w.pmap, w.keys32, w.bag_of,
-                                             w.bag_off, w.err);
+                                             w.bag_off, w.err, h->allow_empty);
   }
   count_launch();
   const int tiles = (T + kTile - 1) / kTile;

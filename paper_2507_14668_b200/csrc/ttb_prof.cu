@@ -98,6 +98,7 @@ int ttb_set_option(ttb_handle* h, int option, int value) {
   if (!h) return TTB_EINVAL;
   switch (option) {
     case 1: h->bwd_split = value ? 1 : 0; return TTB_OK;  // TTB_OPT_BWD_SPLIT
+    case 3: h->allow_empty = value ? 1 : 0; return TTB_OK;  // TTB_OPT_ALLOW_EMPTY
     case 2:                                                // TTB_OPT_FAST
       if (value && !h->fast_ok) return TTB_EINVAL;
       h->fast = value ? 1 : 0;

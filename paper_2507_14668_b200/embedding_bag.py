@@ -46,6 +46,13 @@ class _TTBagFunction(torch.autograd.Function):
             indices, offsets = ctx.saved_tensors
             eng.plan(indices, offsets)
             eng.forward(cores)
+        if module.fused_adagrad is not None:
+            lr, eps = module.fused_adagrad
+            with torch.no_grad():
+                eng.backward_adagrad(cores, grad_out, lr, eps, module.state_sum)
+            if module.check_errors:
+                eng.check_errors()
+            return (None, None, None, *([None] * len(cores)))
         if module.fused_sgd is not None:
             lr, mu = module.fused_sgd
             with torch.no_grad():
@@ -66,7 +73,7 @@ class TTEmbeddingBag(nn.Module):
     def __init__(self, num_embeddings: int, embedding_dim: int, tt_ranks, tt_m=None, tt_n=None, seed: int = 0,
                  target_row_std: float = 0.1, include_last_offset: bool = False, max_indices: int = 1 << 16,
                  max_bags: int | None = None, device=None, check_errors: bool = True, init: bool = True,
-                 deterministic: bool = False):
+                 deterministic: bool = False, allow_empty_bags: bool = False):
         super().__init__()
         tt_ranks = tuple(int(r) for r in tt_ranks)
         d = len(tt_ranks) - 1
@@ -93,8 +100,15 @@ class TTEmbeddingBag(nn.Module):
         # deterministic=True: fixed summation order (bitwise reproducible
         # gradients); otherwise the tensor-core pipeline where supported
         self.engine = TtEngine(self.shape, max_indices, max_bags, dev, deterministic=deterministic)
+        # allow_empty_bags: empty bags pool to zero rows as in torch.nn.EmbeddingBag
+        # (the default keeps the reference's ValueError, lookup.py:90-91)
+        self.allow_empty_bags = bool(allow_empty_bags)
+        if self.allow_empty_bags:
+            self.engine.allow_empty(True)
         self.fused_sgd = None
         self.velocity = None
+        self.fused_adagrad = None
+        self.state_sum = None
 
     # -------------------------------------------------------------- options
     def enable_fused_sgd(self, lr: float, momentum: float = 0.0) -> "TTEmbeddingBag":
@@ -109,6 +123,19 @@ class TTEmbeddingBag(nn.Module):
         self.fused_sgd = None
         return self
 
+    def enable_fused_adagrad(self, lr: float, eps: float = 1e-10,
+                             initial_accumulator_value: float = 0.0) -> "TTEmbeddingBag":
+        """Adagrad (torch.optim.Adagrad semantics) applied inside the backward;
+        state_sum holds the fp64 squared-gradient sums. Replaces a fused SGD."""
+        if lr < 0 or eps < 0 or initial_accumulator_value < 0:
+            raise ValueError("need lr, eps, initial_accumulator_value >= 0")
+        self.fused_sgd = None
+        self.fused_adagrad = (float(lr), float(eps))
+        if self.state_sum is None:
+            self.state_sum = [torch.full(c.shape, float(initial_accumulator_value), dtype=torch.float64,
+                                         device=c.device) for c in self.cores]
+        return self
+
     @property
     def tt_params(self) -> int:
         return self.shape.tt_params
@@ -117,6 +144,9 @@ class TTEmbeddingBag(nn.Module):
     def forward(self, input: torch.Tensor, offsets: torch.Tensor | None = None) -> torch.Tensor:
         off = to_offsets(input, offsets, self.include_last_offset)
         idx = input.reshape(-1)
+        if self.allow_empty_bags and idx.numel() == 0:  # every bag empty: zero rows, zero gradients
+            return torch.zeros((off.numel() - 1, self.embedding_dim), device=self.cores[0].device,
+                               dtype=torch.float32) + 0.0 * sum(c.sum() for c in self.cores)
         return _TTBagFunction.apply(self, idx, off, *self.cores)
 
     def forward_bags(self, bags) -> torch.Tensor:

@@ -89,6 +89,8 @@ class TtEngine:
         self.max_T, self.max_B = T, B
         if self.deterministic:
             self.set_option(nat.OPT_FAST, 0)
+        if getattr(self, "_allow_empty", False):  # options live on the handle: re-apply after a resize
+            self.set_option(nat.OPT_ALLOW_EMPTY, 1)
 
     def ensure_capacity(self, T: int, B: int) -> None:
         if T > self.max_T or B > self.max_B:
@@ -199,8 +201,40 @@ class TtEngine:
                                             _stream()), "backward_sgd")
         self._sig = self._core_sig(cores)
 
+    def backward_adagrad(self, cores, grad_out: torch.Tensor, lr: float, eps: float, state_sum) -> None:
+        """Gradient + in-place Adagrad on the cores (state_sum: fp64 tensors
+        congruent to the cores, updated in place). Fused into the update
+        kernel on the tensor-core pipeline; the deterministic pipeline returns
+        its gradients and applies ttb_adagrad_update, all-or-nothing over the
+        cores (every gradient is checked before any core changes)."""
+        if state_sum is None or len(state_sum) != self.shape.d:
+            raise ValueError("Adagrad needs one fp64 state tensor per core")
+        if self.fast:
+            c = self.native_cores(cores)
+            s = [None, *state_sum] if self.is_d2 else list(state_sum)
+            mask = 0b110 if self.is_d2 else 0b111
+            nat.check(self.lib.ttb_backward_adagrad(self._handle, _ptr(c[0]), _ptr(c[1]), _ptr(c[2]),
+                                                    _ptr(self._gout(grad_out)), _ptr(s[0]), _ptr(s[1]), _ptr(s[2]),
+                                                    float(lr), float(eps), mask, _stream()), "backward_adagrad")
+            self._sig = self._core_sig(cores)
+            return
+        grads = self.backward(cores, grad_out)
+        err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        for g in grads:
+            nat.check(self.lib.ttb_check_finite(_ptr(g), g.numel(), _ptr(err), _stream()), "check_finite")
+        for core, g, st in zip(cores, grads, state_sum):
+            nat.check(self.lib.ttb_adagrad_update(_ptr(core), _ptr(g), _ptr(st), core.numel(), float(lr), float(eps),
+                                                  _ptr(err), _stream()), "adagrad_update")
+        if int(err.item()):
+            raise ValueError("non-finite gradient: cores and Adagrad state left unchanged")
+
     def aggregate(self, grad_out: torch.Tensor) -> None:
         nat.check(self.lib.ttb_aggregate(self._handle, _ptr(self._gout(grad_out)), _stream()), "aggregate")
+
+    def allow_empty(self, on: bool = True) -> None:
+        """Empty bags pool to zero rows (nn.EmbeddingBag) instead of raising."""
+        self._allow_empty = bool(on)
+        self.set_option(nat.OPT_ALLOW_EMPTY, int(bool(on)))
 
     def set_option(self, option: int, value: int) -> None:
         nat.check(self.lib.ttb_set_option(self._handle, int(option), int(value)), "set_option")

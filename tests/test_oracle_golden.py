@@ -192,3 +192,29 @@ def test_dlrm_oracle_matches_reference_run(golden, name, rows, ranks, bs):
         assert loss == z["losses"][step]
         for k, p in params.items():
             assert np.array_equal(p, z[f"step{step}.{k}"]), (step, k)
+
+
+def test_adagrad_oracle_matches_torch_adagrad():
+    """oracle.adagrad_step restates torch.optim.Adagrad (the reference has no
+    Adagrad): three steps in float64 agree with torch bit for bit, and an
+    fp32 core rounds once from the fp64 update."""
+    import torch
+    rng = np.random.default_rng(3)
+    p64 = rng.standard_normal(1000)
+    p = torch.tensor(p64.copy(), dtype=torch.float64, requires_grad=True)
+    opt = torch.optim.Adagrad([p], lr=0.05, eps=1e-10)
+    mine, state = p64.copy(), None
+    for _ in range(3):
+        g = rng.standard_normal(1000)
+        p.grad = torch.tensor(g)
+        opt.step()
+        state = O.adagrad_step(mine, g, 0.05, 1e-10, state)
+        assert np.array_equal(mine, p.detach().numpy())
+    c32 = p64.astype(np.float32)
+    g = rng.standard_normal(1000).astype(np.float32)
+    s = O.adagrad_step(c32, g, 0.05)
+    g64 = g.astype(np.float64)
+    want = (p64.astype(np.float32).astype(np.float64) + (-0.05 * g64) / (np.sqrt(g64 * g64) + 1e-10)).astype(np.float32)
+    assert np.array_equal(c32, want) and np.array_equal(s, g64 * g64)
+    with pytest.raises(ValueError):
+        O.adagrad_step(c32, np.full(1000, np.nan), 0.05)
