@@ -20,6 +20,7 @@ Prints ONE JSON line on rank 0 (contract in the task statement).
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import math
 import os
@@ -185,7 +186,20 @@ def run_ours(args):
         else:
             eng.backward(cores, gout, grads=grads)
 
-    def dp_tail():  # the DP exchange step: NCCL SUM of the core gradients, then the same update on every rank
+    # the DP exchange step: one fused kernel per rank over peer memory
+    # (reduce-scatter -> SGD of the owned shard -> all-gather, ttb_dp.cu) when
+    # every GPU pair has P2P access; else NCCL all-reduce + the same update on
+    # every rank (TTB_DP_EXCHANGE=nccl forces the latter)
+    fused = (world > 1 and dist.get_backend() == "nccl" and os.environ.get("TTB_DP_EXCHANGE", "p2p") == "p2p"
+             and dp.p2p_capable(world))
+    exchange = dp.PeerExchange(flat_p, flat_g) if fused else None
+    err_word = eng.status_word()
+
+    def dp_tail():
+        if exchange is not None:
+            nat.check(lib.ttb_dp_exchange_update(C.byref(exchange.peers), flat_p.numel(), LR, MU, 0, _ptr(flat_v),
+                                                 err_word, 0, _stream()), "dp_exchange_update")
+            return
         dp.allreduce_grads(flat_g)
         nat.check(lib.ttb_sgd_update(_ptr(flat_p), _ptr(flat_g), _ptr(flat_v), flat_p.numel(), LR, MU, _stream()))
 
@@ -218,11 +232,19 @@ def run_ours(args):
                 local_step()
         torch.cuda.current_stream().wait_stream(s_cap)
         torch.cuda.synchronize()
-        if world > 1:
+        if world > 1 and exchange is None:
             def step():
                 graph.replay()
                 dp_tail()
-        else:
+        else:  # the fused exchange is graph-capturable: the whole DP step is one graph
+            if world > 1:
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.stream(s_cap):
+                    with torch.cuda.graph(graph, stream=s_cap):
+                        local_step()
+                        dp_tail()
+                torch.cuda.current_stream().wait_stream(s_cap)
+                torch.cuda.synchronize()
             step = graph.replay
         for _ in range(3):
             step()
@@ -262,9 +284,13 @@ def run_ours(args):
                         "m=(200,200,250) n=(4,4,4), batch 65536 bags, pooling 1, uniform indices; "
                         "step = plan + forward + backward + SGD(lr 0.05, momentum 0.9)",
             "batch_per_gpu": cfg["batch"], "pooling": cfg["pooling"],
-            "parallelism": f"dp{world}" + (f" ({dist.get_backend()} all-reduce of core grads)" if world > 1 else ""),
+            "parallelism": f"dp{world}" + ((" (fused P2P reduce-scatter + SGD + all-gather kernel, ttb_dp.cu)"
+                                            if exchange is not None else
+                                            f" ({dist.get_backend()} all-reduce of core grads + SGD)")
+                                           if world > 1 else ""),
             "l2": "flushed between timed steps (512 MiB write, outside the timed events)",
-            "launch": ("one CUDA graph per step" + (" + NCCL all-reduce and update" if world > 1 else ""))
+            "launch": ("one CUDA graph per step" + (" + all-reduce and update" if world > 1 and exchange is None
+                                                     else ""))
                       if use_graph else "eager launches",
         },
         "counts": host_counts(idx_h, off_h, shape, st),

@@ -62,6 +62,7 @@ extern "C" {
 #define TTB_ERRBIT_EMPTY_BAG 2
 #define TTB_ERRBIT_OFFSETS 4
 #define TTB_ERRBIT_NONFINITE 8
+#define TTB_ERRBIT_PEER 16 /* data-parallel exchange: a peer never arrived */
 
 /*
  * Table geometry, reference TtShape (tt_core.py:41-82) with d = 3.
@@ -168,6 +169,47 @@ int ttb_check_finite(const float *grad, int64_t n, int *err, ttb_stream stream);
 int ttb_sgd_update_checked(float *param, const float *grad, double *velocity,
                            int64_t n, double lr, double momentum, int *err,
                            ttb_stream stream);
+
+/* ---- data parallel: fused exchange over peer memory (NVLink / NVSwitch)
+ * Replaces the DP exchange of Rec-AD (all-reduce of the
+ * TT-core / MLP gradients, then fused_update on every replica,
+ * backward.py:186-204) by ONE kernel per rank: reduce-scatter (P2P loads of
+ * the peers' gradients, fixed peer order, fp64 sum) -> SGD(+momentum) or
+ * Adagrad on this rank's shard -> all-gather (P2P stores of the new values
+ * into every peer's parameters). grad[p] / param[p] / flags[p] are rank p's
+ * buffers as mapped in THIS process (ttb_ipc_open, or plain pointers when all
+ * ranks share one process); flags[p] holds ttb_dp_flag_words(world) u32,
+ * zeroed once before the first call. state: fp64 velocity (momentum > 0) or
+ * Adagrad squared-gradient sums (adagrad = 1, momentum then carries eps),
+ * full length n, only this rank's shard is touched. err (device int, may be
+ * NULL): non-zero on entry marks this rank's gradients bad — then NO rank
+ * updates (TTB_ERRBIT_NONFINITE is latched everywhere); TTB_ERRBIT_PEER is
+ * latched if a peer does not arrive within ~20 s. grid <= 0: one CTA per SM.
+ * Every rank must call it once per step with the same n and world. */
+#define TTB_DP_MAX_PEERS 8
+typedef struct {
+  int rank, world;
+  float *grad[TTB_DP_MAX_PEERS];
+  float *param[TTB_DP_MAX_PEERS];
+  unsigned *flags[TTB_DP_MAX_PEERS];
+} ttb_dp_peers;
+size_t ttb_dp_flag_words(int world);
+int ttb_dp_exchange_update(const ttb_dp_peers *peers, int64_t n, double lr,
+                           double momentum, int adagrad, double *state,
+                           int *err, int grid, ttb_stream stream);
+/* CUDA IPC of a device pointer inside any allocation (e.g. a PyTorch caching
+ * allocator block): handle = 64 bytes of cudaIpcMemHandle_t of the
+ * allocation, offset = dev_ptr - allocation base. */
+int ttb_ipc_handle(const void *dev_ptr, void *handle, int64_t *offset);
+int ttb_ipc_open(const void *handle, int64_t offset, void **dev_ptr);
+int ttb_ipc_close(void *dev_ptr, int64_t offset);
+
+/* The DEVICE int holding the handle's latched error bits (the word
+ * ttb_read_status reports in status[0]) for the current pipeline — e.g. the
+ * `err` of ttb_dp_exchange_update, so a rank's plan / gradient errors cancel
+ * the exchange everywhere and the exchange's own errors surface in
+ * ttb_read_status. Valid until ttb_destroy or a pipeline switch. */
+int *ttb_status_word(ttb_handle *h);
 
 /* SYNCS `stream`. status[0] = device error bits (TTB_ERRBIT_*), [1] = T,
  * [2] = B, [3] = P (distinct prefixes), [4] = S (bag-prefix segments),

@@ -27,6 +27,7 @@ ERRBIT_RANGE = 1
 ERRBIT_EMPTY_BAG = 2
 ERRBIT_OFFSETS = 4
 ERRBIT_NONFINITE = 8
+ERRBIT_PEER = 16
 
 OPT_BWD_SPLIT = 1
 OPT_FAST = 2
@@ -35,9 +36,10 @@ OPT_ALLOW_EMPTY = 3
 # every symbol include/ttb.h declares (tests check the .so exports them all)
 EXPORTS = [
     "ttb_abi_version", "ttb_strerror", "ttb_launch_count", "ttb_workspace_bytes", "ttb_create",
-    "ttb_destroy", "ttb_plan", "ttb_forward", "ttb_backward", "ttb_aggregate", "ttb_backward_sgd", "ttb_cores_modified", "ttb_sgd_update", "ttb_backward_adagrad", "ttb_adagrad_update",
+    "ttb_destroy", "ttb_plan", "ttb_forward", "ttb_backward", "ttb_aggregate", "ttb_backward_sgd", "ttb_cores_modified", "ttb_sgd_update", "ttb_backward_adagrad", "ttb_adagrad_update", "ttb_dp_flag_words", "ttb_dp_exchange_update",
+    "ttb_ipc_handle", "ttb_ipc_open", "ttb_ipc_close",
     "ttb_check_finite", "ttb_sgd_update_checked", "ttb_export_fast_plan", "ttb_plan_counts",
-    "ttb_read_status", "ttb_export_plan", "ttb_export_unique", "ttb_export_slots",
+    "ttb_read_status", "ttb_status_word", "ttb_export_plan", "ttb_export_unique", "ttb_export_slots",
     "ttb_profile_enable", "ttb_profile_read", "ttb_set_option", "ttb_fma_peak",
     "ttb_count_frequencies", "ttb_rank_workspace_bytes", "ttb_rank_rows", "ttb_apply_bijection",
 ]
@@ -68,9 +70,15 @@ _PROTOS = {
     "ttb_sgd_update": (_int, [_vp, _vp, _vp, _i64, _dbl, _dbl, _vp]),
     "ttb_backward_adagrad": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _dbl, _int, _vp]),
     "ttb_adagrad_update": (_int, [_vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _vp]),
+    "ttb_dp_flag_words": (C.c_size_t, [_int]),
+    "ttb_dp_exchange_update": (_int, [_vp, _i64, _dbl, _dbl, _int, _vp, _vp, _int, _vp]),
+    "ttb_ipc_handle": (_int, [_vp, _vp, C.POINTER(_i64)]),
+    "ttb_ipc_open": (_int, [_vp, _i64, C.POINTER(_vp)]),
+    "ttb_ipc_close": (_int, [_vp, _i64]),
     "ttb_check_finite": (_int, [_vp, _i64, _vp, _vp]),
     "ttb_sgd_update_checked": (_int, [_vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _vp]),
     "ttb_read_status": (_int, [_vp, C.POINTER(_i64), _vp]),
+    "ttb_status_word": (_vp, [_vp]),
     "ttb_export_plan": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "ttb_export_unique": (_int, [_vp, _vp, _vp, _vp]),
     "ttb_plan_counts": (_int, [_vp, C.POINTER(_i64), _vp]),
@@ -126,6 +134,15 @@ def check(code: int, what: str = "") -> None:
     raise TtbError(msg)
 
 
+DP_MAX_PEERS = 8
+
+
+class DpPeers(C.Structure):
+    """ttb_dp_peers (include/ttb.h)."""
+    _fields_ = [("rank", _int), ("world", _int), ("grad", _vp * DP_MAX_PEERS), ("param", _vp * DP_MAX_PEERS),
+                ("flags", _vp * DP_MAX_PEERS)]
+
+
 def errbits_to_exception(bits: int):
     if bits & ERRBIT_RANGE:
         return ValueError("bag index outside [0, rows)")
@@ -135,6 +152,8 @@ def errbits_to_exception(bits: int):
         return ValueError("malformed bag offsets")
     if bits & ERRBIT_NONFINITE:
         return ValueError("non-finite gradient")
+    if bits & ERRBIT_PEER:
+        return RuntimeError("data-parallel exchange: a peer rank did not arrive")
     return None
 
 

@@ -403,6 +403,11 @@ int ttb_sgd_update_checked(float* param, const float* grad, double* velocity, in
   return cuda_status(launch_sgd(param, grad, velocity, n, lr, momentum, (cudaStream_t)stream, err));
 }
 
+int* ttb_status_word(ttb_handle* h) {
+  if (!h) return nullptr;
+  return h->fast ? h->w.fast_hdr : h->w.err;
+}
+
 int ttb_read_status(ttb_handle* h, int64_t status[8], ttb_stream stream) {
   if (!h || !status) return TTB_EINVAL;
   int hdr[16];

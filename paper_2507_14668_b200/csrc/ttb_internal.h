@@ -235,6 +235,8 @@ cudaError_t launch_sgd(float* p, const float* g, double* v, int64_t n, double lr
                        const int* err = nullptr);
 cudaError_t launch_adagrad(float* p, const float* g, double* st, int64_t n, double lr, double eps, cudaStream_t s,
                            const int* err = nullptr);
+cudaError_t launch_dp_exchange(const ttb_dp_peers& P, int64_t n, double lr, double mu, int adagrad, double* state,
+                               int* err, int grid, cudaStream_t s);
 cudaError_t launch_gradcheck(const float* g, int64_t n, int* err, int num_sms, cudaStream_t s,
                              const int* suspect = nullptr);
 cudaError_t launch_export_plan(ttb_handle* h, int64_t* work, int64_t* slot_occ, int64_t* seg_ids,

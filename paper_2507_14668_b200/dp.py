@@ -12,6 +12,7 @@ compute runs through TtEngine (CUDA only).
 """
 from __future__ import annotations
 
+import ctypes as C
 import math
 
 import torch
@@ -109,3 +110,105 @@ def checked_update(param: torch.Tensor, grad: torch.Tensor, velocity, lr: float,
         if exc is not None:
             raise exc
     return err
+
+
+# ------------------------------------------------------------------ fused exchange over peer memory
+class PeerExchange:
+    """The data-parallel exchange step as ONE kernel per rank over peer
+    memory (ttb_dp_exchange_update, csrc/ttb_dp.cu): reduce-scatter of the
+    flat gradient buffers, the optimizer update of this rank's shard, and
+    all-gather of the new parameters by P2P stores — instead of an NCCL
+    all-reduce followed by the same update on every rank.
+
+    Ranks in separate processes (one GPU each) map each other's flat
+    param / grad buffers and flag words through CUDA IPC; the handles travel
+    over the process group (all_gather_object). `flat_param` / `flat_grad`
+    must stay allocated (and at the same address) for the object's life."""
+
+    def __init__(self, flat_param: torch.Tensor, flat_grad: torch.Tensor, group=None, grid: int = 0):
+        from . import _native as nat
+        from .engine import _ptr
+        self.lib = nat.load()
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if self.world > 1 else 0
+        if self.world > nat.DP_MAX_PEERS:
+            raise ValueError(f"at most {nat.DP_MAX_PEERS} ranks")
+        if flat_param.numel() != flat_grad.numel():
+            raise ValueError("param and grad buffers differ in length")
+        self.n = flat_param.numel()
+        self.grid = int(grid)
+        self.flags = torch.zeros(int(self.lib.ttb_dp_flag_words(self.world)), dtype=torch.int32,
+                                 device=flat_param.device)
+        self._keep = (flat_param, flat_grad, self.flags)
+        self._opened = []
+        mine = [_ptr(flat_grad), _ptr(flat_param), _ptr(self.flags)]
+        if self.world == 1:
+            table = [mine]
+        else:
+            shared = []
+            for p in mine:
+                h = (C.c_char * 64)()
+                off = C.c_int64(0)
+                nat.check(self.lib.ttb_ipc_handle(p, h, C.byref(off)), "ipc_handle")
+                shared.append((bytes(h), int(off.value)))
+            allh = [None] * self.world
+            dist.all_gather_object(allh, shared, group=group)
+            torch.cuda.synchronize()
+            table = []
+            for r, entries in enumerate(allh):
+                if r == self.rank:
+                    table.append(mine)
+                    continue
+                ptrs, bases = [], {}
+                for h, off in entries:  # buffers may share one allocation: map each handle once
+                    if h not in bases:
+                        out = C.c_void_p()
+                        nat.check(self.lib.ttb_ipc_open(C.c_char_p(h), 0, C.byref(out)), "ipc_open")
+                        self._opened.append((out.value, 0))
+                        bases[h] = out.value
+                    ptrs.append(bases[h] + off)
+                table.append(ptrs)
+        self.peers = make_peers(self.rank, table)
+
+    def step(self, lr: float, momentum: float = 0.0, state: torch.Tensor | None = None, err=None,
+             adagrad: bool = False, eps: float = 1e-10):
+        """One exchange + update. state: fp64, length n (velocity, or Adagrad
+        sums); err: device int32 — non-zero on entry (e.g. a failed local
+        finiteness check) cancels the update on EVERY rank."""
+        from . import _native as nat
+        from .engine import _ptr, _stream
+        nat.check(self.lib.ttb_dp_exchange_update(C.byref(self.peers), self.n, float(lr),
+                                                  float(eps if adagrad else momentum), int(adagrad),
+                                                  _ptr(state) if state is not None else None,
+                                                  _ptr(err) if err is not None else None, self.grid, _stream()),
+                  "dp_exchange_update")
+
+    def close(self):
+        for p, off in self._opened:
+            self.lib.ttb_ipc_close(p, off)
+        self._opened = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def make_peers(rank: int, table):
+    """ttb_dp_peers from [(grad_ptr, param_ptr, flags_ptr)] per rank."""
+    from . import _native as nat
+    P = nat.DpPeers()
+    P.rank, P.world = rank, len(table)
+    for r, (g, p, f) in enumerate(table):
+        P.grad[r], P.param[r], P.flags[r] = g, p, f
+    return P
+
+
+def p2p_capable(world: int) -> bool:
+    """Every pair of the node's first `world` GPUs can access each other
+    (the fused exchange needs peer loads / stores)."""
+    if world < 2 or torch.cuda.device_count() < world:
+        return False
+    return all(torch.cuda.can_device_access_peer(a, b) for a in range(world) for b in range(world) if a != b)

@@ -272,6 +272,10 @@ class TtEngine:
         nat.check(self.lib.ttb_plan_counts(self._handle, su, _stream()), "plan_counts")
         return dict(S=int(su[0]), U=int(su[1]))
 
+    def status_word(self) -> int:
+        """Device address of the latched error word (ttb_status_word)."""
+        return int(self.lib.ttb_status_word(self._handle))
+
     def check_errors(self) -> dict:
         st = self.status()
         exc = nat.errbits_to_exception(st["err"])
