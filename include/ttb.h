@@ -78,6 +78,7 @@ typedef struct ttb_geom {
 } ttb_geom;
 
 typedef struct ttb_handle ttb_handle; /* opaque host-side handle */
+#define TTB_MAX_TABLES 64
 typedef void *ttb_stream;             /* a cudaStream_t */
 
 int ttb_abi_version(void);
@@ -210,6 +211,30 @@ int ttb_ipc_close(void *dev_ptr, int64_t offset);
  * the exchange everywhere and the exchange's own errors surface in
  * ttb_read_status. Valid until ttb_destroy or a pipeline switch. */
 int *ttb_status_word(ttb_handle *h);
+
+/* ---- table-batched handles (the reference loops over fields,
+ * model.py:295-298 lookups and 334-338 gradients; here ONE plan / forward /
+ * backward / update launch set covers every TT field of the model).
+ * ntables <= TTB_MAX_TABLES tables with identical n and ranks (the
+ * tensor-core geometry: n = (4, 4, 4), ranks (1, 32, 32, 1)) and their own
+ * row factors m_f. Their cores are passed STACKED and zero-padded to the
+ * common (M1, M2, M3) = max_f m_f (M3 <= 288): core0 (1, nt M1 4, 32),
+ * core1 (32, nt M2 4, 32), core2 (32, nt M3 4, 1); table f's core k is the
+ * block starting at f M_k along the middle axis (rows past m_f stay zero:
+ * nothing references them, so gradients and updates leave them zero).
+ * A batch: every table's indices (table-local row ids) concatenated table by
+ * table; offsets over nt * bags_per_table bags (table f owns bags
+ * [f bags_per_table, (f + 1) bags_per_table)); the output is
+ * (nt * bags_per_table, N), table-major. Every other entry point takes the
+ * handle as usual (plan, forward, backward[_sgd|_adagrad], read_status);
+ * the reference-ordered exports and per-table counters do not apply. */
+int ttb_batched_workspace_bytes(const ttb_geom *tables, int ntables,
+                                int64_t max_T, int64_t bags_per_table,
+                                size_t *bytes);
+ttb_handle *ttb_create_batched(const ttb_geom *tables, int ntables,
+                               int64_t max_T, int64_t bags_per_table,
+                               void *workspace, size_t bytes,
+                               ttb_stream stream);
 
 /* SYNCS `stream`. status[0] = device error bits (TTB_ERRBIT_*), [1] = T,
  * [2] = B, [3] = P (distinct prefixes), [4] = S (bag-prefix segments),

@@ -36,7 +36,7 @@ OPT_ALLOW_EMPTY = 3
 # every symbol include/ttb.h declares (tests check the .so exports them all)
 EXPORTS = [
     "ttb_abi_version", "ttb_strerror", "ttb_launch_count", "ttb_workspace_bytes", "ttb_create",
-    "ttb_destroy", "ttb_plan", "ttb_forward", "ttb_backward", "ttb_aggregate", "ttb_backward_sgd", "ttb_cores_modified", "ttb_sgd_update", "ttb_backward_adagrad", "ttb_adagrad_update", "ttb_dp_flag_words", "ttb_dp_exchange_update",
+    "ttb_destroy", "ttb_batched_workspace_bytes", "ttb_create_batched", "ttb_plan", "ttb_forward", "ttb_backward", "ttb_aggregate", "ttb_backward_sgd", "ttb_cores_modified", "ttb_sgd_update", "ttb_backward_adagrad", "ttb_adagrad_update", "ttb_dp_flag_words", "ttb_dp_exchange_update",
     "ttb_ipc_handle", "ttb_ipc_open", "ttb_ipc_close",
     "ttb_check_finite", "ttb_sgd_update_checked", "ttb_export_fast_plan", "ttb_plan_counts",
     "ttb_read_status", "ttb_status_word", "ttb_export_plan", "ttb_export_unique", "ttb_export_slots",
@@ -60,6 +60,8 @@ _PROTOS = {
     "ttb_launch_count": (_i64, []),
     "ttb_workspace_bytes": (_int, [C.POINTER(TtbGeom), _i64, _i64, C.POINTER(C.c_size_t)]),
     "ttb_create": (_vp, [C.POINTER(TtbGeom), _i64, _i64, _vp, C.c_size_t, _vp]),
+    "ttb_batched_workspace_bytes": (_int, [C.POINTER(TtbGeom), _int, _i64, _i64, C.POINTER(C.c_size_t)]),
+    "ttb_create_batched": (_vp, [C.POINTER(TtbGeom), _int, _i64, _i64, _vp, C.c_size_t, _vp]),
     "ttb_destroy": (None, [_vp]),
     "ttb_plan": (_int, [_vp, _vp, _int, _vp, _i64, _i64, _vp]),
     "ttb_forward": (_int, [_vp, _vp, _vp, _vp, _vp, _vp]),

@@ -85,6 +85,8 @@ void layout(ttb_handle& h, char* base) {
   const ttb_geom& g = h.geom;
   const int64_t T = h.maxT, B = h.maxB;
   const int64_t m1m2 = g.m[0] * g.m[1];
+  // the deterministic pipeline's buffers (a batched handle has none)
+  const int64_t dT = h.batched ? 0 : T, dB = h.batched ? 0 : B, dK = h.batched ? 0 : m1m2;
   const DynDims& d = h.dims;
   const int64_t N = (int64_t)d.n1 * d.n2 * d.n3;
   const int64_t SL = (int64_t)d.n1 * d.n2 * d.r2, G1S = (int64_t)d.n1 * d.r1, G2S = (int64_t)d.r1 * d.n2 * d.r2,
@@ -122,45 +124,46 @@ void layout(ttb_handle& h, char* base) {
   c.off = (c.off + 255) & ~(size_t)255;
   w.zeroB = base ? base + b0 : nullptr;
   w.zeroB_bytes = c.off - b0;
-  w.grp_done = c.take<int>(g.m[1]);
-  w.pmap = c.take<unsigned>(m1m2);
-  w.pslot = c.take<int>(m1m2);
-  w.work_key = c.take<unsigned>(h.Pmax);
-  w.keys32 = c.take<unsigned>(T);
-  w.bag_of = c.take<int>(T);
-  w.occ_slot = c.take<int>(T);
-  w.seg_inv = c.take<int>(T);
-  w.occ_tmp = c.take<int>(T);
-  w.seg_slot = c.take<int>(T);
-  w.seg_bag = c.take<int>(T);
-  w.bag_seg = c.take<int>(B + 1);
-  w.bag_off = c.take<int>(B + 1);
-  w.slots = c.take<float>((size_t)h.Pmax * SL);
-  w.skA = c.take<unsigned>(T);
-  w.svA = c.take<unsigned>(T);
-  w.skB = c.take<unsigned>(T);
-  w.svB = c.take<unsigned>(T);
-  w.urow = c.take<unsigned>(T + 1);
-  w.urow_start = c.take<int>(T + 1);
-  w.urow_i3 = c.take<unsigned>(T);
-  w.prow_begin = c.take<int>(h.Pmax);
-  w.prow_end = c.take<int>(h.Pmax);
-  w.gU = c.take<float>((size_t)T * N);
-  w.dH = c.take<float>((size_t)T * G3S);
-  w.E = c.take<float>((size_t)h.Pmax * G1S);
-  w.zbuf = c.take<float>((size_t)h.Pmax * SL);
-  w.dG2part = c.take<float>((size_t)g.m[1] * h.cmaxb * G2S);
-  w.i3_start = c.take<int>(g.m[2] + 1);
-  w.grp_cnt = c.take<int>(g.m[1]);
-  w.rkA = c.take<unsigned>(T);
-  w.rvA = c.take<unsigned>(T);
-  w.rkB = c.take<unsigned>(T);
-  w.rvB = c.take<unsigned>(T);
-  w.uid_first = c.take<int>(T);
-  w.qrow = c.take<int>(T);
-  w.agg_hp = c.take<float>((size_t)(T / 64 + 2) * N);
-  w.agg_tp = c.take<float>((size_t)(T / 64 + 2) * N);
-  w.span_list = c.take<int>(T / 64 + 2);
+  const int64_t dP = h.batched ? 0 : h.Pmax;
+  w.grp_done = c.take<int>(h.batched ? 0 : g.m[1]);
+  w.pmap = c.take<unsigned>(dK);
+  w.pslot = c.take<int>(dK);
+  w.work_key = c.take<unsigned>(dP);
+  w.keys32 = c.take<unsigned>(dT);
+  w.bag_of = c.take<int>(T);  // (the tensor-core plan's bag ids too)
+  w.occ_slot = c.take<int>(dT);
+  w.seg_inv = c.take<int>(dT);
+  w.occ_tmp = c.take<int>(dT);
+  w.seg_slot = c.take<int>(dT);
+  w.seg_bag = c.take<int>(dT);
+  w.bag_seg = c.take<int>(dB + 1);
+  w.bag_off = c.take<int>(dB + 1);
+  w.slots = c.take<float>((size_t)dP * SL);
+  w.skA = c.take<unsigned>(dT);
+  w.svA = c.take<unsigned>(dT);
+  w.skB = c.take<unsigned>(dT);
+  w.svB = c.take<unsigned>(dT);
+  w.urow = c.take<unsigned>(dT + 1);
+  w.urow_start = c.take<int>(dT + 1);
+  w.urow_i3 = c.take<unsigned>(dT);
+  w.prow_begin = c.take<int>(dP);
+  w.prow_end = c.take<int>(dP);
+  w.gU = c.take<float>((size_t)dT * N);
+  w.dH = c.take<float>((size_t)dT * G3S);
+  w.E = c.take<float>((size_t)dP * G1S);
+  w.zbuf = c.take<float>((size_t)dP * SL);
+  w.dG2part = c.take<float>(h.batched ? 0 : (size_t)g.m[1] * h.cmaxb * G2S);
+  w.i3_start = c.take<int>(h.batched ? 0 : g.m[2] + 1);
+  w.grp_cnt = c.take<int>(h.batched ? 0 : g.m[1]);
+  w.rkA = c.take<unsigned>(dT);
+  w.rvA = c.take<unsigned>(dT);
+  w.rkB = c.take<unsigned>(dT);
+  w.rvB = c.take<unsigned>(dT);
+  w.uid_first = c.take<int>(dT);
+  w.qrow = c.take<int>(dT);
+  w.agg_hp = c.take<float>((size_t)(dT / 64 + 2) * N);
+  w.agg_tp = c.take<float>((size_t)(dT / 64 + 2) * N);
+  w.span_list = c.take<int>(dT / 64 + 2);
   w.scratch1 = c.take<float>(16);
   const bool fz = h.fast_ok;
   w.f_key = c.take<unsigned>(fz ? T : 0);
@@ -169,17 +172,21 @@ void layout(ttb_handle& h, char* base) {
   w.f_item_start = c.take<int>(fz ? T + 1 : 0);
   w.f_item_key = c.take<unsigned>(fz ? T : 0);
   w.f_rk = c.take<int>(fz ? T : 0);
-  w.f_cnt = c.take<int>(fz ? (size_t)g.m[0] * g.m[1] : 0);
-  w.f_start = c.take<int>(fz ? (size_t)g.m[0] * g.m[1] : 0);
-  w.f_rstart = c.take<int>(fz ? (size_t)g.m[0] * g.m[1] : 0);
-  w.f_split = c.take<int>(fz ? (size_t)g.m[0] * g.m[1] : 0);
+  // tensor-core pipeline: prefix keys (M1 per i2 group), i2 groups, G1 rows,
+  // G3 slices of the (possibly stacked) geometry — KGeom, set before layout()
+  const int64_t fk = h.kg.m1m2, fg = h.kg.m2, fg1 = h.kg.g1rows, fg3 = h.kg.m3;
+  w.f_cnt = c.take<int>(fz ? (size_t)fk : 0);
+  w.f_start = c.take<int>(fz ? (size_t)fk : 0);
+  w.f_rstart = c.take<int>(fz ? (size_t)fk : 0);
+  w.f_split = c.take<int>(fz ? (size_t)fk : 0);
   w.f_cta = c.take<int>(fz ? 1025 : 0);
-  w.f_gtot = c.take<int4>(fz ? g.m[1] : 0);
-  w.f_tile_info = c.take<int4>(fz ? T / 32 + g.m[1] + 2 : 0);
-  w.f_g1img = c.take<float>(fz ? (size_t)g.m[0] * 512 : 0);
-  w.f_img = c.take<float>(fz ? (size_t)g.m[1] * 16384 : 0);
-  w.f_grad = c.take<float>(fz ? (size_t)(G1S * g.m[0] + G2S * g.m[1] + G3S * g.m[2]) : 0);
-  w.f_rowbits = c.take<unsigned>(fz ? (size_t)(g.m[0] * g.m[1] * g.m[2] / 32 + 1) : 0);
+  w.f_gtot = c.take<int4>(fz ? fg : 0);
+  w.f_tile_info = c.take<int4>(fz ? T / 32 + fg + 2 : 0);
+  w.f_g1img = c.take<float>(fz ? (size_t)fg1 * 512 : 0);
+  w.f_img = c.take<float>(fz ? (size_t)fg * 16384 : 0);
+  w.f_grad = c.take<float>(fz ? (size_t)(G1S * fg1 + G2S * fg + G3S * fg3) : 0);
+  w.f_rowbits = c.take<unsigned>(fz && !h.batched ? (size_t)(g.m[0] * g.m[1] * g.m[2] / 32 + 1) : 0);
+  w.f_tgeom = c.take<uint4>(h.kg.nt);
   h.bytes = c.off + 256;
 }
 
@@ -192,6 +199,12 @@ bool init_handle(ttb_handle& h, const ttb_geom* g, int64_t max_T, int64_t max_B)
   h.kg.m3 = (unsigned)g->m[2];
   h.kg.m1m2 = (unsigned)(g->m[0] * g->m[1]);
   h.kg.rows = (unsigned)(g->m[0] * g->m[1] * g->m[2]);
+  h.kg.nt = 1;
+  h.kg.tm2 = h.kg.m2;
+  h.kg.tm3 = h.kg.m3;
+  h.kg.g1rows = h.kg.m1;
+  h.kg.bpt = 0;
+  h.tables[0] = *g;
   h.dims = DynDims{g->n[0], g->n[1], g->n[2], g->r[1], g->r[2]};
   if (!choose_chunks(h.dims, &h.chf, &h.chb)) return false;
   h.maxT = max_T;
@@ -200,6 +213,46 @@ bool init_handle(ttb_handle& h, const ttb_geom* g, int64_t max_T, int64_t max_B)
   h.fast_ok = fast_supported(&h) ? 1 : 0;
   h.fast = h.fast_ok;
   h.i3_bits = bits_for((uint64_t)h.kg.m3 - 1);
+  layout(h, nullptr);
+  return true;
+}
+
+// nt tables sharing n and ranks, stacked at the common (M1, M2, M3); the
+// tensor-core pipeline must support the geometry (n = (4, 4, 4), ranks
+// (1, 32, 32, 1), M3 <= 288). max_B = nt * bags_per_table.
+bool init_handle_batched(ttb_handle& h, const ttb_geom* tables, int nt, int64_t max_T, int64_t bpt) {
+  if (!tables || nt < 1 || nt > TTB_MAX_TABLES || bpt < 1) return false;
+  int64_t M[3] = {1, 1, 1};
+  for (int f = 0; f < nt; ++f) {
+    if (!geom_ok(&tables[f])) return false;
+    for (int k = 0; k < 3; ++k) {
+      if (tables[f].n[k] != tables[0].n[k]) return false;
+      if (tables[f].m[k] > M[k]) M[k] = tables[f].m[k];
+    }
+    for (int k = 0; k < 4; ++k)
+      if (tables[f].r[k] != tables[0].r[k]) return false;
+  }
+  ttb_geom v = tables[0];
+  v.m[0] = M[0];
+  v.m[1] = M[1];
+  v.m[2] = M[2];
+  const int64_t max_B = (int64_t)nt * bpt;
+  if ((double)M[0] * (double)M[1] * (double)nt >= 2147483647.0 || (double)nt * M[2] * 4 >= 2147483647.0) return false;
+  if (!init_handle(h, &v, max_T, max_B)) return false;
+  h.batched = 1;
+  h.kg.nt = (unsigned)nt;
+  h.kg.m2 = (unsigned)(nt * M[1]);
+  h.kg.m3 = (unsigned)(nt * M[2]);
+  h.kg.m1m2 = (unsigned)(M[0] * nt * M[1]);
+  h.kg.tm2 = (unsigned)M[1];
+  h.kg.tm3 = (unsigned)M[2];
+  h.kg.g1rows = (unsigned)(nt * M[0]);
+  h.kg.bpt = (unsigned)bpt;
+  h.kg.rows = 0;  // per table (f_tgeom)
+  for (int f = 0; f < nt; ++f) h.tables[f] = tables[f];
+  h.fast_ok = fast_supported(&h) ? 1 : 0;
+  if (!h.fast_ok) return false;
+  h.fast = 1;
   layout(h, nullptr);
   return true;
 }
@@ -236,10 +289,33 @@ int ttb_workspace_bytes(const ttb_geom* g, int64_t max_T, int64_t max_B, size_t*
   return TTB_OK;
 }
 
+static ttb_handle* create_from(const ttb_handle& tmp, void* workspace, size_t bytes, ttb_stream stream);
+
 ttb_handle* ttb_create(const ttb_geom* g, int64_t max_T, int64_t max_B, void* workspace, size_t bytes,
                        ttb_stream stream) {
   ttb_handle tmp;
-  if (!init_handle(tmp, g, max_T, max_B) || !workspace || bytes < tmp.bytes) return nullptr;
+  if (!init_handle(tmp, g, max_T, max_B)) return nullptr;
+  return create_from(tmp, workspace, bytes, stream);
+}
+
+int ttb_batched_workspace_bytes(const ttb_geom* tables, int ntables, int64_t max_T, int64_t bags_per_table,
+                                size_t* bytes) {
+  if (!bytes) return TTB_EINVAL;
+  ttb_handle h;
+  if (!init_handle_batched(h, tables, ntables, max_T, bags_per_table)) return TTB_EINVAL;
+  *bytes = h.bytes;
+  return TTB_OK;
+}
+
+ttb_handle* ttb_create_batched(const ttb_geom* tables, int ntables, int64_t max_T, int64_t bags_per_table,
+                               void* workspace, size_t bytes, ttb_stream stream) {
+  ttb_handle tmp;
+  if (!init_handle_batched(tmp, tables, ntables, max_T, bags_per_table)) return nullptr;
+  return create_from(tmp, workspace, bytes, stream);
+}
+
+static ttb_handle* create_from(const ttb_handle& tmp, void* workspace, size_t bytes, ttb_stream stream) {
+  if (!workspace || bytes < tmp.bytes) return nullptr;
   ttb_handle* h = (ttb_handle*)malloc(sizeof(ttb_handle));
   if (!h) return nullptr;
   *h = tmp;
@@ -257,10 +333,16 @@ ttb_handle* ttb_create(const ttb_geom* g, int64_t max_T, int64_t max_B, void* wo
       h->num_sms = 148;
   }
   cudaStream_t s = (cudaStream_t)stream;
+  for (unsigned f = 0; f < h->kg.nt; ++f) {
+    const ttb_geom& t = h->tables[f];
+    h->tgeom_host[f] = make_uint4((unsigned)t.m[1], (unsigned)t.m[2], (unsigned)(t.m[0] * t.m[1] * t.m[2]), 0u);
+  }
   if (cudaMemsetAsync(h->w.zeroA, 0, h->w.zeroA_bytes + h->w.zeroB_bytes, s) != cudaSuccess ||
-      cudaMemsetAsync(h->w.grp_done, 0, sizeof(int) * h->kg.m2, s) != cudaSuccess ||
-      cudaMemsetAsync(h->w.pmap, 0xFF, sizeof(unsigned) * h->kg.m1m2, s) != cudaSuccess ||
-      (h->fast_ok && cudaMemsetAsync(h->w.f_cnt, 0, sizeof(int) * h->kg.m1m2, s) != cudaSuccess)) {
+      (!h->batched && cudaMemsetAsync(h->w.grp_done, 0, sizeof(int) * h->kg.m2, s) != cudaSuccess) ||
+      (!h->batched && cudaMemsetAsync(h->w.pmap, 0xFF, sizeof(unsigned) * h->kg.m1m2, s) != cudaSuccess) ||
+      (h->fast_ok && cudaMemsetAsync(h->w.f_cnt, 0, sizeof(int) * h->kg.m1m2, s) != cudaSuccess) ||
+      cudaMemcpyAsync(h->w.f_tgeom, h->tgeom_host, sizeof(uint4) * h->kg.nt, cudaMemcpyHostToDevice, s) !=
+          cudaSuccess) {
     free(h);
     return nullptr;
   }
@@ -274,6 +356,7 @@ int ttb_plan(ttb_handle* h, const void* indices, int idx_is_64, const int64_t* o
   if (!h || !indices || !offsets) return TTB_EINVAL;
   if (T < 1 || B < 1) return TTB_EEMPTY;
   if (T > h->maxT || B > h->maxB) return TTB_EINVAL;
+  if (h->batched && B != (int64_t)h->kg.nt * h->kg.bpt) return TTB_EINVAL;  // bags_per_table bags per table
   h->T = T;
   h->B = B;
   h->planned = 0;
@@ -440,6 +523,7 @@ int ttb_read_status(ttb_handle* h, int64_t status[8], ttb_stream stream) {
 int ttb_plan_counts(ttb_handle* h, int64_t su[2], ttb_stream stream) {
   if (!h || !su) return TTB_EINVAL;
   if (!h->planned) return TTB_ESTATE;
+  if (h->batched) return TTB_ESTATE;  // per-table counters / reference plans: not for batched handles
   if (!h->fast) {  // the deterministic pipeline forms both (U after a backward)
     int64_t st[8];
     int rc = ttb_read_status(h, st, stream);
@@ -462,6 +546,7 @@ int ttb_export_plan(ttb_handle* h, int64_t* work, int64_t* slot_occ, int64_t* se
                     int64_t* digits, ttb_stream stream) {
   if (!h) return TTB_EINVAL;
   if (!h->planned) return TTB_ESTATE;
+  if (h->batched) return TTB_ESTATE;  // per-table counters / reference plans: not for batched handles
   if (!h->legacy_planned) {
     // the reference-ordered plan (first-occurrence slots, segments) on demand
     cudaError_t e = launch_plan(h, h->plan_idx, h->plan_idx64, h->plan_off, (cudaStream_t)stream);

@@ -17,6 +17,16 @@ struct KGeom {
   unsigned m1, m2, m3;  // row factors
   unsigned m1m2;        // number of prefix keys
   unsigned rows;        // padded rows m1 m2 m3 (< 2^31)
+  // Table-batched handles (ttb_create_batched, tensor-core pipeline only): nt
+  // tables with their own row factors, stored stacked and zero-padded to the
+  // common (M1, M2, M3): m1 = M1 (prefix keys per i2 group), m2 = nt M2 (G2
+  // slices = i2 groups), m3 = nt M3 (G3 slices), m1m2 = M1 nt M2. Table f owns
+  // G1 rows [f M1, f M1 + m1_f), G2 slices [f M2, ...), G3 slices [f M3, ...).
+  // A single table is nt = 1, tm2 = m2, tm3 = m3, g1rows = m1.
+  unsigned nt;      // tables
+  unsigned tm2, tm3;  // per-table slice blocks M2, M3
+  unsigned g1rows;  // G1 rows (nt M1)
+  unsigned bpt;     // bags per table (batched plans: table of bag b = b / bpt)
 };
 
 // Core dims. DynDims carries them at run time; FixDims bakes them into the

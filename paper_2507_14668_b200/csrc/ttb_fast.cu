@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
                                                         int* __restrict__ cta_tiles, int ctas,
                                                         unsigned* __restrict__ item_key, int4* __restrict__ tile_info,
                                                         int2* __restrict__ sbi, int* __restrict__ hdr, int dbg,
-                                                        int allow_empty) {
+                                                        int allow_empty, const uint4* __restrict__ tgeom) {
   pdl_enter();
 #define PSTAMP(i)                                                                                          \
   do {                                                                                                     \
@@ -96,6 +96,18 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
   unsigned target = 0;
   const int nthr = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
+  // tables (one unless the handle is batched): table f's lookups are
+  // [offsets[f bpt], offsets[(f + 1) bpt]) and its digits use its own factors
+  __shared__ int s_toff[TTB_MAX_TABLES + 1];
+  __shared__ uint4 s_tg[TTB_MAX_TABLES];
+  const int nt = (int)g.nt;
+  for (int f = threadIdx.x; f <= nt; f += blockDim.x) {
+    if (f < nt) s_tg[f] = tgeom[f];
+    const int64_t b = nt > 1 ? (int64_t)f * g.bpt : (f ? B : 0);
+    const int64_t o = b >= B ? (int64_t)T : offsets[b];
+    s_toff[f] = (int)(o < 0 ? 0 : (o > T ? T : o));
+  }
+  __syncthreads();
   // ---- phase 0
   int bits = 0, multi = 0;
   for (int b = tid; b < B; b += nthr) {
@@ -108,7 +120,6 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
     for (int t = lo; t < hi; ++t) bag_of[t] = b;
     if (hi - lo > 1) multi = 1;
   }
-  const unsigned m2m3 = g.m2 * g.m3;
   // the first kPlanRegs lookups of this thread keep (key, rank, i3) in
   // registers for phase B (same thread <-> lookup mapping there)
   unsigned rkey[kPlanRegs], ri3[kPlanRegs];
@@ -119,14 +130,22 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
     const bool ok = t < T;
     unsigned k = 0xFFFFFFFFu, i3 = 0;
     if (ok) {
+      int f = 0;  // the lookup's table: the last f with s_toff[f] <= t
+      for (int lo2 = 1, hi2 = nt - 1; lo2 <= hi2;) {
+        const int mid = (lo2 + hi2) >> 1;
+        if (s_toff[mid] <= t) f = mid, lo2 = mid + 1;
+        else hi2 = mid - 1;
+      }
+      const uint4 tg = s_tg[f];  // (m2, m3, rows) of the table
       long long v = (long long)idx[t];
-      if (v < 0 || v >= (long long)g.rows) {
+      if (v < 0 || v >= (long long)tg.z) {
         bits |= 1;
         v = 0;
       }
-      const unsigned i = (unsigned)v, i1 = i / m2m3, r = i - i1 * m2m3, i2 = r / g.m3;
-      k = i2 * g.m1 + i1;
-      i3 = r - i2 * g.m3;
+      const unsigned m2m3 = tg.x * tg.y;
+      const unsigned i = (unsigned)v, i1 = i / m2m3, r = i - i1 * m2m3, i2 = r / tg.y;
+      k = ((unsigned)f * g.tm2 + i2) * g.m1 + i1;
+      i3 = r - i2 * tg.y;
       if (iter >= kPlanRegs) {
         key[t] = k;
         i3o[t] = i3;
@@ -389,8 +408,8 @@ __global__ void __launch_bounds__(kImgThreads) k_coreimg(float* __restrict__ G1,
   // non-finite gradient) cancels the update: the images are rebuilt from the
   // unchanged cores and velocities
   if (u.on && u.err && *(volatile const int*)u.err != 0) u.on = 0;
-  const size_t n0 = (size_t)g.m1 * 4 * R1, n1 = (size_t)R1 * g.m2 * C;
-  const unsigned nb12 = g.m2 + (g.m1 + 3) / 4;
+  const size_t n0 = (size_t)g.g1rows * 4 * R1, n1 = (size_t)R1 * g.m2 * C;
+  const unsigned nb12 = g.m2 + (g.g1rows + 3) / 4;
   if (blockIdx.x >= nb12) {  // G3: update only
     const size_t n2 = (size_t)32 * g.m3 * 4;
     for (size_t j = (size_t)(blockIdx.x - nb12) * kImgThreads + threadIdx.x; j < n2;
@@ -404,7 +423,7 @@ __global__ void __launch_bounds__(kImgThreads) k_coreimg(float* __restrict__ G1,
   if (blockIdx.x >= g.m2) {  // G1 images: 4 i1 per block (128 elements each)
     const unsigned i1 = (blockIdx.x - g.m2) * 4 + (threadIdx.x >> 7);
     const int e = threadIdx.x & 127, a = e >> 5, k = e & 31;
-    if (i1 < g.m1) {
+    if (i1 < g.g1rows) {
       const size_t j = (size_t)i1 * 128 + e;
       float v = G1[j];
       if (u.on && (u.mask & 1)) {
@@ -571,19 +590,27 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
   char* b_hi = sm + 2 * kImg;  // G2 cb image
   char* b_lo = sm + 3 * kImg;
   float4* s_g3 = reinterpret_cast<float4*>(sm + 4 * kImg);
-  int2* s_sbi2 = reinterpret_cast<int2*>(sm + 4 * kImg + fwd_g3_bytes(g.m3));  // two (bag, i3) stages
+  int2* s_sbi2 = reinterpret_cast<int2*>(sm + 4 * kImg + fwd_g3_bytes(g.tm3));  // two (bag, i3) stages
   __shared__ TileMeta s_m[3];
   __shared__ uint64_t s_mbar;
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const unsigned m3 = g.m3;
+  const unsigned m3 = g.tm3;  // the resident G3 block: one table's slices (m3 <= kFwdMaxM3, fast_supported)
   const int ntiles = hdr[4];
   const int tb = cta_tiles[blockIdx.x], te = cta_tiles[blockIdx.x + 1];  // weight-balanced (k_fplan)
   (void)ntiles;
   if (warp == 0) umma::tmem_alloc(&s_tmem, 256);  // X, then the quarters' partial sums
   if (threadIdx.x == 32) umma::mbar_init(&s_mbar, 1);
-  for (int e = threadIdx.x; e < 32 * (int)m3; e += kFwdThreads)  // m3 <= kFwdMaxM3 (fast_supported)
-    cp_async16(s_g3 + e, reinterpret_cast<const float4*>(G3) + e);
+  // table f's G3 slices [f M3, (f + 1) M3) of every row c (rows are g.m3 slices long)
+  auto stage_g3 = [&](unsigned f) {
+    const float4* src = reinterpret_cast<const float4*>(G3) + (size_t)f * m3;
+    for (int e = threadIdx.x; e < 32 * (int)m3; e += kFwdThreads) {
+      const int c = e / (int)m3, j = e - c * (int)m3;
+      cp_async16(s_g3 + e, src + (size_t)c * g.m3 + j);
+    }
+  };
+  unsigned g3_table = tb < te ? (unsigned)tile_info[tb].x / g.tm2 : 0u;
+  stage_g3(g3_table);
   int4 pf = make_int4(0, 0, 0, 0);
   if (warp == 15 && tb < te) {
     fetch_meta_async(tile_info[tb], item_start, item_key, &s_m[0]);
@@ -836,7 +863,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
     FSTAMP(4);
     cp_async_wait_all();  // the next tile's operands, list and metadata
     sync_for_mma();       // TMEM read by every epilogue thread; operands visible to the tensor core
-    if (t + 1 < te) issue_mma();
+    if (t + 1 < te) {
+      issue_mma();
+      const unsigned fn = (unsigned)s_m[(t + 1 - tb) % 3].i2 / g.tm2;
+      if (fn != g3_table) {  // batched handle: the next tile belongs to another table
+        stage_g3(fn);
+        cp_async_wait_all();
+        __syncthreads();
+        g3_table = fn;
+      }
+    }
     FSTAMP(3);
   }
   if (warp == 0) umma::tmem_free(tmem, 256);
@@ -910,7 +946,7 @@ __device__ inline void make_chunks(const TileMeta* m, int* ch, int cap, int roun
 }
 
 template <bool kG3>
-__device__ inline void stage_rows_async(int np, const int2* st_sbi, const float* __restrict__ gout,
+__device__ inline void stage_rows_async(int np, unsigned i3b, const int2* st_sbi, const float* __restrict__ gout,
                                         const float* __restrict__ G3, unsigned m3, float4* st_g, float4* st_g3) {
   for (int e = threadIdx.x; e < np * 16; e += kThreads) {
     const int p = e >> 4, k = e & 15;
@@ -919,7 +955,7 @@ __device__ inline void stage_rows_async(int np, const int2* st_sbi, const float*
   if (kG3)
   for (int e = threadIdx.x; e < np * 32; e += kThreads) {
     const int p = e >> 5, cc = e & 31;
-    cp_async16(st_g3 + e, reinterpret_cast<const float4*>(G3) + (size_t)cc * m3 + st_sbi[p].y);
+    cp_async16(st_g3 + e, reinterpret_cast<const float4*>(G3) + (size_t)cc * m3 + i3b + st_sbi[p].y);
   }
 }
 
@@ -1009,7 +1045,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
     stage_g1_rows_async(m, g, g1img, r2_hi, r2_lo);
     cp_async_wait_all();
     __syncthreads();
-    stage_rows_async<!kRows>(np, st_sbi, gout, G3, m3, st_g, st_g3);
+    stage_rows_async<!kRows>(np, tile_i3_base(m, g), st_sbi, gout, G3, m3, st_g, st_g3);
   }
   uint32_t phase = 0;
   bool bad = false;
@@ -1020,6 +1056,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
     const int* chunk = s_chunk[slot];
     const int n = m->n, nchunk = chunk[kTileItems + 1];
     const float* gimg = img + (size_t)m->i2 * kImg;  // kImg floats = 4 images of kImg bytes
+    const unsigned i3b = tile_i3_base(m, g);          // the tile's table's G3 slices (batched handles)
     TSTAMP(0);
     // invariant: chunk 0's positions / rows and the X operands are issued
     cp_async_wait_all();
@@ -1075,7 +1112,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
         for (int e = threadIdx.x; e < np; e += kThreads) cp_async8(st_sbi + e, sbi + p0 + e);
         cp_async_wait_all();
         __syncthreads();
-        stage_rows_async<!kRows>(np, st_sbi, gout, G3, m3, st_g, st_g3);
+        stage_rows_async<!kRows>(np, i3b, st_sbi, gout, G3, m3, st_g, st_g3);
         cp_async_wait_all();
         __syncthreads();
         if ((dbg & 8) && threadIdx.x == 0 && blockIdx.x == 0) s_tacc[10] += clock64() - _c0;
@@ -1093,7 +1130,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
           // (equal i3): a row's gradient rows are summed first, so dG3 gets one
           // reduction and Z one rank-4 update per distinct row of the item
           const int s0 = m->start[it] - p0, nq = m->start[it + 1] - p0 - s0;
-          const int my_i3 = lane < nq ? st_sbi[s0 + lane].y : -1;
+          const int my_i3 = lane < nq ? (int)i3b + st_sbi[s0 + lane].y : -1;
           const unsigned grp = __match_any_sync(0xffffffffu, lane < nq ? my_i3 : (int)(0x80000000u | lane));
           unsigned lead = __ballot_sync(0xffffffffu, lane < nq && (__ffs(grp) - 1) == lane);
           while (lead) {
@@ -1127,7 +1164,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
           // position is one gradient row, one dG3 reduction and one Z update
           const int s1 = (dbg & 64) ? 0 : m->start[it + 1] - p0;  // (ablations: TTB_DBG 64 / 32)
           for (int qq = m->start[it] - p0; qq < s1; ++qq) {
-            const int i3 = st_sbi[qq].y;
+            const unsigned i3 = i3b + st_sbi[qq].y;
             const float4 h3 = st_g3[qq * 32 + lane];
             float dh[4] = {0.f, 0.f, 0.f, 0.f};
             if (!(dbg & 32)) lookup_update(st_g + qq * 16, x, z, h3, dh);
@@ -1234,10 +1271,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
       copy_img_async(r1_hi, img + (size_t)mn->i2 * kImg, 2 * kImg);
       stage_g1_rows_async(mn, g, g1img, r2_hi, r2_lo);
       if (kRows) {
-        stage_rows_async<false>(npn, st_sbi, gout, G3, m3, st_g, st_g3);
+        stage_rows_async<false>(npn, tile_i3_base(mn, g), st_sbi, gout, G3, m3, st_g, st_g3);
       } else {  // the G3 slices (their region held the Z lo image)
         for (int e = threadIdx.x; e < npn * 32; e += kThreads)
-          cp_async16(st_g3 + e, reinterpret_cast<const float4*>(G3) + (size_t)(e & 31) * m3 + st_sbi[e >> 5].y);
+          cp_async16(st_g3 + e, reinterpret_cast<const float4*>(G3) + (size_t)(e & 31) * m3 + tile_i3_base(mn, g) +
+                                    st_sbi[e >> 5].y);
       }
     }
     if (!(dbg & 4)) {
@@ -1365,7 +1403,7 @@ cudaError_t launch_gradcheck(const float* g, int64_t n, int* err, int num_sms, c
 bool fast_supported(const ttb_handle* h) {
   const DynDims& d = h->dims;
   // G3 (32 x m3 x 4 fp32) stays resident in the forward kernel's shared memory
-  return d.n1 == 4 && d.n2 == 4 && d.n3 == 4 && d.r1 == 32 && d.r2 == 32 && h->kg.m3 <= (unsigned)kFwdMaxM3;
+  return d.n1 == 4 && d.n2 == 4 && d.n3 == 4 && d.r1 == 32 && d.r2 == 32 && h->kg.tm3 <= (unsigned)kFwdMaxM3;
 }
 
 cudaError_t fast_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* offsets, cudaStream_t s) {
@@ -1392,12 +1430,14 @@ cudaError_t fast_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* 
   if (idx64)
     e = launch_pdl_coop(k_fplan<long long>, dim3(grid), dim3(kPlanThreads), 0, s, (const long long*)idx, offsets, T, B,
                    h->kg, w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_rstart, w.f_split, w.f_gtot, w.f_item_start, w.f_cta, h->num_sms,
-                   w.f_item_key, w.f_tile_info, w.f_sbi, w.fast_hdr, getenv("TTB_DBG") ? 1 : 0, h->allow_empty);
+                   w.f_item_key, w.f_tile_info, w.f_sbi, w.fast_hdr, getenv("TTB_DBG") ? 1 : 0, h->allow_empty,
+                   (const uint4*)w.f_tgeom);
   else
     e = launch_pdl_coop(k_fplan<int>, dim3(grid), dim3(kPlanThreads), 0, s, (const int*)idx, offsets, T, B, h->kg,
                    w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_rstart, w.f_split, w.f_gtot, w.f_item_start, w.f_cta, h->num_sms,
                    w.f_item_key,
-                   w.f_tile_info, w.f_sbi, w.fast_hdr, getenv("TTB_DBG") ? 1 : 0, h->allow_empty);
+                   w.f_tile_info, w.f_sbi, w.fast_hdr, getenv("TTB_DBG") ? 1 : 0, h->allow_empty,
+                   (const uint4*)w.f_tgeom);
   if (e) return e;
   count_launch();
   return cudaGetLastError();
@@ -1418,7 +1458,7 @@ cudaError_t fast_forward(ttb_handle* h, const float* c0, const float* c1, const 
     // last fused update, or the last forward, still describe these cores)
     ProfScope _ps(h, s, "f_coreimg");
     SgdArgs u = {};
-    if ((e = launch_pdl(k_coreimg, dim3(h->kg.m2 + (h->kg.m1 + 3) / 4), dim3(kImgThreads), img_smem, s,
+    if ((e = launch_pdl(k_coreimg, dim3(h->kg.m2 + (h->kg.g1rows + 3) / 4), dim3(kImgThreads), img_smem, s,
                         const_cast<float*>(c0), const_cast<float*>(c1), h->kg, w.f_img, w.f_g1img, u)))
       return e;
     count_launch();
@@ -1434,7 +1474,7 @@ cudaError_t fast_forward(ttb_handle* h, const float* c0, const float* c1, const 
   {
     ProfScope _ps(h, s, "f_fwd");
     // pooled bags: segments of several lookups (G3 slices summed before the product)
-    if ((e = launch_pdl(h->T > h->B ? k_fwd<true> : k_fwd<false>, dim3(grid), dim3(kFwdThreads), fwd_smem_bytes(h->kg.m3), s, h->kg, (const float*)w.f_g1img, c2,
+    if ((e = launch_pdl(h->T > h->B ? k_fwd<true> : k_fwd<false>, dim3(grid), dim3(kFwdThreads), fwd_smem_bytes(h->kg.tm3), s, h->kg, (const float*)w.f_g1img, c2,
                         (const float*)w.f_img, (const int*)w.fast_hdr, (const int4*)w.f_tile_info,
                         (const int*)w.f_item_start, (const unsigned*)w.f_item_key, (const int2*)w.f_sbi, out,
                         (const int*)w.f_cta, direct, getenv("TTB_DBG") ? atoi(getenv("TTB_DBG")) : 0)))
@@ -1450,7 +1490,7 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
                           double* v2, double lr, double mu, int mask, int mode, cudaStream_t s, int adagrad) {
   Workspace& w = h->w;
   cudaError_t e;
-  const int64_t n0 = (int64_t)h->kg.m1 * 4 * R1, n1 = (int64_t)R1 * h->kg.m2 * C, n2 = (int64_t)32 * h->kg.m3 * 4;
+  const int64_t n0 = (int64_t)h->kg.g1rows * 4 * R1, n1 = (int64_t)R1 * h->kg.m2 * C, n2 = (int64_t)32 * h->kg.m3 * 4;
   if (mode == 1) {
     g0 = w.f_grad;
     g1 = w.f_grad + n0;
@@ -1485,7 +1525,7 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
     }
     SgdArgs u = {w.f_grad, v0, v1, v2, p2, lr, mu, mask, 1, w.fast_hdr, adagrad};
     ProfScope _ps(h, s, "f_sgd");
-    if ((e = launch_pdl(k_coreimg, dim3(h->kg.m2 + (h->kg.m1 + 3) / 4 + (ng3 < 64 ? ng3 : 64)), dim3(kImgThreads),
+    if ((e = launch_pdl(k_coreimg, dim3(h->kg.m2 + (h->kg.g1rows + 3) / 4 + (ng3 < 64 ? ng3 : 64)), dim3(kImgThreads),
                         img_smem, s, p0, p1, h->kg, w.f_img, w.f_g1img, u)))
       return e;
     count_launch();

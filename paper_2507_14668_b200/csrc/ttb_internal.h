@@ -70,6 +70,7 @@ struct Workspace {
   float* scratch1;                  // 1-float sink for the unit core of d = 2 tables
   // tensor-core pipeline (ttb_fast.cu); fast_hdr sits just before zero block A:
   // [0] err bits, [1] multi-index bags, [2] work items, [3] prefixes P, [4] tiles
+  uint4* f_tgeom;  // batched handles: per table (m2, m3, rows, 0) for the plan's digits
   int* fast_hdr;
   unsigned* f_key;        // T: i2-major prefix key
   unsigned* f_i3;         // T
@@ -123,6 +124,9 @@ struct ttb_handle {
   int bwd_split;         // use the split backward (rows kernel + tensor-core GEMM kernel)
   int allow_empty;       // TTB_OPT_ALLOW_EMPTY: empty bags pool to zero rows (nn.EmbeddingBag) instead of an error
   int fast_ok, fast;     // tensor-core pipeline supported / selected (ttb_fast.cu)
+  int batched;           // ttb_create_batched: several tables in one handle (tensor-core pipeline only)
+  ttb_geom tables[TTB_MAX_TABLES];  // their geometries (batched)
+  uint4 tgeom_host[TTB_MAX_TABLES];  // (m2, m3, rows, 0) per table: the source of w.f_tgeom
   int num_sms;
   const void* plan_idx;  // inputs of the current plan (the legacy plan behind
   const int64_t* plan_off;  // ttb_export_plan is built from them on demand)

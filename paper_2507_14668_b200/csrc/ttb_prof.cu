@@ -101,6 +101,7 @@ int ttb_set_option(ttb_handle* h, int option, int value) {
     case 3: h->allow_empty = value ? 1 : 0; return TTB_OK;  // TTB_OPT_ALLOW_EMPTY
     case 2:                                                // TTB_OPT_FAST
       if (value && !h->fast_ok) return TTB_EINVAL;
+      if (!value && h->batched) return TTB_EINVAL;  // a batched handle has only the tensor-core pipeline
       h->fast = value ? 1 : 0;
       h->planned = h->forwarded = h->backwarded = 0;  // a plan belongs to one pipeline
       return TTB_OK;
