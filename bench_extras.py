@@ -179,7 +179,8 @@ def dlrm_samples_per_s(cfg, B, bag_lo, bag_hi, steps, dev, peaks=None, cpu_B=Non
     from paper_2507_14668_b200.model import DlrmModel
     torch.backends.cuda.matmul.allow_tf32 = False
     rng = np.random.default_rng(11)
-    model = DlrmModel(cfg, device=dev, max_indices=B * bag_hi, check_errors=False)
+    model = DlrmModel(cfg, device=dev, max_indices=B * bag_hi * len(cfg.rows_per_field), check_errors=False,
+                      batch_size=B)
     host = _dlrm_host_batch(cfg, B, rng, bag_lo, bag_hi)
     dense, sparse, labels = _dlrm_batch(cfg, B, rng, dev, bag_lo, bag_hi, host=host)
     ms = _time_graph(lambda: model.train_step(dense, sparse, labels, 0.05, 0.9, sync_loss=False), steps)
@@ -224,7 +225,7 @@ def cfg5(dev, world=1, rank=0, steps=5, global_batch=524288):
                       bottom_sizes=(512, 256), top_sizes=(512, 256), loss="bce", seed=0)
     B = global_batch // world
     rng = np.random.default_rng(11 + rank)
-    model = DlrmModel(cfg, device=dev, max_indices=B, check_errors=False)
+    model = DlrmModel(cfg, device=dev, max_indices=B * len(cfg.rows_per_field), check_errors=False, batch_size=B)
     dense, sparse, labels = _dlrm_batch(cfg, B, rng, dev, 1, 1)
     step = lambda: model.train_step_dp(dense, sparse, labels, 0.05, 0.9, global_batch=global_batch)  # noqa: E731
     for _ in range(3):
@@ -282,11 +283,40 @@ def cfg3(dev, steps=3, B=65536, pooling=20, permuted=False, tables=26, peaks=Non
     torch.cuda.synchronize()
     st = eng.check_errors()
     st["U"] = eng.status()["U"]
-    ms = _time_graph(step, steps, warmup=1)
+    ms_loop = _time_graph(step, steps, warmup=1)
+    del eng
+    # the same 26 tables through ONE table-batched handle (§8 f1): one plan /
+    # forward / backward + update launch set over all tables' lookups
+    from paper_2507_14668_b200.collection import BatchedTtEngine
+    beng = BatchedTtEngine([shape] * tables, B, T * tables, dev)
+    M = beng.M
+    bcores = [torch.zeros(beng.shape.core_extent(k), dtype=torch.float32, device=dev) for k in range(3)]
+    for t in range(tables):
+        for k in range(3):
+            w = shape.m[k] * shape.n[k]
+            bcores[k][:, t * M[k] * shape.n[k]: t * M[k] * shape.n[k] + w, :] = cores[t][k]
+    bvel = [torch.zeros(c.shape, dtype=torch.float64, device=dev) for c in bcores]
+    bidx = torch.cat(idxs)
+    boff = torch.arange(0, T * tables + 1, pooling, dtype=torch.int64, device=dev)
+    bgout = gout.repeat(tables, 1)
+    bout = torch.empty((B * tables, 64), device=dev)
+    del cores, vel, idxs, out
+
+    def bstep():
+        beng.plan(bidx, boff)
+        beng.forward(bcores, out=bout)
+        beng.backward_sgd(bcores, bgout, 0.05, 0.9, bvel)
+
+    bstep()
+    torch.cuda.synchronize()
+    beng.check_errors()
+    ms = _time_graph(bstep, steps, warmup=1)
     res = {"value": tables * T / (ms / 1e3), "unit": "lookups/s", "ms_per_step": ms, "tables": tables,
            "lookups_per_table": T, "last_table_counts": {k: st[k] for k in ("P", "S", "U")},
+           "per_table_loop": {"ms_per_step": ms_loop, "value": tables * T / (ms_loop / 1e3)},
            "workload": f"cfg3: {tables} TT tables 10M x 64 ranks 32, Zipf(1.05) {'permuted' if permuted else 'native'} "
-                       f"ids, pooling {pooling}, {B} bags/table, plan+fwd+bwd+SGD per table"}
+                       f"ids, pooling {pooling}, {B} bags/table; step = plan+fwd+bwd+SGD of all tables through "
+                       "one table-batched handle (per_table_loop: the same, one table at a time)"}
     if peaks is not None:  # per table (the last one's counts; the tables' batches are identically distributed)
         c = table_counts(host_ids, np.arange(0, T + 1, pooling), shape.m[-1])
         fl, nb = tt_flops(shape, c)

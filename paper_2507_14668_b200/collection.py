@@ -137,6 +137,12 @@ class TTEmbeddingBagCollection(nn.Module):
     enable_fused_adagrad = _T.enable_fused_adagrad
     del _T
 
+    def set_bags_per_table(self, B: int) -> None:
+        """Bags per table of the next batches (re-sizes the batched handle)."""
+        if int(B) != self.bags_per_table:
+            self.bags_per_table = self.engine.bags_per_table = int(B)
+            self.engine._reserve(self.engine.max_T, 0)
+
     @property
     def num_tables(self) -> int:
         return len(self.shapes)

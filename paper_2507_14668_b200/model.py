@@ -32,6 +32,7 @@ import torch
 from torch import nn
 
 from . import _native as nat
+from .collection import TTEmbeddingBagCollection
 from .embedding_bag import TTEmbeddingBag
 from .engine import _ptr, _stream, require_cuda, to_offsets
 from .geometry import bytes_to_table, factorize_dims, table_to_bytes
@@ -163,23 +164,79 @@ class DenseField(nn.Module):
         return _DenseBagSum.apply(self.rows, indices, bag_of, n_bags)
 
 
+class TTField(nn.Module):
+    """A TT field served by the model's table-batched collection (its table
+    f): the reference's FieldTable seam (model.py:179-243) for one field, the
+    compute shared with every other TT field (one launch set per step)."""
+
+    def __init__(self, coll: list, f: int):
+        super().__init__()
+        self._coll = coll  # [collection], a list so the module is registered once (as DlrmModel.tt)
+        self.f = f
+
+    @property
+    def collection(self) -> TTEmbeddingBagCollection:
+        return self._coll[0]
+
+    @property
+    def shape(self):
+        return self.collection.shapes[self.f]
+
+    @property
+    def cores(self):
+        return self.collection.table_cores(self.f)
+
+
+def _tt_batchable(rows_list, emb_dim, ranks) -> bool:
+    """Every TT field fits the table-batched tensor-core pipeline."""
+    if len(rows_list) < 2 or tuple(ranks) != (1, 32, 32, 1):
+        return False
+    for rows in rows_list:
+        m, n = factorize_dims(int(rows), int(emb_dim), 3)
+        if tuple(n) != (4, 4, 4) or m[2] > 288:
+            return False
+    return True
+
+
+def _is_tt(fld) -> bool:
+    return isinstance(fld, (TTEmbeddingBag, TTField))
+
+
 class DlrmModel(nn.Module):
-    def __init__(self, config: ModelConfig, device=None, max_indices: int = 1 << 16, check_errors: bool = True):
+    def __init__(self, config: ModelConfig, device=None, max_indices: int = 1 << 16, check_errors: bool = True,
+                 batch_tt_fields: bool | None = None, batch_size: int = 1 << 12):
+        """batch_tt_fields: serve every TT field from ONE table-batched
+        collection (one plan / forward / backward / update launch set per step
+        instead of one per field). None: whenever the fields
+        fit the tensor-core pipeline (n = (4, 4, 4), ranks 32, m3 <= 288)."""
         super().__init__()
         config.validate()
         self.config = config
         dev = require_cuda(device)
         self.device = dev
         rng = np.random.default_rng(config.seed)
+        seeds = [int(rng.integers(2 ** 31)) for _ in config.rows_per_field]
+        tt_ids = [f for f, rows in enumerate(config.rows_per_field) if rows >= config.tt_threshold]
+        if batch_tt_fields is None:
+            batch_tt_fields = _tt_batchable([config.rows_per_field[f] for f in tt_ids], config.emb_dim, config.ranks)
+        self.tt = None
+        if batch_tt_fields and tt_ids:
+            self.tt = TTEmbeddingBagCollection([(config.rows_per_field[f], config.emb_dim) for f in tt_ids],
+                                               config.ranks, seeds=[seeds[f] for f in tt_ids],
+                                               bags_per_table=batch_size,
+                                               max_indices=max(max_indices, len(tt_ids) * batch_size),
+                                               include_last_offset=True, device=dev, check_errors=check_errors)
         fields = []
-        for rows in config.rows_per_field:
-            seed = int(rng.integers(2 ** 31))
+        for f, rows in enumerate(config.rows_per_field):
             if rows >= config.tt_threshold:
-                fields.append(TTEmbeddingBag(rows, config.emb_dim, config.ranks, seed=seed, device=dev,
-                                             include_last_offset=True, max_indices=max_indices,
-                                             check_errors=check_errors))
+                if self.tt is not None:
+                    fields.append(TTField([self.tt], tt_ids.index(f)))
+                else:
+                    fields.append(TTEmbeddingBag(rows, config.emb_dim, config.ranks, seed=seeds[f], device=dev,
+                                                 include_last_offset=True, max_indices=max_indices,
+                                                 check_errors=check_errors))
             else:
-                fields.append(DenseField(rows, config.emb_dim, seed, dev, check_errors))
+                fields.append(DenseField(rows, config.emb_dim, seeds[f], dev, check_errors))
         self.fields = nn.ModuleList(fields)
         self.bottom = Mlp((config.n_dense, *config.bottom_sizes, config.emb_dim), rng, dev)
         self.top = Mlp((config.interaction_dim, *config.top_sizes, 1), rng, dev)
@@ -190,7 +247,7 @@ class DlrmModel(nn.Module):
         """(reference name, tensor) in DlrmModel.named_params order (model.py:272-282)."""
         out = []
         for f, fld in enumerate(self.fields):
-            if isinstance(fld, TTEmbeddingBag):
+            if _is_tt(fld):
                 out.extend((f"field_{f}.core{k}", c) for k, c in enumerate(fld.cores))
             else:
                 out.append((f"field_{f}.rows", fld.rows))
@@ -202,17 +259,47 @@ class DlrmModel(nn.Module):
             out.append((f"top.{i}.b", self.top.biases[i]))
         return out
 
+    def _update_params(self):
+        """(name, leaf tensor) of every parameter an optimizer step touches:
+        named_ref_params, with the batched TT fields' per-field core views
+        replaced by the collection's stacked cores (their padding keeps zero
+        gradients, so the same element-wise update leaves it zero)."""
+        out = [(f"tt.core{k}", c) for k, c in enumerate(self.tt.cores)] if self.tt is not None else []
+        return out + [(n, t) for n, t in self.named_ref_params()
+                      if not (self.tt is not None and n.startswith("field_") and ".core" in n)]
+
     # ------------------------------------------------------------ forward
     def forward(self, dense: torch.Tensor, sparse) -> torch.Tensor:
         """dense (B, n_dense) fp32; sparse: per field (indices, offsets (B+1))."""
         if len(sparse) != self.config.n_sparse:
             raise ValueError("batch field count != model field count")
         v0 = self.bottom(dense)
-        vectors = [v0]
-        for fld, (idx, off) in zip(self.fields, sparse):
-            vectors.append(fld(idx, off))
+        vectors = [v0] + [None] * len(self.fields)
+        if self.tt is not None:  # every TT field in one batched lookup
+            tt = [(f, sparse[f]) for f, fld in enumerate(self.fields) if isinstance(fld, TTField)]
+            pooled = self._tt_lookup([s for _, s in tt]).unbind(0)  # (one stack in the backward, not F scatters)
+            for j, (f, _) in enumerate(tt):
+                vectors[f + 1] = pooled[j]
+        for f, (fld, (idx, off)) in enumerate(zip(self.fields, sparse)):
+            if not isinstance(fld, TTField):
+                vectors[f + 1] = fld(idx, off)
         inter = feature_interaction(vectors)
         return self.top(inter).reshape(-1)
+
+    def _tt_lookup(self, inputs):
+        """[(indices (T_f,), offsets (B+1,))] of the TT fields -> (F, B, N):
+        the fields' indices concatenated table by table, their offsets
+        rebased onto one (F B + 1,) list."""
+        B = inputs[0][1].numel() - 1
+        if any(o.numel() - 1 != B for _, o in inputs):
+            raise ValueError("every field needs the same number of bags")
+        self.tt.set_bags_per_table(B)
+        idx = torch.cat([i for i, _ in inputs])
+        offs = torch.stack([o.to(torch.int64) for _, o in inputs])
+        lens = offs[:, -1] - offs[:, 0]
+        base = torch.cumsum(lens, 0) - lens - offs[:, 0]
+        comb = torch.cat([(offs[:, :-1] + base[:, None]).reshape(-1), (offs[-1:, -1] + base[-1:])])
+        return self.tt(idx, comb)
 
     def loss_and_logit_grad(self, z: torch.Tensor, y: torch.Tensor):
         """model.py:77-86: loss value (fp64) and dL/dz = (sigmoid(z) - y) / B."""
@@ -237,6 +324,8 @@ class DlrmModel(nn.Module):
         for fld in self.fields:
             if isinstance(fld, TTEmbeddingBag):
                 fld.enable_fused_sgd(lr, momentum)
+        if self.tt is not None:
+            self.tt.enable_fused_sgd(lr, momentum)
         for p in self.parameters():
             p.grad = None
         z = self.forward(dense, sparse)
@@ -279,12 +368,14 @@ class DlrmModel(nn.Module):
         for fld in self.fields:
             if isinstance(fld, TTEmbeddingBag):
                 fld.disable_fused_sgd()
+        if self.tt is not None:
+            self.tt.disable_fused_sgd()
         for p in self.parameters():
             p.grad = None
         z = self.forward(dense, sparse)
         loss, gz = self.loss_and_logit_grad(z, labels)
         z.backward(gz * (local_b / global_b))
-        named = self.named_ref_params()
+        named = self._update_params()
         flat = torch.cat([(p.grad if p.grad is not None else torch.zeros_like(p)).reshape(-1) for _, p in named])
         if world > 1:
             dist.all_reduce(flat, group=group)
@@ -355,7 +446,7 @@ def checkpoint_bytes(model: DlrmModel) -> bytes:
     the MLP tensors in named_params order (model.py:436-460)."""
     records = [("config", _config_payload(model.config))]
     for f, fld in enumerate(model.fields):
-        if isinstance(fld, TTEmbeddingBag):
+        if _is_tt(fld):
             records.append((f"field_{f}.tt", table_to_bytes(fld.shape, [c.detach().cpu().numpy()
                                                                          for c in fld.cores])))
         else:
@@ -413,7 +504,7 @@ def load_checkpoint(path, device=None, **model_kwargs) -> DlrmModel:
     model = DlrmModel(_config_from_payload(records.pop("config")), device=device, **model_kwargs)
     with torch.no_grad():
         for f, fld in enumerate(model.fields):
-            if not isinstance(fld, TTEmbeddingBag):
+            if not _is_tt(fld):
                 continue
             name = f"field_{f}.tt"
             if name not in records:

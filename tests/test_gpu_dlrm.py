@@ -100,3 +100,38 @@ def test_dlrm_tensor_core_pipeline_matches_reference(golden):
             want = s[f"step{step}.{name}"].astype(np.float64)
             err = np.abs(got - want).max() / max(1e-3, np.abs(want).max())
             assert err < 1e-4, (step, name, err)
+
+
+def test_dlrm_batched_tt_fields_match_per_field():
+    """DlrmModel serves its TT fields from ONE table-batched collection
+    (batch_tt_fields, §8 f1) with the per-field model's exact initial
+    parameters (the reference's init order) and training trajectory (three
+    SGD + momentum steps: losses and every parameter within fp32 noise)."""
+    import numpy as np
+    import torch
+    from paper_2507_14668_b200.model import DlrmModel, ModelConfig, checkpoint_bytes
+    cfg = ModelConfig(n_dense=5, rows_per_field=(12000, 700, 30000, 4000), emb_dim=64, ranks=(1, 32, 32, 1),
+                      tt_threshold=1000, bottom_sizes=(32,), top_sizes=(32,), loss="bce", seed=9)
+    a = DlrmModel(cfg, batch_size=128)
+    b = DlrmModel(cfg, batch_tt_fields=False)
+    assert a.tt is not None and a.tt.num_tables == 3 and b.tt is None
+    assert checkpoint_bytes(a) == checkpoint_bytes(b)
+    rng = np.random.default_rng(4)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    for step in range(3):
+        B = 128
+        dense = torch.from_numpy(rng.standard_normal((B, 5)).astype(np.float32)).cuda()
+        labels = torch.from_numpy((rng.random(B) < 0.3).astype(np.float64)).cuda()
+        sparse = []
+        for rows in cfg.rows_per_field:
+            sizes = rng.integers(1, 4, size=B)
+            idx = rng.integers(0, rows, size=int(sizes.sum()))
+            off = np.concatenate([[0], np.cumsum(sizes)])
+            sparse.append((torch.from_numpy(idx).cuda(), torch.from_numpy(off).cuda()))
+        la = a.train_step(dense, sparse, labels, 0.05, 0.9)
+        lb = b.train_step(dense, sparse, labels, 0.05, 0.9)
+        assert abs(la - lb) <= 1e-6 * max(1.0, abs(lb)), step
+    for (na, pa), (nb, pb) in zip(a.named_ref_params(), b.named_ref_params()):
+        assert na == nb
+        d = (pa.detach() - pb.detach()).abs().max().item()
+        assert d <= 1e-5 * max(1e-3, pb.detach().abs().max().item()), na
