@@ -83,6 +83,9 @@ typedef void *ttb_stream;             /* a cudaStream_t */
 
 int ttb_abi_version(void);
 const char *ttb_strerror(int code);
+/* cudaGetErrorString of the calling thread's last CUDA failure behind a
+ * TTB_ECUDA status (diagnostics; no reference counterpart) */
+const char *ttb_last_cuda_error(void);
 /* number of kernels this library has launched in the process (a counter) */
 int64_t ttb_launch_count(void);
 

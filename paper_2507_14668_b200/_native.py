@@ -35,7 +35,7 @@ OPT_ALLOW_EMPTY = 3
 
 # every symbol include/ttb.h declares (tests check the .so exports them all)
 EXPORTS = [
-    "ttb_abi_version", "ttb_strerror", "ttb_launch_count", "ttb_workspace_bytes", "ttb_create",
+    "ttb_abi_version", "ttb_strerror", "ttb_last_cuda_error", "ttb_launch_count", "ttb_workspace_bytes", "ttb_create",
     "ttb_destroy", "ttb_batched_workspace_bytes", "ttb_create_batched", "ttb_plan", "ttb_forward", "ttb_backward", "ttb_aggregate", "ttb_backward_sgd", "ttb_cores_modified", "ttb_sgd_update", "ttb_backward_adagrad", "ttb_adagrad_update", "ttb_dp_flag_words", "ttb_dp_exchange_update",
     "ttb_ipc_handle", "ttb_ipc_open", "ttb_ipc_close",
     "ttb_check_finite", "ttb_sgd_update_checked", "ttb_export_fast_plan", "ttb_plan_counts",
@@ -57,6 +57,7 @@ _dbl = C.c_double
 _PROTOS = {
     "ttb_abi_version": (_int, []),
     "ttb_strerror": (C.c_char_p, [_int]),
+    "ttb_last_cuda_error": (C.c_char_p, []),
     "ttb_launch_count": (_i64, []),
     "ttb_workspace_bytes": (_int, [C.POINTER(TtbGeom), _i64, _i64, C.POINTER(C.c_size_t)]),
     "ttb_create": (_vp, [C.POINTER(TtbGeom), _i64, _i64, _vp, C.c_size_t, _vp]),
@@ -133,6 +134,8 @@ def check(code: int, what: str = "") -> None:
         msg = f"{what}: {msg}"
     if code in (TTB_EINVAL, TTB_ERANGE, TTB_EEMPTY, TTB_EOFFSETS, TTB_ENONFINITE):
         raise ValueError(msg)
+    if code == TTB_ECUDA:
+        msg = f"{msg} ({load().ttb_last_cuda_error().decode()})"
     raise TtbError(msg)
 
 

@@ -257,7 +257,12 @@ bool init_handle_batched(ttb_handle& h, const ttb_geom* tables, int nt, int64_t 
   return true;
 }
 
-int cuda_status(cudaError_t e) { return e == cudaSuccess ? TTB_OK : TTB_ECUDA; }
+thread_local cudaError_t t_last_cuda = cudaSuccess;  // the calling thread's last failing CUDA call
+int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return TTB_OK;
+  t_last_cuda = e;
+  return TTB_ECUDA;
+}
 
 }  // namespace
 
@@ -278,6 +283,8 @@ const char* ttb_strerror(int code) {
     default: return "unknown error";
   }
 }
+
+const char* ttb_last_cuda_error(void) { return cudaGetErrorString(t_last_cuda); }
 
 int64_t ttb_launch_count(void) { return (int64_t)__atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
 
@@ -369,7 +376,7 @@ int ttb_plan(ttb_handle* h, const void* indices, int idx_is_64, const int64_t* o
   cudaError_t e = h->fast ? fast_plan(h, indices, idx_is_64, offsets, (cudaStream_t)stream)
                           : launch_plan(h, indices, idx_is_64, offsets, (cudaStream_t)stream);
   if (!h->fast) h->legacy_planned = 1;
-  if (e != cudaSuccess) return TTB_ECUDA;
+  if (e != cudaSuccess) return cuda_status(e);
   h->planned = 1;
   ++h->gen;
   return TTB_OK;
@@ -381,7 +388,7 @@ int ttb_forward(ttb_handle* h, const float* c0, const float* c1, const float* c2
   if (!h->fast && h->pmap_clean) return TTB_ESTATE;  // a backward consumed this plan's prefix table
   cudaError_t e = h->fast ? fast_forward(h, c0, c1, c2, out, (cudaStream_t)stream)
                           : launch_forward(h, c0, c1, c2, out, (cudaStream_t)stream);
-  if (e != cudaSuccess) return TTB_ECUDA;
+  if (e != cudaSuccess) return cuda_status(e);
   h->forwarded = 1;
   return TTB_OK;
 }
@@ -394,7 +401,7 @@ int ttb_backward(ttb_handle* h, const float* c0, const float* c1, const float* c
                                           nullptr, nullptr, 0.0, 0.0, 0, 0, (cudaStream_t)stream)
                           : launch_backward(h, c0, c1, c2, grad_out, g0, g1, g2, nullptr, nullptr, nullptr, nullptr,
                                             nullptr, nullptr, 0.0, 0.0, 0, 0, (cudaStream_t)stream);
-  if (e != cudaSuccess) return TTB_ECUDA;
+  if (e != cudaSuccess) return cuda_status(e);
   h->backwarded = 1;
   h->pmap_clean = 1;
   return TTB_OK;
@@ -404,7 +411,7 @@ int ttb_aggregate(ttb_handle* h, const float* grad_out, ttb_stream stream) {
   if (!h || !grad_out) return TTB_EINVAL;
   if (!h->planned || h->fast) return TTB_ESTATE;  // legacy pipeline only
   cudaError_t e = launch_aggregate(h, grad_out, (cudaStream_t)stream);
-  if (e != cudaSuccess) return TTB_ECUDA;
+  if (e != cudaSuccess) return cuda_status(e);
   h->backwarded = 1;
   return TTB_OK;
 }
@@ -421,7 +428,7 @@ int ttb_backward_sgd(ttb_handle* h, float* c0, float* c1, float* c2, const float
                                           lr, momentum, update_mask, 1, (cudaStream_t)stream)
                           : launch_backward(h, c0, c1, c2, grad_out, nullptr, nullptr, nullptr, c0, c1, c2, v0, v1, v2,
                                             lr, momentum, update_mask, 1, (cudaStream_t)stream);
-  if (e != cudaSuccess) return TTB_ECUDA;
+  if (e != cudaSuccess) return cuda_status(e);
   h->backwarded = 1;
   h->pmap_clean = 1;
   return TTB_OK;
@@ -436,7 +443,7 @@ int ttb_backward_adagrad(ttb_handle* h, float* c0, float* c1, float* c2, const f
   if (!h->fast) return TTB_ESTATE;  // deterministic pipeline: ttb_backward, then ttb_adagrad_update
   cudaError_t e = fast_backward(h, c0, c1, c2, grad_out, nullptr, nullptr, nullptr, c0, c1, c2, s0, s1, s2, lr, eps,
                                 update_mask, 1, (cudaStream_t)stream, 1);
-  if (e != cudaSuccess) return TTB_ECUDA;
+  if (e != cudaSuccess) return cuda_status(e);
   h->backwarded = 1;
   h->pmap_clean = 1;
   return TTB_OK;
@@ -550,7 +557,7 @@ int ttb_export_plan(ttb_handle* h, int64_t* work, int64_t* slot_occ, int64_t* se
   if (!h->legacy_planned) {
     // the reference-ordered plan (first-occurrence slots, segments) on demand
     cudaError_t e = launch_plan(h, h->plan_idx, h->plan_idx64, h->plan_off, (cudaStream_t)stream);
-    if (e != cudaSuccess) return TTB_ECUDA;
+    if (e != cudaSuccess) return cuda_status(e);
     h->legacy_planned = 1;
   }
   return cuda_status(launch_export_plan(h, work, slot_occ, seg_ids, seg_inv, digits, (cudaStream_t)stream));

@@ -394,6 +394,17 @@ __global__ void __launch_bounds__(256) k_gradcheck(const float* __restrict__ g, 
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, TTB_ERRBIT_NONFINITE);
 }
 
+// dG3 slice-major (i3, c, n3) -> the reference layout (c, i3, n3)
+__global__ void __launch_bounds__(256) k_g3_unslice(const float* __restrict__ src, float* __restrict__ dst,
+                                                    unsigned m3) {
+  pdl_enter();
+  const unsigned n = 128 * m3;
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const unsigned c = e / (4 * m3), r = e - c * 4 * m3;
+    dst[e] = src[((size_t)(r >> 2) * 32 + c) * 4 + (r & 3)];
+  }
+}
+
 __device__ __forceinline__ float maybe_sgd(float p, const SgdArgs& u, int core, size_t flat, size_t j, double* v) {
   if (!u.on || !((u.mask >> core) & 1)) return p;
   if (u.adagrad) return adagrad_apply(p, u.grad[flat], v + j, u.lr, u.mu);
@@ -415,7 +426,9 @@ __global__ void __launch_bounds__(kImgThreads) k_coreimg(float* __restrict__ G1,
     for (size_t j = (size_t)(blockIdx.x - nb12) * kImgThreads + threadIdx.x; j < n2;
          j += (size_t)(gridDim.x - nb12) * kImgThreads) {
       const float v = u.p2[j];
-      const float w = maybe_sgd(v, u, 2, n0 + n1 + j, j, u.v2);
+      // the backward accumulates dG3 slice-major: (i3, c, n3) (see k_bwd)
+      const size_t c = j / ((size_t)g.m3 * 4), r = j - c * g.m3 * 4;
+      const float w = maybe_sgd(v, u, 2, n0 + n1 + ((r >> 2) * 32 + c) * 4 + (r & 3), j, u.v2);
       if (u.mask & 4) u.p2[j] = w;
     }
     return;
@@ -977,16 +990,30 @@ __device__ __forceinline__ void lookup_update(const float4* src, const float (&x
   }
 }
 
+// Warp roles: warps 0-15 (kThreads) do the SIMT work and synchronise among
+// themselves with named barrier 1; warp 16 issues every tcgen05.mma of the
+// CTA (X, dG2, E) when the SIMT warps signal that its operands are ready, so
+// no SIMT warp blocks in a long MMA issue and the next tile's X GEMM runs
+// under the current tile's dG1 / dG2 reductions.
+constexpr int kBwdThreads = kThreads + 32;
+__device__ __forceinline__ void simt_sync() { named_sync(1, kThreads); }
+__device__ __forceinline__ void simt_sync_for_mma() {
+  umma::fence_smem_to_async();
+  umma::fence_before_sync();
+  simt_sync();
+  umma::fence_after_sync();
+}
+
 template <bool kRows>
-__global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __restrict__ g1img,
-                                                     const float* __restrict__ G3, const float* __restrict__ img,
-                                                     const int4* __restrict__ tile_info,
-                                                     const int* __restrict__ item_start,
-                                                     const unsigned* __restrict__ item_key,
-                                                     const int2* __restrict__ sbi, const float* __restrict__ gout,
-                                                     float* __restrict__ dG1, float* __restrict__ dG2,
-                                                     float* __restrict__ dG3, int* __restrict__ hdr,
-                                                     const int* __restrict__ cta_tiles, int dbg) {
+__global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __restrict__ g1img,
+                                                        const float* __restrict__ G3, const float* __restrict__ img,
+                                                        const int4* __restrict__ tile_info,
+                                                        const int* __restrict__ item_start,
+                                                        const unsigned* __restrict__ item_key,
+                                                        const int2* __restrict__ sbi, const float* __restrict__ gout,
+                                                        float* __restrict__ dG1, float* __restrict__ dG2,
+                                                        float* __restrict__ dG3, int* __restrict__ hdr,
+                                                        const int* __restrict__ cta_tiles, int dbg) {
   pdl_enter();
   extern __shared__ __align__(16) char smem_raw[];
   char* sm = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -1001,21 +1028,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
   float4* st_g = reinterpret_cast<float4*>(sm + 8 * kImg + kCap * 8);
   float4* st_g3 = st_g + kCap * 16;  // per-position G3 slices (bag-run path only)
   float4* st_acc = st_g + kCap * 16;  // row path: per-warp summed gradient row
+  // Z lo image: the dead staging rows past the next tile's (bag, i3) list
+  // (bag-run path: exactly the G3-slice staging, so the next tile's gradient
+  // rows can stream in while the E GEMM runs)
+  char* zlo = sm + 8 * kImg + (kRows ? 4096 : kChunkPos * 8 + kChunkPos * 256);
   __shared__ TileMeta s_m[2];
   __shared__ int s_chunk[2][kTileItems + 2];
-  __shared__ uint64_t s_mbar;
+  // SIMT -> MMA warp: X operands staged / Z^T in TMEM + E operands staged /
+  // Z images written; MMA warp -> SIMT: X done / dG2 + E done
+  __shared__ uint64_t s_mb_xop, s_mb_z, s_mb_zi, s_mb_x, s_mb_e;
+  __shared__ int s_acc2;
   __shared__ long long s_tacc[12];
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ntiles = hdr[4];
-  // contiguous tile range: consecutive tiles mostly share i2, and the dG2
-  // slice accumulates in TMEM until i2 changes
   const int tb = cta_tiles[blockIdx.x], te = cta_tiles[blockIdx.x + 1];  // weight-balanced (k_fplan)
-  (void)ntiles;
   const unsigned m3 = g.m3;
   if (threadIdx.x < 12) s_tacc[threadIdx.x] = 0;
   if (warp == 0) umma::tmem_alloc(&s_tmem, 512);
-  if (threadIdx.x == 32) umma::mbar_init(&s_mbar, 1);
+  if (threadIdx.x == 32) {
+    umma::mbar_init(&s_mb_xop, 1);
+    umma::mbar_init(&s_mb_z, 1);
+    umma::mbar_init(&s_mb_zi, 1);
+    umma::mbar_init(&s_mb_x, 1);
+    umma::mbar_init(&s_mb_e, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   int4 pf = make_int4(0, 0, 0, 0);
   if (warp == kThreads / 32 - 1 && tb < te) {
     fetch_meta_async(tile_info[tb], item_start, item_key, &s_m[0]);
@@ -1026,63 +1063,99 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
   __syncthreads();
   umma::fence_after_sync();
   const uint32_t tmem = s_tmem;
+  // smem descriptors (start addresses are fixed for the kernel)
+  const uint64_t d_r1h = umma::desc_sw128(umma::smem_u32(r1_hi)), d_r1l = umma::desc_sw128(umma::smem_u32(r1_lo));
+  const uint64_t d_r2h = umma::desc_sw128(umma::smem_u32(r2_hi)), d_r2l = umma::desc_sw128(umma::smem_u32(r2_lo));
+  const uint64_t d_zi = umma::desc_sw128(umma::smem_u32(zi)), d_zl = umma::desc_sw128(umma::smem_u32(zlo));
+
+  if (warp == kThreads / 32) {
+    // ---------------- MMA warp
+    uint32_t ph = 0;
+    for (int t = tb; t < te; ++t, ph ^= 1u) {
+      umma::mbar_wait(&s_mb_xop, ph);  // X operands of tile t in R12
+      umma::fence_after_sync();
+      if (lane == 0) {
+        constexpr uint32_t id = umma::idesc_tf32(128, 128, false, false);
+#pragma unroll
+        for (int k0 = 0; k0 < R1; k0 += 8) {
+          const uint32_t o = (uint32_t)((k0 & 31) * 4) >> 4;
+          umma::mma_tf32(tmem, d_r1h + o, d_r2h + o, id, k0 > 0 ? 1u : 0u);
+          umma::mma_tf32(tmem, d_r1h + o, d_r2l + o, id, 1u);
+          umma::mma_tf32(tmem, d_r1l + o, d_r2h + o, id, 1u);
+        }
+        umma::commit(&s_mb_x);
+      }
+      __syncwarp();
+      umma::mbar_wait(&s_mb_z, ph);  // Z^T hi / lo in TMEM, G2 k / G1^T images in R12
+      umma::fence_after_sync();
+      if (lane == 0) {
+        constexpr uint32_t id64 = umma::idesc_tf32(128, 64, false, false);
+        constexpr uint32_t id32 = umma::idesc_tf32(128, 32, false, false);  // B rows 0-31: the hi half
+        const bool acc2 = s_acc2 != 0;  // same i2 as the previous tile: keep accumulating dG2 in TMEM
+        // dG2 tile [(c, b), (hi | lo) k] = sum_(item, a) (Z^T hi + Z^T lo) . G1^T (A from TMEM)
+#pragma unroll
+        for (int k0 = 0; k0 < 128; k0 += 8) {
+          const uint32_t o = (uint32_t)((k0 >> 5) * 64 * 128 + (k0 & 31) * 4) >> 4;
+          umma::mma_tf32_ta(tmem + 384, tmem + 128 + k0, d_r2h + o, id64, (acc2 || k0 > 0) ? 1u : 0u);
+          umma::mma_tf32_ta(tmem + 384, tmem + 256 + k0, d_r2h + o, id32, 1u);  // Z lo . G1 hi only
+        }
+      }
+      __syncwarp();
+      umma::mbar_wait(&s_mb_zi, ph);  // Z images (hi, lo) in shared memory
+      umma::fence_after_sync();
+      if (lane == 0) {
+        constexpr uint32_t id64 = umma::idesc_tf32(128, 64, false, false);
+        constexpr uint32_t id32 = umma::idesc_tf32(128, 32, false, false);
+        // E tile [(item, a), (hi | lo) k] = sum_(c, b) (Z hi . G2^T + Z lo . G2 hi^T)
+#pragma unroll
+        for (int k0 = 0; k0 < 128; k0 += 8) {
+          const uint32_t oa = (uint32_t)((k0 >> 5) * 128 * 128 + (k0 & 31) * 4) >> 4;
+          const uint32_t ob = (uint32_t)((k0 >> 5) * 64 * 128 + (k0 & 31) * 4) >> 4;
+          umma::mma_tf32(tmem + 448, d_zi + oa, d_r1h + ob, id64, k0 > 0 ? 1u : 0u);
+        }
+#pragma unroll
+        for (int k0 = 0; k0 < 128; k0 += 8) {
+          const uint32_t oa = (uint32_t)((k0 >> 5) * 128 * 128 + (k0 & 31) * 4) >> 4;
+          const uint32_t ob = (uint32_t)((k0 >> 5) * 64 * 128 + (k0 & 31) * 4) >> 4;
+          umma::mma_tf32(tmem + 448, d_zl + oa, d_r1h + ob, id32, 1u);  // Z lo . G2 hi only
+        }
+        umma::commit(&s_mb_e);  // tracks the dG2 MMAs too
+      }
+      __syncwarp();
+    }
+  } else {
+  // ---------------- SIMT warps
   const int q4 = warp & 3, qw = warp >> 2;  // lane quadrant, and this warp's share of its columns
   const int row = 32 * q4 + lane;  // TMEM lane of this thread: (c, b) = (row / 4, row % 4)
   const int c = row >> 2, b = row & 3;
   const uint32_t tl = tmem + ((uint32_t)(32 * q4) << 16);
-  // smem descriptors (start addresses are fixed for the kernel)
-  const uint64_t d_r1h = umma::desc_sw128(umma::smem_u32(r1_hi)), d_r1l = umma::desc_sw128(umma::smem_u32(r1_lo));
-  const uint64_t d_r2h = umma::desc_sw128(umma::smem_u32(r2_hi)), d_r2l = umma::desc_sw128(umma::smem_u32(r2_lo));
-  const uint64_t d_zi = umma::desc_sw128(umma::smem_u32(zi));
   // prologue: the first tile's first chunk and X operands
   if (tb < te) {
     const TileMeta* m = &s_m[0];
     if (threadIdx.x == 0) make_chunks(m, s_chunk[0], kCap);
-    __syncthreads();
+    simt_sync();
     const int np = m->start[s_chunk[0][1]] - m->start[0];
     for (int e = threadIdx.x; e < np; e += kThreads) cp_async8(st_sbi + e, sbi + m->start[0] + e);
     copy_img_async(r1_hi, img + (size_t)m->i2 * kImg, 2 * kImg);
     stage_g1_rows_async(m, g, g1img, r2_hi, r2_lo);
     cp_async_wait_all();
-    __syncthreads();
+    simt_sync_for_mma();
+    if (threadIdx.x == 0) umma::mbar_arrive(&s_mb_xop);  // X of the first tile
     stage_rows_async<!kRows>(np, tile_i3_base(m, g), st_sbi, gout, G3, m3, st_g, st_g3);
   }
   uint32_t phase = 0;
   bool bad = false;
   int slot = 0;
   int prev_i2 = -1;
-  for (int t = tb; t < te; ++t, slot ^= 1) {
+  for (int t = tb; t < te; ++t, slot ^= 1, phase ^= 1u) {
     const TileMeta* m = &s_m[slot];
     const int* chunk = s_chunk[slot];
     const int n = m->n, nchunk = chunk[kTileItems + 1];
     const float* gimg = img + (size_t)m->i2 * kImg;  // kImg floats = 4 images of kImg bytes
     const unsigned i3b = tile_i3_base(m, g);          // the tile's table's G3 slices (batched handles)
     TSTAMP(0);
-    // invariant: chunk 0's positions / rows and the X operands are issued
-    cp_async_wait_all();
-    sync_for_mma();
-    if (threadIdx.x == 0) {
-      constexpr uint32_t id = umma::idesc_tf32(128, 128, false, false);
-#pragma unroll
-      for (int k0 = 0; k0 < R1; k0 += 8) {
-        const uint32_t o = (uint32_t)((k0 & 31) * 4) >> 4;
-        umma::mma_tf32(tmem, d_r1h + o, d_r2h + o, id, k0 > 0 ? 1u : 0u);
-        umma::mma_tf32(tmem, d_r1h + o, d_r2l + o, id, 1u);
-        umma::mma_tf32(tmem, d_r1l + o, d_r2h + o, id, 1u);
-      }
-      umma::commit(&s_mbar);
-    }
-    if (warp == kThreads / 32 - 1) {  // next tile's metadata into the other slot
-      const int tn = t + 1;
-      if (tn < te) {
-        fetch_meta_async(pf, item_start, item_key, &s_m[slot ^ 1]);
-        if (tn + 1 < te) pf = tile_info[tn + 1];
-      }
-      cp_async_wait_all();
-    }
     TSTAMP(1);
-    umma::mbar_wait(&s_mbar, phase);
-    phase ^= 1u;
+    umma::mbar_wait(&s_mb_x, phase);  // X of tile t (its operands in R12 are free again)
     umma::fence_after_sync();
     TSTAMP(2);
     // X^T -> item slots (this warp's 32 columns)
@@ -1096,12 +1169,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
         xs[xs_idx(col >> 2, col & 3, b, c)] = __uint_as_float(v0[i]);
       }
     }
-    umma::fence_before_sync();
-    __syncthreads();
     // the second GEMM pair's operands stream in during the Z phase
     copy_img_async(r1_hi, gimg + 2 * kImg / 4, 2 * kImg);
     stage_g1_t_async(m, g, g1img, r2_hi);
     cp_async_commit();
+    umma::fence_before_sync();
+    simt_sync();  // (every warp is past the previous tile: its metadata slot is free)
+    if (warp == kThreads / 32 - 1 && t + 1 < te) {  // next tile's metadata into the other slot
+      fetch_meta_async(pf, item_start, item_key, &s_m[slot ^ 1]);  // (waited for before make_chunks)
+      if (t + 2 < te) pf = tile_info[t + 2];
+    }
     TSTAMP(3);
     for (int ch = 0; ch < nchunk; ++ch) {
       const int it0 = chunk[ch], it1 = chunk[ch + 1];
@@ -1111,10 +1188,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
         const int np = m->start[it1] - p0;
         for (int e = threadIdx.x; e < np; e += kThreads) cp_async8(st_sbi + e, sbi + p0 + e);
         cp_async_wait_all();
-        __syncthreads();
+        simt_sync();
         stage_rows_async<!kRows>(np, i3b, st_sbi, gout, G3, m3, st_g, st_g3);
         cp_async_wait_all();
-        __syncthreads();
+        simt_sync();
         if ((dbg & 8) && threadIdx.x == 0 && blockIdx.x == 0) s_tacc[10] += clock64() - _c0;
       }
       // ---- Z / dG3 phase: warp <-> item, lane <-> c
@@ -1156,7 +1233,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
             float dh[4] = {0.f, 0.f, 0.f, 0.f};
             lookup_update(src, x, z, h3, dh);
             __syncwarp();  // the scratch is rewritten by the next row
-            if (!(dbg & 1)) red_v4(dG3 + ((size_t)lane * m3 + i3) * 4, dh[0], dh[1], dh[2], dh[3]);
+            if (!(dbg & 1)) red_v4(dG3 + ((size_t)i3 * 32 + lane) * 4, dh[0], dh[1], dh[2], dh[3]);
             bad |= suspicious(dh[0]) | suspicious(dh[1]) | suspicious(dh[2]) | suspicious(dh[3]);
           }
         } else {
@@ -1168,7 +1245,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
             const float4 h3 = st_g3[qq * 32 + lane];
             float dh[4] = {0.f, 0.f, 0.f, 0.f};
             if (!(dbg & 32)) lookup_update(st_g + qq * 16, x, z, h3, dh);
-            if (!(dbg & 1)) red_v4(dG3 + ((size_t)lane * m3 + i3) * 4, dh[0], dh[1], dh[2], dh[3]);
+            if (!(dbg & 1)) red_v4(dG3 + ((size_t)i3 * 32 + lane) * 4, dh[0], dh[1], dh[2], dh[3]);
             bad |= suspicious(dh[0]) | suspicious(dh[1]) | suspicious(dh[2]) | suspicious(dh[3]);
           }
         }
@@ -1182,7 +1259,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
       }
       {
         const long long _c0 = clock64();
-        __syncthreads();  // staging reused by the next chunk / tile
+        simt_sync();  // staging reused by the next chunk / tile
         if ((dbg & 8) && threadIdx.x == 0 && blockIdx.x == 0) s_tacc[11] += clock64() - _c0;
       }
     }
@@ -1202,35 +1279,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
     umma::tmem_st32(tl + 256 + kSpan * qw, zl);
     umma::tmem_wait_st();
     cp_async_wait_all();  // G2 k / G1^T images (issued before the Z phase)
-    sync_for_mma();       // every slot read before the image overwrites them; Z^T is in TMEM
-    constexpr uint32_t id64 = umma::idesc_tf32(128, 64, false, false);
-    constexpr uint32_t id32 = umma::idesc_tf32(128, 32, false, false);  // B rows 0-31: the hi half
-    const bool acc2 = m->i2 == prev_i2;  // same i2 as the previous tile: keep accumulating dG2 in TMEM
-    if (threadIdx.x == 0) {
-      const long long _c0 = clock64();
-      // dG2 tile [(c, b), (hi | lo) k] = sum_(item, a) (Z^T hi + Z^T lo) . G1^T (A from TMEM);
-      // issued before the Z image is written (only the E GEMM reads it)
-#pragma unroll
-      for (int k0 = 0; k0 < 128; k0 += 8) {
-        const uint32_t o = (uint32_t)((k0 >> 5) * 64 * 128 + (k0 & 31) * 4) >> 4;
-        umma::mma_tf32_ta(tmem + 384, tmem + 128 + k0, d_r2h + o, id64, (acc2 || k0 > 0) ? 1u : 0u);
-        umma::mma_tf32_ta(tmem + 384, tmem + 256 + k0, d_r2h + o, id32, 1u);  // Z lo . G1 hi only
-      }
-      if ((dbg & 8) && blockIdx.x == 0) s_tacc[9] += clock64() - _c0;
-    }
+    if (threadIdx.x == 0) s_acc2 = m->i2 == prev_i2;
+    simt_sync_for_mma();  // every slot read before the image overwrites them; Z^T is in TMEM
+    if (threadIdx.x == 0) umma::mbar_arrive(&s_mb_z);  // -> dG2 MMAs
     // ---- next tile: chunk list and first chunk's positions
     if (tn < te) {
       if (threadIdx.x == 0) make_chunks(mn, s_chunk[slot ^ 1], kCap);
-      __syncthreads();
+      simt_sync();
       npn = mn->start[s_chunk[slot ^ 1][1]] - mn->start[0];
       for (int e = threadIdx.x; e < npn; e += kThreads) cp_async8(st_sbi + e, sbi + mn->start[0] + e);
       cp_async_commit();
     }
-    // Z image hi (the slots' region) and lo (the dead staging rows, past the
-    // next tile's positions): both E passes back to back
-    // (bag-run path: exactly the G3-slice staging, so the next tile's gradient
-    // rows can stream in while the E GEMM runs)
-    char* zlo = sm + 8 * kImg + (kRows ? 4096 : kChunkPos * 8 + kChunkPos * 256);
+    // Z image hi (the slots' region) and lo (the dead staging rows) for the E GEMM
 #pragma unroll
     for (int i = 0; i < kSpan; ++i) {
       const uint32_t o = umma::sw128_off(kSpan * qw + i, row, 128);
@@ -1238,46 +1298,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
       *(float*)(zlo + o) = zl[i];
     }
     cp_async_wait_all();  // next tile's positions
-    sync_for_mma();
+    simt_sync_for_mma();
+    if (threadIdx.x == 0) umma::mbar_arrive(&s_mb_zi);  // -> E MMAs
     TSTAMP(5);
-    if (threadIdx.x == 0) {
-      // E tile [(item, a), (hi | lo) k] = sum_(c, b) (Z hi . G2^T + Z lo . G2 hi^T)
-      const uint64_t d_zl = umma::desc_sw128(umma::smem_u32(zlo));
-#pragma unroll
-      for (int k0 = 0; k0 < 128; k0 += 8) {
-        const uint32_t oa = (uint32_t)((k0 >> 5) * 128 * 128 + (k0 & 31) * 4) >> 4;
-        const uint32_t ob = (uint32_t)((k0 >> 5) * 64 * 128 + (k0 & 31) * 4) >> 4;
-        umma::mma_tf32(tmem + 448, d_zi + oa, d_r1h + ob, id64, k0 > 0 ? 1u : 0u);
-      }
-#pragma unroll
-      for (int k0 = 0; k0 < 128; k0 += 8) {
-        const uint32_t oa = (uint32_t)((k0 >> 5) * 128 * 128 + (k0 & 31) * 4) >> 4;
-        const uint32_t ob = (uint32_t)((k0 >> 5) * 64 * 128 + (k0 & 31) * 4) >> 4;
-        umma::mma_tf32(tmem + 448, d_zl + oa, d_r1h + ob, id32, 1u);  // Z lo . G2 hi only
-      }
-      umma::commit(&s_mbar);
-    }
     if (!kRows && tn < te)  // the next tile's first-chunk gradient rows
       for (int e = threadIdx.x; e < npn * 16; e += kThreads)
         cp_async16(st_g + e, gout + (size_t)st_sbi[e >> 4].x * NOUT + 4 * (e & 15));
-    umma::mbar_wait(&s_mbar, phase);
-    phase ^= 1u;
+    umma::mbar_wait(&s_mb_e, phase);  // dG2 and E of tile t
     umma::fence_after_sync();
     TSTAMP(6);
-    TSTAMP(7);
     // the next tile's X operands (R12 is free now), then its first-chunk rows
-    // (the staging region is free once the E GEMM has read the Z lo image)
+    // (the staging region is free once the E GEMM has read the Z lo image);
+    // the MMA warp starts the next X GEMM while the reductions below run
     if (tn < te) {
       copy_img_async(r1_hi, img + (size_t)mn->i2 * kImg, 2 * kImg);
       stage_g1_rows_async(mn, g, g1img, r2_hi, r2_lo);
-      if (kRows) {
-        stage_rows_async<false>(npn, tile_i3_base(mn, g), st_sbi, gout, G3, m3, st_g, st_g3);
-      } else {  // the G3 slices (their region held the Z lo image)
-        for (int e = threadIdx.x; e < npn * 32; e += kThreads)
-          cp_async16(st_g3 + e, reinterpret_cast<const float4*>(G3) + (size_t)(e & 31) * m3 + tile_i3_base(mn, g) +
-                                    st_sbi[e >> 5].y);
-      }
+      cp_async_commit();
     }
+    TSTAMP(7);
     if (!(dbg & 4)) {
       float v[kRedCols], w2[kRedCols];
       // dG2[k][i2][b][c] = D[:, k] + D[:, 32 + k], once per run of tiles of one i2
@@ -1306,17 +1344,33 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(KGeom g, const float* __res
         }
       }
     }
+    if (tn < te) {  // next X operands landed: the MMA warp starts the next X GEMM
+      cp_async_wait_all();
+      simt_sync_for_mma();
+      if (threadIdx.x == 0) umma::mbar_arrive(&s_mb_xop);
+      if (kRows) {
+        stage_rows_async<false>(npn, tile_i3_base(mn, g), st_sbi, gout, G3, m3, st_g, st_g3);
+      } else {  // the G3 slices (their region held the Z lo image)
+        for (int e = threadIdx.x; e < npn * 32; e += kThreads)
+          cp_async16(st_g3 + e, reinterpret_cast<const float4*>(G3) + (size_t)(e & 31) * m3 + tile_i3_base(mn, g) +
+                                    st_sbi[e >> 5].y);
+      }
+    }
     TSTAMP(8);
     prev_i2 = m->i2;
+    // TMEM reads done before the next dG2 / E MMAs (issued after the next
+    // tile's barriers); slots free for the next dump (the E GEMM is done)
     umma::fence_before_sync();
-    __syncthreads();
-    umma::fence_after_sync();
   }
   if (bad) hdr[kHdrSuspect] = 1;
   if ((dbg & 8) && threadIdx.x == 0 && blockIdx.x == 0) {
     s_tacc[0] = te - tb;
     for (int q = 0; q < 12; ++q) reinterpret_cast<long long*>(hdr + 16)[q] = s_tacc[q];
   }
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
   if (warp == 0) umma::tmem_free(tmem, 512);
 }
 
@@ -1499,16 +1553,20 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
   } else {
     if ((e = cudaMemsetAsync(g0, 0, sizeof(float) * (size_t)n0, s))) return e;
     if ((e = cudaMemsetAsync(g1, 0, sizeof(float) * (size_t)n1, s))) return e;
-    if ((e = cudaMemsetAsync(g2, 0, sizeof(float) * (size_t)n2, s))) return e;
+    if ((e = cudaMemsetAsync(w.f_grad + n0 + n1, 0, sizeof(float) * (size_t)n2, s))) return e;
   }
+  // dG3 accumulates slice-major, (i3, c, n3): one lookup's 128 contributions
+  // are 512 contiguous bytes (4 L2 lines instead of 32); the update kernel
+  // reads it in that order, the caller's buffer gets the reference layout
+  float* g3s = w.f_grad + n0 + n1;
   const int grid = h->num_sms;  // = the plan's CTA ranges (k_fplan cta_tiles)
   {
     ProfScope _ps(h, s, "f_bwd");
     // pooled bags (more lookups than bags) repeat rows inside a prefix: group
     // by row; otherwise (T = B, bags are single lookups) position by position
-    if ((e = launch_pdl(h->T > h->B ? k_bwd<true> : k_bwd<false>, dim3(grid), dim3(kThreads), kBwdSmem, s, h->kg, (const float*)w.f_g1img, c2,
+    if ((e = launch_pdl(h->T > h->B ? k_bwd<true> : k_bwd<false>, dim3(grid), dim3(kBwdThreads), kBwdSmem, s, h->kg, (const float*)w.f_g1img, c2,
                         (const float*)w.f_img, (const int4*)w.f_tile_info, (const int*)w.f_item_start,
-                        (const unsigned*)w.f_item_key, (const int2*)w.f_sbi, gout, g0, g1, g2, w.fast_hdr,
+                        (const unsigned*)w.f_item_key, (const int2*)w.f_sbi, gout, g0, g1, g3s, w.fast_hdr,
                         (const int*)w.f_cta, getenv("TTB_DBG") ? atoi(getenv("TTB_DBG")) : 0)))
       return e;
   }
@@ -1536,6 +1594,12 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
     // the caller's gradients: a suspect contribution (see kHdrSuspect) gets
     // the exact scan, which latches TTB_ERRBIT_NONFINITE (tt_core_grads
     // rejects non-finite gradients, backward.py:119-128)
+    {
+      const unsigned m3 = h->kg.m3;
+      if ((e = launch_pdl(k_g3_unslice, dim3((128 * m3 + 255) / 256), dim3(256), 0, s, (const float*)g3s, g2, m3)))
+        return e;
+      count_launch();
+    }
     ProfScope _pc(h, s, "f_gradcheck");
     if ((e = launch_gradcheck(g0, n0, w.fast_hdr, h->num_sms, s, w.fast_hdr + kHdrSuspect))) return e;
     if ((e = launch_gradcheck(g1, n1, w.fast_hdr, h->num_sms, s, w.fast_hdr + kHdrSuspect))) return e;
