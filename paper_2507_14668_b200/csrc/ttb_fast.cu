@@ -1169,6 +1169,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
         xs[xs_idx(col >> 2, col & 3, b, c)] = __uint_as_float(v0[i]);
       }
     }
+    cp_async_wait_all();  // chunk 0's positions, gradient rows and G3 slices (staged by the previous tile)
     // the second GEMM pair's operands stream in during the Z phase
     copy_img_async(r1_hi, gimg + 2 * kImg / 4, 2 * kImg);
     stage_g1_t_async(m, g, g1img, r2_hi);
