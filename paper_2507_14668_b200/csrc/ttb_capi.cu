@@ -182,7 +182,8 @@ void layout(ttb_handle& h, char* base) {
   w.f_cta = c.take<int>(fz ? 1025 : 0);
   w.f_gtot = c.take<int4>(fz ? fg : 0);
   w.f_tile_info = c.take<int4>(fz ? T / 32 + fg + 2 : 0);
-  w.f_g1img = c.take<float>(fz ? (size_t)fg1 * 512 : 0);
+  w.f_g1img = c.take<float>(fz ? (size_t)fg1 * 768 : 0);
+  w.f_g3t = c.take<float>(fz ? (size_t)G3S * fg3 : 0);
   w.f_img = c.take<float>(fz ? (size_t)fg * 16384 : 0);
   w.f_grad = c.take<float>(fz ? (size_t)(G1S * fg1 + G2S * fg + G3S * fg3) : 0);
   w.f_rowbits = c.take<unsigned>(fz && !h.batched ? (size_t)(g.m[0] * g.m[1] * g.m[2] / 32 + 1) : 0);

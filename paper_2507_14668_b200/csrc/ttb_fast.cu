@@ -371,6 +371,7 @@ struct SgdArgs {
   int mask, on;
   const int* err;     // device error word: any bit set -> no update (cores untouched)
   int adagrad;        // 0: SGD(+momentum), v = velocity; 1: Adagrad, v = squared-gradient sums
+  float* g3t;         // G3 written slice-major (i3, c, n3) after the update (step kernels' bulk copies)
 };
 
 // Finiteness pre-pass over the final gradients (fused_update rejects a
@@ -421,15 +422,16 @@ __global__ void __launch_bounds__(kImgThreads) k_coreimg(float* __restrict__ G1,
   if (u.on && u.err && *(volatile const int*)u.err != 0) u.on = 0;
   const size_t n0 = (size_t)g.g1rows * 4 * R1, n1 = (size_t)R1 * g.m2 * C;
   const unsigned nb12 = g.m2 + (g.g1rows + 3) / 4;
-  if (blockIdx.x >= nb12) {  // G3: update only
+  if (blockIdx.x >= nb12) {  // G3: update, and its slice-major copy
     const size_t n2 = (size_t)32 * g.m3 * 4;
     for (size_t j = (size_t)(blockIdx.x - nb12) * kImgThreads + threadIdx.x; j < n2;
          j += (size_t)(gridDim.x - nb12) * kImgThreads) {
       const float v = u.p2[j];
-      // the backward accumulates dG3 slice-major: (i3, c, n3) (see k_bwd)
-      const size_t c = j / ((size_t)g.m3 * 4), r = j - c * g.m3 * 4;
-      const float w = maybe_sgd(v, u, 2, n0 + n1 + ((r >> 2) * 32 + c) * 4 + (r & 3), j, u.v2);
-      if (u.mask & 4) u.p2[j] = w;
+      // the backward accumulates dG3 slice-major, (i3, c, n3), as the copy
+      const size_t c = j / ((size_t)g.m3 * 4), r = j - c * g.m3 * 4, jt = ((r >> 2) * 32 + c) * 4 + (r & 3);
+      const float w = maybe_sgd(v, u, 2, n0 + n1 + jt, j, u.v2);
+      if (u.on && (u.mask & 4)) u.p2[j] = w;
+      u.g3t[jt] = w;
     }
     return;
   }
@@ -446,10 +448,14 @@ __global__ void __launch_bounds__(kImgThreads) k_coreimg(float* __restrict__ G1,
       float hi, lo;
       umma::split3(v, hi, lo);
       float* d = g1img + (size_t)i1 * kG1Img;
-      d[e] = hi;
-      d[128 + e] = lo;
-      d[256 + k * 4 + a] = hi;
-      d[384 + k * 4 + a] = lo;
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {  // row a at smem line 4 p + a: 16-byte chunk k / 4 -> (k / 4) ^ (4 p + a)
+        const int o = g1_rows_off(p) + a * 32 + ((((k >> 2) ^ (4 * p + a)) & 7) << 2) + (k & 3);
+        d[o] = hi;
+        d[128 + o] = lo;
+      }
+      d[kG1T + k * 4 + a] = hi;
+      d[kG1T + 128 + k * 4 + a] = lo;
     }
     return;
   }
@@ -528,21 +534,6 @@ __device__ inline void mma3_ss(uint32_t d, uint32_t a_hi, uint32_t a_lo, int a_r
 // last warp fetches tile t + grid's (cp.async) and the tile table entry of
 // t + 2 grid (a register load, consumed an iteration later).
 
-// G1 rows image of the tile's items (rows (item, a), K = k) from the split G1 images
-__device__ inline void stage_g1_rows_async(const TileMeta* m, KGeom g, const float* __restrict__ g1img, char* hi,
-                                           char* lo) {
-#pragma unroll
-  for (int i = 0; i < 1024 / kThreads; ++i) {
-    const int e = threadIdx.x + i * kThreads, ia = e >> 3, kq = e & 7, it = ia >> 2, a = ia & 3;
-    if (it < m->n) {
-      const float* src = g1img + (size_t)item_i1(m, it, g) * kG1Img + a * 32 + 4 * kq;
-      const uint32_t o = umma::sw128_off(ia, 4 * kq, 128);
-      cp_async16(hi + o, src);
-      cp_async16(lo + o, src + 128);
-    }
-  }
-}
-
 // G1^T image of the tile's items (rows k, K = (item, a)); zero columns past n
 // (one 64-row image: rows k = hi, rows 32 + k = lo)
 __device__ inline void stage_g1_t_async(const TileMeta* m, KGeom g, const float* __restrict__ g1img, char* img) {
@@ -551,7 +542,7 @@ __device__ inline void stage_g1_t_async(const TileMeta* m, KGeom g, const float*
     const int e = threadIdx.x + i * kThreads, it = e >> 5, k = e & 31;
     const uint32_t oh = umma::sw128_off(k, 4 * it, 64), ol = umma::sw128_off(32 + k, 4 * it, 64);
     if (it < m->n) {
-      const float* src = g1img + (size_t)item_i1(m, it, g) * kG1Img + 256 + 4 * k;
+      const float* src = g1img + (size_t)item_i1(m, it, g) * kG1Img + kG1T + 4 * k;
       cp_async16(img + oh, src);
       cp_async16(img + ol, src + 128);
     } else {
@@ -648,13 +639,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
       last_i2 = mu->i2;
     }
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {  // the items' G1 rows (hi, lo)
-      const int e = threadIdx.x + i * kFwdThreads, ia = e >> 3, kq = e & 7, iu = ia >> 2, au = ia & 3;
+    for (int i = 0; i < 2; ++i) {  // the items' G1 rows (hi, lo): 512 pre-swizzled bytes per item
+      const int e = threadIdx.x + i * kFwdThreads, iu = e >> 5, q = e & 31;
       if (iu < mu->n) {
-        const float* src = g1img + (size_t)item_i1(mu, iu, g) * kG1Img + au * 32 + 4 * kq;
-        const uint32_t o = umma::sw128_off(ia, 4 * kq, 128);
-        cp_async16(a_hi + o, src);
-        cp_async16(a_lo + o, src + 128);
+        const float* src = g1img + (size_t)item_i1(mu, iu, g) * kG1Img + g1_rows_off(iu & 1) + 4 * q;
+        cp_async16(a_hi + iu * 512 + 16 * q, src);
+        cp_async16(a_lo + iu * 512 + 16 * q, src + 128);
       }
     }
     if (warp == 15 && u + 1 < te) {
@@ -958,19 +948,6 @@ __device__ inline void make_chunks(const TileMeta* m, int* ch, int cap, int roun
   ch[kTileItems + 1] = nc;
 }
 
-template <bool kG3>
-__device__ inline void stage_rows_async(int np, unsigned i3b, const int2* st_sbi, const float* __restrict__ gout,
-                                        const float* __restrict__ G3, unsigned m3, float4* st_g, float4* st_g3) {
-  for (int e = threadIdx.x; e < np * 16; e += kThreads) {
-    const int p = e >> 4, k = e & 15;
-    cp_async16(st_g + e, gout + (size_t)st_sbi[p].x * NOUT + 4 * k);
-  }
-  if (kG3)
-  for (int e = threadIdx.x; e < np * 32; e += kThreads) {
-    const int p = e >> 5, cc = e & 31;
-    cp_async16(st_g3 + e, reinterpret_cast<const float4*>(G3) + (size_t)cc * m3 + i3b + st_sbi[p].y);
-  }
-}
 
 // one gradient row g (16 float4, (a, b) major) against the item's X^T column
 // x[(a, b)] (lane c): dH[c, :] = sum_ab x[ab] g[ab, :] and Z[ab, c] += g[ab, :] . h3
@@ -1006,7 +983,7 @@ __device__ __forceinline__ void simt_sync_for_mma() {
 
 template <bool kRows>
 __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __restrict__ g1img,
-                                                        const float* __restrict__ G3, const float* __restrict__ img,
+                                                        const float* __restrict__ g3t, const float* __restrict__ img,
                                                         const int4* __restrict__ tile_info,
                                                         const int* __restrict__ item_start,
                                                         const unsigned* __restrict__ item_key,
@@ -1034,20 +1011,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
   char* zlo = sm + 8 * kImg + (kRows ? 4096 : kChunkPos * 8 + kChunkPos * 256);
   __shared__ TileMeta s_m[2];
   __shared__ int s_chunk[2][kTileItems + 2];
-  // SIMT -> MMA warp: X operands staged / Z^T in TMEM + E operands staged /
-  // Z images written; MMA warp -> SIMT: X done / dG2 + E done
-  __shared__ uint64_t s_mb_xop, s_mb_z, s_mb_zi, s_mb_x, s_mb_e;
+  // SIMT -> MMA warp: G1 rows staged / Z^T in TMEM + G1^T staged / Z images
+  // written; MMA warp -> SIMT: X done / dG2 + E done; bulk copies of the G2
+  // cb / k images (issued and waited for by the MMA warp)
+  __shared__ uint64_t s_mb_xop, s_mb_z, s_mb_zi, s_mb_x, s_mb_e, s_mb_xtma, s_mb_ktma;
   __shared__ int s_acc2;
   __shared__ long long s_tacc[12];
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tb = cta_tiles[blockIdx.x], te = cta_tiles[blockIdx.x + 1];  // weight-balanced (k_fplan)
-  const unsigned m3 = g.m3;
   if (threadIdx.x < 12) s_tacc[threadIdx.x] = 0;
   if (warp == 0) umma::tmem_alloc(&s_tmem, 512);
   if (threadIdx.x == 32) {
     umma::mbar_init(&s_mb_xop, 1);
     umma::mbar_init(&s_mb_z, 1);
+    umma::mbar_init(&s_mb_xtma, 1);
+    umma::mbar_init(&s_mb_ktma, 1);
     umma::mbar_init(&s_mb_zi, 1);
     umma::mbar_init(&s_mb_x, 1);
     umma::mbar_init(&s_mb_e, 1);
@@ -1069,10 +1048,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
   const uint64_t d_zi = umma::desc_sw128(umma::smem_u32(zi)), d_zl = umma::desc_sw128(umma::smem_u32(zlo));
 
   if (warp == kThreads / 32) {
-    // ---------------- MMA warp
+    // ---------------- MMA warp: also the bulk-copy producer of the G2 images
+    // (one 32 KB copy each: the cb image (hi, lo) for X, the k image for E)
+    auto load_cb = [&](const TileMeta* mt) {
+      if (lane == 0) {
+        umma::mbar_expect_tx(&s_mb_xtma, 2 * kImg);
+        umma::bulk_g2s(r1_hi, img + (size_t)mt->i2 * kImg, 2 * kImg, &s_mb_xtma);
+      }
+      __syncwarp();
+    };
     uint32_t ph = 0;
+    if (tb < te) load_cb(&s_m[0]);
     for (int t = tb; t < te; ++t, ph ^= 1u) {
-      umma::mbar_wait(&s_mb_xop, ph);  // X operands of tile t in R12
+      const TileMeta* mt = &s_m[(t - tb) & 1];
+      umma::mbar_wait(&s_mb_xtma, ph);  // the G2 cb image of tile t
+      umma::mbar_wait(&s_mb_xop, ph);   // its items' G1 rows (SIMT cp.async)
       umma::fence_after_sync();
       if (lane == 0) {
         constexpr uint32_t id = umma::idesc_tf32(128, 128, false, false);
@@ -1086,7 +1076,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
         umma::commit(&s_mb_x);
       }
       __syncwarp();
-      umma::mbar_wait(&s_mb_z, ph);  // Z^T hi / lo in TMEM, G2 k / G1^T images in R12
+      umma::mbar_wait(&s_mb_x, ph);  // X read its operands: the G2 k image replaces the cb image
+      if (lane == 0) {
+        umma::mbar_expect_tx(&s_mb_ktma, 2 * kImg);
+        umma::bulk_g2s(r1_hi, img + (size_t)mt->i2 * kImg + 2 * kImg / 4, 2 * kImg, &s_mb_ktma);
+      }
+      __syncwarp();
+      umma::mbar_wait(&s_mb_z, ph);  // Z^T hi / lo in TMEM, G1^T image in R12
+      umma::mbar_wait(&s_mb_ktma, ph);
       umma::fence_after_sync();
       if (lane == 0) {
         constexpr uint32_t id64 = umma::idesc_tf32(128, 64, false, false);
@@ -1122,9 +1119,34 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
         umma::commit(&s_mb_e);  // tracks the dG2 MMAs too
       }
       __syncwarp();
+      if (t + 1 < te) {  // R12 free once E is done: the next tile's cb image
+        umma::mbar_wait(&s_mb_e, ph);
+        load_cb(&s_m[(t + 1 - tb) & 1]);  // (its metadata: visible since the Z signal)
+      }
     }
   } else {
   // ---------------- SIMT warps
+  // a chunk's per-position rows (cp.async): the bag's gradient row and, one
+  // lookup per bag, the lookup's slice-major G3 slice (512 contiguous bytes)
+  auto stage_rows = [&](int np, unsigned i3base) {
+    for (int e = threadIdx.x; e < np * 16; e += kThreads)
+      cp_async16(st_g + e, gout + (size_t)st_sbi[e >> 4].x * NOUT + 4 * (e & 15));
+    if (!kRows)
+      for (int e = threadIdx.x; e < np * 32; e += kThreads)
+        cp_async16(st_g3 + e, g3t + (size_t)(i3base + st_sbi[e >> 5].y) * 128 + 4 * (e & 31));
+  };
+  // the items' pre-swizzled G1 rows (hi, lo): 512 contiguous bytes per item
+  auto stage_g1_rows = [&](const TileMeta* mt) {
+#pragma unroll
+    for (int i = 0; i < 1024 / kThreads; ++i) {
+      const int e = threadIdx.x + i * kThreads, it = e >> 5, q = e & 31;
+      if (it < mt->n) {
+        const float* src = g1img + (size_t)item_i1(mt, it, g) * kG1Img + g1_rows_off(it & 1) + 4 * q;
+        cp_async16(r2_hi + 512 * it + 16 * q, src);
+        cp_async16(r2_lo + 512 * it + 16 * q, src + 128);
+      }
+    }
+  };
   const int q4 = warp & 3, qw = warp >> 2;  // lane quadrant, and this warp's share of its columns
   const int row = 32 * q4 + lane;  // TMEM lane of this thread: (c, b) = (row / 4, row % 4)
   const int c = row >> 2, b = row & 3;
@@ -1136,12 +1158,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
     simt_sync();
     const int np = m->start[s_chunk[0][1]] - m->start[0];
     for (int e = threadIdx.x; e < np; e += kThreads) cp_async8(st_sbi + e, sbi + m->start[0] + e);
-    copy_img_async(r1_hi, img + (size_t)m->i2 * kImg, 2 * kImg);
-    stage_g1_rows_async(m, g, g1img, r2_hi, r2_lo);
+    stage_g1_rows(m);
     cp_async_wait_all();
     simt_sync_for_mma();
     if (threadIdx.x == 0) umma::mbar_arrive(&s_mb_xop);  // X of the first tile
-    stage_rows_async<!kRows>(np, tile_i3_base(m, g), st_sbi, gout, G3, m3, st_g, st_g3);
+    stage_rows(np, tile_i3_base(m, g));
   }
   uint32_t phase = 0;
   bool bad = false;
@@ -1151,7 +1172,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
     const TileMeta* m = &s_m[slot];
     const int* chunk = s_chunk[slot];
     const int n = m->n, nchunk = chunk[kTileItems + 1];
-    const float* gimg = img + (size_t)m->i2 * kImg;  // kImg floats = 4 images of kImg bytes
     const unsigned i3b = tile_i3_base(m, g);          // the tile's table's G3 slices (batched handles)
     TSTAMP(0);
     TSTAMP(1);
@@ -1169,9 +1189,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
         xs[xs_idx(col >> 2, col & 3, b, c)] = __uint_as_float(v0[i]);
       }
     }
-    cp_async_wait_all();  // chunk 0's positions, gradient rows and G3 slices (staged by the previous tile)
-    // the second GEMM pair's operands stream in during the Z phase
-    copy_img_async(r1_hi, gimg + 2 * kImg / 4, 2 * kImg);
+    cp_async_wait_all();  // chunk 0's gradient rows and G3 slices (staged by the previous tile)
+    // the dG2 GEMM's G1^T image streams in during the Z phase (the MMA warp
+    // loads the G2 k image)
     stage_g1_t_async(m, g, g1img, r2_hi);
     cp_async_commit();
     umma::fence_before_sync();
@@ -1190,7 +1210,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
         for (int e = threadIdx.x; e < np; e += kThreads) cp_async8(st_sbi + e, sbi + p0 + e);
         cp_async_wait_all();
         simt_sync();
-        stage_rows_async<!kRows>(np, i3b, st_sbi, gout, G3, m3, st_g, st_g3);
+        stage_rows(np, i3b);
         cp_async_wait_all();
         simt_sync();
         if ((dbg & 8) && threadIdx.x == 0 && blockIdx.x == 0) s_tacc[10] += clock64() - _c0;
@@ -1216,7 +1236,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
             lead &= lead - 1;
             unsigned mem = __shfl_sync(0xffffffffu, grp, ld);
             const int i3 = __shfl_sync(0xffffffffu, my_i3, ld);
-            const float4 h3 = __ldg(reinterpret_cast<const float4*>(G3) + (size_t)lane * m3 + i3);
+            const float4 h3 = __ldg(reinterpret_cast<const float4*>(g3t) + (size_t)i3 * 32 + lane);
             // the row's summed gradient row: lane-parallel (two floats per
             // lane per member) into the warp's scratch, then broadcast reads
             const float4* src = st_g + (s0 + ld) * 16;
@@ -1302,18 +1322,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
     simt_sync_for_mma();
     if (threadIdx.x == 0) umma::mbar_arrive(&s_mb_zi);  // -> E MMAs
     TSTAMP(5);
-    if (!kRows && tn < te)  // the next tile's first-chunk gradient rows
-      for (int e = threadIdx.x; e < npn * 16; e += kThreads)
-        cp_async16(st_g + e, gout + (size_t)st_sbi[e >> 4].x * NOUT + 4 * (e & 15));
     umma::mbar_wait(&s_mb_e, phase);  // dG2 and E of tile t
     umma::fence_after_sync();
     TSTAMP(6);
-    // the next tile's X operands (R12 is free now), then its first-chunk rows
-    // (the staging region is free once the E GEMM has read the Z lo image);
-    // the MMA warp starts the next X GEMM while the reductions below run
+    // the next tile's G1 rows (R12 is free now) and first-chunk rows (the
+    // staging region held the Z lo image)
     if (tn < te) {
-      copy_img_async(r1_hi, img + (size_t)mn->i2 * kImg, 2 * kImg);
-      stage_g1_rows_async(mn, g, g1img, r2_hi, r2_lo);
+      stage_g1_rows(mn);
+      cp_async_commit();
+      stage_rows(npn, tile_i3_base(mn, g));
       cp_async_commit();
     }
     TSTAMP(7);
@@ -1345,17 +1362,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
         }
       }
     }
-    if (tn < te) {  // next X operands landed: the MMA warp starts the next X GEMM
-      cp_async_wait_all();
+    if (tn < te) {  // the next G1 rows landed: with the cb image, the MMA warp starts the next X GEMM
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
       simt_sync_for_mma();
       if (threadIdx.x == 0) umma::mbar_arrive(&s_mb_xop);
-      if (kRows) {
-        stage_rows_async<false>(npn, tile_i3_base(mn, g), st_sbi, gout, G3, m3, st_g, st_g3);
-      } else {  // the G3 slices (their region held the Z lo image)
-        for (int e = threadIdx.x; e < npn * 32; e += kThreads)
-          cp_async16(st_g3 + e, reinterpret_cast<const float4*>(G3) + (size_t)(e & 31) * m3 + tile_i3_base(mn, g) +
-                                    st_sbi[e >> 5].y);
-      }
     }
     TSTAMP(8);
     prev_i2 = m->i2;
@@ -1508,18 +1518,23 @@ cudaError_t fast_forward(ttb_handle* h, const float* c0, const float* c1, const 
   if ((e = ensure_kernel_smem((const void*)k_fwd<true>, fwd_smem_bytes(kFwdMaxM3)))) return e;
   if ((e = ensure_kernel_smem((const void*)k_bwd<false>, kBwdSmem))) return e;
   if ((e = ensure_kernel_smem((const void*)k_bwd<true>, kBwdSmem))) return e;
-  if (!(h->img_valid && h->img_c0 == c0 && h->img_c1 == c1)) {
+  if (!(h->img_valid && h->img_c0 == c0 && h->img_c1 == c1 && h->img_c2 == c2)) {
     // split tf32 images of the cores (skipped while the images written by the
     // last fused update, or the last forward, still describe these cores)
     ProfScope _ps(h, s, "f_coreimg");
     SgdArgs u = {};
-    if ((e = launch_pdl(k_coreimg, dim3(h->kg.m2 + (h->kg.g1rows + 3) / 4), dim3(kImgThreads), img_smem, s,
-                        const_cast<float*>(c0), const_cast<float*>(c1), h->kg, w.f_img, w.f_g1img, u)))
+    u.p2 = const_cast<float*>(c2);
+    u.g3t = w.f_g3t;
+    const int ng3 = (int)(((int64_t)128 * h->kg.m3 + kImgThreads - 1) / kImgThreads);
+    if ((e = launch_pdl(k_coreimg, dim3(h->kg.m2 + (h->kg.g1rows + 3) / 4 + (ng3 < 64 ? ng3 : 64)),
+                        dim3(kImgThreads), img_smem, s, const_cast<float*>(c0), const_cast<float*>(c1), h->kg,
+                        w.f_img, w.f_g1img, u)))
       return e;
     count_launch();
     h->img_valid = 1;
     h->img_c0 = c0;
     h->img_c1 = c1;
+    h->img_c2 = c2;
   }
   // one store per lookup into its bag's row; with empty bags allowed, T = B
   // no longer means one lookup per bag (and empty rows must read zero)
@@ -1565,7 +1580,7 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
     ProfScope _ps(h, s, "f_bwd");
     // pooled bags (more lookups than bags) repeat rows inside a prefix: group
     // by row; otherwise (T = B, bags are single lookups) position by position
-    if ((e = launch_pdl(h->T > h->B ? k_bwd<true> : k_bwd<false>, dim3(grid), dim3(kBwdThreads), kBwdSmem, s, h->kg, (const float*)w.f_g1img, c2,
+    if ((e = launch_pdl(h->T > h->B ? k_bwd<true> : k_bwd<false>, dim3(grid), dim3(kBwdThreads), kBwdSmem, s, h->kg, (const float*)w.f_g1img, (const float*)w.f_g3t,
                         (const float*)w.f_img, (const int4*)w.f_tile_info, (const int*)w.f_item_start,
                         (const unsigned*)w.f_item_key, (const int2*)w.f_sbi, gout, g0, g1, g3s, w.fast_hdr,
                         (const int*)w.f_cta, getenv("TTB_DBG") ? atoi(getenv("TTB_DBG")) : 0)))
@@ -1582,7 +1597,7 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
       if ((e = launch_gradcheck(w.f_grad, n0 + n1 + n2, w.fast_hdr, h->num_sms, s, w.fast_hdr + kHdrSuspect)))
         return e;
     }
-    SgdArgs u = {w.f_grad, v0, v1, v2, p2, lr, mu, mask, 1, w.fast_hdr, adagrad};
+    SgdArgs u = {w.f_grad, v0, v1, v2, p2, lr, mu, mask, 1, w.fast_hdr, adagrad, w.f_g3t};
     ProfScope _ps(h, s, "f_sgd");
     if ((e = launch_pdl(k_coreimg, dim3(h->kg.m2 + (h->kg.g1rows + 3) / 4 + (ng3 < 64 ? ng3 : 64)), dim3(kImgThreads),
                         img_smem, s, p0, p1, h->kg, w.f_img, w.f_g1img, u)))
@@ -1591,6 +1606,7 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
     h->img_valid = 1;
     h->img_c0 = p0;
     h->img_c1 = p1;
+    h->img_c2 = p2;
   } else {
     // the caller's gradients: a suspect contribution (see kHdrSuspect) gets
     // the exact scan, which latches TTB_ERRBIT_NONFINITE (tt_core_grads

@@ -95,9 +95,13 @@ __device__ __forceinline__ unsigned tile_i3_base(const TileMeta* m, KGeom g) {
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-// per-i1 G1 images written by the update kernel: rows_hi[a][k], rows_lo[a][k],
-// t_hi[k][a], t_lo[k][a]
-constexpr int kG1Img = 512;
+// per-i1 G1 images written by the update kernel (floats): for item parity
+// p = 0, 1 the rows image [256 p: hi, 256 p + 128: lo], rows a = 0..3 already
+// SWIZZLE_128B-permuted for smem lines 4 p + a (an item's 512 bytes of the
+// tile's rows image are one bulk copy); then t_hi[k][a] (512), t_lo[k][a] (640)
+constexpr int kG1Img = 768;
+constexpr int kG1T = 512;
+__host__ __device__ constexpr int g1_rows_off(int parity) { return 256 * parity; }
 
 }  // namespace fast
 }  // namespace ttb

@@ -85,7 +85,8 @@ struct Workspace {
   int* f_cta;             // kMaxCtas + 1: first tile of each step-kernel CTA
   int4* f_gtot;           // m2: (positions, items, prefixes) per i2 group
   int4* f_tile_info;      // tiles (<= T / 32 + m2): (i2, first item, items)
-  float* f_g1img;         // m1 x 512: split G1 rows / transposed images
+  float* f_g1img;         // m1 x 768: split G1 row images (pre-swizzled, both parities) / transposed images
+  float* f_g3t;           // G3 slice-major (i3, c, n3): one slice = 512 contiguous bytes (bulk copies)
   float* f_img;           // m2 x 4 x 16 KB: G2 slice images (cb hi/lo, k hi/lo)
   float* f_grad;          // |G1| + |G2| + |G3|: gradients for the fused update
   unsigned* f_rowbits;    // rows / 32 + 1: row bitmap of the on-demand U count
@@ -150,6 +151,7 @@ struct ttb_handle {
   int img_valid;
   const float* img_c0;
   const float* img_c1;
+  const float* img_c2;
   ttb::Profiler prof;
 };
 
