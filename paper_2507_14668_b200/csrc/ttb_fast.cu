@@ -372,6 +372,8 @@ struct SgdArgs {
   const int* err;     // device error word: any bit set -> no update (cores untouched)
   int adagrad;        // 0: SGD(+momentum), v = velocity; 1: Adagrad, v = squared-gradient sums
   float* g3t;         // G3 written slice-major (i3, c, n3) after the update (step kernels' bulk copies)
+  const int* suspect;  // backward's kHdrSuspect word: set -> exact finiteness scan before updating
+  int64_t ngrad;       // |G1| + |G2| + |G3| (the scan's extent)
 };
 
 // Finiteness pre-pass over the final gradients (fused_update rejects a
@@ -419,7 +421,29 @@ __global__ void __launch_bounds__(kImgThreads) k_coreimg(float* __restrict__ G1,
   // an error latched by the plan or the backward (range, empty bag,
   // non-finite gradient) cancels the update: the images are rebuilt from the
   // unchanged cores and velocities
-  if (u.on && u.err && *(volatile const int*)u.err != 0) u.on = 0;
+  __shared__ int s_gate;  // one read of the words per CTA: every thread takes the same branch
+  if (threadIdx.x == 0)
+    s_gate = !(u.on && u.err) ? 0
+             : *(volatile const int*)u.err != 0 ? 1
+             : (u.suspect && *(volatile const int*)u.suspect != 0) ? 2 : 0;
+  __syncthreads();
+  {
+    const int gate = s_gate;
+    if (gate == 1) {
+      u.on = 0;
+    } else if (gate == 2) {
+      // rare: the backward saw a contribution that is non-finite or >= 2^95.
+      // Every CTA scans every gradient, so all reach the same all-or-nothing
+      // decision without a grid-wide barrier (fused_update rejects a
+      // non-finite gradient before touching any core, backward.py:190-194)
+      bool bad = false;
+      for (int64_t i = threadIdx.x; i < u.ngrad; i += blockDim.x) bad |= !isfinite(u.grad[i]);
+      if (__syncthreads_or(bad)) {
+        if (threadIdx.x == 0) atomicOr(const_cast<int*>(u.err), TTB_ERRBIT_NONFINITE);
+        u.on = 0;
+      }
+    }
+  }
   const size_t n0 = (size_t)g.g1rows * 4 * R1, n1 = (size_t)R1 * g.m2 * C;
   const unsigned nb12 = g.m2 + (g.g1rows + 3) / 4;
   if (blockIdx.x >= nb12) {  // G3: update, and its slice-major copy
@@ -1592,12 +1616,9 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
     // images from the updated values
     const int img_smem = 32 * 129 * 4 + 1024;
     const int ng3 = (int)((n2 + kImgThreads - 1) / kImgThreads);
-    {
-      ProfScope _pc(h, s, "f_gradcheck");
-      if ((e = launch_gradcheck(w.f_grad, n0 + n1 + n2, w.fast_hdr, h->num_sms, s, w.fast_hdr + kHdrSuspect)))
-        return e;
-    }
-    SgdArgs u = {w.f_grad, v0, v1, v2, p2, lr, mu, mask, 1, w.fast_hdr, adagrad, w.f_g3t};
+    // (the finiteness gate runs inside the update kernel, see k_coreimg)
+    SgdArgs u = {w.f_grad, v0, v1, v2, p2, lr, mu, mask, 1, w.fast_hdr, adagrad, w.f_g3t,
+                 w.fast_hdr + kHdrSuspect, n0 + n1 + n2};
     ProfScope _ps(h, s, "f_sgd");
     if ((e = launch_pdl(k_coreimg, dim3(h->kg.m2 + (h->kg.g1rows + 3) / 4 + (ng3 < 64 ? ng3 : 64)), dim3(kImgThreads),
                         img_smem, s, p0, p1, h->kg, w.f_img, w.f_g1img, u)))
