@@ -180,6 +180,7 @@ void layout(ttb_handle& h, char* base) {
   w.f_rstart = c.take<int>(fz ? (size_t)fk : 0);
   w.f_split = c.take<int>(fz ? (size_t)fk : 0);
   w.f_cta = c.take<int>(fz ? 1025 : 0);
+  w.f_chunks = c.take<int2>(fz ? T / 32 + 2 : 0);
   w.f_gtot = c.take<int4>(fz ? fg : 0);
   w.f_tile_info = c.take<int4>(fz ? T / 32 + fg + 2 : 0);
   w.f_g1img = c.take<float>(fz ? (size_t)fg1 * 768 : 0);

@@ -212,6 +212,28 @@ __device__ __forceinline__ float sgd_apply(float p, float g, double* vel, double
   return (float)__dsub_rn((double)p, step);
 }
 
+// register forms of sgd_apply / adagrad_apply (the state is loaded and stored
+// by the caller, so a thread's loads for several elements can all be in flight)
+__device__ __forceinline__ float sgd_step(float p, float g, double v_in, double* v_out, bool has_v, double lr,
+                                          double mu) {
+  double step;
+  if (has_v) {
+    const double v = __dadd_rn(__dmul_rn(v_in, mu), (double)g);
+    *v_out = v;
+    step = __dmul_rn(lr, v);
+  } else {
+    step = __dmul_rn(lr, (double)g);
+  }
+  return (float)__dsub_rn((double)p, step);
+}
+__device__ __forceinline__ float adagrad_step(float p, float g, double s_in, double* s_out, double lr, double eps) {
+  const double gd = (double)g;
+  const double ss = __fma_rn(gd, gd, s_in);
+  *s_out = ss;
+  const double step = __ddiv_rn(__dmul_rn(-lr, gd), __dadd_rn(__dsqrt_rn(ss), eps));
+  return (float)__dadd_rn((double)p, step);
+}
+
 // Adagrad (torch.optim.Adagrad semantics, no weight / lr decay): the
 // squared-gradient sum s in fp64, s <- fma(g, g, s), p <- f32(p + (-lr g) / (sqrt(s) + eps)),
 // one rounding into the parameter like sgd_apply. (The reference has no

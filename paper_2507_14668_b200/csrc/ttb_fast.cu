@@ -79,7 +79,8 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
                                                         int* __restrict__ cta_tiles, int ctas,
                                                         unsigned* __restrict__ item_key, int4* __restrict__ tile_info,
                                                         int2* __restrict__ sbi, int* __restrict__ hdr, int dbg,
-                                                        int allow_empty, const uint4* __restrict__ tgeom) {
+                                                        int allow_empty, const uint4* __restrict__ tgeom,
+                                                        int2* __restrict__ chunks) {
   pdl_enter();
 #define PSTAMP(i)                                                                                          \
   do {                                                                                                     \
@@ -188,6 +189,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
   grid_barrier(bar, target);
   PSTAMP(2);
   // ---- phase A2: group offsets, key starts, item and tile tables
+  const bool pooled = hdr[1] != 0;  // some bag holds several lookups: row-sort chunks for the backward
   for (unsigned i2 = gw; i2 < g.m2; i2 += nw) {
     int pc = 0, pi = 0, pt = 0;
     for (unsigned j = lane; j < i2; j += 32) {
@@ -264,6 +266,15 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
         for (int j = lane; j < snf; j += 32) {
           item_start[pi + sf + j] = sfp + kItemLen * j;
           item_key[pi + sf + j] = sk;
+        }
+        if (pooled && snf >= 2) {  // the key's full items in runs of <= kSortItems (k_rowsort)
+          const int nch = (snf + kSortItems - 1) / kSortItems;
+          int cb = 0;
+          if (lane == 0) cb = atomicAdd(&hdr[kHdrChunks], nch);
+          cb = __shfl_sync(0xffffffffu, cb, 0);
+          for (int j = lane; j < nch; j += 32)
+            chunks[cb + j] = make_int2(sfp + j * kSortItems * kItemLen,
+                                       min(kSortItems, snf - j * kSortItems) * kItemLen);
         }
       }
       if (r) {
@@ -376,6 +387,76 @@ struct SgdArgs {
   int64_t ngrad;       // |G1| + |G2| + |G3| (the scan's extent)
 };
 
+// ------------------------------------------------------------ row sort
+// Pooled batches: before the backward, every run of <= kSortItems full items
+// of one prefix (a plan chunk) is counting-sorted by i3 in shared memory, so
+// the lookups of one row sit together and an item of a hot prefix holds one or
+// two rows instead of a scatter of them — the row-grouped backward then does
+// X^T g, the dG3 reduction and the Z update once per (item, row), with the
+// row's gradient rows summed first (the reference's unique_aggregate,
+// backward.py:72-87, applied inside each chunk). Item boundaries, keys and
+// tiles are unchanged; the forward has already consumed the plan order.
+constexpr int kSortMax = kSortItems * kItemLen;  // positions per chunk
+constexpr int kSortThreads = 512;
+__global__ void __launch_bounds__(kSortThreads) k_rowsort(int2* __restrict__ sbi, const int2* __restrict__ chunks,
+                                                         const int* __restrict__ hdr, unsigned tm3) {
+  pdl_enter();
+  extern __shared__ __align__(16) char smem_raw[];
+  int2* a = reinterpret_cast<int2*>(smem_raw);
+  int2* o = a + kSortMax;
+  __shared__ int hist[320];  // >= m3 of any tensor-core table (kFwdMaxM3 = 288)
+  const int lane = threadIdx.x & 31;
+  const int nch = hdr[kHdrChunks];
+  for (int ci = blockIdx.x; ci < nch; ci += gridDim.x) {
+    const int2 cd = chunks[ci];
+    const int p0 = cd.x, L = cd.y;
+    for (int i = threadIdx.x; i < (int)tm3; i += kSortThreads) hist[i] = 0;
+    __syncthreads();
+    for (int i0 = 0; i0 < L; i0 += kSortThreads) {  // (warp-uniform trip count)
+      const int i = i0 + threadIdx.x;
+      const bool ok = i < L;
+      int2 v = make_int2(0, -1 - lane);
+      if (ok) {
+        v = sbi[p0 + i];
+        a[i] = v;
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, v.y);
+      if (ok && (__ffs(peers) - 1) == lane) atomicAdd(&hist[v.y], __popc(peers));
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan over the slices
+      int carry = 0;
+      for (int b0 = 0; b0 < (int)tm3; b0 += 32) {
+        const int bi = b0 + lane;
+        const int h = bi < (int)tm3 ? hist[bi] : 0;
+        int x = h;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, d);
+          if (lane >= d) x += y;
+        }
+        if (bi < (int)tm3) hist[bi] = carry + x - h;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+      }
+    }
+    __syncthreads();
+    for (int i0 = 0; i0 < L; i0 += kSortThreads) {
+      const int i = i0 + threadIdx.x;
+      const bool ok = i < L;
+      const int2 v = ok ? a[i] : make_int2(0, -1 - lane);
+      const unsigned peers = __match_any_sync(0xffffffffu, v.y);
+      const int ld = __ffs(peers) - 1;
+      int base = 0;
+      if (ok && ld == lane) base = atomicAdd(&hist[v.y], __popc(peers));
+      base = __shfl_sync(0xffffffffu, base, ld);
+      if (ok) o[base + __popc(peers & lanemask_lt())] = v;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < L; i += kSortThreads) sbi[p0 + i] = o[i];
+    __syncthreads();
+  }
+}
+
 // Finiteness pre-pass over the final gradients (fused_update rejects a
 // non-finite gradient before touching any core, backward.py:190-194): sets
 // TTB_ERRBIT_NONFINITE in *err; the update kernel that follows reads it.
@@ -447,15 +528,39 @@ __global__ void __launch_bounds__(kImgThreads) k_coreimg(float* __restrict__ G1,
   const size_t n0 = (size_t)g.g1rows * 4 * R1, n1 = (size_t)R1 * g.m2 * C;
   const unsigned nb12 = g.m2 + (g.g1rows + 3) / 4;
   if (blockIdx.x >= nb12) {  // G3: update, and its slice-major copy
-    const size_t n2 = (size_t)32 * g.m3 * 4;
-    for (size_t j = (size_t)(blockIdx.x - nb12) * kImgThreads + threadIdx.x; j < n2;
-         j += (size_t)(gridDim.x - nb12) * kImgThreads) {
-      const float v = u.p2[j];
-      // the backward accumulates dG3 slice-major, (i3, c, n3), as the copy
-      const size_t c = j / ((size_t)g.m3 * 4), r = j - c * g.m3 * 4, jt = ((r >> 2) * 32 + c) * 4 + (r & 3);
-      const float w = maybe_sgd(v, u, 2, n0 + n1 + jt, j, u.v2);
-      if (u.on && (u.mask & 4)) u.p2[j] = w;
-      u.g3t[jt] = w;
+    const size_t n2 = (size_t)32 * g.m3 * 4, stride = (size_t)(gridDim.x - nb12) * kImgThreads;
+    const bool upd = u.on && (u.mask & 4), has_v = u.adagrad || u.v2 != nullptr;
+    constexpr int kU = 4;  // elements per thread in flight
+    for (size_t j0 = (size_t)(blockIdx.x - nb12) * kImgThreads + threadIdx.x; j0 < n2; j0 += kU * stride) {
+      float pv[kU], gr[kU];
+      double st[kU];
+      size_t jt[kU];
+#pragma unroll
+      for (int q = 0; q < kU; ++q) {
+        const size_t j = j0 + q * stride;
+        // the backward accumulates dG3 slice-major, (i3, c, n3), as the copy
+        const size_t c = j / ((size_t)g.m3 * 4), r = j - c * g.m3 * 4;
+        jt[q] = ((r >> 2) * 32 + c) * 4 + (r & 3);
+        if (j < n2) {
+          pv[q] = u.p2[j];
+          gr[q] = upd ? u.grad[n0 + n1 + jt[q]] : 0.f;
+          st[q] = upd && has_v ? u.v2[j] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kU; ++q) {
+        const size_t j = j0 + q * stride;
+        if (j >= n2) break;
+        float w = pv[q];
+        if (upd) {
+          double ns;
+          w = u.adagrad ? adagrad_step(w, gr[q], st[q], &ns, u.lr, u.mu)
+                        : sgd_step(w, gr[q], st[q], &ns, has_v, u.lr, u.mu);
+          if (has_v) u.v2[j] = ns;
+          u.p2[j] = w;
+        }
+        u.g3t[jt[q]] = w;
+      }
     }
     return;
   }
@@ -494,11 +599,26 @@ __global__ void __launch_bounds__(kImgThreads) k_coreimg(float* __restrict__ G1,
     vals[r] = G2[((size_t)k * g.m2 + i2) * C + (e & 127)];
   }
   if (u.on && (u.mask & 2)) {
+    // every load of the slice's gradients and optimizer state first (one
+    // round trip), then the updates and stores
+    float gr[kPer];
+    double st[kPer];
+    const bool has_v = u.adagrad || u.v1 != nullptr;
 #pragma unroll
     for (int r = 0; r < kPer; ++r) {
       const int e = threadIdx.x + r * kImgThreads, k = e >> 7;
       const size_t j = ((size_t)k * g.m2 + i2) * C + (e & 127);
-      vals[r] = maybe_sgd(vals[r], u, 1, n0 + j, j, u.v1);
+      gr[r] = u.grad[n0 + j];
+      st[r] = has_v ? u.v1[j] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+      const int e = threadIdx.x + r * kImgThreads, k = e >> 7;
+      const size_t j = ((size_t)k * g.m2 + i2) * C + (e & 127);
+      double ns;
+      vals[r] = u.adagrad ? adagrad_step(vals[r], gr[r], st[r], &ns, u.lr, u.mu)
+                          : sgd_step(vals[r], gr[r], st[r], &ns, has_v, u.lr, u.mu);
+      if (has_v) u.v1[j] = ns;
       G2[j] = vals[r];
     }
   }
@@ -1040,6 +1160,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
   // cb / k images (issued and waited for by the MMA warp)
   __shared__ uint64_t s_mb_xop, s_mb_z, s_mb_zi, s_mb_x, s_mb_e, s_mb_xtma, s_mb_ktma;
   __shared__ int s_acc2;
+  // tile of each metadata slot (-1: none). Pooled batches take tiles from a
+  // global counter (hdr[kHdrNextTile]): after the row sort, a tile's cost no
+  // longer follows its lookup count, so the plan's static ranges would leave
+  // CTAs idle; one lookup per bag keeps the static, i2-contiguous ranges
+  __shared__ int s_tile[2];
   __shared__ long long s_tacc[12];
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1056,10 +1181,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
     umma::mbar_init(&s_mb_e, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  int4 pf = make_int4(0, 0, 0, 0);
-  if (warp == kThreads / 32 - 1 && tb < te) {
-    fetch_meta_async(tile_info[tb], item_start, item_key, &s_m[0]);
-    if (tb + 1 < te) pf = tile_info[tb + 1];
+  const int ntiles = hdr[4];
+  // the tile after `t` (this CTA's next): -1 when there is none
+  auto next_tile = [&](int t) -> int {
+    if (kRows) {
+      const int u = atomicAdd(&hdr[kHdrNextTile], 1);
+      return u < ntiles ? u : -1;
+    }
+    return t + 1 < te ? t + 1 : -1;
+  };
+  if (warp == kThreads / 32 - 1) {
+    int t0 = 0;
+    if (lane == 0) t0 = kRows ? next_tile(-1) : (tb < te ? tb : -1);
+    t0 = __shfl_sync(0xffffffffu, t0, 0);
+    if (lane == 0) s_tile[0] = t0;
+    if (t0 >= 0) fetch_meta_async(tile_info[t0], item_start, item_key, &s_m[0]);
   }
   cp_async_wait_all();
   umma::fence_before_sync();
@@ -1082,9 +1218,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
       __syncwarp();
     };
     uint32_t ph = 0;
-    if (tb < te) load_cb(&s_m[0]);
-    for (int t = tb; t < te; ++t, ph ^= 1u) {
-      const TileMeta* mt = &s_m[(t - tb) & 1];
+    if (s_tile[0] >= 0) load_cb(&s_m[0]);
+    for (int k = 0; s_tile[k & 1] >= 0; ++k, ph ^= 1u) {
+      const TileMeta* mt = &s_m[k & 1];
       umma::mbar_wait(&s_mb_xtma, ph);  // the G2 cb image of tile t
       umma::mbar_wait(&s_mb_xop, ph);   // its items' G1 rows (SIMT cp.async)
       umma::fence_after_sync();
@@ -1143,9 +1279,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
         umma::commit(&s_mb_e);  // tracks the dG2 MMAs too
       }
       __syncwarp();
-      if (t + 1 < te) {  // R12 free once E is done: the next tile's cb image
+      if (s_tile[(k + 1) & 1] >= 0) {  // R12 free once E is done: the next tile's cb image
         umma::mbar_wait(&s_mb_e, ph);
-        load_cb(&s_m[(t + 1 - tb) & 1]);  // (its metadata: visible since the Z signal)
+        load_cb(&s_m[(k + 1) & 1]);  // (its slot and metadata: visible since the Z signal)
+      } else {
+        break;
       }
     }
   } else {
@@ -1176,7 +1314,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
   const int c = row >> 2, b = row & 3;
   const uint32_t tl = tmem + ((uint32_t)(32 * q4) << 16);
   // prologue: the first tile's first chunk and X operands
-  if (tb < te) {
+  if (s_tile[0] >= 0) {
     const TileMeta* m = &s_m[0];
     if (threadIdx.x == 0) make_chunks(m, s_chunk[0], kCap);
     simt_sync();
@@ -1192,7 +1330,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
   bool bad = false;
   int slot = 0;
   int prev_i2 = -1;
-  for (int t = tb; t < te; ++t, slot ^= 1, phase ^= 1u) {
+  int ntile_done = 0;
+  for (; s_tile[slot] >= 0; slot ^= 1, phase ^= 1u, ++ntile_done) {
+    const int t = s_tile[slot];
     const TileMeta* m = &s_m[slot];
     const int* chunk = s_chunk[slot];
     const int n = m->n, nchunk = chunk[kTileItems + 1];
@@ -1220,9 +1360,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
     cp_async_commit();
     umma::fence_before_sync();
     simt_sync();  // (every warp is past the previous tile: its metadata slot is free)
-    if (warp == kThreads / 32 - 1 && t + 1 < te) {  // next tile's metadata into the other slot
-      fetch_meta_async(pf, item_start, item_key, &s_m[slot ^ 1]);  // (waited for before make_chunks)
-      if (t + 2 < te) pf = tile_info[t + 2];
+    if (warp == kThreads / 32 - 1) {  // next tile and its metadata into the other slot
+      int tn = 0;
+      if (lane == 0) tn = next_tile(t);
+      tn = __shfl_sync(0xffffffffu, tn, 0);
+      if (lane == 0) s_tile[slot ^ 1] = tn;  // (read by everyone after the Z^T barrier)
+      if (tn >= 0) fetch_meta_async(tile_info[tn], item_start, item_key, &s_m[slot ^ 1]);  // (waited for before make_chunks)
     }
     TSTAMP(3);
     for (int ch = 0; ch < nchunk; ++ch) {
@@ -1309,7 +1452,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
       }
     }
     TSTAMP(4);
-    const int tn = t + 1;
+    const bool has_next = s_tile[slot ^ 1] >= 0;  // (written before the Z phase's barriers)
     const TileMeta* mn = &s_m[slot ^ 1];
     int npn = 0;
     // ---- Z^T into TMEM (hi / lo) and the Z image (hi) for the E GEMM
@@ -1328,7 +1471,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
     simt_sync_for_mma();  // every slot read before the image overwrites them; Z^T is in TMEM
     if (threadIdx.x == 0) umma::mbar_arrive(&s_mb_z);  // -> dG2 MMAs
     // ---- next tile: chunk list and first chunk's positions
-    if (tn < te) {
+    if (has_next) {
       if (threadIdx.x == 0) make_chunks(mn, s_chunk[slot ^ 1], kCap);
       simt_sync();
       npn = mn->start[s_chunk[slot ^ 1][1]] - mn->start[0];
@@ -1351,7 +1494,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
     TSTAMP(6);
     // the next tile's G1 rows (R12 is free now) and first-chunk rows (the
     // staging region held the Z lo image)
-    if (tn < te) {
+    if (has_next) {
       stage_g1_rows(mn);
       cp_async_commit();
       stage_rows(npn, tile_i3_base(mn, g));
@@ -1361,7 +1504,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
     if (!(dbg & 4)) {
       float v[kRedCols], w2[kRedCols];
       // dG2[k][i2][b][c] = D[:, k] + D[:, 32 + k], once per run of tiles of one i2
-      if (tn >= te || mn->i2 != m->i2) {
+      if (!has_next || mn->i2 != m->i2) {
         umma::tmem_ld8(tl + 384 + kRedCols * qw, v);
         umma::tmem_ld8(tl + 384 + 32 + kRedCols * qw, w2);
         float* d2 = dG2 + ((size_t)m->i2 * 4 + b) * 32 + c;
@@ -1386,7 +1529,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
         }
       }
     }
-    if (tn < te) {  // the next G1 rows landed: with the cb image, the MMA warp starts the next X GEMM
+    if (has_next) {  // the next G1 rows landed: with the cb image, the MMA warp starts the next X GEMM
       asm volatile("cp.async.wait_group 1;" ::: "memory");
       simt_sync_for_mma();
       if (threadIdx.x == 0) umma::mbar_arrive(&s_mb_xop);
@@ -1399,7 +1542,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
   }
   if (bad) hdr[kHdrSuspect] = 1;
   if ((dbg & 8) && threadIdx.x == 0 && blockIdx.x == 0) {
-    s_tacc[0] = te - tb;
+    s_tacc[0] = ntile_done;
     for (int q = 0; q < 12; ++q) reinterpret_cast<long long*>(hdr + 16)[q] = s_tacc[q];
   }
   }
@@ -1520,13 +1663,13 @@ cudaError_t fast_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* 
     e = launch_pdl_coop(k_fplan<long long>, dim3(grid), dim3(kPlanThreads), 0, s, (const long long*)idx, offsets, T, B,
                    h->kg, w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_rstart, w.f_split, w.f_gtot, w.f_item_start, w.f_cta, h->num_sms,
                    w.f_item_key, w.f_tile_info, w.f_sbi, w.fast_hdr, getenv("TTB_DBG") ? 1 : 0, h->allow_empty,
-                   (const uint4*)w.f_tgeom);
+                   (const uint4*)w.f_tgeom, w.f_chunks);
   else
     e = launch_pdl_coop(k_fplan<int>, dim3(grid), dim3(kPlanThreads), 0, s, (const int*)idx, offsets, T, B, h->kg,
                    w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_rstart, w.f_split, w.f_gtot, w.f_item_start, w.f_cta, h->num_sms,
                    w.f_item_key,
                    w.f_tile_info, w.f_sbi, w.fast_hdr, getenv("TTB_DBG") ? 1 : 0, h->allow_empty,
-                   (const uint4*)w.f_tgeom);
+                   (const uint4*)w.f_tgeom, w.f_chunks);
   if (e) return e;
   count_launch();
   return cudaGetLastError();
@@ -1600,6 +1743,16 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
   // reads it in that order, the caller's buffer gets the reference layout
   float* g3s = w.f_grad + n0 + n1;
   const int grid = h->num_sms;  // = the plan's CTA ranges (k_fplan cta_tiles)
+  if (h->T > h->B) {  // pooled: each multi-item prefix's lookups grouped by row
+    if ((e = cudaMemsetAsync(w.fast_hdr + kHdrNextTile, 0, sizeof(int), s))) return e;
+    constexpr int sort_smem = 2 * kSortMax * (int)sizeof(int2);
+    if ((e = ensure_kernel_smem((const void*)k_rowsort, sort_smem))) return e;
+    ProfScope _pr(h, s, "f_rowsort");
+    if ((e = launch_pdl(k_rowsort, dim3(2 * h->num_sms), dim3(kSortThreads), sort_smem, s, w.f_sbi,
+                        (const int2*)w.f_chunks, (const int*)w.fast_hdr, h->kg.tm3)))
+      return e;
+    count_launch();
+  }
   {
     ProfScope _ps(h, s, "f_bwd");
     // pooled bags (more lookups than bags) repeat rows inside a prefix: group
@@ -1620,7 +1773,7 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
     SgdArgs u = {w.f_grad, v0, v1, v2, p2, lr, mu, mask, 1, w.fast_hdr, adagrad, w.f_g3t,
                  w.fast_hdr + kHdrSuspect, n0 + n1 + n2};
     ProfScope _ps(h, s, "f_sgd");
-    if ((e = launch_pdl(k_coreimg, dim3(h->kg.m2 + (h->kg.g1rows + 3) / 4 + (ng3 < 64 ? ng3 : 64)), dim3(kImgThreads),
+    if ((e = launch_pdl(k_coreimg, dim3(h->kg.m2 + (h->kg.g1rows + 3) / 4 + (ng3 < 16 ? ng3 : 16)), dim3(kImgThreads),
                         img_smem, s, p0, p1, h->kg, w.f_img, w.f_g1img, u)))
       return e;
     count_launch();

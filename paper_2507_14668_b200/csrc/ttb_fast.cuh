@@ -10,6 +10,7 @@ namespace fast {
 
 constexpr int kItemLen = 32;    // max lookups per work item
 constexpr int kTileItems = 32;  // items per tile: M = 32 * n1 = 128
+constexpr int kSortItems = 256; // full items per row-sort chunk (k_rowsort, pooled batches)
 constexpr int R1 = 32, C = 128, NOUT = 64;
 constexpr int kImg = 16384;     // bytes of one 128 x 32 / 32 x 128 fp32 image
 
@@ -26,6 +27,8 @@ __device__ __forceinline__ void red_f32(float* p, float a) {
 // moves by at most twice the addend (|fl(s + x) - s| <= 2|x|), so it stays
 // below 2^127. The finiteness scan before the fused update runs only if set.
 constexpr int kHdrSuspect = 6;
+constexpr int kHdrChunks = 7;  // fast_hdr word: number of row-sort chunks (f_chunks) of the plan
+constexpr int kHdrNextTile = 5;  // fast_hdr word: the pooled backward's tile counter (reset per launch)
 __device__ __forceinline__ bool suspicious(float v) { return !(fabsf(v) < 0x1p95f); }
 
 __device__ __forceinline__ int warp_sum(int v) {

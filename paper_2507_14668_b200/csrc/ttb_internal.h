@@ -83,6 +83,7 @@ struct Workspace {
   int* f_rstart;          // m1 m2: position of its remainder item, minus the full items' lookups
   int* f_split;           // m1 m2: lookups of the key in full items
   int* f_cta;             // kMaxCtas + 1: first tile of each step-kernel CTA
+  int2* f_chunks;         // <= T / 32 + 2: runs of a multi-item prefix's full items (position, count) sorted by row before the backward
   int4* f_gtot;           // m2: (positions, items, prefixes) per i2 group
   int4* f_tile_info;      // tiles (<= T / 32 + m2): (i2, first item, items)
   float* f_g1img;         // m1 x 768: split G1 row images (pre-swizzled, both parities) / transposed images
