@@ -398,62 +398,112 @@ struct SgdArgs {
 // tiles are unchanged; the forward has already consumed the plan order.
 constexpr int kSortMax = kSortItems * kItemLen;  // positions per chunk
 constexpr int kSortThreads = 512;
+constexpr int kSortPer = kSortMax / kSortThreads;  // positions per thread (CTA-wide chunks), in registers
+constexpr int kSortSmall = 1024;                    // chunks up to this size: one warp each
+constexpr int kSortHist = 320;                      // >= m3 of any tensor-core table (kFwdMaxM3 = 288)
+constexpr int kSortSmem = (kSortMax > (kSortThreads / 32) * kSortSmall ? kSortMax : (kSortThreads / 32) * kSortSmall) *
+                          (int)sizeof(int2);
+__device__ __forceinline__ void warp_exclusive_scan(int* hist, unsigned n, int lane) {
+  int carry = 0;
+  for (unsigned b0 = 0; b0 < n; b0 += 32) {
+    const unsigned bi = b0 + lane;
+    const int h = bi < n ? hist[bi] : 0;
+    int x = h;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += y;
+    }
+    if (bi < n) hist[bi] = carry + x - h;
+    carry += __shfl_sync(0xffffffffu, x, 31);
+  }
+}
 __global__ void __launch_bounds__(kSortThreads) k_rowsort(int2* __restrict__ sbi, const int2* __restrict__ chunks,
                                                          const int* __restrict__ hdr, unsigned tm3) {
   pdl_enter();
   extern __shared__ __align__(16) char smem_raw[];
-  int2* a = reinterpret_cast<int2*>(smem_raw);
-  int2* o = a + kSortMax;
-  __shared__ int hist[320];  // >= m3 of any tensor-core table (kFwdMaxM3 = 288)
-  const int lane = threadIdx.x & 31;
+  int2* o = reinterpret_cast<int2*>(smem_raw);  // CTA-wide chunk output; per warp 1024 entries for small chunks
+  __shared__ int hist[kSortThreads / 32][kSortHist];  // per warp; warp 0's row is the CTA-wide histogram
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nch = hdr[kHdrChunks];
+  // large chunks: the whole CTA, every load of the chunk in flight at once
   for (int ci = blockIdx.x; ci < nch; ci += gridDim.x) {
     const int2 cd = chunks[ci];
     const int p0 = cd.x, L = cd.y;
-    for (int i = threadIdx.x; i < (int)tm3; i += kSortThreads) hist[i] = 0;
-    __syncthreads();
-    for (int i0 = 0; i0 < L; i0 += kSortThreads) {  // (warp-uniform trip count)
-      const int i = i0 + threadIdx.x;
-      const bool ok = i < L;
-      int2 v = make_int2(0, -1 - lane);
-      if (ok) {
-        v = sbi[p0 + i];
-        a[i] = v;
-      }
-      const unsigned peers = __match_any_sync(0xffffffffu, v.y);
-      if (ok && (__ffs(peers) - 1) == lane) atomicAdd(&hist[v.y], __popc(peers));
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {  // exclusive scan over the slices
-      int carry = 0;
-      for (int b0 = 0; b0 < (int)tm3; b0 += 32) {
-        const int bi = b0 + lane;
-        const int h = bi < (int)tm3 ? hist[bi] : 0;
-        int x = h;
+    if (L <= kSortSmall) continue;  // (uniform)
+    int* hc = hist[0];
+    int2 v[kSortPer];
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, x, d);
-          if (lane >= d) x += y;
-        }
-        if (bi < (int)tm3) hist[bi] = carry + x - h;
-        carry += __shfl_sync(0xffffffffu, x, 31);
-      }
+    for (int r = 0; r < kSortPer; ++r) {
+      const int i = r * kSortThreads + threadIdx.x;
+      v[r] = i < L ? sbi[p0 + i] : make_int2(0, -1 - lane);
+    }
+    for (int i = threadIdx.x; i < (int)tm3; i += kSortThreads) hc[i] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kSortPer; ++r) {
+      if (r * kSortThreads >= L) break;  // (uniform)
+      const unsigned peers = __match_any_sync(0xffffffffu, v[r].y);
+      if (v[r].y >= 0 && (__ffs(peers) - 1) == lane) atomicAdd(&hc[v[r].y], __popc(peers));
     }
     __syncthreads();
-    for (int i0 = 0; i0 < L; i0 += kSortThreads) {
-      const int i = i0 + threadIdx.x;
-      const bool ok = i < L;
-      const int2 v = ok ? a[i] : make_int2(0, -1 - lane);
-      const unsigned peers = __match_any_sync(0xffffffffu, v.y);
+    if (warp == 0) warp_exclusive_scan(hc, tm3, lane);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kSortPer; ++r) {
+      if (r * kSortThreads >= L) break;
+      const unsigned peers = __match_any_sync(0xffffffffu, v[r].y);
       const int ld = __ffs(peers) - 1;
       int base = 0;
-      if (ok && ld == lane) base = atomicAdd(&hist[v.y], __popc(peers));
+      if (v[r].y >= 0 && ld == lane) base = atomicAdd(&hc[v[r].y], __popc(peers));
       base = __shfl_sync(0xffffffffu, base, ld);
-      if (ok) o[base + __popc(peers & lanemask_lt())] = v;
+      if (v[r].y >= 0) o[base + __popc(peers & lanemask_lt())] = v[r];
     }
     __syncthreads();
     for (int i = threadIdx.x; i < L; i += kSortThreads) sbi[p0 + i] = o[i];
     __syncthreads();
+  }
+  // small chunks (most keys): one warp each, no CTA barriers
+  int* hw = hist[warp];
+  int2* ow = o + warp * kSortSmall;
+  const int gw = blockIdx.x * (kSortThreads / 32) + warp, nw = gridDim.x * (kSortThreads / 32);
+  for (int ci = gw; ci < nch; ci += nw) {
+    const int2 cd = chunks[ci];
+    const int p0 = cd.x, L = cd.y;
+    if (L > kSortSmall) continue;
+    int2 v[kSortSmall / 32];
+#pragma unroll
+    for (int r = 0; r < kSortSmall / 32; ++r) {
+      const int i = r * 32 + lane;
+      v[r] = i < L ? sbi[p0 + i] : make_int2(0, -1 - lane);
+    }
+    for (int i = lane; i < (int)tm3; i += 32) hw[i] = 0;
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < kSortSmall / 32; ++r) {
+      if (r * 32 >= L) break;
+      const unsigned peers = __match_any_sync(0xffffffffu, v[r].y);
+      if (v[r].y >= 0 && (__ffs(peers) - 1) == lane) hw[v[r].y] += __popc(peers);
+      __syncwarp();
+    }
+    warp_exclusive_scan(hw, tm3, lane);
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < kSortSmall / 32; ++r) {
+      if (r * 32 >= L) break;
+      const unsigned peers = __match_any_sync(0xffffffffu, v[r].y);
+      const int ld = __ffs(peers) - 1;
+      int base = 0;
+      if (v[r].y >= 0 && ld == lane) {
+        base = hw[v[r].y];
+        hw[v[r].y] = base + __popc(peers);
+      }
+      base = __shfl_sync(0xffffffffu, base, ld);
+      if (v[r].y >= 0) ow[base + __popc(peers & lanemask_lt())] = v[r];
+      __syncwarp();
+    }
+    for (int i = lane; i < L; i += 32) sbi[p0 + i] = ow[i];
+    __syncwarp();
   }
 }
 
@@ -1409,10 +1459,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
             const float4* src = st_g + (s0 + ld) * 16;
             if (mem & (mem - 1)) {
               float2 acc = make_float2(0.f, 0.f);
-              for (; mem; mem &= mem - 1) {
-                const float2 v = reinterpret_cast<const float2*>(st_g + (s0 + __ffs(mem) - 1) * 16)[lane];
-                acc.x += v.x;
-                acc.y += v.y;
+              while (mem) {  // four members' loads in flight per round
+                float2 w[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  w[q] = make_float2(0.f, 0.f);
+                  if (mem) {
+                    w[q] = reinterpret_cast<const float2*>(st_g + (s0 + __ffs(mem) - 1) * 16)[lane];
+                    mem &= mem - 1;
+                  }
+                }
+                acc.x += (w[0].x + w[1].x) + (w[2].x + w[3].x);
+                acc.y += (w[0].y + w[1].y) + (w[2].y + w[3].y);
               }
               reinterpret_cast<float2*>(st_acc + warp * 16)[lane] = acc;
               __syncwarp();
@@ -1745,10 +1803,10 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
   const int grid = h->num_sms;  // = the plan's CTA ranges (k_fplan cta_tiles)
   if (h->T > h->B) {  // pooled: each multi-item prefix's lookups grouped by row
     if ((e = cudaMemsetAsync(w.fast_hdr + kHdrNextTile, 0, sizeof(int), s))) return e;
-    constexpr int sort_smem = 2 * kSortMax * (int)sizeof(int2);
+    constexpr int sort_smem = kSortSmem;
     if ((e = ensure_kernel_smem((const void*)k_rowsort, sort_smem))) return e;
     ProfScope _pr(h, s, "f_rowsort");
-    if ((e = launch_pdl(k_rowsort, dim3(2 * h->num_sms), dim3(kSortThreads), sort_smem, s, w.f_sbi,
+    if ((e = launch_pdl(k_rowsort, dim3(h->num_sms), dim3(kSortThreads), sort_smem, s, w.f_sbi,
                         (const int2*)w.f_chunks, (const int*)w.fast_hdr, h->kg.tm3)))
       return e;
     count_launch();
