@@ -88,12 +88,14 @@ __device__ inline void fetch_meta_async(const int4& info, const int* __restrict_
 
 // G1 row (image index) of item `it`: its table's block (tables are stacked
 // at M1 rows, M2 slices) plus the key's i1 digit
+// (one table: no division — these run per staged element)
 __device__ __forceinline__ int item_i1(const TileMeta* m, int it, KGeom g) {
-  return (int)(m->key[it] - (unsigned)m->i2 * g.m1 + ((unsigned)m->i2 / g.tm2) * g.m1);
+  const unsigned base = m->key[it] - (unsigned)m->i2 * g.m1;
+  return (int)(g.nt == 1 ? base : base + ((unsigned)m->i2 / g.tm2) * g.m1);
 }
 // G3 slice offset of a tile's table (its lookups' i3 digits are table-local)
 __device__ __forceinline__ unsigned tile_i3_base(const TileMeta* m, KGeom g) {
-  return ((unsigned)m->i2 / g.tm2) * g.tm3;
+  return g.nt == 1 ? 0u : ((unsigned)m->i2 / g.tm2) * g.tm3;
 }
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
