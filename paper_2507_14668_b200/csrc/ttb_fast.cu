@@ -1547,15 +1547,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
     simt_sync_for_mma();
     if (threadIdx.x == 0) umma::mbar_arrive(&s_mb_zi);  // -> E MMAs
     TSTAMP(5);
+    if (!kRows && has_next) {  // one lookup per bag: the gradient rows' region is not the Z lo image's
+      for (int e = threadIdx.x; e < npn * 16; e += kThreads)
+        cp_async16(st_g + e, gout + (size_t)st_sbi[e >> 4].x * NOUT + 4 * (e & 15));
+      cp_async_commit();
+    }
     umma::mbar_wait(&s_mb_e, phase);  // dG2 and E of tile t
     umma::fence_after_sync();
     TSTAMP(6);
-    // the next tile's G1 rows (R12 is free now) and first-chunk rows (the
-    // staging region held the Z lo image)
+    // the next tile's G1 rows (R12 is free now) and the rest of its first
+    // chunk (the staging region held the Z lo image)
     if (has_next) {
       stage_g1_rows(mn);
       cp_async_commit();
-      stage_rows(npn, tile_i3_base(mn, g));
+      if (kRows) {
+        stage_rows(npn, tile_i3_base(mn, g));
+      } else {
+        const unsigned i3n = tile_i3_base(mn, g);
+        for (int e = threadIdx.x; e < npn * 32; e += kThreads)
+          cp_async16(st_g3 + e, g3t + (size_t)(i3n + st_sbi[e >> 5].y) * 128 + 4 * (e & 31));
+      }
       cp_async_commit();
     }
     TSTAMP(7);
