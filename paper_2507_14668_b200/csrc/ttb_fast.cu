@@ -320,18 +320,20 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
   PSTAMP(3);
   // ---- phase B: per-CTA tile ranges for the step kernels (grid = ctas):
   // contiguous tile runs of equal weight (lookups + kTileCost per tile)
+  // cta_tiles[b] = #{tiles t : W_t < wtot b / ctas} with W_t = position of t
+  // + kTileCost t (increasing): thread t writes it for every b whose target
+  // lies in (W_{t-1}, W_t] — one load per tile instead of a dependent
+  // binary search per CTA boundary
   {
     const int nt = hdr[4];
     const long long wtot = (long long)T + (long long)kTileCost * nt;
-    for (int b = tid; b <= ctas; b += nthr) {
-      const long long target = wtot * b / ctas;
-      int lo = 0, hi = nt;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if ((long long)tile_info[mid].w + (long long)kTileCost * mid < target) lo = mid + 1;
-        else hi = mid;
-      }
-      cta_tiles[b] = lo;
+    for (int t = tid; t <= nt; t += nthr) {
+      const long long lo_w = t == 0 ? -1 : (long long)tile_info[t - 1].w + (long long)kTileCost * (t - 1);
+      const long long hi_w = t == nt ? wtot : (long long)tile_info[t].w + (long long)kTileCost * t;
+      // first b with wtot b / ctas > lo_w, i.e. b >= ceil((lo_w + 1) ctas / wtot)
+      long long b = lo_w < 0 ? 0 : ((lo_w + 1) * ctas + wtot - 1) / wtot;
+      for (; b <= ctas && wtot * b / ctas <= hi_w; ++b)
+        if (wtot * b / ctas > lo_w) cta_tiles[b] = t;
     }
   }
   // ---- phase B: scatter (bag, i3) into item order
