@@ -794,6 +794,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
   __shared__ TileMeta s_m[3];
   __shared__ uint64_t s_mbar;
   __shared__ uint32_t s_tmem;
+  __shared__ unsigned s_segm[kTileItems];  // per item of the tile: its segments' first positions (bit mask)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned m3 = g.tm3;  // the resident G3 block: one table's slices (m3 <= kFwdMaxM3, fast_supported)
   const int ntiles = hdr[4];
@@ -874,9 +875,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
     phase ^= 1u;
     umma::fence_after_sync();
     FSTAMP(1);
+    const int p0 = m->start[0];
+    // segments (runs of one bag) of each item as a bit mask of their first
+    // positions: one ballot per item instead of every epilogue thread
+    // re-scanning its item's (bag, i3) list
+    for (int j = warp; j < m->n; j += kFwdThreads / 32) {
+      const int j0 = m->start[j] - p0, len = m->start[j + 1] - m->start[j];
+      const int bg = lane < len ? s_sbi[j0 + lane].x : -1;
+      const int pv = __shfl_up_sync(0xffffffffu, bg, 1);
+      const unsigned mk = __ballot_sync(0xffffffffu, lane < len && (lane == 0 || bg != pv));
+      if (lane == 0) s_segm[j] = mk;
+    }
+    __syncthreads();
     if (t + 1 < te) stage(t + 1);  // lands while this tile is closed
     FSTAMP(2);
-    const int p0 = m->start[0];
     // ---- epilogue. The four warps of a lane quadrant share its 32 rows
     // (item, a) and split each segment's contraction over c: quarter q
     // closes c in [8q, 8q + 8) (its 32 X columns stay in registers for the
@@ -884,27 +896,27 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
     // four and stores the bag row. Every segment of a row costs each warp a
     // quarter of the work, whatever the item lengths of the tile.
     const bool live = it < m->n;
-    const int s1 = live ? m->start[it + 1] - p0 : 0;
-    int qq = live ? m->start[it] - p0 : 0;
-    int nseg = 0;  // segments (runs of one bag) of this row
-    for (int e = qq; e < s1;) {
-      const int bag = s_sbi[e].x;
-      ++e;
-      while (e < s1 && s_sbi[e].x == bag) ++e;
-      ++nseg;
-    }
+    const int q0 = live ? m->start[it] - p0 : 0, len = live ? m->start[it + 1] - p0 - q0 : 0;
+    const unsigned smask = live ? s_segm[it] : 0u;  // first positions of this row's segments
+    const int nseg = __popc(smask);
+    // segment [qq, e) of the row from the remaining start bits
+    auto seg_next = [&](unsigned& rem, int& qq, int& e) {
+      qq = q0 + __ffs(rem) - 1;
+      rem &= rem - 1;
+      e = q0 + (rem ? __ffs(rem) - 1 : len);
+    };
     const int rounds = __reduce_max_sync(0xffffffffu, nseg);  // same rows -> same count in all 4 warps
     if (rounds <= kFwdSplitRounds) {
       float x[32];  // x[4 c' + b] = X[item][a][b][8 quarter + c']
       umma::tmem_ld32(trow + 32 * quarter, x);
       const uint32_t tpart = trow + 128;  // partial sums: 16 columns per quarter
+      unsigned rem = smask;
       for (int r = 0; r < rounds; ++r) {
         const bool have = r < nseg;
-        int bag = 0, e = qq;
+        int bag = 0, qq = 0, e = 0;
         if (have) {
+          seg_next(rem, qq, e);
           bag = s_sbi[qq].x;
-          e = qq + 1;
-          while (e < s1 && s_sbi[e].x == bag) ++e;
         }
         float acc[16];
   #pragma unroll
@@ -956,25 +968,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
         umma::fence_before_sync();
         named_sync(1 + q4, 128);  // partial columns free for the next round
         umma::fence_after_sync();
-        qq = e;
       }
     } else {
       // long items (hot prefixes): the quarters take alternate segments, each
       // closing all 32 values of c (two 64-column halves of the X row)
-      int ord = 0;
+      unsigned rem = smask;  // quarter q takes segments q, q + 4, ...
+      for (int k = 0; k < quarter && rem; ++k) rem &= rem - 1;
       for (;;) {
-        bool have = false;
-        int bag = 0, e = qq;
-        while (qq < s1) {
+        const bool have = rem != 0;
+        int bag = 0, qq = 0, e = 0;
+        if (have) {
+          seg_next(rem, qq, e);
           bag = s_sbi[qq].x;
-          e = qq + 1;
-          while (e < s1 && s_sbi[e].x == bag) ++e;
-          if ((ord & 3) == quarter) {
-            have = true;
-            break;
-          }
-          ++ord;
-          qq = e;
+          for (int k = 0; k < 3 && rem; ++k) rem &= rem - 1;
         }
         if (!__any_sync(0xffffffffu, have)) break;
         float acc[16];
@@ -1053,8 +1059,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
 #pragma unroll
             for (int b = 0; b < 4; ++b) red_v4(o + 4 * b, acc[4 * b], acc[4 * b + 1], acc[4 * b + 2], acc[4 * b + 3]);
           }
-          ++ord;
-          qq = e;
         }
       }
     }
