@@ -879,14 +879,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
     // segments (runs of one bag) of each item as a bit mask of their first
     // positions: one ballot per item instead of every epilogue thread
     // re-scanning its item's (bag, i3) list
-    for (int j = warp; j < m->n; j += kFwdThreads / 32) {
-      const int j0 = m->start[j] - p0, len = m->start[j + 1] - m->start[j];
-      const int bg = lane < len ? s_sbi[j0 + lane].x : -1;
-      const int pv = __shfl_up_sync(0xffffffffu, bg, 1);
-      const unsigned mk = __ballot_sync(0xffffffffu, lane < len && (lane == 0 || bg != pv));
-      if (lane == 0) s_segm[j] = mk;
+    // (one lookup per bag: every position starts a segment)
+    if (!direct) {
+      for (int j = warp; j < m->n; j += kFwdThreads / 32) {
+        const int j0 = m->start[j] - p0, len = m->start[j + 1] - m->start[j];
+        const int bg = lane < len ? s_sbi[j0 + lane].x : -1;
+        const int pv = __shfl_up_sync(0xffffffffu, bg, 1);
+        const unsigned mk = __ballot_sync(0xffffffffu, lane < len && (lane == 0 || bg != pv));
+        if (lane == 0) s_segm[j] = mk;
+      }
+      __syncthreads();
     }
-    __syncthreads();
     if (t + 1 < te) stage(t + 1);  // lands while this tile is closed
     FSTAMP(2);
     // ---- epilogue. The four warps of a lane quadrant share its 32 rows
@@ -897,7 +900,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
     // quarter of the work, whatever the item lengths of the tile.
     const bool live = it < m->n;
     const int q0 = live ? m->start[it] - p0 : 0, len = live ? m->start[it + 1] - p0 - q0 : 0;
-    const unsigned smask = live ? s_segm[it] : 0u;  // first positions of this row's segments
+    const unsigned smask = !live ? 0u : direct ? (len >= 32 ? 0xffffffffu : (1u << len) - 1u) : s_segm[it];
     const int nseg = __popc(smask);
     // segment [qq, e) of the row from the remaining start bits
     auto seg_next = [&](unsigned& rem, int& qq, int& e) {
