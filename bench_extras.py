@@ -282,7 +282,7 @@ def cfg3(dev, steps=3, B=65536, pooling=20, permuted=False, tables=26, peaks=Non
     step()
     torch.cuda.synchronize()
     st = eng.check_errors()
-    st["U"] = eng.status()["U"]
+    st.update(eng.plan_counts())  # S and U of the last table's plan, counted on the device
     ms_loop = _time_graph(step, steps, warmup=1)
     del eng
     # the same 26 tables through ONE table-batched handle (§8 f1): one plan /
