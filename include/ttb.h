@@ -163,6 +163,20 @@ int ttb_cores_modified(ttb_handle *h);
 int ttb_sgd_update(float *param, const float *grad, double *velocity,
                    int64_t n, double lr, double momentum, ttb_stream stream);
 
+/* ttb_sgd_update over several parameters in ONE launch (DlrmModel's
+ * per-parameter update loop, model.py:353-364): the same arithmetic per
+ * element (fp64 velocity, one rounding), so the result is bitwise that of
+ * `count` ttb_sgd_update calls. velocity may be NULL per tensor when
+ * momentum == 0. The array lives in host memory (copied at launch). */
+typedef struct {
+  float *param;
+  const float *grad;
+  double *velocity;
+  int64_t n;
+} ttb_sgd_tensor;
+int ttb_sgd_update_multi(const ttb_sgd_tensor *tensors, int count, double lr, double momentum,
+                         ttb_stream stream);
+
 /* fused_update with the reference's validation (backward.py:186-204): the
  * gradient is checked for non-finite values first (TTB_ERRBIT_NONFINITE is
  * OR-ed into the caller's DEVICE int *err), and the update runs only if *err

@@ -36,7 +36,7 @@ OPT_ALLOW_EMPTY = 3
 # every symbol include/ttb.h declares (tests check the .so exports them all)
 EXPORTS = [
     "ttb_abi_version", "ttb_strerror", "ttb_last_cuda_error", "ttb_launch_count", "ttb_workspace_bytes", "ttb_create",
-    "ttb_destroy", "ttb_batched_workspace_bytes", "ttb_create_batched", "ttb_plan", "ttb_forward", "ttb_backward", "ttb_aggregate", "ttb_backward_sgd", "ttb_cores_modified", "ttb_sgd_update", "ttb_backward_adagrad", "ttb_adagrad_update", "ttb_dp_flag_words", "ttb_dp_exchange_update",
+    "ttb_destroy", "ttb_batched_workspace_bytes", "ttb_create_batched", "ttb_plan", "ttb_forward", "ttb_backward", "ttb_aggregate", "ttb_backward_sgd", "ttb_cores_modified", "ttb_sgd_update", "ttb_sgd_update_multi", "ttb_backward_adagrad", "ttb_adagrad_update", "ttb_dp_flag_words", "ttb_dp_exchange_update",
     "ttb_ipc_handle", "ttb_ipc_open", "ttb_ipc_close",
     "ttb_check_finite", "ttb_sgd_update_checked", "ttb_export_fast_plan", "ttb_plan_counts",
     "ttb_read_status", "ttb_status_word", "ttb_export_plan", "ttb_export_unique", "ttb_export_slots",
@@ -47,6 +47,11 @@ EXPORTS = [
 
 class TtbGeom(C.Structure):
     _fields_ = [("m", C.c_int64 * 3), ("n", C.c_int32 * 3), ("r", C.c_int32 * 4)]
+
+
+class TtbSgdTensor(C.Structure):
+    """ttb_sgd_tensor (include/ttb.h): one parameter of ttb_sgd_update_multi."""
+    _fields_ = [("param", C.c_void_p), ("grad", C.c_void_p), ("velocity", C.c_void_p), ("n", C.c_int64)]
 
 
 _vp = C.c_void_p
@@ -71,6 +76,7 @@ _PROTOS = {
     "ttb_backward_sgd": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _dbl, _int, _vp]),
     "ttb_cores_modified": (_int, [_vp]),
     "ttb_sgd_update": (_int, [_vp, _vp, _vp, _i64, _dbl, _dbl, _vp]),
+    "ttb_sgd_update_multi": (_int, [C.POINTER(TtbSgdTensor), _int, _dbl, _dbl, _vp]),
     "ttb_backward_adagrad": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _dbl, _int, _vp]),
     "ttb_adagrad_update": (_int, [_vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _vp]),
     "ttb_dp_flag_words": (C.c_size_t, [_int]),

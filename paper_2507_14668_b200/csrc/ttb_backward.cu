@@ -349,6 +349,50 @@ cudaError_t launch_sgd(float* p, const float* g, double* v, int64_t n, double lr
   return cudaGetLastError();
 }
 
+// several parameters in one launch: a thread's element i of the packed range
+// belongs to the last tensor whose start is <= i (<= kSgdMulti tensors)
+struct SgdMulti {
+  float* p[kSgdMulti];
+  const float* g[kSgdMulti];
+  double* v[kSgdMulti];
+  int64_t start[kSgdMulti + 1];
+  int count;
+};
+__global__ void k_sgd_multi(SgdMulti a, double lr, double mu) {
+  pdl_enter();
+  const int64_t total = a.start[a.count];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = a.count - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (a.start[mid] <= i) lo = mid;
+      else hi = mid - 1;
+    }
+    const int64_t j = i - a.start[lo];
+    a.p[lo][j] = sgd_apply(a.p[lo][j], a.g[lo][j], a.v[lo] ? a.v[lo] + j : nullptr, lr, mu);
+  }
+}
+
+cudaError_t launch_sgd_multi(const ttb_sgd_tensor* t, int count, double lr, double mu, cudaStream_t s) {
+  for (int b = 0; b < count; b += kSgdMulti) {
+    SgdMulti a = {};
+    a.count = count - b < kSgdMulti ? count - b : kSgdMulti;
+    for (int k = 0; k < a.count; ++k) {
+      a.p[k] = t[b + k].param;
+      a.g[k] = t[b + k].grad;
+      a.v[k] = t[b + k].velocity;
+      a.start[k + 1] = a.start[k] + t[b + k].n;
+    }
+    if (a.start[a.count] == 0) continue;
+    int64_t grid = (a.start[a.count] + kBlock - 1) / kBlock;
+    if (grid > 148 * 8) grid = 148 * 8;
+    cudaError_t e = launch_pdl(k_sgd_multi, dim3((int)grid), dim3(kBlock), 0, s, a, lr, mu);
+    if (e) return e;
+    count_launch();
+  }
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- dispatch
 template <class D>
 static size_t prefix_smem(const D& d, int ch) {

@@ -1,3 +1,4 @@
+#include <vector>
 // extern "C" entry points (include/ttb.h): handle, workspace layout, checks.
 #include <stdlib.h>
 #include <string.h>
@@ -475,6 +476,17 @@ int ttb_sgd_update(float* param, const float* grad, double* velocity, int64_t n,
   if (momentum > 0.0 && !velocity) return TTB_EINVAL;
   if (momentum == 0.0) velocity = nullptr;
   return cuda_status(launch_sgd(param, grad, velocity, n, lr, momentum, (cudaStream_t)stream));
+}
+
+int ttb_sgd_update_multi(const ttb_sgd_tensor* tensors, int count, double lr, double momentum, ttb_stream stream) {
+  if (count < 0 || (count > 0 && !tensors) || !(lr >= 0.0) || !(momentum >= 0.0 && momentum < 1.0)) return TTB_EINVAL;
+  std::vector<ttb_sgd_tensor> t(tensors, tensors + count);
+  for (auto& x : t) {
+    if (x.n < 0 || (x.n > 0 && (!x.param || !x.grad)) || (momentum > 0.0 && x.n > 0 && !x.velocity))
+      return TTB_EINVAL;
+    if (momentum == 0.0) x.velocity = nullptr;  // (as ttb_sgd_update)
+  }
+  return cuda_status(launch_sgd_multi(t.data(), count, lr, momentum, (cudaStream_t)stream));
 }
 
 int ttb_check_finite(const float* grad, int64_t n, int* err, ttb_stream stream) {

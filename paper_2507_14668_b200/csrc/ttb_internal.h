@@ -238,6 +238,8 @@ cudaError_t fast_forward(ttb_handle* h, const float* c0, const float* c1, const 
 cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const float* c2, const float* gout,
                           float* g0, float* g1, float* g2, float* p0, float* p1, float* p2, double* v0, double* v1,
                           double* v2, double lr, double mu, int mask, int mode, cudaStream_t s, int adagrad = 0);
+constexpr int kSgdMulti = 32;  // tensors per k_sgd_multi launch
+cudaError_t launch_sgd_multi(const ttb_sgd_tensor* t, int count, double lr, double mu, cudaStream_t s);
 cudaError_t launch_sgd(float* p, const float* g, double* v, int64_t n, double lr, double mu, cudaStream_t s,
                        const int* err = nullptr);
 cudaError_t launch_adagrad(float* p, const float* g, double* st, int64_t n, double lr, double eps, cudaStream_t s,

@@ -333,6 +333,9 @@ class DlrmModel(nn.Module):
         z.backward(gz)
         lib = nat.load()
         with torch.no_grad():
+            # every non-core parameter in one launch (ttb_sgd_update_multi:
+            # the arithmetic of ttb_sgd_update per element)
+            upd, keep = [], []
             for name, p in self.named_ref_params():
                 if ".core" in name:
                     continue  # TT cores: fused update already applied
@@ -344,8 +347,10 @@ class DlrmModel(nn.Module):
                     if v is None:
                         v = torch.zeros(p.shape, dtype=torch.float64, device=p.device)
                         self._velocity[name] = v
-                nat.check(lib.ttb_sgd_update(_ptr(p), _ptr(g), _ptr(v), p.numel(), float(lr), float(momentum),
-                                             _stream()), "sgd_update")
+                keep.append(g)
+                upd.append((p.data_ptr(), g.data_ptr(), v.data_ptr() if v is not None else None, p.numel()))
+            arr = (nat.TtbSgdTensor * max(len(upd), 1))(*[nat.TtbSgdTensor(*u) for u in upd])
+            nat.check(lib.ttb_sgd_update_multi(arr, len(upd), float(lr), float(momentum), _stream()), "sgd_update")
         return float(loss) if sync_loss else loss
 
 

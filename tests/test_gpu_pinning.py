@@ -310,3 +310,33 @@ def test_dense_field_empty_and_multi_index_bags():
     out = f(idx, off)
     rows = f.rows.detach()
     assert torch.allclose(out[0], rows[3] + rows[7]) and torch.equal(out[1], torch.zeros_like(out[1]))
+
+
+def test_sgd_update_multi_matches_single_updates():
+    """ttb_sgd_update_multi (DlrmModel's one-launch update of every non-core
+    parameter) is bitwise `count` ttb_sgd_update calls, with and without
+    momentum, across more tensors than one launch holds (32)."""
+    import ctypes as C
+    from paper_2507_14668_b200 import _native as nat
+    from paper_2507_14668_b200.engine import _ptr, _stream
+    lib = nat.load()
+    torch.manual_seed(0)
+    sizes = [1, 3, 64, 1000, 17] * 8  # 40 tensors
+    for mu in (0.0, 0.9):
+        ps = [torch.randn(n, device="cuda") for n in sizes]
+        gs = [torch.randn(n, device="cuda") for n in sizes]
+        vs = [torch.randn(n, device="cuda", dtype=torch.float64) for n in sizes]
+        p1, v1 = [p.clone() for p in ps], [v.clone() for v in vs]
+        for p, g, v in zip(p1, gs, v1):
+            nat.check(lib.ttb_sgd_update(_ptr(p), _ptr(g), _ptr(v), p.numel(), 0.05, mu, _stream()))
+        arr = (nat.TtbSgdTensor * len(sizes))(*[nat.TtbSgdTensor(p.data_ptr(), g.data_ptr(), v.data_ptr(), p.numel())
+                                                for p, g, v in zip(ps, gs, vs)])
+        nat.check(lib.ttb_sgd_update_multi(arr, len(sizes), 0.05, mu, _stream()))
+        torch.cuda.synchronize()
+        for a, b in zip(ps, p1):
+            assert torch.equal(a, b)
+        if mu > 0:
+            for a, b in zip(vs, v1):
+                assert torch.equal(a, b)
+    with pytest.raises(ValueError):
+        nat.check(lib.ttb_sgd_update_multi(arr, len(sizes), -1.0, 0.9, _stream()))
