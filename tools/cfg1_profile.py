@@ -22,4 +22,5 @@ with profile(activities=[ProfilerActivity.CUDA]) as prof:
     torch.cuda.synchronize()
 ka = prof.key_averages()
 print("kernels per step:", sum(k.count for k in ka), "gpu us:", sum(k.device_time_total for k in ka))
-print(ka.table(sort_by="cuda_time_total", row_limit=40, max_name_column_width=60))
+for k in sorted(ka, key=lambda k: -k.device_time_total)[:40]:
+    print(f"{k.count:4d} {k.device_time_total:9.1f} us  {k.key[:90]}")
