@@ -390,14 +390,15 @@ struct SgdArgs {
 };
 
 // ------------------------------------------------------------ row sort
-// Pooled batches: before the backward, every run of <= kSortItems full items
-// of one prefix (a plan chunk) is counting-sorted by i3 in shared memory, so
-// the lookups of one row sit together and an item of a hot prefix holds one or
-// two rows instead of a scatter of them — the row-grouped backward then does
-// X^T g, the dG3 reduction and the Z update once per (item, row), with the
-// row's gradient rows summed first (the reference's unique_aggregate,
+// Pooled batches, at the end of the plan: every run of <= kSortItems full
+// items of one prefix (a plan chunk) is counting-sorted by i3 in shared
+// memory, so the lookups of one row sit together and an item of a hot prefix
+// holds one or two rows instead of a scatter of them: the forward closes each
+// row once per item and pools it into every lookup's bag, and the row-grouped
+// backward does X^T g, the dG3 reduction and the Z update once per (item, row)
+// with the row's gradient rows summed first (the reference's unique_aggregate,
 // backward.py:72-87, applied inside each chunk). Item boundaries, keys and
-// tiles are unchanged; the forward has already consumed the plan order.
+// tiles are unchanged.
 constexpr int kSortMax = kSortItems * kItemLen;  // positions per chunk
 constexpr int kSortThreads = 512;
 constexpr int kSortPer = kSortMax / kSortThreads;  // positions per thread (CTA-wide chunks), in registers
@@ -879,11 +880,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
     // segments (runs of one bag) of each item as a bit mask of their first
     // positions: one ballot per item instead of every epilogue thread
     // re-scanning its item's (bag, i3) list
-    // (one lookup per bag: every position starts a segment)
+    // (one lookup per bag: every position starts a segment). Pooled bags:
+    // a segment is a run of one ROW (equal i3; the plan's row sort groups a
+    // hot prefix's lookups by row), closed once and pooled into each of its
+    // lookups' bags
     if (!direct) {
       for (int j = warp; j < m->n; j += kFwdThreads / 32) {
         const int j0 = m->start[j] - p0, len = m->start[j + 1] - m->start[j];
-        const int bg = lane < len ? s_sbi[j0 + lane].x : -1;
+        const int bg = lane < len ? (kPooled ? s_sbi[j0 + lane].y : s_sbi[j0 + lane].x) : -1;
         const int pv = __shfl_up_sync(0xffffffffu, bg, 1);
         const unsigned mk = __ballot_sync(0xffffffffu, lane < len && (lane == 0 || bg != pv));
         if (lane == 0) s_segm[j] = mk;
@@ -925,7 +929,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
   #pragma unroll
         for (int i = 0; i < 16; ++i) acc[i] = 0.f;
         if (have) {
-          for (int l = qq; l < e; ++l) {
+          for (int l = qq; l < (kPooled ? qq + 1 : e); ++l) {  // (pooled: one row, one slice)
             const float4* g3 = s_g3 + (unsigned)s_sbi[l].y + 8 * quarter * m3;
   #pragma unroll
             for (int c = 0; c < 8; ++c) {
@@ -962,9 +966,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
                 reinterpret_cast<float4*>(o)[bb] =
                     make_float4(acc[4 * bb], acc[4 * bb + 1], acc[4 * bb + 2], acc[4 * bb + 3]);
             } else {
+              for (int l = qq; l < (kPooled ? e : qq + 1); ++l) {  // (pooled: the row into each lookup's bag)
+                float* ol = kPooled ? out + (size_t)s_sbi[l].x * NOUT + a * 16 : o;
   #pragma unroll
-              for (int bb = 0; bb < 4; ++bb)
-                red_v4(o + 4 * bb, acc[4 * bb], acc[4 * bb + 1], acc[4 * bb + 2], acc[4 * bb + 3]);
+                for (int bb = 0; bb < 4; ++bb)
+                  red_v4(ol + 4 * bb, acc[4 * bb], acc[4 * bb + 1], acc[4 * bb + 2], acc[4 * bb + 3]);
+              }
             }
           }
         }
@@ -990,30 +997,18 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
 #pragma unroll
         for (int i = 0; i < 16; ++i) acc[i] = 0.f;
         if (kPooled) {
-          // per quarter of c: the segment's G3 slices summed first, then one
-          // rank-8 update of the 16 outputs (a segment of k lookups costs 512
-          // FMA + 128 (k - 1) adds instead of 512 k FMA)
+          // per quarter of c: the run's row closed once (a rank-8 update of
+          // the 16 outputs per quarter), then pooled into each lookup's bag
 #pragma unroll
           for (int cq = 0; cq < 4; ++cq) {
             float xq[32];  // xq[4 c' + b] = X[item][a][b][8 cq + c']
             umma::tmem_ld32(trow + 32 * cq, xq);
             if (have) {
-              float4 gs[8];
+              float4 gs[8];  // the run's row: one G3 slice
               {
                 const float4* g3 = s_g3 + (unsigned)s_sbi[qq].y + 8 * cq * m3;
 #pragma unroll
                 for (int c = 0; c < 8; ++c) gs[c] = g3[c * m3];
-              }
-              for (int l = qq + 1; l < e; ++l) {
-                const float4* g3 = s_g3 + (unsigned)s_sbi[l].y + 8 * cq * m3;
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                  const float4 gv = g3[c * m3];
-                  gs[c].x += gv.x;
-                  gs[c].y += gv.y;
-                  gs[c].z += gv.z;
-                  gs[c].w += gv.w;
-                }
               }
 #pragma unroll
               for (int c = 0; c < 8; ++c)
@@ -1059,8 +1054,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
             for (int b = 0; b < 4; ++b)
               reinterpret_cast<float4*>(o)[b] = make_float4(acc[4 * b], acc[4 * b + 1], acc[4 * b + 2], acc[4 * b + 3]);
           } else {
+            for (int l = qq; l < (kPooled ? e : qq + 1); ++l) {  // (pooled: the row into each lookup's bag)
+              float* ol = kPooled ? out + (size_t)s_sbi[l].x * NOUT + a * 16 : o;
 #pragma unroll
-            for (int b = 0; b < 4; ++b) red_v4(o + 4 * b, acc[4 * b], acc[4 * b + 1], acc[4 * b + 2], acc[4 * b + 3]);
+              for (int b = 0; b < 4; ++b)
+                red_v4(ol + 4 * b, acc[4 * b], acc[4 * b + 1], acc[4 * b + 2], acc[4 * b + 3]);
+            }
           }
         }
       }
@@ -1736,6 +1735,7 @@ cudaError_t fast_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* 
       return e;
     if (occ < 1) return cudaErrorCooperativeLaunchTooLarge;
   }
+  {
   ProfScope _ps(h, s, "f_plan");
   if (idx64)
     e = launch_pdl_coop(k_fplan<long long>, dim3(grid), dim3(kPlanThreads), 0, s, (const long long*)idx, offsets, T, B,
@@ -1748,8 +1748,18 @@ cudaError_t fast_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* 
                    w.f_item_key,
                    w.f_tile_info, w.f_sbi, w.fast_hdr, getenv("TTB_DBG") ? 1 : 0, h->allow_empty,
                    (const uint4*)w.f_tgeom, w.f_chunks);
+  }
   if (e) return e;
   count_launch();
+  if (T > B) {  // pooled: each multi-item prefix's lookups grouped by row (forward and backward use it)
+    constexpr int sort_smem = kSortSmem;
+    if ((e = ensure_kernel_smem((const void*)k_rowsort, sort_smem))) return e;
+    ProfScope _pr(h, s, "f_rowsort");
+    if ((e = launch_pdl(k_rowsort, dim3(h->num_sms), dim3(kSortThreads), sort_smem, s, w.f_sbi,
+                        (const int2*)w.f_chunks, (const int*)w.fast_hdr, h->kg.tm3)))
+      return e;
+    count_launch();
+  }
   return cudaGetLastError();
 }
 
@@ -1821,16 +1831,8 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
   // reads it in that order, the caller's buffer gets the reference layout
   float* g3s = w.f_grad + n0 + n1;
   const int grid = h->num_sms;  // = the plan's CTA ranges (k_fplan cta_tiles)
-  if (h->T > h->B) {  // pooled: each multi-item prefix's lookups grouped by row
+  if (h->T > h->B)  // pooled: the backward's tile counter
     if ((e = cudaMemsetAsync(w.fast_hdr + kHdrNextTile, 0, sizeof(int), s))) return e;
-    constexpr int sort_smem = kSortSmem;
-    if ((e = ensure_kernel_smem((const void*)k_rowsort, sort_smem))) return e;
-    ProfScope _pr(h, s, "f_rowsort");
-    if ((e = launch_pdl(k_rowsort, dim3(h->num_sms), dim3(kSortThreads), sort_smem, s, w.f_sbi,
-                        (const int2*)w.f_chunks, (const int*)w.fast_hdr, h->kg.tm3)))
-      return e;
-    count_launch();
-  }
   {
     ProfScope _ps(h, s, "f_bwd");
     // pooled bags (more lookups than bags) repeat rows inside a prefix: group
