@@ -945,6 +945,30 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
             }
           }
         }
+        if (kPooled) {
+          // a row run pools into several bags: every quarter writes its
+          // partials and takes the sum of one b block (4 outputs), so the
+          // run's reductions into its lookups' bags are split four ways
+          umma::tmem_st16(tpart + 16 * quarter, acc);
+          umma::tmem_wait_st();
+          named_sync(1 + q4, 128);
+          uint32_t pq[4][4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) umma::tmem_ld4_nw(tpart + 16 * j + 4 * quarter, pq[j]);
+          umma::tmem_wait_ld();
+          float sb[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            sb[i] = (__uint_as_float(pq[0][i]) + __uint_as_float(pq[1][i])) +
+                    (__uint_as_float(pq[2][i]) + __uint_as_float(pq[3][i]));
+          if (have)
+            for (int l = qq; l < e; ++l)
+              red_v4(out + (size_t)s_sbi[l].x * NOUT + a * 16 + 4 * quarter, sb[0], sb[1], sb[2], sb[3]);
+          umma::fence_before_sync();
+          named_sync(1 + q4, 128);  // partial columns free for the next round
+          umma::fence_after_sync();
+          continue;
+        }
         if (quarter != 0) {
           umma::tmem_st16(tpart + 16 * quarter, acc);
           umma::tmem_wait_st();
