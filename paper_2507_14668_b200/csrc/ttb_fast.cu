@@ -1144,7 +1144,6 @@ constexpr int kStSbi = kChunkPos * 8, kStG = kChunkPos * 256, kStG3 = kChunkPos 
 constexpr int kBwdSmem = 4 * kImg + 4 * kImg + kStSbi + kStG + kStG3 + 1024;
 // row-grouped backward (pooled batches): G3 slices are read per distinct row
 // from L2 instead of staged per position, so a chunk holds 3x the positions
-constexpr int kChunkRows = (kStSbi + kStG + kStG3 - (kThreads / 32) * 256) / (8 + 256) & ~7;  // + per-warp 256 B row scratch
 // warps per TMEM lane quadrant, and the columns each takes of a 128- / 32-column operand
 constexpr int kQuadWarps = kThreads / 128, kSpan = 128 / kQuadWarps, kRedCols = 32 / kQuadWarps;
 static_assert(kSpan == 32 && kRedCols == 8, "column split below assumes 16 warps");
@@ -1226,15 +1225,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
   char* r2_lo = sm + 3 * kImg;
   char* zi = sm + 4 * kImg;  // X / Z slots, then the Z image
   float* xs = reinterpret_cast<float*>(zi);
-  constexpr int kCap = kRows ? kChunkRows : kChunkPos;  // positions per staged chunk
+  // staged per chunk: the (bag, i3) list and, one lookup per bag, the
+  // gradient rows and G3 slices. The row path stages the whole tile's list
+  // only: a row's gradient rows are summed straight from L2 (after the plan's
+  // row sort an item holds one or two rows, so few sums per item)
+  constexpr int kCap = kRows ? kMaxTilePos : kChunkPos;  // positions per staged chunk
   int2* st_sbi = reinterpret_cast<int2*>(sm + 8 * kImg);
   float4* st_g = reinterpret_cast<float4*>(sm + 8 * kImg + kCap * 8);
   float4* st_g3 = st_g + kCap * 16;  // per-position G3 slices (bag-run path only)
-  float4* st_acc = st_g + kCap * 16;  // row path: per-warp summed gradient row
-  // Z lo image: the dead staging rows past the next tile's (bag, i3) list
-  // (bag-run path: exactly the G3-slice staging, so the next tile's gradient
-  // rows can stream in while the E GEMM runs)
-  char* zlo = sm + 8 * kImg + (kRows ? 4096 : kChunkPos * 8 + kChunkPos * 256);
+  float4* st_acc = st_g;             // row path: per-warp summed gradient row (16 x 256 B)
+  // Z lo image: the dead staging past the next tile's (bag, i3) list (bag-run
+  // path: exactly the G3-slice staging, so the next tile's gradient rows can
+  // stream in while the E GEMM runs; row path: past the row scratch)
+  char* zlo = sm + 8 * kImg + (kRows ? kMaxTilePos * 8 + 4096 : kChunkPos * 8 + kChunkPos * 256);
   __shared__ TileMeta s_m[2];
   __shared__ int s_chunk[2][kTileItems + 2];
   // SIMT -> MMA warp: G1 rows staged / Z^T in TMEM + G1^T staged / Z images
@@ -1373,6 +1376,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
   // a chunk's per-position rows (cp.async): the bag's gradient row and, one
   // lookup per bag, the lookup's slice-major G3 slice (512 contiguous bytes)
   auto stage_rows = [&](int np, unsigned i3base) {
+    if (kRows) return;  // (row path: gradient rows read from L2 when summed)
     for (int e = threadIdx.x; e < np * 16; e += kThreads)
       cp_async16(st_g + e, gout + (size_t)st_sbi[e >> 4].x * NOUT + 4 * (e & 15));
     if (!kRows)
@@ -1478,6 +1482,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
           // reduction and Z one rank-4 update per distinct row of the item
           const int s0 = m->start[it] - p0, nq = m->start[it + 1] - p0 - s0;
           const int my_i3 = lane < nq ? (int)i3b + st_sbi[s0 + lane].y : -1;
+          const int my_bag = lane < nq ? st_sbi[s0 + lane].x : 0;
           const unsigned grp = __match_any_sync(0xffffffffu, lane < nq ? my_i3 : (int)(0x80000000u | lane));
           unsigned lead = __ballot_sync(0xffffffffu, lane < nq && (__ffs(grp) - 1) == lane);
           while (lead) {
@@ -1486,28 +1491,29 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
             unsigned mem = __shfl_sync(0xffffffffu, grp, ld);
             const int i3 = __shfl_sync(0xffffffffu, my_i3, ld);
             const float4 h3 = __ldg(reinterpret_cast<const float4*>(g3t) + (size_t)i3 * 32 + lane);
-            // the row's summed gradient row: lane-parallel (two floats per
-            // lane per member) into the warp's scratch, then broadcast reads
-            const float4* src = st_g + (s0 + ld) * 16;
-            if (mem & (mem - 1)) {
+            // the row's summed gradient row: its lookups' bag rows read from
+            // L2 (two floats per lane per member, eight members in flight)
+            // into the warp's scratch, then broadcast reads
+            {
               float2 acc = make_float2(0.f, 0.f);
-              while (mem) {  // four members' loads in flight per round
-                float2 w[4];
+              while (mem) {
+                float2 w[8];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < 8; ++q) {
                   w[q] = make_float2(0.f, 0.f);
                   if (mem) {
-                    w[q] = reinterpret_cast<const float2*>(st_g + (s0 + __ffs(mem) - 1) * 16)[lane];
+                    const int bg = __shfl_sync(0xffffffffu, my_bag, __ffs(mem) - 1);
                     mem &= mem - 1;
+                    w[q] = __ldg(reinterpret_cast<const float2*>(gout + (size_t)bg * NOUT) + lane);
                   }
                 }
-                acc.x += (w[0].x + w[1].x) + (w[2].x + w[3].x);
-                acc.y += (w[0].y + w[1].y) + (w[2].y + w[3].y);
+                acc.x += ((w[0].x + w[1].x) + (w[2].x + w[3].x)) + ((w[4].x + w[5].x) + (w[6].x + w[7].x));
+                acc.y += ((w[0].y + w[1].y) + (w[2].y + w[3].y)) + ((w[4].y + w[5].y) + (w[6].y + w[7].y));
               }
               reinterpret_cast<float2*>(st_acc + warp * 16)[lane] = acc;
               __syncwarp();
-              src = st_acc + warp * 16;
             }
+            const float4* src = st_acc + warp * 16;
             float dh[4] = {0.f, 0.f, 0.f, 0.f};
             lookup_update(src, x, z, h3, dh);
             __syncwarp();  // the scratch is rewritten by the next row
