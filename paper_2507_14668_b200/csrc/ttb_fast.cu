@@ -434,23 +434,46 @@ __global__ void __launch_bounds__(kSortThreads) k_rowsort(int2* __restrict__ sbi
     const int2 cd = chunks[ci];
     const int p0 = cd.x, L = cd.y;
     if (L <= kSortSmall) continue;  // (uniform)
-    int* hc = hist[0];
+    // per-warp histograms (no atomics: a bin's count is updated by its
+    // match leader only), combined into per-warp cursors
     int2 v[kSortPer];
 #pragma unroll
     for (int r = 0; r < kSortPer; ++r) {
       const int i = r * kSortThreads + threadIdx.x;
       v[r] = i < L ? sbi[p0 + i] : make_int2(0, -1 - lane);
     }
-    for (int i = threadIdx.x; i < (int)tm3; i += kSortThreads) hc[i] = 0;
+    constexpr int NW = kSortThreads / 32;
+    for (int i = threadIdx.x; i < NW * kSortHist; i += kSortThreads) (&hist[0][0])[i] = 0;
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kSortPer; ++r) {
       if (r * kSortThreads >= L) break;  // (uniform)
       const unsigned peers = __match_any_sync(0xffffffffu, v[r].y);
-      if (v[r].y >= 0 && (__ffs(peers) - 1) == lane) atomicAdd(&hc[v[r].y], __popc(peers));
+      if (v[r].y >= 0 && (__ffs(peers) - 1) == lane) hist[warp][v[r].y] += __popc(peers);
+      __syncwarp();
     }
     __syncthreads();
-    if (warp == 0) warp_exclusive_scan(hc, tm3, lane);
+    // bin b: warp w's cursor = start_b + (counts of warps < w); bin totals in
+    // hist[NW - 1] (scanned by warp 0), then added back
+    __shared__ int s_tot[kSortHist];
+    for (int b = threadIdx.x; b < (int)tm3; b += kSortThreads) {
+      int run = 0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        const int h = hist[w][b];
+        hist[w][b] = run;
+        run += h;
+      }
+      s_tot[b] = run;
+    }
+    __syncthreads();
+    if (warp == 0) warp_exclusive_scan(s_tot, tm3, lane);
+    __syncthreads();
+    for (int b = threadIdx.x; b < (int)tm3; b += kSortThreads) {
+      const int st = s_tot[b];
+#pragma unroll
+      for (int w = 0; w < NW; ++w) hist[w][b] += st;
+    }
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kSortPer; ++r) {
@@ -458,9 +481,13 @@ __global__ void __launch_bounds__(kSortThreads) k_rowsort(int2* __restrict__ sbi
       const unsigned peers = __match_any_sync(0xffffffffu, v[r].y);
       const int ld = __ffs(peers) - 1;
       int base = 0;
-      if (v[r].y >= 0 && ld == lane) base = atomicAdd(&hc[v[r].y], __popc(peers));
+      if (v[r].y >= 0 && ld == lane) {
+        base = hist[warp][v[r].y];
+        hist[warp][v[r].y] = base + __popc(peers);
+      }
       base = __shfl_sync(0xffffffffu, base, ld);
       if (v[r].y >= 0) o[base + __popc(peers & lanemask_lt())] = v[r];
+      __syncwarp();
     }
     __syncthreads();
     for (int i = threadIdx.x; i < L; i += kSortThreads) sbi[p0 + i] = o[i];
