@@ -1589,14 +1589,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
     umma::tmem_st32(tl + 128 + kSpan * qw, zh);
     umma::tmem_st32(tl + 256 + kSpan * qw, zl);
     umma::tmem_wait_st();
-    cp_async_wait_all();  // G2 k / G1^T images (issued before the Z phase)
+    cp_async_wait_all();  // G1^T image (issued before the Z phase), next tile's metadata (warp 15)
     if (threadIdx.x == 0) s_acc2 = m->i2 == prev_i2;
+    if (warp == kThreads / 32 - 1 && has_next) {  // the next tile's chunk list, from the metadata this warp fetched
+      __syncwarp();
+      if (lane == 0) make_chunks(mn, s_chunk[slot ^ 1], kCap);
+    }
     simt_sync_for_mma();  // every slot read before the image overwrites them; Z^T is in TMEM
     if (threadIdx.x == 0) umma::mbar_arrive(&s_mb_z);  // -> dG2 MMAs
-    // ---- next tile: chunk list and first chunk's positions
+    // ---- next tile: first chunk's positions
     if (has_next) {
-      if (threadIdx.x == 0) make_chunks(mn, s_chunk[slot ^ 1], kCap);
-      simt_sync();
       npn = mn->start[s_chunk[slot ^ 1][1]] - mn->start[0];
       for (int e = threadIdx.x; e < npn; e += kThreads) cp_async8(st_sbi + e, sbi + mn->start[0] + e);
       cp_async_commit();
