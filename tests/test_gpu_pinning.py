@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 
 FWD_TOL = 1e-5
 GRAD_TOL = 1e-4
-ITEM_LEN, TILE_ITEMS = 32, 32
+ITEM_LEN, TILE_ITEMS, SORT_ITEMS = 32, 32, 256  # ttb_fast.cuh kItemLen, kTileItems, kSortItems
 
 
 def rel_err(got, want, floor=1e-3):
@@ -181,6 +181,20 @@ def test_fast_plan_structure_bit_exact(case):
     # CTA ranges
     cta = fp["cta_tiles"].astype(np.int64)
     assert cta[0] == 0 and cta[-1] == tiles and np.all(np.diff(cta) >= 0)
+    # pooled batches (k_rowsort): a prefix with >= 2 full items has them on
+    # contiguous positions, sorted by i3 inside each run of SORT_ITEMS items
+    if idx.size > off.size - 1:
+        i3 = sbi[:, 1].astype(np.int64)
+        full = lens == ITEM_LEN
+        for k in ik[icnt >= 2]:
+            fi = np.nonzero((key == k) & full)[0]
+            if fi.size < 2:
+                continue
+            p0 = start[fi[0]]
+            assert np.array_equal(start[fi], p0 + ITEM_LEN * np.arange(fi.size)), (name, k)
+            for c in range(0, fi.size, SORT_ITEMS):
+                seg = i3[p0 + c * ITEM_LEN: p0 + min(fi.size, c + SORT_ITEMS) * ITEM_LEN]
+                assert np.all(np.diff(seg) >= 0), (name, k, c)
 
 
 @pytest.mark.parametrize("pool,permuted", [(1, False), (20, False), (20, True)])
