@@ -1172,6 +1172,10 @@ constexpr int kBwdSmem = 4 * kImg + 4 * kImg + kStSbi + kStG + kStG3 + 1024;
 // row-grouped backward (pooled batches): G3 slices are read per distinct row
 // from L2 instead of staged per position, so a chunk holds 3x the positions
 // warps per TMEM lane quadrant, and the columns each takes of a 128- / 32-column operand
+// row path: per-warp ring of row slots in the Z lo image's region (dead
+// during the Z phase): gradient row (256 B) + G3 slice (512 B) per slot
+constexpr int kRing = 4, kRingSlot = 768;
+static_assert((kThreads / 32) * kRing * kRingSlot <= 4 * kImg, "ring exceeds the Z lo image's region");
 constexpr int kQuadWarps = kThreads / 128, kSpan = 128 / kQuadWarps, kRedCols = 32 / kQuadWarps;
 static_assert(kSpan == 32 && kRedCols == 8, "column split below assumes 16 warps");
 
@@ -1272,6 +1276,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
   // cb / k images (issued and waited for by the MMA warp)
   __shared__ uint64_t s_mb_xop, s_mb_z, s_mb_zi, s_mb_x, s_mb_e, s_mb_xtma, s_mb_ktma;
   __shared__ int s_acc2;
+  // row path: the Z phase's next item of the tile in each slot (warps take
+  // items dynamically: an item's cost follows its distinct rows, not its length)
+  __shared__ int s_itc[2];
   // tile of each metadata slot (-1: none). Pooled batches take tiles from a
   // global counter (hdr[kHdrNextTile]): after the row sort, a tile's cost no
   // longer follows its lookup count, so the plan's static ranges would leave
@@ -1282,6 +1289,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tb = cta_tiles[blockIdx.x], te = cta_tiles[blockIdx.x + 1];  // weight-balanced (k_fplan)
   if (threadIdx.x < 12) s_tacc[threadIdx.x] = 0;
+  if (threadIdx.x < 2) s_itc[threadIdx.x] = 0;
   if (warp == 0) umma::tmem_alloc(&s_tmem, 512);
   if (threadIdx.x == 32) {
     umma::mbar_init(&s_mb_xop, 1);
@@ -1496,7 +1504,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
         if ((dbg & 8) && threadIdx.x == 0 && blockIdx.x == 0) s_tacc[10] += clock64() - _c0;
       }
       // ---- Z / dG3 phase: warp <-> item, lane <-> c
-      for (int it = it0 + warp; it < it1; it += kThreads / 32) {
+      auto take_item = [&](int prev) -> int {
+        if (!kRows) return prev < 0 ? it0 + warp : prev + kThreads / 32;
+        int v = 0;
+        if (lane == 0) v = atomicAdd(&s_itc[slot], 1);
+        return it0 + __shfl_sync(0xffffffffu, v, 0);
+      };
+      for (int it = take_item(-1); it < it1; it = take_item(it)) {
         float x[16], z[16];
 #pragma unroll
         for (int ab = 0; ab < 16; ++ab) {
@@ -1512,16 +1526,44 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
           const int my_bag = lane < nq ? st_sbi[s0 + lane].x : 0;
           const unsigned grp = __match_any_sync(0xffffffffu, lane < nq ? my_i3 : (int)(0x80000000u | lane));
           unsigned lead = __ballot_sync(0xffffffffu, lane < nq && (__ffs(grp) - 1) == lane);
+          // rows stream through this warp's ring of kRing slots (cp.async):
+          // the G3 slice of every row and the gradient row of a one-lookup
+          // row land kRing - 1 rows ahead of their use, so a warp keeps
+          // several rows' L2 / HBM reads in flight instead of one
+          char* ring = zlo + warp * (kRing * kRingSlot);
+          unsigned lead_iss = lead;
+          auto issue = [&](int sl) {
+            if (lead_iss) {
+              const int ld = __ffs(lead_iss) - 1;
+              lead_iss &= lead_iss - 1;
+              const unsigned mem = __shfl_sync(0xffffffffu, grp, ld);
+              const int i3 = __shfl_sync(0xffffffffu, my_i3, ld);
+              const int bg = __shfl_sync(0xffffffffu, my_bag, ld);
+              char* d = ring + sl * kRingSlot;
+              cp_async16(d + 256 + 16 * lane, g3t + ((size_t)i3 * 32 + lane) * 4);
+              if ((mem & (mem - 1)) == 0 && lane < 16) cp_async16(d + 16 * lane, gout + (size_t)bg * NOUT + 4 * lane);
+            }
+            cp_async_commit();
+          };
+#pragma unroll
+          for (int j = 0; j < kRing - 1; ++j) issue(j);
+          int sl = 0;
           while (lead) {
+            issue(sl == 0 ? kRing - 1 : sl - 1);
+            cp_async_wait_group<kRing - 1>();
+            __syncwarp();
             const int ld = __ffs(lead) - 1;
             lead &= lead - 1;
             unsigned mem = __shfl_sync(0xffffffffu, grp, ld);
             const int i3 = __shfl_sync(0xffffffffu, my_i3, ld);
-            const float4 h3 = __ldg(reinterpret_cast<const float4*>(g3t) + (size_t)i3 * 32 + lane);
-            // the row's summed gradient row: its lookups' bag rows read from
-            // L2 (two floats per lane per member, eight members in flight)
-            // into the warp's scratch, then broadcast reads
-            {
+            const char* d = ring + sl * kRingSlot;
+            sl = sl == kRing - 1 ? 0 : sl + 1;
+            const float4 h3 = reinterpret_cast<const float4*>(d + 256)[lane];
+            const float4* src = reinterpret_cast<const float4*>(d);
+            // a row of several lookups: its lookups' bag rows summed from L2
+            // (two floats per lane per member, eight members in flight) into
+            // the warp's scratch, then broadcast reads
+            if (mem & (mem - 1)) {
               float2 acc = make_float2(0.f, 0.f);
               while (mem) {
                 float2 w[8];
@@ -1539,11 +1581,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
               }
               reinterpret_cast<float2*>(st_acc + warp * 16)[lane] = acc;
               __syncwarp();
+              src = st_acc + warp * 16;
             }
-            const float4* src = st_acc + warp * 16;
             float dh[4] = {0.f, 0.f, 0.f, 0.f};
             lookup_update(src, x, z, h3, dh);
-            __syncwarp();  // the scratch is rewritten by the next row
+            __syncwarp();  // the scratch and the slot are rewritten by later rows
             if (!(dbg & 1)) red_v4(dG3 + ((size_t)i3 * 32 + lane) * 4, dh[0], dh[1], dh[2], dh[3]);
             bad |= suspicious(dh[0]) | suspicious(dh[1]) | suspicious(dh[2]) | suspicious(dh[3]);
           }
@@ -1590,7 +1632,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
     umma::tmem_st32(tl + 256 + kSpan * qw, zl);
     umma::tmem_wait_st();
     cp_async_wait_all();  // G1^T image (issued before the Z phase), next tile's metadata (warp 15)
-    if (threadIdx.x == 0) s_acc2 = m->i2 == prev_i2;
+    if (threadIdx.x == 0) {
+      s_acc2 = m->i2 == prev_i2;
+      s_itc[slot] = 0;  // (every warp is past this tile's Z phase; the slot's next tile is two away)
+    }
     if (warp == kThreads / 32 - 1 && has_next) {  // the next tile's chunk list, from the metadata this warp fetched
       __syncwarp();
       if (lane == 0) make_chunks(mn, s_chunk[slot ^ 1], kCap);
