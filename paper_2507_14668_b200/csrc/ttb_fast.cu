@@ -1700,13 +1700,41 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
       umma::tmem_ld8(tl + 448 + kRedCols * qw, v);
       umma::tmem_ld8(tl + 448 + 32 + kRedCols * qw, w2);
       const int it = row >> 2, a = row & 3;
-      if (it < n) {
-        float* d1 = dG1 + ((size_t)item_i1(m, it, g) * 4 + a) * R1 + kRedCols * qw;
+      // a key's full items are contiguous in its tile (and one i2 per tile
+      // makes equal i1 mean equal key): each run of equal i1 is summed inside
+      // the warp (8 items, segmented suffix sums over item offsets 1, 2, 4)
+      // and its first item reduces it, so a hot key's dG1 rows get one
+      // reduction per warp instead of one per item (all CTAs of a hot key hit
+      // the same 512 B)
+      const unsigned i1v = it < n ? item_i1(m, it, g) : 0xFFFFFFFFu;
+      const unsigned prev_i1 = __shfl_up_sync(0xffffffffu, i1v, 4);  // (every lane: full-mask shuffles)
+      const bool head = lane < 4 || prev_i1 != i1v;
+#pragma unroll
+      for (int i = 0; i < kRedCols; ++i) v[i] += w2[i];
+      if (__any_sync(0xffffffffu, !head && it < n)) {  // (warp-uniform; distinct keys only: no sums)
+        int rs = head ? lane >> 2 : -1;  // first item of this item's run (a key may also recur later in the tile)
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, rs, o);
+          if (lane >= o) rs = max(rs, t);
+        }
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+          const int nrs = __shfl_down_sync(0xffffffffu, rs, o);
+          const bool take = nrs == rs && lane + o < 32;
+#pragma unroll
+          for (int i = 0; i < kRedCols; ++i) {
+            const float t = __shfl_down_sync(0xffffffffu, v[i], o);
+            if (take) v[i] += t;
+          }
+        }
+      }
+      if (it < n && head) {
+        float* d1 = dG1 + ((size_t)i1v * 4 + a) * R1 + kRedCols * qw;
 #pragma unroll
         for (int i = 0; i < kRedCols; i += 4) {
-          bad |= suspicious(v[i] + w2[i]) | suspicious(v[i + 1] + w2[i + 1]) | suspicious(v[i + 2] + w2[i + 2]) |
-                 suspicious(v[i + 3] + w2[i + 3]);
-          red_v4(d1 + i, v[i] + w2[i], v[i + 1] + w2[i + 1], v[i + 2] + w2[i + 2], v[i + 3] + w2[i + 3]);
+          bad |= suspicious(v[i]) | suspicious(v[i + 1]) | suspicious(v[i + 2]) | suspicious(v[i + 3]);
+          red_v4(d1 + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
         }
       }
     }
