@@ -759,19 +759,47 @@ __device__ inline void mma3_ss(uint32_t d, uint32_t a_hi, uint32_t a_lo, int a_r
 // t + 2 grid (a register load, consumed an iteration later).
 
 // G1^T image of the tile's items (rows k, K = (item, a)); zero columns past n
-// (one 64-row image: rows k = hi, rows 32 + k = lo)
+// (one 64-row image: rows k = hi, rows 32 + k = lo). Only the first item of
+// each run of one key is copied from global memory: a hot key fills whole
+// tiles with items of one i1, and thousands of copies of the same 512 bytes
+// from every CTA serialise in the memory system; the run's other items are
+// filled from the first one by g1_t_replicate once the copies landed.
+__device__ __forceinline__ unsigned tile_run_heads(const TileMeta* m, int lane) {
+  const unsigned kl = lane < m->n ? m->key[lane] : 0xFFFFFFFFu;
+  const unsigned kp = __shfl_up_sync(0xffffffffu, kl, 1);
+  return __ballot_sync(0xffffffffu, lane == 0 || kl != kp);
+}
 __device__ inline void stage_g1_t_async(const TileMeta* m, KGeom g, const float* __restrict__ g1img, char* img) {
+  const unsigned heads = tile_run_heads(m, threadIdx.x & 31);
 #pragma unroll
   for (int i = 0; i < 1024 / kThreads; ++i) {
     const int e = threadIdx.x + i * kThreads, it = e >> 5, k = e & 31;
     const uint32_t oh = umma::sw128_off(k, 4 * it, 64), ol = umma::sw128_off(32 + k, 4 * it, 64);
     if (it < m->n) {
-      const float* src = g1img + (size_t)item_i1(m, it, g) * kG1Img + kG1T + 4 * k;
-      cp_async16(img + oh, src);
-      cp_async16(img + ol, src + 128);
+      if ((heads >> it) & 1u) {
+        const float* src = g1img + (size_t)item_i1(m, it, g) * kG1Img + kG1T + 4 * k;
+        cp_async16(img + oh, src);
+        cp_async16(img + ol, src + 128);
+      }
     } else {
       *reinterpret_cast<float4*>(img + oh) = make_float4(0.f, 0.f, 0.f, 0.f);
       *reinterpret_cast<float4*>(img + ol) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+}
+// after the copies landed and a barrier: each run's other items from its first
+__device__ inline void g1_t_replicate(const TileMeta* m, char* img) {
+  const unsigned heads = tile_run_heads(m, threadIdx.x & 31);
+  if (m->n == 32 ? heads == 0xFFFFFFFFu : (~heads & ((1u << m->n) - 1u)) == 0u) return;  // distinct keys (uniform)
+#pragma unroll
+  for (int i = 0; i < 1024 / kThreads; ++i) {
+    const int e = threadIdx.x + i * kThreads, it = e >> 5, k = e & 31;
+    if (it < m->n && !((heads >> it) & 1u)) {
+      const int src = 31 - __clz(heads & (0xFFFFFFFFu >> (31 - it)));  // the run's first item
+      *reinterpret_cast<float4*>(img + umma::sw128_off(k, 4 * it, 64)) =
+          *reinterpret_cast<const float4*>(img + umma::sw128_off(k, 4 * src, 64));
+      *reinterpret_cast<float4*>(img + umma::sw128_off(32 + k, 4 * it, 64)) =
+          *reinterpret_cast<const float4*>(img + umma::sw128_off(32 + k, 4 * src, 64));
     }
   }
 }
@@ -1610,6 +1638,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
 #pragma unroll
           for (int ab = 0; ab < 16; ++ab) xs[xs_idx(it, ab >> 2, ab & 3, lane)] = 0.f;
       }
+      if (ch == nchunk - 1) cp_async_wait_all();  // the G1^T image's copies (replicated after the barrier)
       {
         const long long _c0 = clock64();
         simt_sync();  // staging reused by the next chunk / tile
@@ -1630,6 +1659,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
     }
     umma::tmem_st32(tl + 128 + kSpan * qw, zh);
     umma::tmem_st32(tl + 256 + kSpan * qw, zl);
+    g1_t_replicate(m, r2_hi);
     umma::tmem_wait_st();
     cp_async_wait_all();  // G1^T image (issued before the Z phase), next tile's metadata (warp 15)
     if (threadIdx.x == 0) {
