@@ -1712,6 +1712,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
       cp_async_commit();
     }
     TSTAMP(7);
+    // the next X GEMM is released before this tile's dG2 / dG1 reductions: the
+    // proxy fence of the release would otherwise wait for them to drain (the
+    // dG2 / E columns are rewritten only after the next tile's Z phase)
+    if (has_next) {  // the next G1 rows landed: with the cb image, the MMA warp starts the next X GEMM
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      simt_sync_for_mma();
+      if (threadIdx.x == 0) umma::mbar_arrive(&s_mb_xop);
+    }
     if (!(dbg & 4)) {
       float v[kRedCols], w2[kRedCols];
       // dG2[k][i2][b][c] = D[:, k] + D[:, 32 + k], once per run of tiles of one i2
@@ -1767,11 +1775,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
           red_v4(d1 + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
         }
       }
-    }
-    if (has_next) {  // the next G1 rows landed: with the cb image, the MMA warp starts the next X GEMM
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-      simt_sync_for_mma();
-      if (threadIdx.x == 0) umma::mbar_arrive(&s_mb_xop);
     }
     TSTAMP(8);
     prev_i2 = m->i2;
