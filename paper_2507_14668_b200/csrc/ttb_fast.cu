@@ -1592,21 +1592,24 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
             // (two floats per lane per member, eight members in flight) into
             // the warp's scratch, then broadcast reads
             if (mem & (mem - 1)) {
+              // the member lanes publish their bags in the warp's scratch (by
+              // rank), so the eight loads of a batch issue without a chain of
+              // shuffles
+              int* mb = reinterpret_cast<int*>(st_acc + warp * 16);
+              if ((mem >> lane) & 1u) mb[__popc(mem & lanemask_lt())] = my_bag;
+              __syncwarp();
+              const int nm = __popc(mem);
               float2 acc = make_float2(0.f, 0.f);
-              while (mem) {
+              for (int q0 = 0; q0 < nm; q0 += 8) {
                 float2 w[8];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                  w[q] = make_float2(0.f, 0.f);
-                  if (mem) {
-                    const int bg = __shfl_sync(0xffffffffu, my_bag, __ffs(mem) - 1);
-                    mem &= mem - 1;
-                    w[q] = __ldg(reinterpret_cast<const float2*>(gout + (size_t)bg * NOUT) + lane);
-                  }
-                }
+                for (int q = 0; q < 8; ++q)
+                  w[q] = q0 + q < nm ? __ldg(reinterpret_cast<const float2*>(gout + (size_t)mb[q0 + q] * NOUT) + lane)
+                                     : make_float2(0.f, 0.f);
                 acc.x += ((w[0].x + w[1].x) + (w[2].x + w[3].x)) + ((w[4].x + w[5].x) + (w[6].x + w[7].x));
                 acc.y += ((w[0].y + w[1].y) + (w[2].y + w[3].y)) + ((w[4].y + w[5].y) + (w[6].y + w[7].y));
               }
+              __syncwarp();  // every bag read before the sum overwrites the scratch
               reinterpret_cast<float2*>(st_acc + warp * 16)[lane] = acc;
               __syncwarp();
               src = st_acc + warp * 16;
