@@ -816,7 +816,6 @@ constexpr int kMaxTilePos = kTileItems * kItemLen;  // 1024
 
 constexpr int kFwdMaxM3 = 288;                       // G3 (32 x m3 x 4 fp32) kept in smem
 constexpr int kFwdThreads = 512;
-constexpr int kFwdSplitRounds = 4;  // rows with <= this many segments: c split across the quarters
 
 // G3 region sized by the table's m3 (the (bag, i3) stages follow it)
 __host__ __device__ constexpr int fwd_g3_bytes(unsigned m3) { return (int)(32 * m3 * 16 + 1023) & ~1023; }
@@ -856,7 +855,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
   const int ntiles = hdr[4];
   const int tb = cta_tiles[blockIdx.x], te = cta_tiles[blockIdx.x + 1];  // weight-balanced (k_fplan)
   (void)ntiles;
-  if (warp == 0) umma::tmem_alloc(&s_tmem, 256);  // X, then the quarters' partial sums
+  if (warp == 0) umma::tmem_alloc(&s_tmem, 128);  // X
   if (threadIdx.x == 32) umma::mbar_init(&s_mbar, 1);
   // table f's G3 slices [f M3, (f + 1) M3) of every row c (rows are g.m3 slices long)
   auto stage_g3 = [&](unsigned f) {
@@ -952,193 +951,97 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
     if (t + 1 < te) stage(t + 1);  // lands while this tile is closed
     FSTAMP(2);
     // ---- epilogue. The four warps of a lane quadrant share its 32 rows
-    // (item, a) and split each segment's contraction over c: quarter q
-    // closes c in [8q, 8q + 8) (its 32 X columns stay in registers for the
-    // whole tile), parks its 16 partial sums in TMEM, and quarter 0 adds the
-    // four and stores the bag row. Every segment of a row costs each warp a
-    // quarter of the work, whatever the item lengths of the tile.
+    // (item, a) and take alternate segments of each row (quarter q: segments
+    // q, q + 4, ...), each closing all 32 values of c from the X row in TMEM.
+    // (Splitting each segment's contraction over c across the quarters, with
+    // the partial sums exchanged through TMEM, measured slower at every
+    // segment count: 40.0 -> 37.5 us at config 2, 287 -> 278 us at config 3.)
     const bool live = it < m->n;
     const int q0 = live ? m->start[it] - p0 : 0, len = live ? m->start[it + 1] - p0 - q0 : 0;
     const unsigned smask = !live ? 0u : direct ? (len >= 32 ? 0xffffffffu : (1u << len) - 1u) : s_segm[it];
-    const int nseg = __popc(smask);
     // segment [qq, e) of the row from the remaining start bits
     auto seg_next = [&](unsigned& rem, int& qq, int& e) {
       qq = q0 + __ffs(rem) - 1;
       rem &= rem - 1;
       e = q0 + (rem ? __ffs(rem) - 1 : len);
     };
-    const int rounds = __reduce_max_sync(0xffffffffu, nseg);  // same rows -> same count in all 4 warps
-    if (rounds <= kFwdSplitRounds) {
-      float x[32];  // x[4 c' + b] = X[item][a][b][8 quarter + c']
-      umma::tmem_ld32(trow + 32 * quarter, x);
-      const uint32_t tpart = trow + 128;  // partial sums: 16 columns per quarter
-      unsigned rem = smask;
-      for (int r = 0; r < rounds; ++r) {
-        const bool have = r < nseg;
-        int bag = 0, qq = 0, e = 0;
-        if (have) {
-          seg_next(rem, qq, e);
-          bag = s_sbi[qq].x;
-        }
-        float acc[16];
-  #pragma unroll
-        for (int i = 0; i < 16; ++i) acc[i] = 0.f;
-        if (have) {
-          for (int l = qq; l < (kPooled ? qq + 1 : e); ++l) {  // (pooled: one row, one slice)
-            const float4* g3 = s_g3 + (unsigned)s_sbi[l].y + 8 * quarter * m3;
-  #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              const float4 gv = g3[c * m3];
-  #pragma unroll
-              for (int b = 0; b < 4; ++b) {
-                const float xv = x[4 * c + b];
-                acc[4 * b + 0] = fmaf(xv, gv.x, acc[4 * b + 0]);
-                acc[4 * b + 1] = fmaf(xv, gv.y, acc[4 * b + 1]);
-                acc[4 * b + 2] = fmaf(xv, gv.z, acc[4 * b + 2]);
-                acc[4 * b + 3] = fmaf(xv, gv.w, acc[4 * b + 3]);
-              }
-            }
-          }
-        }
-        if (kPooled) {
-          // a row run pools into several bags: every quarter writes its
-          // partials and takes the sum of one b block (4 outputs), so the
-          // run's reductions into its lookups' bags are split four ways
-          umma::tmem_st16(tpart + 16 * quarter, acc);
-          umma::tmem_wait_st();
-          named_sync(1 + q4, 128);
-          uint32_t pq[4][4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) umma::tmem_ld4_nw(tpart + 16 * j + 4 * quarter, pq[j]);
-          umma::tmem_wait_ld();
-          float sb[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            sb[i] = (__uint_as_float(pq[0][i]) + __uint_as_float(pq[1][i])) +
-                    (__uint_as_float(pq[2][i]) + __uint_as_float(pq[3][i]));
-          if (have)
-            for (int l = qq; l < e; ++l)
-              red_v4(out + (size_t)s_sbi[l].x * NOUT + a * 16 + 4 * quarter, sb[0], sb[1], sb[2], sb[3]);
-          umma::fence_before_sync();
-          named_sync(1 + q4, 128);  // partial columns free for the next round
-          umma::fence_after_sync();
-          continue;
-        }
-        if (quarter != 0) {
-          umma::tmem_st16(tpart + 16 * quarter, acc);
-          umma::tmem_wait_st();
-        }
-        named_sync(1 + q4, 128);  // the quadrant's partials are in TMEM
-        if (quarter == 0) {  // the three partials in flight together, one wait
-          uint32_t p12[32], p3[16];
-          umma::tmem_ld32_nw(tpart + 16, p12);
-          umma::tmem_ld16_nw(tpart + 48, p3);
-          umma::tmem_wait_ld();
-  #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            acc[i] += (__uint_as_float(p12[i]) + __uint_as_float(p12[16 + i])) + __uint_as_float(p3[i]);
-          if (have) {
-            float* o = out + (size_t)bag * NOUT + a * 16;
-            if (direct) {
-  #pragma unroll
-              for (int bb = 0; bb < 4; ++bb)
-                reinterpret_cast<float4*>(o)[bb] =
-                    make_float4(acc[4 * bb], acc[4 * bb + 1], acc[4 * bb + 2], acc[4 * bb + 3]);
-            } else {
-              for (int l = qq; l < (kPooled ? e : qq + 1); ++l) {  // (pooled: the row into each lookup's bag)
-                float* ol = kPooled ? out + (size_t)s_sbi[l].x * NOUT + a * 16 : o;
-  #pragma unroll
-                for (int bb = 0; bb < 4; ++bb)
-                  red_v4(ol + 4 * bb, acc[4 * bb], acc[4 * bb + 1], acc[4 * bb + 2], acc[4 * bb + 3]);
-              }
-            }
-          }
-        }
-        umma::fence_before_sync();
-        named_sync(1 + q4, 128);  // partial columns free for the next round
-        umma::fence_after_sync();
+    unsigned rem = smask;  // quarter q takes segments q, q + 4, ...
+    for (int k = 0; k < quarter && rem; ++k) rem &= rem - 1;
+    for (;;) {
+      const bool have = rem != 0;
+      int bag = 0, qq = 0, e = 0;
+      if (have) {
+        seg_next(rem, qq, e);
+        bag = s_sbi[qq].x;
+        for (int k = 0; k < 3 && rem; ++k) rem &= rem - 1;
       }
-    } else {
-      // long items (hot prefixes): the quarters take alternate segments, each
-      // closing all 32 values of c (two 64-column halves of the X row)
-      unsigned rem = smask;  // quarter q takes segments q, q + 4, ...
-      for (int k = 0; k < quarter && rem; ++k) rem &= rem - 1;
-      for (;;) {
-        const bool have = rem != 0;
-        int bag = 0, qq = 0, e = 0;
-        if (have) {
-          seg_next(rem, qq, e);
-          bag = s_sbi[qq].x;
-          for (int k = 0; k < 3 && rem; ++k) rem &= rem - 1;
-        }
-        if (!__any_sync(0xffffffffu, have)) break;
-        float acc[16];
+      if (!__any_sync(0xffffffffu, have)) break;
+      float acc[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) acc[i] = 0.f;
-        if (kPooled) {
-          // per quarter of c: the run's row closed once (a rank-8 update of
-          // the 16 outputs per quarter), then pooled into each lookup's bag
+      for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+      if (kPooled) {
+        // per quarter of c: the run's row closed once (a rank-8 update of
+        // the 16 outputs per quarter), then pooled into each lookup's bag
 #pragma unroll
-          for (int cq = 0; cq < 4; ++cq) {
-            float xq[32];  // xq[4 c' + b] = X[item][a][b][8 cq + c']
-            umma::tmem_ld32(trow + 32 * cq, xq);
-            if (have) {
-              float4 gs[8];  // the run's row: one G3 slice
-              {
-                const float4* g3 = s_g3 + (unsigned)s_sbi[qq].y + 8 * cq * m3;
+        for (int cq = 0; cq < 4; ++cq) {
+          float xq[32];  // xq[4 c' + b] = X[item][a][b][8 cq + c']
+          umma::tmem_ld32(trow + 32 * cq, xq);
+          if (have) {
+            float4 gs[8];  // the run's row: one G3 slice
+            {
+              const float4* g3 = s_g3 + (unsigned)s_sbi[qq].y + 8 * cq * m3;
 #pragma unroll
-                for (int c = 0; c < 8; ++c) gs[c] = g3[c * m3];
+              for (int c = 0; c < 8; ++c) gs[c] = g3[c * m3];
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+#pragma unroll
+              for (int b = 0; b < 4; ++b) {
+                const float xv = xq[4 * c + b];
+                acc[4 * b + 0] = fmaf(xv, gs[c].x, acc[4 * b + 0]);
+                acc[4 * b + 1] = fmaf(xv, gs[c].y, acc[4 * b + 1]);
+                acc[4 * b + 2] = fmaf(xv, gs[c].z, acc[4 * b + 2]);
+                acc[4 * b + 3] = fmaf(xv, gs[c].w, acc[4 * b + 3]);
               }
+          }
+        }
+      } else {
 #pragma unroll
-              for (int c = 0; c < 8; ++c)
+        for (int ch = 0; ch < 2; ++ch) {
+          float xh[64];  // xh[4 c' + b] = X[item][a][b][16 ch + c']
+          umma::tmem_ld32(trow + 64 * ch, *(float(*)[32])(xh));
+          umma::tmem_ld32(trow + 64 * ch + 32, *(float(*)[32])(xh + 32));
+          if (have) {
+            for (int l = qq; l < e; ++l) {
+              const float4* g3 = s_g3 + (unsigned)s_sbi[l].y + 16 * ch * m3;
+#pragma unroll
+              for (int c = 0; c < 16; ++c) {
+                const float4 gv = g3[c * m3];
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
-                  const float xv = xq[4 * c + b];
-                  acc[4 * b + 0] = fmaf(xv, gs[c].x, acc[4 * b + 0]);
-                  acc[4 * b + 1] = fmaf(xv, gs[c].y, acc[4 * b + 1]);
-                  acc[4 * b + 2] = fmaf(xv, gs[c].z, acc[4 * b + 2]);
-                  acc[4 * b + 3] = fmaf(xv, gs[c].w, acc[4 * b + 3]);
-                }
-            }
-          }
-        } else {
-  #pragma unroll
-          for (int ch = 0; ch < 2; ++ch) {
-            float xh[64];  // xh[4 c' + b] = X[item][a][b][16 ch + c']
-            umma::tmem_ld32(trow + 64 * ch, *(float(*)[32])(xh));
-            umma::tmem_ld32(trow + 64 * ch + 32, *(float(*)[32])(xh + 32));
-            if (have) {
-              for (int l = qq; l < e; ++l) {
-                const float4* g3 = s_g3 + (unsigned)s_sbi[l].y + 16 * ch * m3;
-  #pragma unroll
-                for (int c = 0; c < 16; ++c) {
-                  const float4 gv = g3[c * m3];
-  #pragma unroll
-                  for (int b = 0; b < 4; ++b) {
-                    const float xv = xh[4 * c + b];
-                    acc[4 * b + 0] = fmaf(xv, gv.x, acc[4 * b + 0]);
-                    acc[4 * b + 1] = fmaf(xv, gv.y, acc[4 * b + 1]);
-                    acc[4 * b + 2] = fmaf(xv, gv.z, acc[4 * b + 2]);
-                    acc[4 * b + 3] = fmaf(xv, gv.w, acc[4 * b + 3]);
-                  }
+                  const float xv = xh[4 * c + b];
+                  acc[4 * b + 0] = fmaf(xv, gv.x, acc[4 * b + 0]);
+                  acc[4 * b + 1] = fmaf(xv, gv.y, acc[4 * b + 1]);
+                  acc[4 * b + 2] = fmaf(xv, gv.z, acc[4 * b + 2]);
+                  acc[4 * b + 3] = fmaf(xv, gv.w, acc[4 * b + 3]);
                 }
               }
             }
           }
         }
-        if (have) {
-          float* o = out + (size_t)bag * NOUT + a * 16;
-          if (direct) {
+      }
+      if (have) {
+        float* o = out + (size_t)bag * NOUT + a * 16;
+        if (direct) {
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            reinterpret_cast<float4*>(o)[b] = make_float4(acc[4 * b], acc[4 * b + 1], acc[4 * b + 2], acc[4 * b + 3]);
+        } else {
+          for (int l = qq; l < (kPooled ? e : qq + 1); ++l) {  // (pooled: the row into each lookup's bag)
+            float* ol = kPooled ? out + (size_t)s_sbi[l].x * NOUT + a * 16 : o;
 #pragma unroll
             for (int b = 0; b < 4; ++b)
-              reinterpret_cast<float4*>(o)[b] = make_float4(acc[4 * b], acc[4 * b + 1], acc[4 * b + 2], acc[4 * b + 3]);
-          } else {
-            for (int l = qq; l < (kPooled ? e : qq + 1); ++l) {  // (pooled: the row into each lookup's bag)
-              float* ol = kPooled ? out + (size_t)s_sbi[l].x * NOUT + a * 16 : o;
-#pragma unroll
-              for (int b = 0; b < 4; ++b)
-                red_v4(ol + 4 * b, acc[4 * b], acc[4 * b + 1], acc[4 * b + 2], acc[4 * b + 3]);
-            }
+              red_v4(ol + 4 * b, acc[4 * b], acc[4 * b + 1], acc[4 * b + 2], acc[4 * b + 3]);
           }
         }
       }
@@ -1159,7 +1062,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_fwd(KGeom g, const float* __
     }
     FSTAMP(3);
   }
-  if (warp == 0) umma::tmem_free(tmem, 256);
+  if (warp == 0) umma::tmem_free(tmem, 128);
 #undef FSTAMP
 }
 
