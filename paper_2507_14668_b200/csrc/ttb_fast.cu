@@ -1205,7 +1205,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
   // SIMT -> MMA warp: G1 rows staged / Z^T in TMEM + G1^T staged / Z images
   // written; MMA warp -> SIMT: X done / dG2 + E done; bulk copies of the G2
   // cb / k images (issued and waited for by the MMA warp)
-  __shared__ uint64_t s_mb_xop, s_mb_z, s_mb_zi, s_mb_x, s_mb_e, s_mb_xtma, s_mb_ktma;
+  __shared__ uint64_t s_mb_xop, s_mb_z, s_mb_zi, s_mb_x, s_mb_d2, s_mb_e, s_mb_xtma, s_mb_ktma;
   __shared__ int s_acc2;
   // row path: the Z phase's next item of the tile in each slot (warps take
   // items dynamically: an item's cost follows its distinct rows, not its length)
@@ -1229,6 +1229,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
     umma::mbar_init(&s_mb_ktma, 1);
     umma::mbar_init(&s_mb_zi, 1);
     umma::mbar_init(&s_mb_x, 1);
+    umma::mbar_init(&s_mb_d2, 1);
     umma::mbar_init(&s_mb_e, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1307,6 +1308,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
           umma::mma_tf32_ta(tmem + 384, tmem + 128 + k0, d_r2h + o, id64, (acc2 || k0 > 0) ? 1u : 0u);
           umma::mma_tf32_ta(tmem + 384, tmem + 256 + k0, d_r2h + o, id32, 1u);  // Z lo . G1 hi only
         }
+        umma::commit(&s_mb_d2);  // -> SIMT: the G1^T image is free for the next tile's G1 rows
       }
       __syncwarp();
       umma::mbar_wait(&s_mb_zi, ph);  // Z images (hi, lo) in shared memory
@@ -1600,14 +1602,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_bwd(KGeom g, const float* __
         cp_async16(st_g + e, gout + (size_t)st_sbi[e >> 4].x * NOUT + 4 * (e & 15));
       cp_async_commit();
     }
-    umma::mbar_wait(&s_mb_e, phase);  // dG2 and E of tile t
+    // the next tile's G1 rows as soon as dG2 has read the G1^T image (R2),
+    // the rest of its first chunk once E has read the Z lo image
+    umma::mbar_wait(&s_mb_d2, phase);
     umma::fence_after_sync();
-    TSTAMP(6);
-    // the next tile's G1 rows (R12 is free now) and the rest of its first
-    // chunk (the staging region held the Z lo image)
     if (has_next) {
       stage_g1_rows(mn);
       cp_async_commit();
+    }
+    umma::mbar_wait(&s_mb_e, phase);  // E of tile t
+    umma::fence_after_sync();
+    TSTAMP(6);
+    if (has_next) {
       if (kRows) {
         stage_rows(npn, tile_i3_base(mn, g));
       } else {
