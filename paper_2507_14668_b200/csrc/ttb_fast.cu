@@ -80,8 +80,14 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
                                                         unsigned* __restrict__ item_key, int4* __restrict__ tile_info,
                                                         int2* __restrict__ sbi, int* __restrict__ hdr, int dbg,
                                                         int allow_empty, const uint4* __restrict__ tgeom,
-                                                        int2* __restrict__ chunks) {
+                                                        int2* __restrict__ chunks, float4* __restrict__ zgrad,
+                                                        int64_t nzgrad4) {
   pdl_enter();
+  // the backward's flat gradient buffer cleared here, off the step's
+  // critical path (a memset node between the forward and the backward would
+  // also break their programmatic overlap); fast_backward skips its memset
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nzgrad4; i += (int64_t)gridDim.x * blockDim.x)
+    zgrad[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 #define PSTAMP(i)                                                                                          \
   do {                                                                                                     \
     if (dbg && threadIdx.x == 0 && blockIdx.x == 0) {                                                      \
@@ -1812,21 +1818,24 @@ cudaError_t fast_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* 
       return e;
     if (occ < 1) return cudaErrorCooperativeLaunchTooLarge;
   }
+  // |G1| + |G2| + |G3| gradients (multiples of 4: every core has n = 4)
+  const int64_t ngrad4 = ((int64_t)h->kg.g1rows * 4 * R1 + (int64_t)R1 * h->kg.m2 * C + (int64_t)32 * h->kg.m3 * 4) / 4;
   {
   ProfScope _ps(h, s, "f_plan");
   if (idx64)
     e = launch_pdl_coop(k_fplan<long long>, dim3(grid), dim3(kPlanThreads), 0, s, (const long long*)idx, offsets, T, B,
                    h->kg, w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_rstart, w.f_split, w.f_gtot, w.f_item_start, w.f_cta, h->num_sms,
                    w.f_item_key, w.f_tile_info, w.f_sbi, w.fast_hdr, getenv("TTB_DBG") ? 1 : 0, h->allow_empty,
-                   (const uint4*)w.f_tgeom, w.f_chunks);
+                   (const uint4*)w.f_tgeom, w.f_chunks, (float4*)w.f_grad, ngrad4);
   else
     e = launch_pdl_coop(k_fplan<int>, dim3(grid), dim3(kPlanThreads), 0, s, (const int*)idx, offsets, T, B, h->kg,
                    w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_rstart, w.f_split, w.f_gtot, w.f_item_start, w.f_cta, h->num_sms,
                    w.f_item_key,
                    w.f_tile_info, w.f_sbi, w.fast_hdr, getenv("TTB_DBG") ? 1 : 0, h->allow_empty,
-                   (const uint4*)w.f_tgeom, w.f_chunks);
+                   (const uint4*)w.f_tgeom, w.f_chunks, (float4*)w.f_grad, ngrad4);
   }
   if (e) return e;
+  h->fgrad_zeroed = 1;
   count_launch();
   if (T > B) {  // pooled: each multi-item prefix's lookups grouped by row (forward and backward use it)
     constexpr int sort_smem = kSortSmem;
@@ -1897,12 +1906,13 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
     g0 = w.f_grad;
     g1 = w.f_grad + n0;
     g2 = w.f_grad + n0 + n1;
-    if ((e = cudaMemsetAsync(w.f_grad, 0, sizeof(float) * (size_t)(n0 + n1 + n2), s))) return e;
+    if (!h->fgrad_zeroed && (e = cudaMemsetAsync(w.f_grad, 0, sizeof(float) * (size_t)(n0 + n1 + n2), s))) return e;
   } else {
     if ((e = cudaMemsetAsync(g0, 0, sizeof(float) * (size_t)n0, s))) return e;
     if ((e = cudaMemsetAsync(g1, 0, sizeof(float) * (size_t)n1, s))) return e;
-    if ((e = cudaMemsetAsync(w.f_grad + n0 + n1, 0, sizeof(float) * (size_t)n2, s))) return e;
+    if (!h->fgrad_zeroed && (e = cudaMemsetAsync(w.f_grad + n0 + n1, 0, sizeof(float) * (size_t)n2, s))) return e;
   }
+  h->fgrad_zeroed = 0;  // this backward accumulates into it
   // dG3 accumulates slice-major, (i3, c, n3): one lookup's 128 contributions
   // are 512 contiguous bytes (4 L2 lines instead of 32); the update kernel
   // reads it in that order, the caller's buffer gets the reference layout
