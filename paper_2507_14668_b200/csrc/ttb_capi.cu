@@ -351,6 +351,7 @@ static ttb_handle* create_from(const ttb_handle& tmp, void* workspace, size_t by
       (!h->batched && cudaMemsetAsync(h->w.grp_done, 0, sizeof(int) * h->kg.m2, s) != cudaSuccess) ||
       (!h->batched && cudaMemsetAsync(h->w.pmap, 0xFF, sizeof(unsigned) * h->kg.m1m2, s) != cudaSuccess) ||
       (h->fast_ok && cudaMemsetAsync(h->w.f_cnt, 0, sizeof(int) * h->kg.m1m2, s) != cudaSuccess) ||
+      cudaMemsetAsync(h->w.fast_hdr, 0, 64 * sizeof(int), s) != cudaSuccess ||  // the plan's grid barrier words
       cudaMemcpyAsync(h->w.f_tgeom, h->tgeom_host, sizeof(uint4) * h->kg.nt, cudaMemcpyHostToDevice, s) !=
           cudaSuccess) {
     free(h);

@@ -99,8 +99,12 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
   PSTAMP(0);
   __shared__ int s_hist[kPlanThreads / 32][2 * (kItemLen + 1)];
   __shared__ int s_poff[kPlanThreads / 32][kItemLen + 1];
-  unsigned* bar = reinterpret_cast<unsigned*>(hdr + 12);
+  unsigned* bar = reinterpret_cast<unsigned*>(hdr + 12);  // [0] barrier arrivals, [1] CTAs done (reset by the last)
   unsigned target = 0;
+  // the plan's header words (errors, counts, the backward's tile counter and
+  // suspect flag) are cleared here instead of by a memset node before the
+  // launch; every other write to them comes after the first grid barrier
+  if (blockIdx.x == 0 && threadIdx.x < 12) hdr[threadIdx.x] = 0;
   const int nthr = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   // tables (one unless the handle is batched): table f's lookups are
@@ -173,9 +177,9 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
       }
     if (ok && iter >= kPlanRegs) rk[t] = rank;
   }
-  if (bits) atomicOr(&hdr[0], bits);
-  if (multi) hdr[1] = 1;
   grid_barrier(bar, target);
+  if (bits) atomicOr(&hdr[0], bits);  // (after the first barrier: block 0 has cleared the words)
+  if (multi) hdr[1] = 1;
   PSTAMP(1);
   // ---- phase A1: per-i2 totals (positions, items, present prefixes)
   const int gw = tid >> 5, nw = nthr >> 5;
@@ -366,6 +370,12 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
     }
   }
   __syncthreads();
+  // the last CTA out (every CTA is past every barrier) resets the barrier
+  // words for the next plan
+  if (threadIdx.x == 0 && atomicAdd(&bar[1], 1u) == gridDim.x - 1) {
+    bar[0] = 0u;
+    bar[1] = 0u;
+  }
   PSTAMP(4);
 #undef PSTAMP
 }
@@ -1802,8 +1812,9 @@ cudaError_t fast_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* 
   Workspace& w = h->w;
   const int T = (int)h->T, B = (int)h->B;
   cudaError_t e;
-  if ((e = cudaMemsetAsync(w.fast_hdr, 0, (size_t)(w.zeroB + w.zeroB_bytes - (char*)w.fast_hdr), s))) return e;
-  h->bwd_zeroed = 1;
+  // (no memset: k_fplan clears its header words itself; the other pipeline's
+  // backward clears its zero block B when it runs)
+  h->bwd_zeroed = 0;
   int work = T > B ? T : B;
   if ((int)h->kg.m1m2 > work) work = (int)h->kg.m1m2;
   int grid = (work + kPlanThreads - 1) / kPlanThreads;
@@ -1836,6 +1847,7 @@ cudaError_t fast_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* 
   }
   if (e) return e;
   h->fgrad_zeroed = 1;
+  h->tilectr_zeroed = 1;
   count_launch();
   if (T > B) {  // pooled: each multi-item prefix's lookups grouped by row (forward and backward use it)
     constexpr int sort_smem = kSortSmem;
@@ -1918,8 +1930,9 @@ cudaError_t fast_backward(ttb_handle* h, const float* c0, const float* c1, const
   // reads it in that order, the caller's buffer gets the reference layout
   float* g3s = w.f_grad + n0 + n1;
   const int grid = h->num_sms;  // = the plan's CTA ranges (k_fplan cta_tiles)
-  if (h->T > h->B)  // pooled: the backward's tile counter
+  if (h->T > h->B && !h->tilectr_zeroed)  // pooled: the backward's tile counter (cleared by the plan)
     if ((e = cudaMemsetAsync(w.fast_hdr + kHdrNextTile, 0, sizeof(int), s))) return e;
+  h->tilectr_zeroed = 0;
   {
     ProfScope _ps(h, s, "f_bwd");
     // pooled bags (more lookups than bags) repeat rows inside a prefix: group

@@ -144,6 +144,7 @@ struct ttb_handle {
   int pmap_clean;   // prefix table already reset (by the last backward)
   int bwd_zeroed;   // zero block B is clear for the next backward
   int fgrad_zeroed;  // the tensor-core pipeline's flat gradient buffer was cleared by the last plan
+  int tilectr_zeroed;  // the pooled backward's tile counter was cleared by the last plan
   int64_t gen;
   // the f_img / f_g1img core images describe the cores at img_c0 / img_c1
   // (written by the last forward or fused update; cleared by
