@@ -182,7 +182,8 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
   if (multi) hdr[1] = 1;
   PSTAMP(1);
   // ---- phase A1: per-i2 totals (positions, items, present prefixes)
-  const int gw = tid >> 5, nw = nthr >> 5;
+  // group i2 -> CTA i2 % grid, warp i2 / grid: the groups spread over every SM
+  const int gw = (threadIdx.x >> 5) * gridDim.x + blockIdx.x, nw = nthr >> 5;
   for (unsigned i2 = gw; i2 < g.m2; i2 += nw) {
     int c = 0, it = 0, p = 0;
     for (unsigned i1 = lane; i1 < g.m1; i1 += 32) {
