@@ -354,3 +354,32 @@ def test_sgd_update_multi_matches_single_updates():
                 assert torch.equal(a, b)
     with pytest.raises(ValueError):
         nat.check(lib.ttb_sgd_update_multi(arr, len(sizes), -1.0, 0.9, _stream()))
+
+
+# ------------------------------------------------------------------ plan / backward state across calls
+def test_plans_of_different_grid_sizes_and_repeated_backward():
+    """The plan clears its own header words and the backward's flat gradient
+    buffer (no memset nodes), and its grid barrier words are reset by the
+    last CTA out: plans whose grids differ (T = 65,536 / 1,500 / 65,536
+    pooled) must each give the oracle's forward and gradients, and a second
+    backward on the same plan must not see the first one's gradients."""
+    rows = 10_000_000
+    emb = module(rows, 3, 65_536 * 2, 65_536)
+    g = O.Geometry(emb.shape.m, emb.shape.n, emb.shape.ranks)
+    rng = np.random.default_rng(41)
+    cases = [(rng.integers(0, rows, 65_536), 1), (rng.integers(0, rows, 1_500), 1),
+             (zipf_ids(rows, 65_536 * 2, 9, False), 2)]
+    for idx, pool in cases:
+        off = np.arange(0, idx.size + 1, pool, dtype=np.int64)
+        gout = rng.standard_normal((off.size - 1, 64)).astype(np.float32)
+        out, grads, c64 = run_fast(emb, idx, off, gout)
+        assert rel_err(out, O.forward(c64, g, idx, off)) < FWD_TOL, (idx.size, pool)
+        want = oracle_grads_chunked(c64, g, idx, off, gout)
+        for k in range(3):
+            assert rel_err(grads[k], want[k]) < GRAD_TOL, (idx.size, pool, k)
+        # the same plan again: fresh gradients, not accumulated onto the first
+        again = [x.cpu().numpy() for x in emb.engine.backward([c.detach() for c in emb.cores],
+                                                               torch.from_numpy(gout).cuda())]
+        for k in range(3):
+            assert np.array_equal(again[k], grads[k]) or rel_err(again[k], want[k]) < GRAD_TOL, (idx.size, k)
+        emb.engine.check_errors()
