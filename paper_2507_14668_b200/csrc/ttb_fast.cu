@@ -48,6 +48,7 @@ constexpr int kThreads = 512;  // backward: 16 warps, four per TMEM lane quadran
 constexpr int kPlanThreads = 512;
 constexpr int kTileCost = 32;
 constexpr int kA2Regs = 8;
+constexpr int kPlanUnroll = 4;  // lookups per thread per round in phases 0 and B
 constexpr int kPlanRegs = 4;   // lookups per thread whose plan fields stay in registers (phase 0 -> B)     // per-lane registers caching an i2 group's prefix counters (m1 <= 256)  // per-tile fixed cost in lookup units (CTA range balancing)
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
@@ -68,7 +69,7 @@ __device__ inline void grid_barrier(unsigned* bar, unsigned& target) {
 }
 
 
-template <typename IdxT>
+template <typename IdxT, bool kMany>  // kMany: more than two lookups per thread (phases 0 / B unrolled)
 __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__ idx,
                                                         const int64_t* __restrict__ offsets, int T, int B, KGeom g,
                                                         unsigned* __restrict__ key, unsigned* __restrict__ i3o,
@@ -135,47 +136,97 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
   // registers for phase B (same thread <-> lookup mapping there)
   unsigned rkey[kPlanRegs], ri3[kPlanRegs];
   int rrk[kPlanRegs];
-  int iter = 0;
-  for (int t0 = blockIdx.x * blockDim.x; t0 < T; t0 += nthr, ++iter) {  // warp-uniform trip count
-    const int t = t0 + threadIdx.x;
-    const bool ok = t < T;
-    unsigned k = 0xFFFFFFFFu, i3 = 0;
-    if (ok) {
-      int f = 0;  // the lookup's table: the last f with s_toff[f] <= t
-      for (int lo2 = 1, hi2 = nt - 1; lo2 <= hi2;) {
-        const int mid = (lo2 + hi2) >> 1;
-        if (s_toff[mid] <= t) f = mid, lo2 = mid + 1;
-        else hi2 = mid - 1;
+  if constexpr (!kMany) {  // at most two lookups per thread (config 2): one lookup per round
+    int iter = 0;
+    for (int t0 = blockIdx.x * blockDim.x; t0 < T; t0 += nthr, ++iter) {  // warp-uniform trip count
+      const int t = t0 + threadIdx.x;
+      const bool ok = t < T;
+      unsigned k = 0xFFFFFFFFu, i3 = 0;
+      if (ok) {
+        int f = 0;  // the lookup's table: the last f with s_toff[f] <= t
+        for (int lo2 = 1, hi2 = nt - 1; lo2 <= hi2;) {
+          const int mid = (lo2 + hi2) >> 1;
+          if (s_toff[mid] <= t) f = mid, lo2 = mid + 1;
+          else hi2 = mid - 1;
+        }
+        const uint4 tg = s_tg[f];  // (m2, m3, rows) of the table
+        long long v = (long long)idx[t];
+        if (v < 0 || v >= (long long)tg.z) {
+          bits |= 1;
+          v = 0;
+        }
+        const unsigned m2m3 = tg.x * tg.y;
+        const unsigned i = (unsigned)v, i1 = i / m2m3, r = i - i1 * m2m3, i2 = r / tg.y;
+        k = ((unsigned)f * g.tm2 + i2) * g.m1 + i1;
+        i3 = r - i2 * tg.y;
+        if (iter >= kPlanRegs) {
+          key[t] = k;
+          i3o[t] = i3;
+        }
       }
-      const uint4 tg = s_tg[f];  // (m2, m3, rows) of the table
-      long long v = (long long)idx[t];
-      if (v < 0 || v >= (long long)tg.z) {
-        bits |= 1;
-        v = 0;
+      const unsigned peers = __match_any_sync(0xffffffffu, k);
+      const int leader = __ffs(peers) - 1;
+      int base = 0;
+      if (ok && lane == leader) base = atomicAdd(&cnt[k], __popc(peers));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      const int rank = base + __popc(peers & lanemask_lt());
+#pragma unroll
+      for (int q = 0; q < kPlanRegs; ++q)
+        if (q == iter) {
+          rkey[q] = k;
+          ri3[q] = i3;
+          rrk[q] = rank;
+        }
+      if (ok && iter >= kPlanRegs) rk[t] = rank;
+    }
+  } else {
+    // kPlanUnroll lookups per thread per round: their index loads, then their
+    // counter atomics, are in flight together (one round trip per round
+    // instead of one per lookup when a thread has many lookups)
+    for (int g0 = blockIdx.x * blockDim.x; g0 < T; g0 += kPlanUnroll * nthr) {
+      unsigned kk[kPlanUnroll], ii3[kPlanUnroll];
+#pragma unroll
+      for (int u = 0; u < kPlanUnroll; ++u) {
+        const int t = g0 + u * nthr + threadIdx.x;
+        kk[u] = 0xFFFFFFFFu;
+        ii3[u] = 0;
+        if (t < T) {
+          int f = 0;  // the lookup's table: the last f with s_toff[f] <= t
+          for (int lo2 = 1, hi2 = nt - 1; lo2 <= hi2;) {
+            const int mid = (lo2 + hi2) >> 1;
+            if (s_toff[mid] <= t) f = mid, lo2 = mid + 1;
+            else hi2 = mid - 1;
+          }
+          const uint4 tg = s_tg[f];  // (m2, m3, rows) of the table
+          long long v = (long long)idx[t];
+          if (v < 0 || v >= (long long)tg.z) {
+            bits |= 1;
+            v = 0;
+          }
+          const unsigned m2m3 = tg.x * tg.y;
+          const unsigned i = (unsigned)v, i1 = i / m2m3, r = i - i1 * m2m3, i2 = r / tg.y;
+          kk[u] = ((unsigned)f * g.tm2 + i2) * g.m1 + i1;
+          ii3[u] = r - i2 * tg.y;
+          key[t] = kk[u];  // (many lookups per thread: none kept in registers)
+          i3o[t] = ii3[u];
+        }
       }
-      const unsigned m2m3 = tg.x * tg.y;
-      const unsigned i = (unsigned)v, i1 = i / m2m3, r = i - i1 * m2m3, i2 = r / tg.y;
-      k = ((unsigned)f * g.tm2 + i2) * g.m1 + i1;
-      i3 = r - i2 * tg.y;
-      if (iter >= kPlanRegs) {
-        key[t] = k;
-        i3o[t] = i3;
+      unsigned peers[kPlanUnroll];
+      int base[kPlanUnroll];
+#pragma unroll
+      for (int u = 0; u < kPlanUnroll; ++u) {  // (warp-uniform: every lane takes part in every match)
+        peers[u] = __match_any_sync(0xffffffffu, kk[u]);
+        base[u] = 0;
+        if (g0 + u * nthr + threadIdx.x < T && lane == __ffs(peers[u]) - 1)
+          base[u] = atomicAdd(&cnt[kk[u]], __popc(peers[u]));
+      }
+#pragma unroll
+      for (int u = 0; u < kPlanUnroll; ++u) {
+        const int t = g0 + u * nthr + threadIdx.x;
+        const int rank = __shfl_sync(0xffffffffu, base[u], __ffs(peers[u]) - 1) + __popc(peers[u] & lanemask_lt());
+        if (t < T) rk[t] = rank;
       }
     }
-    const unsigned peers = __match_any_sync(0xffffffffu, k);
-    const int leader = __ffs(peers) - 1;
-    int base = 0;
-    if (ok && lane == leader) base = atomicAdd(&cnt[k], __popc(peers));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    const int rank = base + __popc(peers & lanemask_lt());
-#pragma unroll
-    for (int q = 0; q < kPlanRegs; ++q)
-      if (q == iter) {
-        rkey[q] = k;
-        ri3[q] = i3;
-        rrk[q] = rank;
-      }
-    if (ok && iter >= kPlanRegs) rk[t] = rank;
   }
   grid_barrier(bar, target);
   if (bits) atomicOr(&hdr[0], bits);  // (after the first barrier: block 0 has cleared the words)
@@ -350,24 +401,54 @@ __global__ void __launch_bounds__(kPlanThreads) k_fplan(const IdxT* __restrict__
   // ---- phase B: scatter (bag, i3) into item order
   {
     const bool one = hdr[1] == 0 && T == B;  // one lookup per bag: bag id = lookup index
-    int it2 = 0;
-    for (int t = tid; t < T; t += nthr, ++it2) {
-      unsigned k, i3;
-      int r;
-      if (it2 < kPlanRegs) {
+    if constexpr (!kMany) {
+      int it2 = 0;
+      for (int t = tid; t < T; t += nthr, ++it2) {
+        unsigned k, i3;
+        int r;
+        if (it2 < kPlanRegs) {
 #pragma unroll
-        for (int q = 0; q < kPlanRegs; ++q)
-          if (q == it2) {
-            k = rkey[q];
-            i3 = ri3[q];
-            r = rrk[q];
-          }
-      } else {
-        k = key[t];
-        i3 = i3o[t];
-        r = rk[t];
+          for (int q = 0; q < kPlanRegs; ++q)
+            if (q == it2) {
+              k = rkey[q];
+              i3 = ri3[q];
+              r = rrk[q];
+            }
+        } else {
+          k = key[t];
+          i3 = i3o[t];
+          r = rk[t];
+        }
+        sbi[(r < split[k] ? start[k] : rstart[k]) + r] = make_int2(one ? t : bag_of[t], (int)i3);
       }
-      sbi[(r < split[k] ? start[k] : rstart[k]) + r] = make_int2(one ? t : bag_of[t], (int)i3);
+    } else {
+      for (int t0 = tid; t0 < T; t0 += kPlanUnroll * nthr) {
+        unsigned k[kPlanUnroll], i3[kPlanUnroll];
+        int r[kPlanUnroll], bg[kPlanUnroll];
+#pragma unroll
+        for (int u = 0; u < kPlanUnroll; ++u) {  // every load of the round first
+          const int t = t0 + u * nthr;
+          k[u] = 0;
+          i3[u] = 0;
+          r[u] = 0;
+          bg[u] = 0;
+          if (t < T) {
+            k[u] = key[t];
+            i3[u] = i3o[t];
+            r[u] = rk[t];
+            bg[u] = one ? t : bag_of[t];
+          }
+        }
+        int pos[kPlanUnroll];
+#pragma unroll
+        for (int u = 0; u < kPlanUnroll; ++u) {  // (the key's three words loaded together)
+          const int sp = split[k[u]], st = start[k[u]], rs = rstart[k[u]];
+          pos[u] = (r[u] < sp ? st : rs) + r[u];
+        }
+#pragma unroll
+        for (int u = 0; u < kPlanUnroll; ++u)
+          if (t0 + u * nthr < T) sbi[pos[u]] = make_int2(bg[u], (int)i3[u]);
+      }
     }
   }
   __syncthreads();
@@ -1820,13 +1901,14 @@ cudaError_t fast_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* 
   if ((int)h->kg.m1m2 > work) work = (int)h->kg.m1m2;
   int grid = (work + kPlanThreads - 1) / kPlanThreads;
   if (grid > h->num_sms) grid = h->num_sms;  // co-resident: grid barriers
+  const bool many = T > 2 * grid * kPlanThreads;  // (the kernel's own test, T > 2 nthr)
   {
     // the grid barriers need every CTA resident at once: bound the grid by
     // the occupancy of this device and launch cooperatively (an SM partition
     // too small for the grid then fails the launch instead of hanging)
     int occ = 0;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-             &occ, idx64 ? (const void*)k_fplan<long long> : (const void*)k_fplan<int>, kPlanThreads, 0)))
+             &occ, idx64 ? (const void*)k_fplan<long long, true> : (const void*)k_fplan<int, true>, kPlanThreads, 0)))
       return e;
     if (occ < 1) return cudaErrorCooperativeLaunchTooLarge;
   }
@@ -1835,12 +1917,12 @@ cudaError_t fast_plan(ttb_handle* h, const void* idx, int idx64, const int64_t* 
   {
   ProfScope _ps(h, s, "f_plan");
   if (idx64)
-    e = launch_pdl_coop(k_fplan<long long>, dim3(grid), dim3(kPlanThreads), 0, s, (const long long*)idx, offsets, T, B,
+    e = launch_pdl_coop(many ? k_fplan<long long, true> : k_fplan<long long, false>, dim3(grid), dim3(kPlanThreads), 0, s, (const long long*)idx, offsets, T, B,
                    h->kg, w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_rstart, w.f_split, w.f_gtot, w.f_item_start, w.f_cta, h->num_sms,
                    w.f_item_key, w.f_tile_info, w.f_sbi, w.fast_hdr, getenv("TTB_DBG") ? 1 : 0, h->allow_empty,
                    (const uint4*)w.f_tgeom, w.f_chunks, (float4*)w.f_grad, ngrad4);
   else
-    e = launch_pdl_coop(k_fplan<int>, dim3(grid), dim3(kPlanThreads), 0, s, (const int*)idx, offsets, T, B, h->kg,
+    e = launch_pdl_coop(many ? k_fplan<int, true> : k_fplan<int, false>, dim3(grid), dim3(kPlanThreads), 0, s, (const int*)idx, offsets, T, B, h->kg,
                    w.f_key, w.f_i3, w.f_rk, w.bag_of, w.f_cnt, w.f_start, w.f_rstart, w.f_split, w.f_gtot, w.f_item_start, w.f_cta, h->num_sms,
                    w.f_item_key,
                    w.f_tile_info, w.f_sbi, w.fast_hdr, getenv("TTB_DBG") ? 1 : 0, h->allow_empty,
