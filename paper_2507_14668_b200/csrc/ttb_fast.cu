@@ -48,7 +48,7 @@ constexpr int kThreads = 512;  // backward: 16 warps, four per TMEM lane quadran
 constexpr int kPlanThreads = 512;
 constexpr int kTileCost = 32;
 constexpr int kA2Regs = 8;
-constexpr int kPlanUnroll = 4;  // lookups per thread per round in phases 0 and B
+constexpr int kPlanUnroll = 8;  // lookups per thread per round in phases 0 and B
 constexpr int kPlanRegs = 4;   // lookups per thread whose plan fields stay in registers (phase 0 -> B)     // per-lane registers caching an i2 group's prefix counters (m1 <= 256)  // per-tile fixed cost in lookup units (CTA range balancing)
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
