@@ -673,7 +673,7 @@ __device__ __forceinline__ float maybe_sgd(float p, const SgdArgs& u, int core, 
   return sgd_apply(p, u.grad[flat], v ? v + j : nullptr, u.lr, u.mu);
 }
 
-__global__ void __launch_bounds__(kImgThreads) k_coreimg(float* __restrict__ G1, float* __restrict__ G2, KGeom g,
+__global__ void __launch_bounds__(kImgThreads, 2) k_coreimg(float* __restrict__ G1, float* __restrict__ G2, KGeom g,
                                                          float* __restrict__ img, float* __restrict__ g1img,
                                                          SgdArgs u) {
   pdl_enter();
@@ -712,12 +712,12 @@ __global__ void __launch_bounds__(kImgThreads) k_coreimg(float* __restrict__ G1,
     for (size_t j0 = (size_t)(blockIdx.x - nb12) * kImgThreads + threadIdx.x; j0 < n2; j0 += kU * stride) {
       float pv[kU], gr[kU];
       double st[kU];
-      size_t jt[kU];
+      unsigned jt[kU];
 #pragma unroll
       for (int q = 0; q < kU; ++q) {
         const size_t j = j0 + q * stride;
         // the backward accumulates dG3 slice-major, (i3, c, n3), as the copy
-        const size_t c = j / ((size_t)g.m3 * 4), r = j - c * g.m3 * 4;
+        const unsigned jj = (unsigned)j, c = jj / (g.m3 * 4), r = jj - c * g.m3 * 4;  // n2 < 2^32
         jt[q] = ((r >> 2) * 32 + c) * 4 + (r & 3);
         if (j < n2) {
           pv[q] = u.p2[j];
