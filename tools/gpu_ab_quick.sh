@@ -7,3 +7,4 @@ for v in base new base new; do
   if [ $v = base ]; then export TTB_LIB_PATH=ab/libttb_base.so; else unset TTB_LIB_PATH; fi
   for c in cfg2 cfg3; do echo "$v $(timeout 300 python tools/cfg_kernels.py $c 2>&1 | tail -1)"; done
 done 2>&1 | tee gpurun_out/ab_kernels.log
+timeout 200 python tools/fwd_stamps.py 2>&1 | tail -6 > gpurun_out/fwd_stamps_new.txt
