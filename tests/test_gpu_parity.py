@@ -625,15 +625,41 @@ def test_large_m3_runs_deterministic_pipeline():
         assert rel_err(res["grads"][k], want[k]) < GRAD_TOL, k
 
 
-@pytest.mark.parametrize("m,B,max_bag", [((300, 7, 25), 700, 3), ((20, 20, 25), 1, 1), ((20, 20, 25), 3, 2)])
+@pytest.mark.parametrize("m,B,max_bag", [((300, 7, 25), 700, 3), ((20, 20, 25), 1, 1), ((20, 20, 25), 3, 2),
+                                         ((6, 5, 288), 600, 4), ((9, 11, 1), 500, 3), ((1, 40, 30), 400, 3),
+                                         ((50, 1, 40), 400, 3)])
 def test_fast_edge_geometries(m, B, max_bag):
     """Tensor-core pipeline edge cases: m1 > 256 (the plan's per-group counters
-    no longer fit its register cache), a single lookup, a three-bag batch."""
+    no longer fit its register cache), a single lookup, a three-bag batch, the
+    largest G3 the forward keeps resident (m3 = 288), one-slice G3 (m3 = 1),
+    and a single prefix group on either side (m1 = 1: one key per i2 group;
+    m2 = 1: every lookup in one i2 group)."""
     g = O.Geometry(m, (4, 4, 4), (1, 32, 32, 1))
     cores32 = [c.astype(np.float32) for c in O.init_cores(g, 8)]
     rng = np.random.default_rng(B)
     idx, off = random_batch(rng, g.rows, B, max_bag, skew=False)
     gout = rng.standard_normal((B, g.cols)).astype(np.float32)
+    res = run_case(g, cores32, idx, off, gout)
+    assert res["eng"].fast
+    c64 = [c.astype(np.float64) for c in cores32]
+    assert rel_err(res["out"], O.forward(c64, g, idx, off)) < FWD_TOL
+    ur, ug = O.unique_aggregate(idx, np.repeat(gout.astype(np.float64), np.diff(off), axis=0))
+    want = O.core_grads(c64, g, ur, ug)
+    for k in range(3):
+        assert rel_err(res["grads"][k], want[k]) < GRAD_TOL, k
+
+
+@pytest.mark.parametrize("m", [(6, 5, 288), (50, 1, 40), (1, 40, 30)])
+def test_fast_edge_geometries_pooled_hot(m):
+    """Pooled Zipf batches (hot keys: full items, the row sort's chunks and
+    the row-grouped backward) on the boundary geometries of the tensor-core
+    pipeline: the largest resident G3 and a single prefix group on either
+    side. Forward and core gradients against the fp64 oracle."""
+    g = O.Geometry(m, (4, 4, 4), (1, 32, 32, 1))
+    cores32 = [c.astype(np.float32) for c in O.init_cores(g, 21)]
+    rng = np.random.default_rng(sum(m))
+    idx, off = random_batch(rng, g.rows, 1500, 20, skew=True)
+    gout = rng.standard_normal((off.size - 1, g.cols)).astype(np.float32)
     res = run_case(g, cores32, idx, off, gout)
     assert res["eng"].fast
     c64 = [c.astype(np.float64) for c in cores32]
